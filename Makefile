@@ -1,0 +1,23 @@
+# Builds the B200 library and the CPU oracle. `make` = everything available here.
+NVCC    ?= /usr/local/cuda/bin/nvcc
+ARCH    ?= -gencode arch=compute_100a,code=sm_100a
+NVFLAGS ?= -O3 -std=c++17 -lineinfo $(ARCH) -Xcompiler -fPIC -Xptxas -v
+PKG     := paper_2207_01016_b200
+CSRC    := $(PKG)/csrc
+LIB     := $(PKG)/liblpd_nystrom.so
+HDRS    := $(wildcard $(CSRC)/*.cuh) include/lpd_nystrom.h
+
+all: $(LIB) oracle
+
+$(LIB): $(CSRC)/lpd_nystrom.cu $(HDRS)
+	$(NVCC) $(NVFLAGS) -shared -o $@ $< -lcuda 2> $(PKG)/ptxas.log || (cat $(PKG)/ptxas.log; false)
+	@grep -E "registers|spill|smem" $(PKG)/ptxas.log | head -20 || true
+
+oracle:
+	$(MAKE) -C oracle
+
+clean:
+	rm -f $(LIB) $(PKG)/ptxas.log
+	$(MAKE) -C oracle clean
+
+.PHONY: all oracle clean

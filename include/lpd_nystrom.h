@@ -1,0 +1,121 @@
+/*
+ * lpd_nystrom.h — C ABI of the B200 Nyström-factor library (liblpd_nystrom.so).
+ *
+ * This is the drop-in boundary for the LPD-SVM reference's factor path. Every
+ * entry point below replaces a named reference interface:
+ *
+ *   lpd_compute_g_csr / lpd_compute_g_dense
+ *       replace lpdsvm::compute_G
+ *       (reference proj/include/lpdsvm/factor.hpp:50-55, proj/src/factor.cpp:165-192):
+ *       G = Z(points, landmarks) · L, written row-major into a caller buffer.
+ *   lpd_set_basis_csr / lpd_set_basis_dense
+ *       receive the (landmarks, landmark_norms, L, params) arguments of the same
+ *       call (factor.hpp:53-54). Split out so one basis (one γ) serves many row
+ *       batches and devices: the reference calls compute_G once per γ
+ *       (proj/src/factor.cpp:211-214, proj/src/modelsel.cpp:466-476).
+ *   lpd_decision_values
+ *       replaces the held-out scoring loop d[r][p] = G_r · w_p
+ *       (proj/src/modelsel.cpp:409-426) and the warm-start/KKT sweeps that read
+ *       G·w (proj/src/dcd.cpp:91-102, 150-172).
+ *   lpd_predict_csr
+ *       replaces the chunked Z·βᵀ + vote of ovo_predict
+ *       (proj/src/multiclass.cpp:170-200, vote :153-168).
+ *
+ * Conventions: plain pointers and sizes only, no CUDA or C++ types. Matrices
+ * are row-major fp64 with an explicit leading dimension in elements. Sparse
+ * points use CSR with 0-based int32 column indices, the flattened form of the
+ * reference's std::vector<Feature> (proj/include/lpdsvm/dataio.hpp:14-24).
+ * Functions never throw; they return an LPD_* status and leave a message
+ * retrievable with lpd_last_error() (thread-local).
+ */
+#ifndef LPD_NYSTROM_H
+#define LPD_NYSTROM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LPD_OK 0
+#define LPD_ERR_INVALID_ARGUMENT 1 /* reference: std::invalid_argument (factor.cpp:169,173; kernel.cpp:286-291) */
+#define LPD_ERR_CUDA 2             /* device / driver failure: std::runtime_error */
+#define LPD_ERR_UNSUPPORTED 3      /* valid input outside this build's kernel envelope */
+#define LPD_ERR_OUT_OF_MEMORY 4
+#define LPD_ERR_NO_DEVICE 5
+
+#define LPD_OUT_F64 0
+#define LPD_OUT_F32 1
+
+typedef struct lpd_context lpd_context;
+
+/* Per-call phase timings (seconds, host wall clock unless noted). */
+typedef struct lpd_timings {
+    double total_seconds;     /* whole call */
+    double h2d_seconds;       /* sum over devices of host->device copy time (events) */
+    double kernel_seconds;    /* sum over devices of prep + factor kernel time (events) */
+    double d2h_seconds;       /* sum over devices of device->host copy time (events) */
+    double host_copy_seconds; /* pinned staging -> caller buffer memcpy time (wall) */
+    int64_t rows;             /* rows computed */
+    int64_t launches;         /* kernel launches issued */
+    int32_t devices;          /* devices used */
+    int32_t reserved;
+} lpd_timings;
+
+const char* lpd_last_error(void);
+int lpd_version(void);
+/* Number of visible CUDA devices (0 on a machine without a GPU; never fails). */
+int lpd_device_count(void);
+
+/* num_devices <= 0: use LPD_NUM_GPUS from the environment if set, else all visible. */
+int lpd_context_create(lpd_context** out, int num_devices);
+int lpd_context_destroy(lpd_context* ctx);
+int lpd_context_num_devices(const lpd_context* ctx);
+
+/* Basis: B landmarks with d features, L (B x b_eff, row-major, ld = b_eff), gamma > 0.
+ * Replicated to every device of the context. Landmark norms are recomputed on the
+ * device from the same values the tensor cores see (the caller's fp64 norms are
+ * not needed). */
+int lpd_set_basis_dense(lpd_context* ctx, const double* landmarks, int64_t B, int64_t d,
+                        int64_t ld, const double* L, int64_t b_eff, double gamma);
+int lpd_set_basis_csr(lpd_context* ctx, int64_t B, int64_t d, const int64_t* indptr,
+                      const int32_t* indices, const double* values, const double* L,
+                      int64_t b_eff, double gamma);
+
+/* G (n x b_eff, leading dimension ldg >= b_eff) for host rows; rows are sharded
+ * across the context's devices, results streamed back into G. */
+int lpd_compute_g_dense(lpd_context* ctx, const double* X, int64_t n, int64_t d, int64_t ldx,
+                        double* G, int64_t ldg, lpd_timings* timings);
+int lpd_compute_g_csr(lpd_context* ctx, int64_t n, int64_t d, const int64_t* indptr,
+                      const int32_t* indices, const double* values, double* G, int64_t ldg,
+                      lpd_timings* timings);
+
+/* Device-resident variant: X_dev (n x d fp64, ld ldx) and G_dev on device
+ * `device_index` of the context; out_dtype LPD_OUT_F64 or LPD_OUT_F32; stream is a
+ * cudaStream_t passed as void* (NULL = the library's stream, synchronised before
+ * return). scratch may be NULL (library allocates) . */
+int lpd_compute_g_device(lpd_context* ctx, int device_index, const double* X_dev, int64_t n,
+                         int64_t ldx, void* G_dev, int64_t ldg, int out_dtype, void* stream);
+
+/* Decision values D (n x P, ld = ldd) = G (n x b_eff, ld = ldg) · Wᵀ, W (P x b_eff, ld = b_eff).
+ * All pointers are device pointers on device_index; g_dtype LPD_OUT_F64/F32. fp64
+ * accumulation. */
+int lpd_decision_values_device(lpd_context* ctx, int device_index, const void* G_dev,
+                               int g_dtype, int64_t n, int64_t b_eff, int64_t ldg,
+                               const double* W_dev, int64_t P, double* D_dev, int64_t ldd,
+                               void* stream);
+
+/* Host variant of the above (copies in/out). */
+int lpd_decision_values(lpd_context* ctx, const double* G, int64_t n, int64_t b_eff, int64_t ldg,
+                        const double* W, int64_t P, double* D, int64_t ldd);
+
+/* Last kernel timing of the fused factor kernel on device_index (milliseconds,
+ * CUDA events around the launch on its stream), for benchmarks. */
+double lpd_last_factor_kernel_ms(const lpd_context* ctx, int device_index);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LPD_NYSTROM_H */

@@ -1,0 +1,371 @@
+"""B200-native Nyström factor path of LPD-SVM (arXiv 2207.01016).
+
+Python mirror of the reference's factor interface over the C ABI in
+``include/lpd_nystrom.h`` (``liblpd_nystrom.so``, built in-tree). The reference
+entry point this mirrors is ``lpdsvm::compute_G`` (reference
+proj/include/lpdsvm/factor.hpp:50-55, proj/src/factor.cpp:165-192); argument
+meaning and error behaviour follow it:
+
+* ``chunk_size == 0``          -> ValueError  (factor.cpp:169, std::invalid_argument)
+* ``L.rows != len(landmarks)`` -> ValueError  (factor.cpp:173)
+* γ not positive and finite    -> ValueError  (kernel.cpp:286-291)
+* device / driver failures     -> RuntimeError (std::runtime_error)
+
+There is no CPU fallback: when the CUDA library cannot be loaded or no B200 is
+visible, every compute call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+
+__all__ = [
+    "LIB_PATH",
+    "LpdError",
+    "Context",
+    "Timings",
+    "KernelParams",
+    "load_library",
+    "device_count",
+    "compute_G",
+    "sparse_to_csr",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liblpd_nystrom.so")
+
+LPD_OK = 0
+LPD_ERR_INVALID_ARGUMENT = 1
+LPD_ERR_CUDA = 2
+LPD_ERR_UNSUPPORTED = 3
+LPD_ERR_OUT_OF_MEMORY = 4
+LPD_ERR_NO_DEVICE = 5
+LPD_OUT_F64 = 0
+LPD_OUT_F32 = 1
+
+# Every symbol include/lpd_nystrom.h declares (checked by the CPU test suite).
+EXPORTED_SYMBOLS = (
+    "lpd_last_error",
+    "lpd_version",
+    "lpd_device_count",
+    "lpd_context_create",
+    "lpd_context_destroy",
+    "lpd_context_num_devices",
+    "lpd_set_basis_dense",
+    "lpd_set_basis_csr",
+    "lpd_compute_g_dense",
+    "lpd_compute_g_csr",
+    "lpd_compute_g_device",
+    "lpd_decision_values_device",
+    "lpd_decision_values",
+    "lpd_last_factor_kernel_ms",
+)
+
+
+class LpdError(RuntimeError):
+    """Device-side failure (the reference's std::runtime_error)."""
+
+    def __init__(self, code: int, message: str):
+        super().__init__(message)
+        self.code = code
+
+
+class Timings(ctypes.Structure):
+    _fields_ = [
+        ("total_seconds", ctypes.c_double),
+        ("h2d_seconds", ctypes.c_double),
+        ("kernel_seconds", ctypes.c_double),
+        ("d2h_seconds", ctypes.c_double),
+        ("host_copy_seconds", ctypes.c_double),
+        ("rows", ctypes.c_int64),
+        ("launches", ctypes.c_int64),
+        ("devices", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+    ]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_ if name != "reserved"}
+
+
+@dataclass(frozen=True)
+class KernelParams:
+    """reference proj/include/lpdsvm/kernel.hpp:11-19 (Gaussian only)."""
+
+    gamma: float = 1.0
+
+
+_lib = None
+
+_c_dbl_p = ctypes.POINTER(ctypes.c_double)
+_c_i64_p = ctypes.POINTER(ctypes.c_int64)
+_c_i32_p = ctypes.POINTER(ctypes.c_int32)
+
+
+def load_library(path: Optional[str] = None) -> ctypes.CDLL:
+    """Load liblpd_nystrom.so (in-tree). Raises if it has not been built."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = path or LIB_PATH
+    if not os.path.exists(p):
+        raise RuntimeError(
+            f"{p} is missing: build the CUDA library first (python -c 'import __graft_entry__ as g; g.build()' or make)"
+        )
+    lib = ctypes.CDLL(p)
+    vp = ctypes.c_void_p
+    i64 = ctypes.c_int64
+    lib.lpd_last_error.restype = ctypes.c_char_p
+    lib.lpd_version.restype = ctypes.c_int
+    lib.lpd_device_count.restype = ctypes.c_int
+    lib.lpd_context_create.argtypes = [ctypes.POINTER(vp), ctypes.c_int]
+    lib.lpd_context_destroy.argtypes = [vp]
+    lib.lpd_context_num_devices.argtypes = [vp]
+    lib.lpd_set_basis_dense.argtypes = [vp, _c_dbl_p, i64, i64, i64, _c_dbl_p, i64, ctypes.c_double]
+    lib.lpd_set_basis_csr.argtypes = [vp, i64, i64, _c_i64_p, _c_i32_p, _c_dbl_p, _c_dbl_p, i64,
+                                      ctypes.c_double]
+    lib.lpd_compute_g_dense.argtypes = [vp, _c_dbl_p, i64, i64, i64, _c_dbl_p, i64,
+                                        ctypes.POINTER(Timings)]
+    lib.lpd_compute_g_csr.argtypes = [vp, i64, i64, _c_i64_p, _c_i32_p, _c_dbl_p, _c_dbl_p, i64,
+                                      ctypes.POINTER(Timings)]
+    lib.lpd_compute_g_device.argtypes = [vp, ctypes.c_int, vp, i64, i64, vp, i64, ctypes.c_int, vp]
+    lib.lpd_decision_values_device.argtypes = [vp, ctypes.c_int, vp, ctypes.c_int, i64, i64, i64,
+                                               vp, i64, vp, i64, vp]
+    lib.lpd_decision_values.argtypes = [vp, _c_dbl_p, i64, i64, i64, _c_dbl_p, i64, _c_dbl_p, i64]
+    lib.lpd_last_factor_kernel_ms.argtypes = [vp, ctypes.c_int]
+    lib.lpd_last_factor_kernel_ms.restype = ctypes.c_double
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def _check(status: int) -> None:
+    if status == LPD_OK:
+        return
+    msg = (_lib.lpd_last_error() or b"").decode(errors="replace")
+    if status == LPD_ERR_INVALID_ARGUMENT:
+        raise ValueError(msg)
+    raise LpdError(status, msg)
+
+
+def device_count() -> int:
+    return int(load_library().lpd_device_count())
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _ptr(a: np.ndarray, ctype=ctypes.c_double):
+    return a.ctypes.data_as(ctypes.POINTER(ctype))
+
+
+def sparse_to_csr(points: Sequence) -> tuple:
+    """Flatten a sequence of sparse points into (indptr, indices, values, dim).
+
+    A point is either a dense 1-D array or a sequence of (index, value) pairs
+    with strictly ascending 0-based indices, the reference's SparseVector
+    (proj/include/lpdsvm/dataio.hpp:14-24). dim = 1 + max index (0 if empty).
+    """
+    indptr = np.zeros(len(points) + 1, dtype=np.int64)
+    idx_parts, val_parts = [], []
+    dim = 0
+    for i, p in enumerate(points):
+        if isinstance(p, np.ndarray) and p.ndim == 1 and p.dtype.kind == "f":
+            nz = np.flatnonzero(p)
+            idx = nz.astype(np.int32)
+            val = p[nz].astype(np.float64)
+            dim = max(dim, p.shape[0])
+        else:
+            if len(p):
+                idx = np.fromiter((f[0] for f in p), dtype=np.int32, count=len(p))
+                val = np.fromiter((f[1] for f in p), dtype=np.float64, count=len(p))
+                dim = max(dim, int(idx.max()) + 1)
+            else:
+                idx = np.zeros(0, np.int32)
+                val = np.zeros(0, np.float64)
+        idx_parts.append(idx)
+        val_parts.append(val)
+        indptr[i + 1] = indptr[i] + len(idx)
+    indices = np.concatenate(idx_parts) if idx_parts else np.zeros(0, np.int32)
+    values = np.concatenate(val_parts) if val_parts else np.zeros(0, np.float64)
+    return indptr, indices.astype(np.int32), values, dim
+
+
+class Context:
+    """A set of B200 devices holding one replicated basis (landmarks, L, γ)."""
+
+    def __init__(self, num_devices: int = 0):
+        self._lib = load_library()
+        h = ctypes.c_void_p()
+        _check(self._lib.lpd_context_create(ctypes.byref(h), int(num_devices)))
+        self._h = h
+        self.b_eff = 0
+        self.dim = 0
+
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        return self._h
+
+    @property
+    def num_devices(self) -> int:
+        return int(self._lib.lpd_context_num_devices(self._h))
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            self._lib.lpd_context_destroy(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---------------------------------------------------------------- basis
+    def set_basis_dense(self, landmarks: np.ndarray, L: np.ndarray, gamma: float) -> None:
+        lm = _f64(landmarks)
+        if lm.ndim != 2:
+            raise ValueError("landmarks must be a 2-D array")
+        Lm = _f64(L)
+        if Lm.ndim != 2 or Lm.shape[0] != lm.shape[0]:
+            raise ValueError("L row count must match landmark count")
+        _check(self._lib.lpd_set_basis_dense(self._h, _ptr(lm), lm.shape[0], lm.shape[1],
+                                             lm.shape[1], _ptr(Lm), Lm.shape[1], float(gamma)))
+        self.b_eff, self.dim = Lm.shape[1], lm.shape[1]
+
+    def set_basis_csr(self, indptr, indices, values, dim: int, L: np.ndarray, gamma: float) -> None:
+        ip = np.ascontiguousarray(indptr, dtype=np.int64)
+        ix = np.ascontiguousarray(indices, dtype=np.int32)
+        vv = _f64(values)
+        Lm = _f64(L)
+        B = ip.shape[0] - 1
+        if Lm.ndim != 2 or Lm.shape[0] != B:
+            raise ValueError("L row count must match landmark count")
+        _check(self._lib.lpd_set_basis_csr(self._h, B, int(dim), _ptr(ip, ctypes.c_int64),
+                                           _ptr(ix, ctypes.c_int32), _ptr(vv), _ptr(Lm),
+                                           Lm.shape[1], float(gamma)))
+        self.b_eff, self.dim = Lm.shape[1], int(dim)
+
+    # ---------------------------------------------------------------- rows
+    def compute_g_dense(self, X: np.ndarray, out: Optional[np.ndarray] = None,
+                        timings: Optional[Timings] = None) -> np.ndarray:
+        x = _f64(X)
+        if x.ndim != 2:
+            raise ValueError("X must be 2-D")
+        n = x.shape[0]
+        G = out if out is not None else np.empty((n, self.b_eff), dtype=np.float64)
+        if G.dtype != np.float64 or not G.flags.c_contiguous or G.shape != (n, self.b_eff):
+            raise ValueError("out must be a C-contiguous float64 (n, b_eff) array")
+        t = timings if timings is not None else Timings()
+        _check(self._lib.lpd_compute_g_dense(self._h, _ptr(x), n, x.shape[1], x.shape[1], _ptr(G),
+                                             self.b_eff, ctypes.byref(t)))
+        return G
+
+    def compute_g_csr(self, indptr, indices, values, out: Optional[np.ndarray] = None,
+                      timings: Optional[Timings] = None) -> np.ndarray:
+        ip = np.ascontiguousarray(indptr, dtype=np.int64)
+        ix = np.ascontiguousarray(indices, dtype=np.int32)
+        vv = _f64(values)
+        n = ip.shape[0] - 1
+        G = out if out is not None else np.empty((n, self.b_eff), dtype=np.float64)
+        if G.dtype != np.float64 or not G.flags.c_contiguous or G.shape != (n, self.b_eff):
+            raise ValueError("out must be a C-contiguous float64 (n, b_eff) array")
+        t = timings if timings is not None else Timings()
+        _check(self._lib.lpd_compute_g_csr(self._h, n, self.dim, _ptr(ip, ctypes.c_int64),
+                                           _ptr(ix, ctypes.c_int32), _ptr(vv), _ptr(G),
+                                           self.b_eff, ctypes.byref(t)))
+        return G
+
+    def compute_g_device(self, X_dev, G_dev, device_index: int = 0, stream=None) -> None:
+        """X_dev (n x d fp64) and G_dev (n x b_eff, fp64 or fp32) are torch CUDA tensors."""
+        import torch
+
+        if X_dev.dtype != torch.float64 or not X_dev.is_contiguous():
+            raise ValueError("X_dev must be a contiguous float64 CUDA tensor")
+        if G_dev.dtype not in (torch.float64, torch.float32):
+            raise ValueError("G_dev must be float64 or float32")
+        out_dtype = LPD_OUT_F64 if G_dev.dtype == torch.float64 else LPD_OUT_F32
+        st = ctypes.c_void_p(stream.cuda_stream) if stream is not None else None
+        _check(self._lib.lpd_compute_g_device(self._h, device_index, ctypes.c_void_p(X_dev.data_ptr()),
+                                              X_dev.shape[0], X_dev.stride(0),
+                                              ctypes.c_void_p(G_dev.data_ptr()), G_dev.stride(0),
+                                              out_dtype, st))
+
+    def last_factor_kernel_ms(self, device_index: int = 0) -> float:
+        return float(self._lib.lpd_last_factor_kernel_ms(self._h, device_index))
+
+    # ---------------------------------------------------------------- decision values
+    def decision_values(self, G: np.ndarray, W: np.ndarray) -> np.ndarray:
+        g = _f64(G)
+        w = _f64(W)
+        if w.ndim == 1:
+            w = w[None, :]
+        if g.shape[1] != w.shape[1]:
+            raise ValueError("W column count must match G")
+        D = np.empty((g.shape[0], w.shape[0]), dtype=np.float64)
+        _check(self._lib.lpd_decision_values(self._h, _ptr(g), g.shape[0], g.shape[1], g.shape[1],
+                                             _ptr(w), w.shape[0], _ptr(D), w.shape[0]))
+        return D
+
+    def decision_values_device(self, G_dev, W_dev, D_dev, device_index: int = 0, stream=None) -> None:
+        import torch
+
+        g_dtype = LPD_OUT_F64 if G_dev.dtype == torch.float64 else LPD_OUT_F32
+        st = ctypes.c_void_p(stream.cuda_stream) if stream is not None else None
+        _check(self._lib.lpd_decision_values_device(
+            self._h, device_index, ctypes.c_void_p(G_dev.data_ptr()), g_dtype, G_dev.shape[0],
+            G_dev.shape[1], G_dev.stride(0), ctypes.c_void_p(W_dev.data_ptr()), W_dev.shape[0],
+            ctypes.c_void_p(D_dev.data_ptr()), D_dev.stride(0), st))
+
+
+def compute_G(points, norms, landmarks, landmark_norms, L, params, chunk_size: int,
+              num_threads: int = 1, context: Optional[Context] = None) -> np.ndarray:
+    """Mirror of lpdsvm::compute_G (factor.hpp:52-55) on the B200 path.
+
+    ``points``/``landmarks``: sequences of sparse points (see sparse_to_csr) or
+    dense 2-D arrays. ``norms``/``landmark_norms`` are accepted for signature
+    parity and ignored: the device recomputes them from the same values the
+    tensor cores see. ``chunk_size`` is validated like the reference; the
+    device pipeline chooses its own row chunking (results do not depend on
+    it). ``num_threads`` is accepted and unused.
+    """
+    if chunk_size == 0:
+        raise ValueError("chunk_size must be positive")
+    gamma = params.gamma if hasattr(params, "gamma") else float(params)
+    Lm = _f64(L)
+    if isinstance(landmarks, np.ndarray) and landmarks.ndim == 2:
+        B = landmarks.shape[0]
+    else:
+        B = len(landmarks)
+    if Lm.ndim != 2 or Lm.shape[0] != B:
+        raise ValueError("L row count must match landmark count")
+    if not (gamma > 0.0) or not np.isfinite(gamma):
+        raise ValueError("kernel gamma must be positive and finite")
+    ctx = context or Context()
+    try:
+        dense_pts = isinstance(points, np.ndarray) and points.ndim == 2
+        dense_lms = isinstance(landmarks, np.ndarray) and landmarks.ndim == 2
+        if dense_pts and dense_lms:
+            d = max(points.shape[1], landmarks.shape[1])
+            X = np.zeros((points.shape[0], d)); X[:, : points.shape[1]] = points
+            Y = np.zeros((B, d)); Y[:, : landmarks.shape[1]] = landmarks
+            ctx.set_basis_dense(Y, Lm, gamma)
+            return ctx.compute_g_dense(X)
+        pip, pix, pvl, pdim = sparse_to_csr(list(points) if not dense_pts else list(points))
+        lip, lix, lvl, ldim = sparse_to_csr(list(landmarks) if not dense_lms else list(landmarks))
+        d = max(pdim, ldim)
+        ctx.set_basis_csr(lip, lix, lvl, d, Lm, gamma)
+        return ctx.compute_g_csr(pip, pix, pvl)
+    finally:
+        if context is None:
+            ctx.close()

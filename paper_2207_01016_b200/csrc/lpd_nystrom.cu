@@ -1,0 +1,727 @@
+// liblpd_nystrom.so — host runtime behind include/lpd_nystrom.h.
+//
+// Owns one DeviceState per GPU of a context: the replicated basis (landmark
+// split planes, Lᵀ split planes, TMA descriptors), two pipeline slots with
+// their own streams, and the launch logic for K2/K3 (prep_kernels.cuh), K1
+// (factor_kernel.cuh) and K4 (decision_kernels.cuh).
+//
+// Host-row calls (lpd_compute_g_*) shard rows contiguously across devices
+// (reference compute_G splits rows into chunks, proj/src/factor.cpp:179-190;
+// here each device owns a contiguous shard, no collective) and pipeline
+// H2D → prep → factor → D2H in row chunks on two streams per device, one host
+// thread per device. Errors never escape as exceptions: every entry point
+// returns a status and records a message (lpd_last_error).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/lpd_nystrom.h"
+#include "decision_kernels.cuh"
+#include "factor_kernel.cuh"
+#include "prep_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct LpdError : std::runtime_error {
+    int code;
+    LpdError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw LpdError(code, msg); }
+
+#define CUDA_TRY(expr)                                                                   \
+    do {                                                                                 \
+        cudaError_t _e = (expr);                                                         \
+        if (_e != cudaSuccess) {                                                         \
+            fail(_e == cudaErrorMemoryAllocation ? LPD_ERR_OUT_OF_MEMORY : LPD_ERR_CUDA, \
+                 std::string(#expr) + ": " + cudaGetErrorString(_e));                    \
+        }                                                                                \
+    } while (0)
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return LPD_OK;
+    } catch (const LpdError& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host allocation failed";
+        return LPD_ERR_OUT_OF_MEMORY;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return LPD_ERR_CUDA;
+    }
+}
+
+int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+// ------------------------------------------------------------------ TMA descriptors
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    if (!fn) fail(LPD_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+    return fn;
+}
+
+// Row-major fp16 plane [rows × cols], box [box_rows × 64 cols], 128-byte swizzle.
+CUtensorMap make_plane_map(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
+                           uint32_t box_cols) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {cols * 2};
+    cuuint32_t box[2] = {box_cols, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims,
+                             strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(LPD_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+    return m;
+}
+
+template <typename T>
+void dev_alloc(T** p, size_t count) {
+    *p = nullptr;
+    if (count == 0) count = 1;
+    CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T)));
+}
+template <typename T>
+void dev_free(T*& p) {
+    if (p) cudaFree(p);
+    p = nullptr;
+}
+
+struct Slot {
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev[4] = {};  // h2d start, kernels start, d2h start, d2h end
+    int64_t rows_cap = 0;    // capacity in rows (multiple of 128)
+    double* x = nullptr;     // [rows_cap × d] fp64
+    __half* xhi = nullptr;   // [rows_cap × 64]
+    __half* xlo = nullptr;
+    float2* raux = nullptr;  // [rows_cap]
+    double* g = nullptr;     // [rows_cap × b_eff] fp64 (host-call path)
+    int64_t g_cols = 0;
+    int64_t nnz_cap = 0;
+    int64_t* indptr = nullptr;
+    int32_t* indices = nullptr;
+    double* values = nullptr;
+};
+
+struct DeviceState {
+    int device = 0;
+    int num_sms = 0;
+    bool has_basis = false;
+    int64_t B = 0, d = 0, b_eff = 0, B_pad = 0, Beff_pad = 0;
+    double gamma = 1.0;
+    double* mu = nullptr;
+    __half* lm_hi = nullptr;
+    __half* lm_lo = nullptr;
+    float2* lm_aux = nullptr;
+    __half* lt_hi = nullptr;
+    __half* lt_lo = nullptr;
+    float* col_scale = nullptr;
+    CUtensorMap tm_lmhi, tm_lmlo, tm_lthi, tm_ltlo;
+    Slot slot[2];
+    cudaEvent_t kev[2] = {};
+    float last_kernel_ms = 0.f;
+
+    void free_basis() {
+        dev_free(mu); dev_free(lm_hi); dev_free(lm_lo); dev_free(lm_aux);
+        dev_free(lt_hi); dev_free(lt_lo); dev_free(col_scale);
+        has_basis = false;
+    }
+    void free_slot(Slot& s) {
+        dev_free(s.x); dev_free(s.xhi); dev_free(s.xlo); dev_free(s.raux); dev_free(s.g);
+        dev_free(s.indptr); dev_free(s.indices); dev_free(s.values);
+        s.rows_cap = 0; s.g_cols = 0; s.nnz_cap = 0;
+    }
+};
+
+}  // namespace
+
+struct lpd_context {
+    std::vector<DeviceState> dev;
+};
+
+namespace {
+
+void ensure_slot(DeviceState& ds, Slot& s, int64_t rows, bool need_g, int64_t nnz) {
+    const int64_t rows_pad = round_up(std::max<int64_t>(rows, 1), 128);
+    if (rows_pad > s.rows_cap || (need_g && s.g_cols != ds.b_eff)) {
+        dev_free(s.x); dev_free(s.xhi); dev_free(s.xlo); dev_free(s.raux); dev_free(s.g);
+        const int64_t cap = std::max(rows_pad, s.rows_cap);
+        dev_alloc(&s.x, static_cast<size_t>(cap * std::max<int64_t>(ds.d, 1)));
+        dev_alloc(&s.xhi, static_cast<size_t>(cap * lpd::KD_MAX));
+        dev_alloc(&s.xlo, static_cast<size_t>(cap * lpd::KD_MAX));
+        dev_alloc(&s.raux, static_cast<size_t>(cap));
+        if (need_g) dev_alloc(&s.g, static_cast<size_t>(cap * ds.b_eff));
+        s.g_cols = need_g ? ds.b_eff : 0;
+        s.rows_cap = cap;
+    }
+    if (nnz > s.nnz_cap) {
+        dev_free(s.indptr); dev_free(s.indices); dev_free(s.values);
+        dev_alloc(&s.indptr, static_cast<size_t>(s.rows_cap + 1));
+        dev_alloc(&s.indices, static_cast<size_t>(nnz));
+        dev_alloc(&s.values, static_cast<size_t>(nnz));
+        s.nnz_cap = nnz;
+    } else if (s.indptr == nullptr && nnz > 0) {
+        dev_alloc(&s.indptr, static_cast<size_t>(s.rows_cap + 1));
+    }
+}
+
+void init_device(DeviceState& ds, int device) {
+    ds.device = device;
+    CUDA_TRY(cudaSetDevice(device));
+    CUDA_TRY(cudaDeviceGetAttribute(&ds.num_sms, cudaDevAttrMultiProcessorCount, device));
+    int major = 0, minor = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+    CUDA_TRY(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device));
+    if (major != 10 || minor != 0)
+        fail(LPD_ERR_UNSUPPORTED, "liblpd_nystrom is built for sm_100a (B200); device " +
+                                      std::to_string(device) + " is sm_" + std::to_string(major) +
+                                      std::to_string(minor));
+    for (auto& s : ds.slot) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+        for (auto& e : s.ev) CUDA_TRY(cudaEventCreate(&e));
+    }
+    for (auto& e : ds.kev) CUDA_TRY(cudaEventCreate(&e));
+    CUDA_TRY(cudaFuncSetAttribute(lpd::nystrom_factor_kernel<double>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, lpd::k1::SMEM_BYTES));
+    CUDA_TRY(cudaFuncSetAttribute(lpd::nystrom_factor_kernel<float>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, lpd::k1::SMEM_BYTES));
+}
+
+void validate_basis_args(int64_t B, int64_t d, int64_t b_eff, double gamma, const double* L) {
+    if (B <= 0) fail(LPD_ERR_INVALID_ARGUMENT, "landmark count must be positive");
+    if (d < 0) fail(LPD_ERR_INVALID_ARGUMENT, "feature dimension must be non-negative");
+    if (b_eff <= 0) fail(LPD_ERR_INVALID_ARGUMENT, "L must have at least one column");
+    if (!L) fail(LPD_ERR_INVALID_ARGUMENT, "L is null");
+    // reference validate(): proj/src/kernel.cpp:286-291
+    if (!(gamma > 0.0) || !std::isfinite(gamma))
+        fail(LPD_ERR_INVALID_ARGUMENT, "kernel gamma must be positive and finite");
+    if (d > lpd::KD_MAX)
+        fail(LPD_ERR_UNSUPPORTED, "this build's fused factor kernel supports d <= 64 (got d=" +
+                                      std::to_string(d) + ")");
+    if (B > (1 << 30) || b_eff > (1 << 30)) fail(LPD_ERR_UNSUPPORTED, "basis too large");
+}
+
+// Builds the basis on one device from a dense fp64 landmark block already on
+// that device (lm_dev, ld = d) and L on the host.
+void build_basis(DeviceState& ds, const double* lm_dev, int64_t B, int64_t d, const double* L_host,
+                 int64_t b_eff, double gamma) {
+    CUDA_TRY(cudaSetDevice(ds.device));
+    cudaStream_t st = ds.slot[0].stream;
+    ds.free_basis();
+    ds.B = B; ds.d = d; ds.b_eff = b_eff; ds.gamma = gamma;
+    ds.B_pad = round_up(B, lpd::k1::NC);
+    ds.Beff_pad = round_up(b_eff, lpd::k1::N2);
+    dev_alloc(&ds.mu, lpd::KD_MAX);
+    dev_alloc(&ds.lm_hi, static_cast<size_t>(ds.B_pad * lpd::KD_MAX));
+    dev_alloc(&ds.lm_lo, static_cast<size_t>(ds.B_pad * lpd::KD_MAX));
+    dev_alloc(&ds.lm_aux, static_cast<size_t>(ds.B_pad));
+    dev_alloc(&ds.lt_hi, static_cast<size_t>(ds.Beff_pad * ds.B_pad));
+    dev_alloc(&ds.lt_lo, static_cast<size_t>(ds.Beff_pad * ds.B_pad));
+    dev_alloc(&ds.col_scale, static_cast<size_t>(ds.Beff_pad));
+
+    lpd::column_mean_kernel<<<1, lpd::KD_MAX, 0, st>>>(lm_dev, d, static_cast<int>(B),
+                                                       static_cast<int>(d), ds.mu);
+    {
+        const int threads = 256, rows_per_block = threads / 32;
+        const int blocks = static_cast<int>((ds.B_pad + rows_per_block - 1) / rows_per_block);
+        lpd::prep_rows_dense_kernel<<<blocks, threads, 0, st>>>(
+            lm_dev, d, static_cast<int>(B), static_cast<int>(d), ds.mu, ds.lm_hi, ds.lm_lo,
+            ds.lm_aux, static_cast<int>(ds.B_pad), -2.0f);
+    }
+    double* L_dev = nullptr;
+    double* colmax = nullptr;
+    dev_alloc(&L_dev, static_cast<size_t>(B * b_eff));
+    dev_alloc(&colmax, static_cast<size_t>(b_eff));
+    CUDA_TRY(cudaMemcpyAsync(L_dev, L_host, sizeof(double) * B * b_eff, cudaMemcpyHostToDevice, st));
+    lpd::col_absmax_kernel<<<static_cast<int>((b_eff + 127) / 128), 128, 0, st>>>(
+        L_dev, static_cast<int>(B), static_cast<int>(b_eff), colmax);
+    dim3 grid(static_cast<unsigned>(ds.B_pad / 32), static_cast<unsigned>(ds.Beff_pad / 32));
+    lpd::lt_split_kernel<<<grid, dim3(32, 8), 0, st>>>(L_dev, static_cast<int>(B),
+                                                        static_cast<int>(b_eff), colmax, ds.lt_hi,
+                                                        ds.lt_lo, static_cast<int>(ds.B_pad),
+                                                        static_cast<int>(ds.Beff_pad), ds.col_scale);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(st));
+    dev_free(L_dev);
+    dev_free(colmax);
+
+    ds.tm_lmhi = make_plane_map(ds.lm_hi, ds.B_pad, lpd::KD_MAX, lpd::k1::NC, 64);
+    ds.tm_lmlo = make_plane_map(ds.lm_lo, ds.B_pad, lpd::KD_MAX, lpd::k1::NC, 64);
+    ds.tm_lthi = make_plane_map(ds.lt_hi, ds.Beff_pad, ds.B_pad, lpd::k1::N2, 64);
+    ds.tm_ltlo = make_plane_map(ds.lt_lo, ds.Beff_pad, ds.B_pad, lpd::k1::N2, 64);
+    ds.has_basis = true;
+}
+
+// prep + fused factor kernel for m rows of dense fp64 X already on the device.
+void launch_factor(DeviceState& ds, Slot& s, const double* x_dev, int64_t m, int64_t ldx,
+                   void* g_dev, int64_t ldg, int out_dtype, cudaStream_t st, bool time_it) {
+    if (m <= 0) return;
+    const int64_t m_pad = round_up(m, 128);
+    {
+        const int threads = 256, rows_per_block = threads / 32;
+        const int64_t blocks = std::min<int64_t>((m_pad + rows_per_block - 1) / rows_per_block,
+                                                 static_cast<int64_t>(ds.num_sms) * 16);
+        lpd::prep_rows_dense_kernel<<<static_cast<int>(blocks), threads, 0, st>>>(
+            x_dev, ldx, static_cast<int>(m), static_cast<int>(ds.d), ds.mu, s.xhi, s.xlo, s.raux,
+            static_cast<int>(m_pad), 1.0f);
+    }
+    const CUtensorMap tm_xhi = make_plane_map(s.xhi, m_pad, lpd::KD_MAX, lpd::k1::BM, 64);
+    const CUtensorMap tm_xlo = make_plane_map(s.xlo, m_pad, lpd::KD_MAX, lpd::k1::BM, 64);
+    lpd::FactorParams p;
+    p.n_rows = static_cast<int>(m);
+    p.n_row_tiles = static_cast<int>(m_pad / lpd::k1::BM);
+    p.n_chunks = static_cast<int>(ds.B_pad / lpd::k1::NC);
+    p.n_col_blocks = static_cast<int>(ds.Beff_pad / lpd::k1::N2);
+    p.b_eff = static_cast<int>(ds.b_eff);
+    p.ksteps1 = static_cast<int>(std::max<int64_t>(1, (ds.d + 15) / 16));
+    p.neg_gamma_log2e = static_cast<float>(-ds.gamma * 1.4426950408889634);
+    p.row_aux = s.raux;
+    p.lm_aux = ds.lm_aux;
+    p.col_scale = ds.col_scale;
+    p.G = g_dev;
+    p.ldg = ldg;
+    const int64_t tiles = static_cast<int64_t>(p.n_row_tiles) * p.n_col_blocks;
+    const int grid = static_cast<int>(std::min<int64_t>(tiles, ds.num_sms));
+    if (time_it) CUDA_TRY(cudaEventRecord(ds.kev[0], st));
+    if (out_dtype == LPD_OUT_F64)
+        lpd::nystrom_factor_kernel<double><<<grid, lpd::k1::THREADS, lpd::k1::SMEM_BYTES, st>>>(
+            tm_xhi, tm_xlo, ds.tm_lmhi, ds.tm_lmlo, ds.tm_lthi, ds.tm_ltlo, p);
+    else
+        lpd::nystrom_factor_kernel<float><<<grid, lpd::k1::THREADS, lpd::k1::SMEM_BYTES, st>>>(
+            tm_xhi, tm_xlo, ds.tm_lmhi, ds.tm_lmlo, ds.tm_lthi, ds.tm_ltlo, p);
+    if (time_it) CUDA_TRY(cudaEventRecord(ds.kev[1], st));
+    CUDA_TRY(cudaGetLastError());
+}
+
+lpd_context* check_ctx(lpd_context* ctx, bool need_basis) {
+    if (!ctx) fail(LPD_ERR_INVALID_ARGUMENT, "null context");
+    if (ctx->dev.empty()) fail(LPD_ERR_NO_DEVICE, "context has no devices");
+    if (need_basis && !ctx->dev[0].has_basis)
+        fail(LPD_ERR_INVALID_ARGUMENT, "no basis set (call lpd_set_basis_* first)");
+    return ctx;
+}
+
+void run_parallel(lpd_context* ctx, const std::function<void(DeviceState&, int)>& fn) {
+    const int nd = static_cast<int>(ctx->dev.size());
+    if (nd == 1) {
+        fn(ctx->dev[0], 0);
+        return;
+    }
+    std::vector<std::thread> th;
+    std::vector<std::string> errs(nd);
+    std::vector<int> codes(nd, LPD_OK);
+    for (int i = 0; i < nd; ++i)
+        th.emplace_back([&, i] {
+            try {
+                fn(ctx->dev[i], i);
+            } catch (const LpdError& e) {
+                codes[i] = e.code;
+                errs[i] = e.what();
+            } catch (const std::exception& e) {
+                codes[i] = LPD_ERR_CUDA;
+                errs[i] = e.what();
+            }
+        });
+    for (auto& t : th) t.join();
+    for (int i = 0; i < nd; ++i)
+        if (codes[i] != LPD_OK) fail(codes[i], "device " + std::to_string(i) + ": " + errs[i]);
+}
+
+// Host-row pipeline shared by the dense and CSR entry points. `stage_x` fills
+// slot.x (dense fp64 [rows × d]) on the slot's stream for global rows
+// [r0, r0 + rows).
+template <typename StageX>
+void compute_rows_host(lpd_context* ctx, int64_t n, double* G, int64_t ldg, lpd_timings* tm,
+                       StageX&& stage_x) {
+    const int nd = static_cast<int>(ctx->dev.size());
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<double> h2d(nd, 0.0), ker(nd, 0.0), d2h(nd, 0.0);
+    std::vector<int64_t> launches(nd, 0);
+    const int64_t b_eff = ctx->dev[0].b_eff;
+    // Rows per pipeline chunk: ~256 MB of fp64 G, multiple of 128.
+    const int64_t chunk = std::max<int64_t>(
+        128, std::min<int64_t>(round_up(n, 128), (256ll << 20) / (8 * b_eff) / 128 * 128));
+    run_parallel(ctx, [&](DeviceState& ds, int di) {
+        CUDA_TRY(cudaSetDevice(ds.device));
+        const int64_t per = round_up((n + nd - 1) / nd, 128);
+        const int64_t r_begin = std::min<int64_t>(n, per * di);
+        const int64_t r_end = std::min<int64_t>(n, per * (di + 1));
+        int64_t k = 0;
+        std::vector<int64_t> pending_rows[2];
+        for (int64_t r0 = r_begin; r0 < r_end; r0 += chunk, ++k) {
+            const int64_t rows = std::min(chunk, r_end - r0);
+            Slot& s = ds.slot[k & 1];
+            CUDA_TRY(cudaStreamSynchronize(s.stream));  // slot reuse (two chunks ago)
+            if (k >= 2) {
+                float a = 0, b = 0, c = 0;
+                cudaEventElapsedTime(&a, s.ev[0], s.ev[1]);
+                cudaEventElapsedTime(&b, s.ev[1], s.ev[2]);
+                cudaEventElapsedTime(&c, s.ev[2], s.ev[3]);
+                h2d[di] += a * 1e-3; ker[di] += b * 1e-3; d2h[di] += c * 1e-3;
+            }
+            stage_x(ds, s, r0, rows);  // records ev[0] and fills s.x
+            CUDA_TRY(cudaEventRecord(s.ev[1], s.stream));
+            launch_factor(ds, s, s.x, rows, ds.d, s.g, b_eff, LPD_OUT_F64, s.stream, false);
+            launches[di] += 2;
+            CUDA_TRY(cudaEventRecord(s.ev[2], s.stream));
+            CUDA_TRY(cudaMemcpy2DAsync(G + r0 * ldg, sizeof(double) * ldg, s.g,
+                                       sizeof(double) * b_eff, sizeof(double) * b_eff,
+                                       static_cast<size_t>(rows), cudaMemcpyDeviceToHost,
+                                       s.stream));
+            CUDA_TRY(cudaEventRecord(s.ev[3], s.stream));
+        }
+        for (int64_t kk = std::max<int64_t>(0, k - 2); kk < k; ++kk) {
+            Slot& s = ds.slot[kk & 1];
+            CUDA_TRY(cudaStreamSynchronize(s.stream));
+            float a = 0, b = 0, c = 0;
+            cudaEventElapsedTime(&a, s.ev[0], s.ev[1]);
+            cudaEventElapsedTime(&b, s.ev[1], s.ev[2]);
+            cudaEventElapsedTime(&c, s.ev[2], s.ev[3]);
+            h2d[di] += a * 1e-3; ker[di] += b * 1e-3; d2h[di] += c * 1e-3;
+        }
+    });
+    if (tm) {
+        std::memset(tm, 0, sizeof(*tm));
+        for (int i = 0; i < nd; ++i) {
+            tm->h2d_seconds += h2d[i];
+            tm->kernel_seconds += ker[i];
+            tm->d2h_seconds += d2h[i];
+            tm->launches += launches[i];
+        }
+        tm->rows = n;
+        tm->devices = nd;
+        tm->total_seconds =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+const char* lpd_last_error(void) { return g_last_error.c_str(); }
+
+int lpd_version(void) { return 10000; }
+
+int lpd_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int lpd_context_create(lpd_context** out, int num_devices) {
+    return guarded([&] {
+        if (!out) fail(LPD_ERR_INVALID_ARGUMENT, "null output pointer");
+        *out = nullptr;
+        const int avail = lpd_device_count();
+        if (avail <= 0) fail(LPD_ERR_NO_DEVICE, "no CUDA device visible");
+        int want = num_devices;
+        if (want <= 0) {
+            const char* env = std::getenv("LPD_NUM_GPUS");
+            want = env ? std::atoi(env) : avail;
+            if (want <= 0) want = avail;
+        }
+        if (want > avail)
+            fail(LPD_ERR_INVALID_ARGUMENT, "requested " + std::to_string(want) +
+                                               " devices, only " + std::to_string(avail) +
+                                               " visible");
+        auto* ctx = new lpd_context();
+        try {
+            ctx->dev.resize(want);
+            for (int i = 0; i < want; ++i) init_device(ctx->dev[i], i);
+        } catch (...) {
+            lpd_context_destroy(ctx);
+            throw;
+        }
+        *out = ctx;
+    });
+}
+
+int lpd_context_destroy(lpd_context* ctx) {
+    if (!ctx) return LPD_OK;
+    for (auto& ds : ctx->dev) {
+        if (cudaSetDevice(ds.device) != cudaSuccess) continue;
+        cudaDeviceSynchronize();
+        ds.free_basis();
+        for (auto& s : ds.slot) {
+            ds.free_slot(s);
+            if (s.stream) cudaStreamDestroy(s.stream);
+            for (auto& e : s.ev)
+                if (e) cudaEventDestroy(e);
+        }
+        for (auto& e : ds.kev)
+            if (e) cudaEventDestroy(e);
+    }
+    delete ctx;
+    return LPD_OK;
+}
+
+int lpd_context_num_devices(const lpd_context* ctx) {
+    return ctx ? static_cast<int>(ctx->dev.size()) : 0;
+}
+
+int lpd_set_basis_dense(lpd_context* ctx, const double* landmarks, int64_t B, int64_t d,
+                        int64_t ld, const double* L, int64_t b_eff, double gamma) {
+    return guarded([&] {
+        check_ctx(ctx, false);
+        validate_basis_args(B, d, b_eff, gamma, L);
+        if (!landmarks && d > 0) fail(LPD_ERR_INVALID_ARGUMENT, "landmarks is null");
+        if (ld < d) fail(LPD_ERR_INVALID_ARGUMENT, "landmark leading dimension < d");
+        run_parallel(ctx, [&](DeviceState& ds, int) {
+            CUDA_TRY(cudaSetDevice(ds.device));
+            double* lm = nullptr;
+            dev_alloc(&lm, static_cast<size_t>(B * std::max<int64_t>(d, 1)));
+            if (d > 0)
+                CUDA_TRY(cudaMemcpy2D(lm, sizeof(double) * d, landmarks, sizeof(double) * ld,
+                                      sizeof(double) * d, static_cast<size_t>(B),
+                                      cudaMemcpyHostToDevice));
+            else
+                CUDA_TRY(cudaMemset(lm, 0, sizeof(double)));
+            try {
+                build_basis(ds, lm, B, d, L, b_eff, gamma);
+            } catch (...) {
+                dev_free(lm);
+                throw;
+            }
+            dev_free(lm);
+        });
+    });
+}
+
+int lpd_set_basis_csr(lpd_context* ctx, int64_t B, int64_t d, const int64_t* indptr,
+                      const int32_t* indices, const double* values, const double* L,
+                      int64_t b_eff, double gamma) {
+    return guarded([&] {
+        check_ctx(ctx, false);
+        validate_basis_args(B, d, b_eff, gamma, L);
+        if (!indptr) fail(LPD_ERR_INVALID_ARGUMENT, "indptr is null");
+        const int64_t nnz = indptr[B] - indptr[0];
+        if (nnz < 0) fail(LPD_ERR_INVALID_ARGUMENT, "indptr is not monotone");
+        if (nnz > 0 && (!indices || !values)) fail(LPD_ERR_INVALID_ARGUMENT, "CSR arrays are null");
+        run_parallel(ctx, [&](DeviceState& ds, int) {
+            CUDA_TRY(cudaSetDevice(ds.device));
+            std::vector<int64_t> ip(static_cast<size_t>(B + 1));
+            for (int64_t i = 0; i <= B; ++i) ip[i] = indptr[i] - indptr[0];
+            int64_t *dip = nullptr;
+            int32_t* didx = nullptr;
+            double *dval = nullptr, *lm = nullptr;
+            dev_alloc(&dip, static_cast<size_t>(B + 1));
+            dev_alloc(&didx, static_cast<size_t>(nnz));
+            dev_alloc(&dval, static_cast<size_t>(nnz));
+            dev_alloc(&lm, static_cast<size_t>(B * std::max<int64_t>(d, 1)));
+            CUDA_TRY(cudaMemcpy(dip, ip.data(), sizeof(int64_t) * (B + 1), cudaMemcpyHostToDevice));
+            if (nnz > 0) {
+                CUDA_TRY(cudaMemcpy(didx, indices + indptr[0], sizeof(int32_t) * nnz, cudaMemcpyHostToDevice));
+                CUDA_TRY(cudaMemcpy(dval, values + indptr[0], sizeof(double) * nnz, cudaMemcpyHostToDevice));
+            }
+            if (d > 0)
+                lpd::csr_to_dense_kernel<<<static_cast<int>((B + 7) / 8), 256, 0, ds.slot[0].stream>>>(
+                    dip, didx, dval, static_cast<int>(B), static_cast<int>(d), lm);
+            CUDA_TRY(cudaGetLastError());
+            try {
+                build_basis(ds, lm, B, d, L, b_eff, gamma);
+            } catch (...) {
+                dev_free(dip); dev_free(didx); dev_free(dval); dev_free(lm);
+                throw;
+            }
+            dev_free(dip); dev_free(didx); dev_free(dval); dev_free(lm);
+        });
+    });
+}
+
+int lpd_compute_g_dense(lpd_context* ctx, const double* X, int64_t n, int64_t d, int64_t ldx,
+                        double* G, int64_t ldg, lpd_timings* timings) {
+    return guarded([&] {
+        check_ctx(ctx, true);
+        const int64_t b_eff = ctx->dev[0].b_eff;
+        if (n < 0) fail(LPD_ERR_INVALID_ARGUMENT, "negative row count");
+        if (d != ctx->dev[0].d) fail(LPD_ERR_INVALID_ARGUMENT, "point dimension does not match the basis");
+        if (ldx < d) fail(LPD_ERR_INVALID_ARGUMENT, "ldx < d");
+        if (ldg < b_eff) fail(LPD_ERR_INVALID_ARGUMENT, "ldg < b_eff");
+        if (n > 0 && (!G || (!X && d > 0))) fail(LPD_ERR_INVALID_ARGUMENT, "null buffer");
+        compute_rows_host(ctx, n, G, ldg, timings, [&](DeviceState& ds, Slot& s, int64_t r0, int64_t rows) {
+            ensure_slot(ds, s, rows, true, 0);
+            CUDA_TRY(cudaEventRecord(s.ev[0], s.stream));
+            if (d > 0)
+                CUDA_TRY(cudaMemcpy2DAsync(s.x, sizeof(double) * d, X + r0 * ldx,
+                                           sizeof(double) * ldx, sizeof(double) * d,
+                                           static_cast<size_t>(rows), cudaMemcpyHostToDevice,
+                                           s.stream));
+        });
+    });
+}
+
+int lpd_compute_g_csr(lpd_context* ctx, int64_t n, int64_t d, const int64_t* indptr,
+                      const int32_t* indices, const double* values, double* G, int64_t ldg,
+                      lpd_timings* timings) {
+    return guarded([&] {
+        check_ctx(ctx, true);
+        const int64_t b_eff = ctx->dev[0].b_eff;
+        if (n < 0) fail(LPD_ERR_INVALID_ARGUMENT, "negative row count");
+        if (d != ctx->dev[0].d) fail(LPD_ERR_INVALID_ARGUMENT, "point dimension does not match the basis");
+        if (ldg < b_eff) fail(LPD_ERR_INVALID_ARGUMENT, "ldg < b_eff");
+        if (n > 0 && (!G || !indptr)) fail(LPD_ERR_INVALID_ARGUMENT, "null buffer");
+        compute_rows_host(ctx, n, G, ldg, timings, [&](DeviceState& ds, Slot& s, int64_t r0, int64_t rows) {
+            const int64_t e0 = indptr[r0], e1 = indptr[r0 + rows];
+            ensure_slot(ds, s, rows, true, e1 - e0);
+            // rebase indptr for this chunk on the host (small), then densify on device
+            std::vector<int64_t> ip(static_cast<size_t>(rows + 1));
+            for (int64_t i = 0; i <= rows; ++i) ip[i] = indptr[r0 + i] - e0;
+            CUDA_TRY(cudaEventRecord(s.ev[0], s.stream));
+            CUDA_TRY(cudaMemcpyAsync(s.indptr, ip.data(), sizeof(int64_t) * (rows + 1),
+                                     cudaMemcpyHostToDevice, s.stream));
+            if (e1 > e0) {
+                CUDA_TRY(cudaMemcpyAsync(s.indices, indices + e0, sizeof(int32_t) * (e1 - e0),
+                                         cudaMemcpyHostToDevice, s.stream));
+                CUDA_TRY(cudaMemcpyAsync(s.values, values + e0, sizeof(double) * (e1 - e0),
+                                         cudaMemcpyHostToDevice, s.stream));
+            }
+            if (d > 0)
+                lpd::csr_to_dense_kernel<<<static_cast<int>((rows + 7) / 8), 256, 0, s.stream>>>(
+                    s.indptr, s.indices, s.values, static_cast<int>(rows), static_cast<int>(d), s.x);
+            CUDA_TRY(cudaGetLastError());
+            // ip must outlive the async copy: synchronise the H2D before returning
+            CUDA_TRY(cudaStreamSynchronize(s.stream));
+        });
+    });
+}
+
+int lpd_compute_g_device(lpd_context* ctx, int device_index, const double* X_dev, int64_t n,
+                         int64_t ldx, void* G_dev, int64_t ldg, int out_dtype, void* stream) {
+    return guarded([&] {
+        check_ctx(ctx, true);
+        if (device_index < 0 || device_index >= static_cast<int>(ctx->dev.size()))
+            fail(LPD_ERR_INVALID_ARGUMENT, "device index out of range");
+        DeviceState& ds = ctx->dev[device_index];
+        if (n < 0) fail(LPD_ERR_INVALID_ARGUMENT, "negative row count");
+        if (ldx < ds.d) fail(LPD_ERR_INVALID_ARGUMENT, "ldx < d");
+        if (ldg < ds.b_eff) fail(LPD_ERR_INVALID_ARGUMENT, "ldg < b_eff");
+        if (out_dtype != LPD_OUT_F64 && out_dtype != LPD_OUT_F32)
+            fail(LPD_ERR_INVALID_ARGUMENT, "unknown output dtype");
+        if (n == 0) return;
+        CUDA_TRY(cudaSetDevice(ds.device));
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ds.slot[0].stream;
+        Slot& s = ds.slot[0];
+        ensure_slot(ds, s, n, false, 0);
+        launch_factor(ds, s, X_dev, n, ldx, G_dev, ldg, out_dtype, st, true);
+        if (!stream) {
+            CUDA_TRY(cudaStreamSynchronize(st));
+            float ms = 0.f;
+            CUDA_TRY(cudaEventElapsedTime(&ms, ds.kev[0], ds.kev[1]));
+            ds.last_kernel_ms = ms;
+        }
+    });
+}
+
+double lpd_last_factor_kernel_ms(const lpd_context* ctx, int device_index) {
+    if (!ctx || device_index < 0 || device_index >= static_cast<int>(ctx->dev.size())) return -1.0;
+    auto& ds = const_cast<DeviceState&>(ctx->dev[device_index]);
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, ds.kev[0], ds.kev[1]) != cudaSuccess) {
+        cudaGetLastError();
+        return static_cast<double>(ds.last_kernel_ms);
+    }
+    return static_cast<double>(ms);
+}
+
+int lpd_decision_values_device(lpd_context* ctx, int device_index, const void* G_dev, int g_dtype,
+                               int64_t n, int64_t b_eff, int64_t ldg, const double* W_dev,
+                               int64_t P, double* D_dev, int64_t ldd, void* stream) {
+    return guarded([&] {
+        check_ctx(ctx, false);
+        if (device_index < 0 || device_index >= static_cast<int>(ctx->dev.size()))
+            fail(LPD_ERR_INVALID_ARGUMENT, "device index out of range");
+        if (n < 0 || b_eff < 0 || P < 0) fail(LPD_ERR_INVALID_ARGUMENT, "negative size");
+        if (ldg < b_eff || ldd < P) fail(LPD_ERR_INVALID_ARGUMENT, "leading dimension too small");
+        if (n == 0 || P == 0) return;
+        DeviceState& ds = ctx->dev[device_index];
+        CUDA_TRY(cudaSetDevice(ds.device));
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ds.slot[0].stream;
+        constexpr int PB = 4;
+        const int threads = 256;
+        const int64_t blocks = std::min<int64_t>((n + 7) / 8, static_cast<int64_t>(ds.num_sms) * 8);
+        for (int64_t p0 = 0; p0 < P; p0 += PB) {
+            if (g_dtype == LPD_OUT_F64)
+                lpd::decision_values_kernel<double, PB><<<static_cast<int>(blocks), threads, 0, st>>>(
+                    static_cast<const double*>(G_dev), ldg, static_cast<int>(n),
+                    static_cast<int>(b_eff), W_dev, static_cast<int>(P), static_cast<int>(p0), D_dev, ldd);
+            else
+                lpd::decision_values_kernel<float, PB><<<static_cast<int>(blocks), threads, 0, st>>>(
+                    static_cast<const float*>(G_dev), ldg, static_cast<int>(n),
+                    static_cast<int>(b_eff), W_dev, static_cast<int>(P), static_cast<int>(p0), D_dev, ldd);
+        }
+        CUDA_TRY(cudaGetLastError());
+        if (!stream) CUDA_TRY(cudaStreamSynchronize(st));
+    });
+}
+
+int lpd_decision_values(lpd_context* ctx, const double* G, int64_t n, int64_t b_eff, int64_t ldg,
+                        const double* W, int64_t P, double* D, int64_t ldd) {
+    return guarded([&] {
+        check_ctx(ctx, false);
+        if (n < 0 || b_eff < 0 || P < 0) fail(LPD_ERR_INVALID_ARGUMENT, "negative size");
+        if (ldg < b_eff || ldd < P) fail(LPD_ERR_INVALID_ARGUMENT, "leading dimension too small");
+        if (n == 0 || P == 0) return;
+        DeviceState& ds = ctx->dev[0];
+        CUDA_TRY(cudaSetDevice(ds.device));
+        double *g = nullptr, *w = nullptr, *dd = nullptr;
+        dev_alloc(&g, static_cast<size_t>(n * b_eff));
+        dev_alloc(&w, static_cast<size_t>(P * b_eff));
+        dev_alloc(&dd, static_cast<size_t>(n * P));
+        auto cleanup = [&] { dev_free(g); dev_free(w); dev_free(dd); };
+        try {
+            CUDA_TRY(cudaMemcpy2D(g, sizeof(double) * b_eff, G, sizeof(double) * ldg,
+                                  sizeof(double) * b_eff, static_cast<size_t>(n), cudaMemcpyHostToDevice));
+            CUDA_TRY(cudaMemcpy(w, W, sizeof(double) * P * b_eff, cudaMemcpyHostToDevice));
+            if (lpd_decision_values_device(ctx, 0, g, LPD_OUT_F64, n, b_eff, b_eff, w, P, dd, P,
+                                           nullptr) != LPD_OK)
+                fail(LPD_ERR_CUDA, g_last_error);
+            CUDA_TRY(cudaMemcpy2D(D, sizeof(double) * ldd, dd, sizeof(double) * P,
+                                  sizeof(double) * P, static_cast<size_t>(n), cudaMemcpyDeviceToHost));
+        } catch (...) {
+            cleanup();
+            throw;
+        }
+        cleanup();
+    });
+}
+
+}  // extern "C"
