@@ -1,0 +1,206 @@
+"""Parity of the B200 path (through the C ABI) against the oracle and the
+reference build. Run on a B200 with `pytest -m gpu`.
+
+Tolerances (north star: "G must match the reference's CPU factor within a
+stated relative tolerance"): row-normwise relative error
+    max_i ||G_i - G_ref,i|| / ||G_ref,i||  <= 1e-4
+for well-conditioned bases (elementwise relative error is
+ill-posed on G's near-zero entries). The ill-conditioned SUSY-shaped fixture
+(γ=2^-7, τ=1e-6) amplifies fp32-level rounding of Z by 1/sqrt(λ_min); its bound
+is 5e-4 (exact-fp32 emulation gives 1.35e-4 there).
+Kernel values Z themselves (L = I) must agree to 2e-5 absolute (Z in (0, 1]).
+
+For arbitrary (possibly ill-conditioned) bases the achievable accuracy of any
+fp32-level kernel is bounded by conditioning, ‖ΔG_i‖ = ‖ΔZ_i·L‖ ≤ ‖ΔZ_i‖·‖L‖₂,
+so the random edge-shape tests assert per row
+    ‖ΔG_i‖ ≤ max(1e-4·‖G_ref,i‖, 1e-5·‖Z_i‖·‖L‖₂)
+(elementwise relative Z accuracy 1e-5 implies the second term).
+"""
+import numpy as np
+import pytest
+
+import paper_2207_01016_b200 as P
+from conftest import load_golden, np_gaussian_L, row_rel_err
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TOL_G = 1e-4
+TOL_G_ILL = 5e-4
+TOL_Z = 2e-5
+
+
+def _oracle_G(X, Y, L, gamma):
+    return O.ora_compute_g(O.dense_to_csr(X), O.dense_to_csr(Y), L, gamma, 4096)
+
+
+def assert_conditioned_parity(G, X, Y, L, gamma):
+    R = _oracle_G(X, Y, L, gamma)
+    Z = O.ora_kernel_block(O.dense_to_csr(X), O.dense_to_csr(Y), gamma)
+    l2 = np.linalg.norm(L, 2)
+    err = np.linalg.norm(G - R, axis=1)
+    bound = np.maximum(TOL_G * np.linalg.norm(R, axis=1), 1e-5 * np.linalg.norm(Z, axis=1) * l2)
+    assert np.all(err <= bound), float(np.max(err / bound))
+    return R
+
+
+@pytest.mark.parametrize("name,tol", [("c1_mini.npz", TOL_G), ("sparse_mini.npz", TOL_G),
+                                      ("susy_mini.npz", TOL_G_ILL)])
+def test_golden_fixtures(gpu_ctx, name, tol):
+    g = load_golden(name)
+    X = g["X"].astype(np.float64)
+    Y = X[g["ids"]]
+    gpu_ctx.set_basis_dense(Y, g["L"], float(g["gamma"]))
+    G = gpu_ctx.compute_g_dense(X)
+    assert G.shape == g["G"].shape
+    assert np.all(np.isfinite(G))
+    assert row_rel_err(G, g["G"]) <= tol
+    # CSR entry point on the same data must agree bitwise with the dense one
+    ip, ix, vv = O.dense_to_csr(X)
+    lp, li, lv = O.dense_to_csr(Y)
+    gpu_ctx.set_basis_csr(lp, li, lv, X.shape[1], g["L"], float(g["gamma"]))
+    G2 = gpu_ctx.compute_g_csr(ip, ix, vv)
+    assert np.array_equal(G, G2)
+
+
+def test_kernel_values_identity_basis(gpu_ctx):
+    """L = I exposes Z directly: the fused epilogue's exp(-γ max(0, ...)) vs the oracle."""
+    rng = np.random.default_rng(1)
+    X = rng.standard_normal((700, 50)).astype(np.float32).astype(np.float64)
+    Y = X[rng.choice(700, 200, replace=False)]
+    gpu_ctx.set_basis_dense(Y, np.eye(200), 0.02)
+    Z = gpu_ctx.compute_g_dense(X)
+    Zr = O.ora_kernel_block(O.dense_to_csr(X), O.dense_to_csr(Y), 0.02)
+    assert np.abs(Z - Zr).max() <= TOL_Z
+    assert Z.max() <= 1.0 + TOL_Z and Z.min() >= 0.0
+
+
+@pytest.mark.parametrize("n,d,B,beff_cut,gamma", [
+    (1, 5, 1, 0, 0.5),        # single row, single landmark
+    (127, 3, 65, 0, 1.0),     # ragged rows (< one tile), landmarks = 64 + 1
+    (129, 64, 64, 0, 0.05),   # max d, rows = tile + 1
+    (300, 17, 300, 1, 0.2),   # b_eff = 299 (odd leading dimension)
+    (1000, 50, 257, 0, 0.02),  # b_eff = 257 (two column blocks, second nearly empty)
+    (513, 1, 40, 0, 3.0),     # d = 1
+])
+def test_edge_shapes(gpu_ctx, n, d, B, beff_cut, gamma):
+    rng = np.random.default_rng(n * 31 + d)
+    X = rng.standard_normal((n, d)).astype(np.float32).astype(np.float64)
+    Y = X[rng.choice(n, min(B, n), replace=False)] if B <= n else rng.standard_normal((B, d))
+    L = np_gaussian_L(Y, gamma, 1e-10)
+    if beff_cut:
+        L = np.ascontiguousarray(L[:, : L.shape[1] - beff_cut])
+    gpu_ctx.set_basis_dense(Y, L, gamma)
+    G = gpu_ctx.compute_g_dense(X)
+    assert_conditioned_parity(G, X, Y, L, gamma)
+
+
+def test_empty_and_duplicate_points(gpu_ctx):
+    rng = np.random.default_rng(4)
+    X = rng.standard_normal((260, 12))
+    X[[0, 5, 200]] = 0.0            # empty SparseVectors
+    X[10] = X[11]                    # duplicates (singular K is handled by truncation)
+    Y = X[[0, 10, 11, 20, 30, 40, 50, 60]]
+    L = O.ref_build_L(O.dense_to_csr(Y), 0.3, 1e-12) if O.ref_available() else np_gaussian_L(Y, 0.3)
+    gpu_ctx.set_basis_dense(Y, L, 0.3)
+    G = gpu_ctx.compute_g_dense(X)
+    assert_conditioned_parity(G, X, Y, L, 0.3)
+
+
+def test_zero_rows_call(gpu_ctx):
+    Y = np.eye(4)
+    gpu_ctx.set_basis_dense(Y, np.eye(4), 1.0)
+    G = gpu_ctx.compute_g_dense(np.zeros((0, 4)))
+    assert G.shape == (0, 4)
+
+
+def test_batch_invariance_bitwise(gpu_ctx):
+    """Each row's arithmetic is independent of the batch it is computed in, so G
+    is bitwise identical across chunkings / device counts."""
+    g = load_golden("c1_mini.npz")
+    X = g["X"].astype(np.float64)
+    gpu_ctx.set_basis_dense(X[g["ids"]], g["L"], 0.02)
+    full = gpu_ctx.compute_g_dense(X)
+    parts = np.concatenate([gpu_ctx.compute_g_dense(X[a:b]) for a, b in [(0, 1), (1, 300), (300, 1024)]])
+    assert np.array_equal(full, parts)
+
+
+def test_device_entry_fp32_and_fp64(gpu_ctx):
+    import torch
+
+    g = load_golden("c1_mini.npz")
+    X = g["X"].astype(np.float64)
+    gpu_ctx.set_basis_dense(X[g["ids"]], g["L"], 0.02)
+    ref = gpu_ctx.compute_g_dense(X)
+    Xd = torch.from_numpy(X).cuda()
+    G64 = torch.empty((X.shape[0], g["L"].shape[1]), dtype=torch.float64, device="cuda")
+    G32 = torch.empty((X.shape[0], g["L"].shape[1]), dtype=torch.float32, device="cuda")
+    gpu_ctx.compute_g_device(Xd, G64)
+    gpu_ctx.compute_g_device(Xd, G32)
+    torch.cuda.synchronize()
+    assert np.array_equal(G64.cpu().numpy(), ref)
+    assert np.array_equal(G32.cpu().numpy(), ref.astype(np.float32))
+
+
+def test_error_behaviour(gpu_ctx):
+    Y = np.random.default_rng(0).standard_normal((10, 5))
+    with pytest.raises(ValueError, match="gamma"):
+        gpu_ctx.set_basis_dense(Y, np.eye(10), 0.0)
+    with pytest.raises(ValueError):
+        gpu_ctx.set_basis_dense(Y, np.eye(9), 1.0)
+    gpu_ctx.set_basis_dense(Y, np.eye(10), 1.0)
+    with pytest.raises(ValueError, match="dimension"):
+        gpu_ctx.compute_g_dense(np.zeros((3, 6)))
+    with pytest.raises(P.LpdError):
+        gpu_ctx.set_basis_dense(np.zeros((4, 65)), np.eye(4), 1.0)  # d > 64: outside this kernel's envelope
+
+
+def test_decision_values(gpu_ctx):
+    rng = np.random.default_rng(6)
+    for b_eff, P_ in [(1000, 1), (4096, 3), (777, 9), (1, 1)]:
+        G = rng.standard_normal((1500, b_eff))
+        W = rng.standard_normal((P_, b_eff))
+        D = gpu_ctx.decision_values(G, W)
+        R = O.ora_decision_values(G, W)
+        assert np.abs(D - R).max() <= 1e-12 * max(1.0, np.abs(R).max())
+
+
+def test_c1_full_config_vs_reference():
+    """C1 end-to-end factor (n=20,000, d=50, B=1,000, γ=0.02) against the
+    reference's own compute_G (oracle/_ref), same landmarks and L."""
+    if not O.ref_available():
+        pytest.fail("reference build oracle/_ref missing on this box")
+    from paper_2207_01016_b200 import synthetic
+
+    cfg = synthetic.CONFIGS["c1"]
+    X, _ = synthetic.make(cfg)
+    ids = O.ref_select_landmarks(cfg.n, cfg.budget, 1)
+    csr, lcsr = O.dense_to_csr(X), O.dense_to_csr(X[ids])
+    L = O.ref_build_L(lcsr, cfg.gamma, 1e-12, threads=8)
+    R = O.ref_compute_g(csr, lcsr, L, cfg.gamma, 4096, threads=O.ref_lib().ref_hardware_threads())
+    with P.Context(1) as ctx:
+        ctx.set_basis_dense(X[ids], L, cfg.gamma)
+        G = ctx.compute_g_dense(X)
+    assert row_rel_err(G, R) <= TOL_G
+    # Nyström identity on the landmark rows: G_S G_S^T ≈ K (1e-6·λ_max scale)
+    K = O.ora_kernel_block(lcsr, lcsr, cfg.gamma)
+    GS = G[ids]
+    assert np.abs(GS @ GS.T - K).max() <= 1e-3
+
+
+def test_compute_G_mirror_sparse_points():
+    """The Python mirror of lpdsvm::compute_G on SparseVector-style input."""
+    rng = np.random.default_rng(8)
+    pts = []
+    for i in range(150):
+        idx = np.sort(rng.choice(30, rng.integers(0, 8), replace=False))
+        pts.append([(int(j), float(np.float32(rng.standard_normal()))) for j in idx])
+    lms = pts[:40]
+    ip, ix, vv, dim = P.sparse_to_csr(pts)
+    lp, li, lv, _ = P.sparse_to_csr(lms)
+    L = O.ref_build_L((lp, li, lv), 0.4, 1e-12) if O.ref_available() else None
+    if L is None:
+        pytest.fail("reference build missing")
+    G = P.compute_G(pts, None, lms, None, L, P.KernelParams(0.4), 4096)
+    R = O.ora_compute_g((ip, ix, vv), (lp, li, lv), L, 0.4, 4096)
+    assert row_rel_err(G, R) <= TOL_G
