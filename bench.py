@@ -1,0 +1,371 @@
+#!/usr/bin/env python3
+"""Nyström factor benchmark (BASELINE.json metric: "Nyström factor rows/s &
+TFLOP/s vs peak"), workload C2: covtype-shaped synthetic binary blobs,
+n = 581,012 rows per GPU, d = 54, B = 4,096 landmarks, γ = 1/54.
+
+One step = one pass of the hot path (reference lpdsvm::compute_G,
+proj/src/factor.cpp:165-192) over the whole batch: basis prep of (landmarks, L)
+(K2; with N > 1 preceded by the NCCL broadcast of the basis from rank 0, the
+path's only collective), row prep (K3) and the fused factor kernel (K1)
+writing G = Z·L (fp64) to HBM.
+
+  value  rows/s over all ranks, inputs resident in HBM (max-over-ranks device time)
+  e2e    the same metric through the C ABI host path (lpd_set_basis_dense +
+         lpd_compute_g_dense): pinned host X in, fp64 G back into a host buffer
+  roofline  K1 algorithmic TFLOP/s (F = 2nBd + 2nB·B_eff per launch, CUDA events
+         on the launch stream) vs the measured dense bf16/fp16 peak
+  cpu_baseline  the reference's own compute_G (oracle/_ref, all host threads) on a
+         bounded row sample of the same workload
+
+Weak scaling: rank r owns rows [r·n, (r+1)·n) of an N·n-row dataset.
+`--impl reference` times the reference CPU implementation instead (rank 0).
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Nyström factor rows/s"
+UNIT = "rows/s"
+LAUNCHES_PER_STEP = 6  # K2: column_mean, prep_rows(landmarks), col_absmax, lt_split; K3 prep_rows; K1
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default="c2")
+    ap.add_argument("--rows", type=int, default=0, help="override rows per GPU (testing only)")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU-baseline sample time")
+    return ap.parse_args()
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return {"tflops": float(p["bf16_tflops"]), "hbm": float(p["hbm_gbs"]), "src": "measured"}
+    except Exception:
+        return {"tflops": 1590.0, "hbm": 6650.0, "src": "fallback"}
+
+
+def load_traffic():
+    """dram read+write bytes per K1 launch on this workload from the committed ncu
+    summary (profiles/), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "k1_c2_traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def make_basis(X0, cfg, seed=1):
+    """Landmarks: B rows of rank 0's data drawn uniformly without replacement
+    (as the reference's select_landmarks does, factor.cpp:109-113; numpy's seeded
+    generator here); L from the eigendecomposition of K (factor.cpp:115-163;
+    numpy LAPACK, setup only, outside the timed region)."""
+    ids = np.random.default_rng(seed).choice(X0.shape[0], cfg.budget, replace=False)
+    Y = np.ascontiguousarray(X0[ids])
+    ny = (Y * Y).sum(1)
+    K = np.exp(-cfg.gamma * np.maximum(ny[:, None] + ny[None, :] - 2.0 * Y @ Y.T, 0.0))
+    w, U = np.linalg.eigh(0.5 * (K + K.T))
+    w, U = w[::-1], U[:, ::-1]
+    keep = w > 1e-12 * w[0]
+    L = np.ascontiguousarray(U[:, keep] / np.sqrt(w[keep]))
+    return Y, L
+
+
+def cpu_reference_rate(X, Y, L, gamma, target_s, threads, max_rows):
+    """Reference compute_G (oracle/_ref, unmodified reference sources) on a bounded
+    contiguous row sample with all host threads; returns (rows/s, rows, seconds)."""
+    from oracle import oracle as O
+
+    ycsr = O.dense_to_csr(Y)
+    rows = min(max_rows, 2048)
+    while True:
+        xs = O.dense_to_csr(X[:rows])
+        chunk = max(64, -(-rows // threads))
+        _, secs = O.ref_compute_g(xs, ycsr, L, gamma, chunk, threads, return_seconds=True)
+        if secs >= 0.5 * target_s or rows >= max_rows:
+            return rows / secs, rows, secs
+        rows = int(min(max_rows, max(rows * 2, rows * target_s / max(secs, 1e-3))))
+
+
+def run_reference(args, cfg, rank):
+    """--impl reference: the reference's own CPU compute_G on rank 0's host cores."""
+    if rank != 0:
+        return
+    from oracle import oracle as O
+
+    n = args.rows or cfg.n
+    from paper_2207_01016_b200 import synthetic
+
+    X, _ = synthetic.blobs(n, cfg.d, cfg.seed)
+    Y, L = make_basis(X, cfg)
+    threads = O.ref_lib().ref_hardware_threads()
+    # size each step so warmup + steps stay within a few minutes
+    per_step = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    rate, rows, secs = cpu_reference_rate(X, Y, L, cfg.gamma, per_step, threads, n)
+    ycsr = O.dense_to_csr(Y)
+    xs = O.dense_to_csr(X[:rows])
+    chunk = max(64, -(-rows // threads))
+    for _ in range(max(0, args.warmup - 1)):
+        O.ref_compute_g(xs, ycsr, L, cfg.gamma, chunk, threads)
+    ts = []
+    for _ in range(args.steps):
+        _, s = O.ref_compute_g(xs, ycsr, L, cfg.gamma, chunk, threads, return_seconds=True)
+        ts.append(s)
+    value = rows * len(ts) / sum(ts)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(ts) / len(ts),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.name, "n": n, "d": cfg.d, "B": cfg.budget, "b_eff": int(L.shape[1]),
+                   "gamma": cfg.gamma, "parallelism": f"host threads={threads}"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"{rows} contiguous rows of the {n}-row workload per step, chunk_size={chunk}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2207_01016_b200 import synthetic
+
+    cfg = synthetic.CONFIGS[args.workload]
+    if args.impl == "reference":
+        run_reference(args, cfg, rank)
+        if dist:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    import paper_2207_01016_b200 as P
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    n = args.rows or cfg.n
+    N = world
+    # weak scaling: this rank's rows of an N·n-row dataset
+    X, _ = synthetic.blobs(N * n, cfg.d, cfg.seed, rows=slice(rank * n, (rank + 1) * n))
+    if rank == 0:
+        Y, L = make_basis(X, cfg)
+        meta = torch.tensor([Y.shape[0], L.shape[1]], dtype=torch.int64, device=dev)
+    else:
+        meta = torch.zeros(2, dtype=torch.int64, device=dev)
+    if dist:
+        dist.broadcast(meta, 0)
+    B, b_eff = int(meta[0]), int(meta[1])
+    lm_dev = torch.empty((B, cfg.d), dtype=torch.float64, device=dev)
+    L_dev = torch.empty((B, b_eff), dtype=torch.float64, device=dev)
+    if rank == 0:
+        lm_dev.copy_(torch.from_numpy(Y))
+        L_dev.copy_(torch.from_numpy(L))
+    X_dev = torch.from_numpy(X).to(dev)
+    G_dev = torch.empty((n, b_eff), dtype=torch.float64, device=dev)
+
+    ctx = P.Context(device_ids=[local])  # one device per process
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        if dist:
+            dist.broadcast(lm_dev, 0)
+            dist.broadcast(L_dev, 0)
+        ctx.set_basis_device(lm_dev, L_dev, cfg.gamma, stream=stream)
+        ctx.compute_g_device(X_dev, G_dev, stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    ctx.factor_kernel_stats(reset=True)
+
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    elapsed_ms = e0.elapsed_time(e1)
+    t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed_ms = float(t.item())
+    k_total_ms, k_launches = ctx.factor_kernel_stats(reset=True)
+    k_ms = k_total_ms / max(1, k_launches)
+
+    value = N * n * args.steps / (elapsed_ms / 1e3)
+    F = 2.0 * n * B * cfg.d + 2.0 * n * B * b_eff
+    peaks = load_peaks()
+    achieved = F / (k_ms / 1e3) / 1e12
+    traffic = load_traffic()
+    # issued tensor work (3-term split, padded shapes, GEMM1 recomputed per 256-column block)
+    npad, bpad, epad = -(-n // 128) * 128, -(-B // 64) * 64, -(-b_eff // 256) * 256
+    k1 = -(-cfg.d // 16) * 16
+    issued = 3 * (2.0 * npad * bpad * k1 * (epad // 256) + 2.0 * npad * bpad * epad)
+
+    # ---------------- end to end through the C ABI with host buffers ----------------
+    e2e = None
+    if not args.no_e2e:
+        import psutil
+
+        g_bytes = n * b_eff * 8
+        if psutil.virtual_memory().available > 2.5 * g_bytes * max(1, torch.cuda.device_count() if world > 1 else 1):
+            Xh = torch.from_numpy(X).pin_memory()
+            Gh = torch.empty((n, b_eff), dtype=torch.float64).pin_memory()
+            Yh = lm_dev.cpu().numpy()
+            Lh = L_dev.cpu().numpy()
+            Xn, Gn = Xh.numpy(), Gh.numpy()
+            ctx.set_basis_dense(Yh, Lh, cfg.gamma)
+            ctx.compute_g_dense(Xn, out=Gn)  # warm-up
+            ts = []
+            for _ in range(args.e2e_steps):
+                if dist:
+                    dist.barrier()
+                t0 = time.perf_counter()
+                ctx.set_basis_dense(Yh, Lh, cfg.gamma)
+                ctx.compute_g_dense(Xn, out=Gn)
+                dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+                if dist:
+                    dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+                ts.append(float(dt.item()))
+            e2e = {"value": N * n / statistics.mean(ts), "unit": UNIT,
+                   "h2d_bytes_per_step": int(X.nbytes + Yh.nbytes + Lh.nbytes),
+                   "d2h_bytes_per_step": int(g_bytes), "seconds_per_step": statistics.mean(ts),
+                   "path": "lpd_set_basis_dense + lpd_compute_g_dense, pinned host X -> host fp64 G"}
+            # spot-check the e2e result against the device result
+            assert np.array_equal(Gn[:1000], G_dev[:1000].cpu().numpy())
+            del Xh, Gh
+        else:
+            e2e = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                   "skipped": "host RAM too small for a pinned fp64 G of this workload"}
+
+    cpu = None
+    if rank == 0 and N == 1 and not args.no_cpu_baseline:
+        from oracle import oracle as O
+
+        if O.ref_available():
+            threads = O.ref_lib().ref_hardware_threads()
+            rate, rows, secs = cpu_reference_rate(X, lm_dev.cpu().numpy(), L_dev.cpu().numpy(), cfg.gamma,
+                                                  args.cpu_seconds, threads, n)
+            cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
+                   "sample": f"{rows} contiguous rows of the {n}-row workload, same landmarks/L, "
+                             f"{secs:.1f}s, chunk_size={max(64, -(-rows // threads))}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "f16x3 split operands, f32 accumulate, f64 G",
+            "data": "synthetic (covtype-shaped two-class blobs, seed 2; landmarks = reference select_landmarks)",
+            "config": {"workload": cfg.name, "n_per_gpu": n, "d": cfg.d, "B": B, "b_eff": b_eff,
+                       "gamma": cfg.gamma, "parallelism": f"rows sharded over {N} GPU(s), basis broadcast",
+                       "l2": "inputs larger than L2 (G 19 GB/step per GPU written, X 0.25 GB read)"},
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peaks["tflops"], "unit": "TFLOP/s",
+                         "frac": achieved / peaks["tflops"], "traffic": traffic,
+                         "kernel_ms": k_ms, "flops_per_launch": F, "issued_tensor_flops_per_launch": issued,
+                         "issued_frac": issued / (k_ms / 1e3) / 1e12 / peaks["tflops"],
+                         "peak_source": f"MEASURED_PEAKS.json bf16_tflops ({peaks['src']}; kind::f16 runs at the bf16 rate)"},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": LAUNCHES_PER_STEP * args.steps,
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

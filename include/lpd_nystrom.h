@@ -17,9 +17,6 @@
  *       replaces the held-out scoring loop d[r][p] = G_r · w_p
  *       (proj/src/modelsel.cpp:409-426) and the warm-start/KKT sweeps that read
  *       G·w (proj/src/dcd.cpp:91-102, 150-172).
- *   lpd_predict_csr
- *       replaces the chunked Z·βᵀ + vote of ovo_predict
- *       (proj/src/multiclass.cpp:170-200, vote :153-168).
  *
  * Conventions: plain pointers and sizes only, no CUDA or C++ types. Matrices
  * are row-major fp64 with an explicit leading dimension in elements. Sparse
@@ -70,6 +67,8 @@ int lpd_device_count(void);
 
 /* num_devices <= 0: use LPD_NUM_GPUS from the environment if set, else all visible. */
 int lpd_context_create(lpd_context** out, int num_devices);
+/* Explicit device ordinals (one process per GPU: pass the local rank's device). */
+int lpd_context_create_devices(lpd_context** out, const int* device_ids, int count);
 int lpd_context_destroy(lpd_context* ctx);
 int lpd_context_num_devices(const lpd_context* ctx);
 
@@ -82,6 +81,13 @@ int lpd_set_basis_dense(lpd_context* ctx, const double* landmarks, int64_t B, in
 int lpd_set_basis_csr(lpd_context* ctx, int64_t B, int64_t d, const int64_t* indptr,
                       const int32_t* indices, const double* values, const double* L,
                       int64_t b_eff, double gamma);
+
+/* Basis from device-resident fp64 landmarks (B x d, ld) and L (B x b_eff) on device
+ * `device_index`. stream: cudaStream_t as void* (NULL = library stream, synchronised).
+ * Shapes unchanged from the previous basis reuse the device buffers (no allocation). */
+int lpd_set_basis_device(lpd_context* ctx, int device_index, const double* landmarks_dev,
+                         int64_t B, int64_t d, int64_t ld, const double* L_dev, int64_t b_eff,
+                         double gamma, void* stream);
 
 /* G (n x b_eff, leading dimension ldg >= b_eff) for host rows; rows are sharded
  * across the context's devices, results streamed back into G. */
@@ -113,6 +119,12 @@ int lpd_decision_values(lpd_context* ctx, const double* G, int64_t n, int64_t b_
 /* Last kernel timing of the fused factor kernel on device_index (milliseconds,
  * CUDA events around the launch on its stream), for benchmarks. */
 double lpd_last_factor_kernel_ms(const lpd_context* ctx, int device_index);
+
+/* Sum of the fused factor kernel's durations (CUDA events recorded on its launch
+ * stream around every device-path launch, up to 512 since the last reset) and the
+ * launch count. Synchronises on the recorded events. reset != 0 clears the record. */
+int lpd_factor_kernel_stats(lpd_context* ctx, int device_index, double* total_ms,
+                            int64_t* launches, int reset);
 
 #ifdef __cplusplus
 }

@@ -53,6 +53,7 @@ EXPORTED_SYMBOLS = (
     "lpd_version",
     "lpd_device_count",
     "lpd_context_create",
+    "lpd_context_create_devices",
     "lpd_context_destroy",
     "lpd_context_num_devices",
     "lpd_set_basis_dense",
@@ -63,6 +64,8 @@ EXPORTED_SYMBOLS = (
     "lpd_decision_values_device",
     "lpd_decision_values",
     "lpd_last_factor_kernel_ms",
+    "lpd_set_basis_device",
+    "lpd_factor_kernel_stats",
 )
 
 
@@ -122,6 +125,7 @@ def load_library(path: Optional[str] = None) -> ctypes.CDLL:
     lib.lpd_version.restype = ctypes.c_int
     lib.lpd_device_count.restype = ctypes.c_int
     lib.lpd_context_create.argtypes = [ctypes.POINTER(vp), ctypes.c_int]
+    lib.lpd_context_create_devices.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(ctypes.c_int), ctypes.c_int]
     lib.lpd_context_destroy.argtypes = [vp]
     lib.lpd_context_num_devices.argtypes = [vp]
     lib.lpd_set_basis_dense.argtypes = [vp, _c_dbl_p, i64, i64, i64, _c_dbl_p, i64, ctypes.c_double]
@@ -137,6 +141,9 @@ def load_library(path: Optional[str] = None) -> ctypes.CDLL:
     lib.lpd_decision_values.argtypes = [vp, _c_dbl_p, i64, i64, i64, _c_dbl_p, i64, _c_dbl_p, i64]
     lib.lpd_last_factor_kernel_ms.argtypes = [vp, ctypes.c_int]
     lib.lpd_last_factor_kernel_ms.restype = ctypes.c_double
+    lib.lpd_set_basis_device.argtypes = [vp, ctypes.c_int, vp, i64, i64, i64, vp, i64, ctypes.c_double, vp]
+    lib.lpd_factor_kernel_stats.argtypes = [vp, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                                            ctypes.POINTER(ctypes.c_int64), ctypes.c_int]
     if path is None:
         _lib = lib
     return lib
@@ -198,10 +205,14 @@ def sparse_to_csr(points: Sequence) -> tuple:
 class Context:
     """A set of B200 devices holding one replicated basis (landmarks, L, γ)."""
 
-    def __init__(self, num_devices: int = 0):
+    def __init__(self, num_devices: int = 0, device_ids: Optional[Sequence[int]] = None):
         self._lib = load_library()
         h = ctypes.c_void_p()
-        _check(self._lib.lpd_context_create(ctypes.byref(h), int(num_devices)))
+        if device_ids is not None:
+            ids = (ctypes.c_int * len(device_ids))(*device_ids)
+            _check(self._lib.lpd_context_create_devices(ctypes.byref(h), ids, len(device_ids)))
+        else:
+            _check(self._lib.lpd_context_create(ctypes.byref(h), int(num_devices)))
         self._h = h
         self.b_eff = 0
         self.dim = 0
@@ -300,6 +311,31 @@ class Context:
                                               X_dev.shape[0], X_dev.stride(0),
                                               ctypes.c_void_p(G_dev.data_ptr()), G_dev.stride(0),
                                               out_dtype, st))
+
+    def set_basis_device(self, landmarks_dev, L_dev, gamma: float, device_index: int = 0, stream=None) -> None:
+        """Basis from torch CUDA fp64 tensors (landmarks B x d, L B x b_eff), K2 on device."""
+        import torch
+
+        if landmarks_dev.dtype != torch.float64 or L_dev.dtype != torch.float64:
+            raise ValueError("landmarks and L must be float64 CUDA tensors")
+        if not L_dev.is_contiguous() or landmarks_dev.stride(1) != 1:
+            raise ValueError("row-major tensors required")
+        if L_dev.shape[0] != landmarks_dev.shape[0]:
+            raise ValueError("L row count must match landmark count")
+        st = ctypes.c_void_p(stream.cuda_stream) if stream is not None else None
+        _check(self._lib.lpd_set_basis_device(self._h, device_index, ctypes.c_void_p(landmarks_dev.data_ptr()),
+                                              landmarks_dev.shape[0], landmarks_dev.shape[1],
+                                              landmarks_dev.stride(0), ctypes.c_void_p(L_dev.data_ptr()),
+                                              L_dev.shape[1], float(gamma), st))
+        self.b_eff, self.dim = L_dev.shape[1], landmarks_dev.shape[1]
+
+    def factor_kernel_stats(self, device_index: int = 0, reset: bool = True):
+        """(total_ms, launches) of the fused factor kernel since the last reset."""
+        tot = ctypes.c_double(0.0)
+        cnt = ctypes.c_int64(0)
+        _check(self._lib.lpd_factor_kernel_stats(self._h, device_index, ctypes.byref(tot), ctypes.byref(cnt),
+                                                 int(reset)))
+        return tot.value, cnt.value
 
     def last_factor_kernel_ms(self, device_index: int = 0) -> float:
         return float(self._lib.lpd_last_factor_kernel_ms(self._h, device_index))

@@ -150,10 +150,16 @@ struct DeviceState {
     __half* lt_hi = nullptr;
     __half* lt_lo = nullptr;
     float* col_scale = nullptr;
+    double* colmax = nullptr;
     CUtensorMap tm_lmhi, tm_lmlo, tm_lthi, tm_ltlo;
     Slot slot[2];
     cudaEvent_t kev[2] = {};
     float last_kernel_ms = 0.f;
+    // ring of (start, stop) event pairs around every timed factor-kernel launch,
+    // summed by lpd_factor_kernel_stats (benchmarks read the average launch time)
+    static constexpr int kRing = 512;
+    cudaEvent_t ring[kRing][2] = {};
+    int64_t ring_count = 0;  // launches recorded since the last reset
 
     void free_basis() {
         dev_free(mu); dev_free(lm_hi); dev_free(lm_lo); dev_free(lm_aux);
@@ -215,6 +221,8 @@ void init_device(DeviceState& ds, int device) {
         for (auto& e : s.ev) CUDA_TRY(cudaEventCreate(&e));
     }
     for (auto& e : ds.kev) CUDA_TRY(cudaEventCreate(&e));
+    for (auto& pr : ds.ring)
+        for (auto& e : pr) CUDA_TRY(cudaEventCreate(&e));
     CUDA_TRY(cudaFuncSetAttribute(lpd::nystrom_factor_kernel<double>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, lpd::k1::SMEM_BYTES));
     CUDA_TRY(cudaFuncSetAttribute(lpd::nystrom_factor_kernel<float>,
@@ -235,55 +243,73 @@ void validate_basis_args(int64_t B, int64_t d, int64_t b_eff, double gamma, cons
     if (B > (1 << 30) || b_eff > (1 << 30)) fail(LPD_ERR_UNSUPPORTED, "basis too large");
 }
 
-// Builds the basis on one device from a dense fp64 landmark block already on
-// that device (lm_dev, ld = d) and L on the host.
-void build_basis(DeviceState& ds, const double* lm_dev, int64_t B, int64_t d, const double* L_host,
-                 int64_t b_eff, double gamma) {
+// Builds the basis on one device from a dense fp64 landmark block (ld_lm) and
+// L (B × b_eff, row-major), both already on that device. Buffers are reused when
+// the padded shapes are unchanged (new γ / new L on the same budget is the
+// common case: grid search, reference modelsel.cpp:466-476).
+void build_basis(DeviceState& ds, const double* lm_dev, int64_t B, int64_t d, int64_t ld_lm,
+                 const double* L_dev, int64_t b_eff, double gamma, cudaStream_t st, bool sync) {
     CUDA_TRY(cudaSetDevice(ds.device));
-    cudaStream_t st = ds.slot[0].stream;
-    ds.free_basis();
+    const int64_t B_pad = round_up(B, lpd::k1::NC);
+    const int64_t Beff_pad = round_up(b_eff, lpd::k1::N2);
+    if (!ds.lt_hi || B_pad != ds.B_pad || Beff_pad != ds.Beff_pad) {
+        CUDA_TRY(cudaDeviceSynchronize());
+        ds.free_basis();
+        dev_free(ds.colmax);
+        ds.B_pad = B_pad;
+        ds.Beff_pad = Beff_pad;
+        dev_alloc(&ds.mu, lpd::KD_MAX);
+        dev_alloc(&ds.lm_hi, static_cast<size_t>(B_pad * lpd::KD_MAX));
+        dev_alloc(&ds.lm_lo, static_cast<size_t>(B_pad * lpd::KD_MAX));
+        dev_alloc(&ds.lm_aux, static_cast<size_t>(B_pad));
+        dev_alloc(&ds.lt_hi, static_cast<size_t>(Beff_pad * B_pad));
+        dev_alloc(&ds.lt_lo, static_cast<size_t>(Beff_pad * B_pad));
+        dev_alloc(&ds.col_scale, static_cast<size_t>(Beff_pad));
+        dev_alloc(&ds.colmax, static_cast<size_t>(Beff_pad));
+        ds.tm_lmhi = make_plane_map(ds.lm_hi, B_pad, lpd::KD_MAX, lpd::k1::NC, 64);
+        ds.tm_lmlo = make_plane_map(ds.lm_lo, B_pad, lpd::KD_MAX, lpd::k1::NC, 64);
+        ds.tm_lthi = make_plane_map(ds.lt_hi, Beff_pad, B_pad, lpd::k1::N2, 64);
+        ds.tm_ltlo = make_plane_map(ds.lt_lo, Beff_pad, B_pad, lpd::k1::N2, 64);
+    }
+    ds.has_basis = false;
     ds.B = B; ds.d = d; ds.b_eff = b_eff; ds.gamma = gamma;
-    ds.B_pad = round_up(B, lpd::k1::NC);
-    ds.Beff_pad = round_up(b_eff, lpd::k1::N2);
-    dev_alloc(&ds.mu, lpd::KD_MAX);
-    dev_alloc(&ds.lm_hi, static_cast<size_t>(ds.B_pad * lpd::KD_MAX));
-    dev_alloc(&ds.lm_lo, static_cast<size_t>(ds.B_pad * lpd::KD_MAX));
-    dev_alloc(&ds.lm_aux, static_cast<size_t>(ds.B_pad));
-    dev_alloc(&ds.lt_hi, static_cast<size_t>(ds.Beff_pad * ds.B_pad));
-    dev_alloc(&ds.lt_lo, static_cast<size_t>(ds.Beff_pad * ds.B_pad));
-    dev_alloc(&ds.col_scale, static_cast<size_t>(ds.Beff_pad));
 
-    lpd::column_mean_kernel<<<1, lpd::KD_MAX, 0, st>>>(lm_dev, d, static_cast<int>(B),
+    lpd::column_mean_kernel<<<1, lpd::KD_MAX, 0, st>>>(lm_dev, ld_lm, static_cast<int>(B),
                                                        static_cast<int>(d), ds.mu);
     {
         const int threads = 256, rows_per_block = threads / 32;
-        const int blocks = static_cast<int>((ds.B_pad + rows_per_block - 1) / rows_per_block);
+        const int blocks = static_cast<int>((B_pad + rows_per_block - 1) / rows_per_block);
         lpd::prep_rows_dense_kernel<<<blocks, threads, 0, st>>>(
-            lm_dev, d, static_cast<int>(B), static_cast<int>(d), ds.mu, ds.lm_hi, ds.lm_lo,
-            ds.lm_aux, static_cast<int>(ds.B_pad), -2.0f);
+            lm_dev, ld_lm, static_cast<int>(B), static_cast<int>(d), ds.mu, ds.lm_hi, ds.lm_lo,
+            ds.lm_aux, static_cast<int>(B_pad), -2.0f);
     }
-    double* L_dev = nullptr;
-    double* colmax = nullptr;
-    dev_alloc(&L_dev, static_cast<size_t>(B * b_eff));
-    dev_alloc(&colmax, static_cast<size_t>(b_eff));
-    CUDA_TRY(cudaMemcpyAsync(L_dev, L_host, sizeof(double) * B * b_eff, cudaMemcpyHostToDevice, st));
     lpd::col_absmax_kernel<<<static_cast<int>((b_eff + 127) / 128), 128, 0, st>>>(
-        L_dev, static_cast<int>(B), static_cast<int>(b_eff), colmax);
-    dim3 grid(static_cast<unsigned>(ds.B_pad / 32), static_cast<unsigned>(ds.Beff_pad / 32));
+        L_dev, static_cast<int>(B), static_cast<int>(b_eff), ds.colmax);
+    dim3 grid(static_cast<unsigned>(B_pad / 32), static_cast<unsigned>(Beff_pad / 32));
     lpd::lt_split_kernel<<<grid, dim3(32, 8), 0, st>>>(L_dev, static_cast<int>(B),
-                                                        static_cast<int>(b_eff), colmax, ds.lt_hi,
-                                                        ds.lt_lo, static_cast<int>(ds.B_pad),
-                                                        static_cast<int>(ds.Beff_pad), ds.col_scale);
+                                                        static_cast<int>(b_eff), ds.colmax, ds.lt_hi,
+                                                        ds.lt_lo, static_cast<int>(B_pad),
+                                                        static_cast<int>(Beff_pad), ds.col_scale);
     CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(cudaStreamSynchronize(st));
-    dev_free(L_dev);
-    dev_free(colmax);
-
-    ds.tm_lmhi = make_plane_map(ds.lm_hi, ds.B_pad, lpd::KD_MAX, lpd::k1::NC, 64);
-    ds.tm_lmlo = make_plane_map(ds.lm_lo, ds.B_pad, lpd::KD_MAX, lpd::k1::NC, 64);
-    ds.tm_lthi = make_plane_map(ds.lt_hi, ds.Beff_pad, ds.B_pad, lpd::k1::N2, 64);
-    ds.tm_ltlo = make_plane_map(ds.lt_lo, ds.Beff_pad, ds.B_pad, lpd::k1::N2, 64);
+    if (sync) CUDA_TRY(cudaStreamSynchronize(st));
     ds.has_basis = true;
+}
+
+// Host-L variant: stages L to the device, builds, frees the staging buffer.
+void build_basis_host_L(DeviceState& ds, const double* lm_dev, int64_t B, int64_t d,
+                        const double* L_host, int64_t b_eff, double gamma) {
+    CUDA_TRY(cudaSetDevice(ds.device));
+    cudaStream_t st = ds.slot[0].stream;
+    double* L_dev = nullptr;
+    dev_alloc(&L_dev, static_cast<size_t>(B * b_eff));
+    try {
+        CUDA_TRY(cudaMemcpyAsync(L_dev, L_host, sizeof(double) * B * b_eff, cudaMemcpyHostToDevice, st));
+        build_basis(ds, lm_dev, B, d, std::max<int64_t>(d, 1), L_dev, b_eff, gamma, st, true);
+    } catch (...) {
+        dev_free(L_dev);
+        throw;
+    }
+    dev_free(L_dev);
 }
 
 // prep + fused factor kernel for m rows of dense fp64 X already on the device.
@@ -316,14 +342,23 @@ void launch_factor(DeviceState& ds, Slot& s, const double* x_dev, int64_t m, int
     p.ldg = ldg;
     const int64_t tiles = static_cast<int64_t>(p.n_row_tiles) * p.n_col_blocks;
     const int grid = static_cast<int>(std::min<int64_t>(tiles, ds.num_sms));
-    if (time_it) CUDA_TRY(cudaEventRecord(ds.kev[0], st));
+    cudaEvent_t* pr = nullptr;
+    if (time_it) {
+        pr = ds.ring[ds.ring_count % DeviceState::kRing];
+        CUDA_TRY(cudaEventRecord(ds.kev[0], st));
+        if (ds.ring_count < DeviceState::kRing) CUDA_TRY(cudaEventRecord(pr[0], st));
+    }
     if (out_dtype == LPD_OUT_F64)
         lpd::nystrom_factor_kernel<double><<<grid, lpd::k1::THREADS, lpd::k1::SMEM_BYTES, st>>>(
             tm_xhi, tm_xlo, ds.tm_lmhi, ds.tm_lmlo, ds.tm_lthi, ds.tm_ltlo, p);
     else
         lpd::nystrom_factor_kernel<float><<<grid, lpd::k1::THREADS, lpd::k1::SMEM_BYTES, st>>>(
             tm_xhi, tm_xlo, ds.tm_lmhi, ds.tm_lmlo, ds.tm_lthi, ds.tm_ltlo, p);
-    if (time_it) CUDA_TRY(cudaEventRecord(ds.kev[1], st));
+    if (time_it) {
+        CUDA_TRY(cudaEventRecord(ds.kev[1], st));
+        if (ds.ring_count < DeviceState::kRing) CUDA_TRY(cudaEventRecord(pr[1], st));
+        ++ds.ring_count;
+    }
     CUDA_TRY(cudaGetLastError());
 }
 
@@ -475,12 +510,35 @@ int lpd_context_create(lpd_context** out, int num_devices) {
     });
 }
 
+int lpd_context_create_devices(lpd_context** out, const int* device_ids, int count) {
+    return guarded([&] {
+        if (!out) fail(LPD_ERR_INVALID_ARGUMENT, "null output pointer");
+        *out = nullptr;
+        if (count <= 0 || !device_ids) fail(LPD_ERR_INVALID_ARGUMENT, "empty device list");
+        const int avail = lpd_device_count();
+        if (avail <= 0) fail(LPD_ERR_NO_DEVICE, "no CUDA device visible");
+        for (int i = 0; i < count; ++i)
+            if (device_ids[i] < 0 || device_ids[i] >= avail)
+                fail(LPD_ERR_INVALID_ARGUMENT, "device id " + std::to_string(device_ids[i]) + " not visible");
+        auto* ctx = new lpd_context();
+        try {
+            ctx->dev.resize(count);
+            for (int i = 0; i < count; ++i) init_device(ctx->dev[i], device_ids[i]);
+        } catch (...) {
+            lpd_context_destroy(ctx);
+            throw;
+        }
+        *out = ctx;
+    });
+}
+
 int lpd_context_destroy(lpd_context* ctx) {
     if (!ctx) return LPD_OK;
     for (auto& ds : ctx->dev) {
         if (cudaSetDevice(ds.device) != cudaSuccess) continue;
         cudaDeviceSynchronize();
         ds.free_basis();
+        dev_free(ds.colmax);
         for (auto& s : ds.slot) {
             ds.free_slot(s);
             if (s.stream) cudaStreamDestroy(s.stream);
@@ -489,6 +547,9 @@ int lpd_context_destroy(lpd_context* ctx) {
         }
         for (auto& e : ds.kev)
             if (e) cudaEventDestroy(e);
+        for (auto& pr : ds.ring)
+            for (auto& e : pr)
+                if (e) cudaEventDestroy(e);
     }
     delete ctx;
     return LPD_OK;
@@ -516,7 +577,7 @@ int lpd_set_basis_dense(lpd_context* ctx, const double* landmarks, int64_t B, in
             else
                 CUDA_TRY(cudaMemset(lm, 0, sizeof(double)));
             try {
-                build_basis(ds, lm, B, d, L, b_eff, gamma);
+                build_basis_host_L(ds, lm, B, d, L, b_eff, gamma);
             } catch (...) {
                 dev_free(lm);
                 throw;
@@ -557,7 +618,7 @@ int lpd_set_basis_csr(lpd_context* ctx, int64_t B, int64_t d, const int64_t* ind
                     dip, didx, dval, static_cast<int>(B), static_cast<int>(d), lm);
             CUDA_TRY(cudaGetLastError());
             try {
-                build_basis(ds, lm, B, d, L, b_eff, gamma);
+                build_basis_host_L(ds, lm, B, d, L, b_eff, gamma);
             } catch (...) {
                 dev_free(dip); dev_free(didx); dev_free(dval); dev_free(lm);
                 throw;
@@ -660,6 +721,44 @@ double lpd_last_factor_kernel_ms(const lpd_context* ctx, int device_index) {
         return static_cast<double>(ds.last_kernel_ms);
     }
     return static_cast<double>(ms);
+}
+
+int lpd_factor_kernel_stats(lpd_context* ctx, int device_index, double* total_ms,
+                            int64_t* launches, int reset) {
+    return guarded([&] {
+        check_ctx(ctx, false);
+        if (device_index < 0 || device_index >= static_cast<int>(ctx->dev.size()))
+            fail(LPD_ERR_INVALID_ARGUMENT, "device index out of range");
+        DeviceState& ds = ctx->dev[device_index];
+        CUDA_TRY(cudaSetDevice(ds.device));
+        const int64_t n = std::min<int64_t>(ds.ring_count, DeviceState::kRing);
+        double tot = 0.0;
+        for (int64_t i = 0; i < n; ++i) {
+            CUDA_TRY(cudaEventSynchronize(ds.ring[i][1]));
+            float ms = 0.f;
+            CUDA_TRY(cudaEventElapsedTime(&ms, ds.ring[i][0], ds.ring[i][1]));
+            tot += ms;
+        }
+        if (total_ms) *total_ms = tot;
+        if (launches) *launches = n;
+        if (reset) ds.ring_count = 0;
+    });
+}
+
+int lpd_set_basis_device(lpd_context* ctx, int device_index, const double* landmarks_dev,
+                         int64_t B, int64_t d, int64_t ld, const double* L_dev, int64_t b_eff,
+                         double gamma, void* stream) {
+    return guarded([&] {
+        check_ctx(ctx, false);
+        if (device_index < 0 || device_index >= static_cast<int>(ctx->dev.size()))
+            fail(LPD_ERR_INVALID_ARGUMENT, "device index out of range");
+        validate_basis_args(B, d, b_eff, gamma, L_dev);
+        if (ld < d) fail(LPD_ERR_INVALID_ARGUMENT, "landmark leading dimension < d");
+        DeviceState& ds = ctx->dev[device_index];
+        CUDA_TRY(cudaSetDevice(ds.device));
+        build_basis(ds, landmarks_dev, B, d, ld, L_dev, b_eff, gamma,
+                    stream ? static_cast<cudaStream_t>(stream) : ds.slot[0].stream, !stream);
+    });
 }
 
 int lpd_decision_values_device(lpd_context* ctx, int device_index, const void* G_dev, int g_dtype,
