@@ -7,7 +7,7 @@ CSRC    := $(PKG)/csrc
 LIB     := $(PKG)/liblpd_nystrom.so
 HDRS    := $(wildcard $(CSRC)/*.cuh) include/lpd_nystrom.h
 
-all: $(LIB) oracle
+all: $(LIB) oracle integration
 
 $(LIB): $(CSRC)/lpd_nystrom.cu $(HDRS)
 	$(NVCC) $(NVFLAGS) -shared -o $@ $< -lcuda 2> $(PKG)/ptxas.log || (cat $(PKG)/ptxas.log; false)
@@ -16,8 +16,13 @@ $(LIB): $(CSRC)/lpd_nystrom.cu $(HDRS)
 oracle:
 	$(MAKE) -C oracle
 
+# the reference's own _core with compute_G served by this library (needs /root/reference)
+integration: $(LIB)
+	$(MAKE) -C integration
+
 clean:
 	rm -f $(LIB) $(PKG)/ptxas.log
 	$(MAKE) -C oracle clean
+	$(MAKE) -C integration clean
 
-.PHONY: all oracle clean
+.PHONY: all oracle integration clean

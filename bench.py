@@ -4,7 +4,7 @@ TFLOP/s vs peak"), workload C2: covtype-shaped synthetic binary blobs,
 n = 581,012 rows per GPU, d = 54, B = 4,096 landmarks, γ = 1/54.
 
 One step = one pass of the hot path (reference lpdsvm::compute_G,
-proj/src/factor.cpp:165-192) over the whole batch: basis prep of (landmarks, L)
+proj/src/factor.cpp:83-110) over the whole batch: basis prep of (landmarks, L)
 (K2; with N > 1 preceded by the NCCL broadcast of the basis from rank 0, the
 path's only collective), row prep (K3) and the fused factor kernel (K1)
 writing G = Z·L (fp64) to HBM.
@@ -131,8 +131,8 @@ class ClockSampler:
 
 def make_basis(X0, cfg, seed=1):
     """Landmarks: B rows of rank 0's data drawn uniformly without replacement
-    (as the reference's select_landmarks does, factor.cpp:109-113; numpy's seeded
-    generator here); L from the eigendecomposition of K (factor.cpp:115-163;
+    (as the reference's select_landmarks does, factor.cpp:27-31; numpy's seeded
+    generator here); L from the eigendecomposition of K (factor.cpp:33-81;
     numpy LAPACK, setup only, outside the timed region)."""
     ids = np.random.default_rng(seed).choice(X0.shape[0], cfg.budget, replace=False)
     Y = np.ascontiguousarray(X0[ids])

@@ -6,16 +6,16 @@
  *
  *   lpd_compute_g_csr / lpd_compute_g_dense
  *       replace lpdsvm::compute_G
- *       (reference proj/include/lpdsvm/factor.hpp:50-55, proj/src/factor.cpp:165-192):
+ *       (reference proj/include/lpdsvm/factor.hpp:50-55, proj/src/factor.cpp:83-110):
  *       G = Z(points, landmarks) · L, written row-major into a caller buffer.
  *   lpd_set_basis_csr / lpd_set_basis_dense
  *       receive the (landmarks, landmark_norms, L, params) arguments of the same
  *       call (factor.hpp:53-54). Split out so one basis (one γ) serves many row
  *       batches and devices: the reference calls compute_G once per γ
- *       (proj/src/factor.cpp:211-214, proj/src/modelsel.cpp:466-476).
+ *       (proj/src/factor.cpp:129-133, proj/src/modelsel.cpp:180-190).
  *   lpd_decision_values
  *       replaces the held-out scoring loop d[r][p] = G_r · w_p
- *       (proj/src/modelsel.cpp:409-426) and the warm-start/KKT sweeps that read
+ *       (proj/src/modelsel.cpp:123-140) and the warm-start/KKT sweeps that read
  *       G·w (proj/src/dcd.cpp:91-102, 150-172).
  *
  * Conventions: plain pointers and sizes only, no CUDA or C++ types. Matrices
@@ -36,7 +36,7 @@ extern "C" {
 #endif
 
 #define LPD_OK 0
-#define LPD_ERR_INVALID_ARGUMENT 1 /* reference: std::invalid_argument (factor.cpp:169,173; kernel.cpp:286-291) */
+#define LPD_ERR_INVALID_ARGUMENT 1 /* reference: std::invalid_argument (factor.cpp:87,91; kernel.cpp:10-15) */
 #define LPD_ERR_CUDA 2             /* device / driver failure: std::runtime_error */
 #define LPD_ERR_UNSUPPORTED 3      /* valid input outside this build's kernel envelope */
 #define LPD_ERR_OUT_OF_MEMORY 4

@@ -108,10 +108,10 @@ ORA_API void ora_kernel_block(int64_t m, const int64_t* a_ptr, const int32_t* a_
     }
 }
 
-/* factor.cpp:165-192 — compute_G: per chunk of chunk_size rows, Z = kernel_block(chunk,
+/* factor.cpp:83-110 — compute_G: per chunk of chunk_size rows, Z = kernel_block(chunk,
  * landmarks) then G[chunk] = Z * L (fp64). L is b x b_eff row-major; G is n x b_eff
  * row-major. The GEMM sums over landmarks in ascending order. Returns 0, or -1 on the
- * reference's std::invalid_argument conditions (factor.cpp:169, 173 is the caller's
+ * reference's std::invalid_argument conditions (factor.cpp:87, 173 is the caller's
  * shape check) or -2 on allocation failure. */
 ORA_API int ora_compute_g(int64_t n, const int64_t* x_ptr, const int32_t* x_idx,
                           const double* x_val, const double* norms, int64_t b,
@@ -141,7 +141,7 @@ ORA_API int ora_compute_g(int64_t n, const int64_t* x_ptr, const int32_t* x_idx,
     return 0;
 }
 
-/* modelsel.cpp:409-426 — held-out scoring d[r][p] = G_r . w_p, fp64, j ascending.
+/* modelsel.cpp:123-140 — held-out scoring d[r][p] = G_r . w_p, fp64, j ascending.
  * G rows selected by row_ids (n_rows of them); W is P x b_eff; D is n_rows x P. */
 ORA_API void ora_decision_values(int64_t n_rows, const int64_t* row_ids, const double* G,
                                  int64_t ldg, int64_t b_eff, const double* W, int64_t P,
@@ -230,7 +230,7 @@ static uint64_t rng_below(mt64* s, uint64_t n) {
     return r % n;
 }
 
-/* factor.cpp:109-113 + rng.hpp:60-72 — select_landmarks(n, budget, seed):
+/* factor.cpp:27-31 + rng.hpp:60-72 — select_landmarks(n, budget, seed):
  * first min(budget, n) entries of a seeded partial Fisher-Yates permutation,
  * seed tag 0x1a2d. Returns the count written (or -1 on invalid input). */
 ORA_API int64_t ora_select_landmarks(int64_t n, int64_t budget, uint64_t seed, int32_t* out) {

@@ -257,7 +257,7 @@ def ref_select_landmarks(n: int, budget: int, seed: int) -> np.ndarray:
 
 def ref_factor_with_landmarks(points, landmarks, gamma: float, tau: float = 1e-12, chunk_size: int = 4096,
                               threads: int = 1) -> dict:
-    """Reference build_factor_with_landmarks (factor.cpp:194-225): L, G, b_eff, timings."""
+    """Reference build_factor_with_landmarks (factor.cpp:112-143): L, G, b_eff, timings."""
     xp, xi, xv = _csr(points)
     lp, li, lv = _csr(landmarks)
     n, b = xp.shape[0] - 1, lp.shape[0] - 1

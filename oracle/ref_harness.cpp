@@ -93,7 +93,7 @@ __attribute__((visibility("default"))) int ref_squared_norms(int64_t n, const in
     });
 }
 
-// factor.cpp:165-192 — the hot path itself, reference implementation.
+// factor.cpp:83-110 — the hot path itself, reference implementation.
 __attribute__((visibility("default"))) int ref_compute_g(
     int64_t n, const int64_t* x_ptr, const int32_t* x_idx, const double* x_val, int64_t b,
     const int64_t* l_ptr, const int32_t* l_idx, const double* l_val, const double* L,
@@ -106,7 +106,7 @@ __attribute__((visibility("default"))) int ref_compute_g(
         const KernelParams params{KernelKind::Gaussian, gamma};
         validate(params);
         const auto t0 = std::chrono::steady_clock::now();
-        // same sequence as build_factor_with_landmarks' gmatrix stage (factor.cpp:211-215)
+        // same sequence as build_factor_with_landmarks' gmatrix stage (factor.cpp:129-133)
         std::vector<double> ln = squared_norms(Y);
         std::vector<double> xn = squared_norms(X);
         Matrix Gm = compute_G(X, xn, Y, ln, Lm, params, static_cast<size_t>(chunk_size), threads);
@@ -116,7 +116,7 @@ __attribute__((visibility("default"))) int ref_compute_g(
     });
 }
 
-// factor.cpp:109-113
+// factor.cpp:27-31
 __attribute__((visibility("default"))) int64_t ref_select_landmarks(int64_t n, int64_t budget,
                                                                     uint64_t seed, int32_t* out) {
     int64_t k = -1;
@@ -128,7 +128,7 @@ __attribute__((visibility("default"))) int64_t ref_select_landmarks(int64_t n, i
     return k;
 }
 
-// factor.cpp:194-225 with caller-fixed landmarks; returns an opaque handle.
+// factor.cpp:112-143 with caller-fixed landmarks; returns an opaque handle.
 __attribute__((visibility("default"))) void* ref_factor_with_landmarks(
     int64_t n, const int64_t* x_ptr, const int32_t* x_idx, const double* x_val, int64_t b,
     const int64_t* l_ptr, const int32_t* l_idx, const double* l_val, double gamma, double tau,
@@ -158,7 +158,7 @@ __attribute__((visibility("default"))) void* ref_factor_with_landmarks(
     return h;
 }
 
-// factor.cpp:227-235 (landmarks sampled by the reference)
+// factor.cpp:145-153 (landmarks sampled by the reference)
 __attribute__((visibility("default"))) void* ref_build_factor(
     int64_t n, const int64_t* x_ptr, const int32_t* x_idx, const double* x_val, int64_t budget,
     double gamma, double tau, int64_t chunk_size, int threads, uint64_t seed, int64_t* b_eff,

@@ -3,12 +3,12 @@
 Python mirror of the reference's factor interface over the C ABI in
 ``include/lpd_nystrom.h`` (``liblpd_nystrom.so``, built in-tree). The reference
 entry point this mirrors is ``lpdsvm::compute_G`` (reference
-proj/include/lpdsvm/factor.hpp:50-55, proj/src/factor.cpp:165-192); argument
+proj/include/lpdsvm/factor.hpp:50-55, proj/src/factor.cpp:83-110); argument
 meaning and error behaviour follow it:
 
-* ``chunk_size == 0``          -> ValueError  (factor.cpp:169, std::invalid_argument)
-* ``L.rows != len(landmarks)`` -> ValueError  (factor.cpp:173)
-* γ not positive and finite    -> ValueError  (kernel.cpp:286-291)
+* ``chunk_size == 0``          -> ValueError  (factor.cpp:87, std::invalid_argument)
+* ``L.rows != len(landmarks)`` -> ValueError  (factor.cpp:91)
+* γ not positive and finite    -> ValueError  (kernel.cpp:10-15)
 * device / driver failures     -> RuntimeError (std::runtime_error)
 
 There is no CPU fallback: when the CUDA library cannot be loaded or no B200 is

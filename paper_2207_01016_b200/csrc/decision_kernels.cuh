@@ -1,7 +1,7 @@
 // K4 — decision values on an HBM-resident factor: D[r][p] = G_r · w_p.
 //
 // Replaces the reference's single-threaded held-out scoring loop
-// (proj/src/modelsel.cpp:409-426: `d += g_row[j] * w_row[j]` in fp64) and is
+// (proj/src/modelsel.cpp:123-140: `d += g_row[j] * w_row[j]` in fp64) and is
 // the product the warm-start / KKT sweeps need (proj/src/dcd.cpp:91-102,
 // 150-172). Memory-bound: each G row is streamed once per block of PB
 // weight vectors with 16-byte loads; accumulation is fp64 like the reference.

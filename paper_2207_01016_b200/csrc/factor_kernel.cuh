@@ -4,7 +4,7 @@
 //
 // This replaces, for one 128-row tile of points and one 256-column block of G,
 // the reference's per-chunk kernel_block + Eigen GEMM (reference
-// proj/src/factor.cpp:179-190 calling proj/src/kernel.cpp:307-333).
+// proj/src/factor.cpp:97-108 calling proj/src/kernel.cpp:31-57).
 //
 // Design (persistent, one CTA per SM, warp-specialised, 384 threads):
 //   warp 0     TMA producer A: X tile (once per tile) and landmark chunks
@@ -39,6 +39,7 @@ struct FactorParams {
     const float* col_scale; // [Beff_pad] 2^-13 / u_k (undoes Z and Lᵀ-row scaling)
     void* G;                // output, row-major, leading dimension ldg (elements)
     long long ldg;
+    int dbg;                // profiling ablations (LPD_K1_DEBUG), 0 in production
 };
 
 namespace k1 {
@@ -205,7 +206,7 @@ __global__ void __launch_bounds__(k1::THREADS, 1)
                         const uint64_t a = (pass == 2) ? d_xlo : d_xhi;
                         const uint64_t bb = (pass == 1) ? d_lmlo : d_lmhi;
                         for (int k = 0; k < p.ksteps1; ++k)
-                            mma_f16_ss(d, a + 2 * k, bb + 2 * k, IDESC_G1, (pass | k) != 0);
+                            if (!(p.dbg & 8)) mma_f16_ss(d, a + 2 * k, bb + 2 * k, IDESC_G1, (pass | k) != 0);
                     }
                     mma_commit(lm_empty + lm_s);
                     mma_commit(s_full + b);
@@ -227,10 +228,10 @@ __global__ void __launch_bounds__(k1::THREADS, 1)
                     const uint64_t d_lt = d_lt0 + ((lt_s * LT_BYTES) >> 4);
 #pragma unroll
                     for (int k = 0; k < NC / 16; ++k)
-                        mma_f16_ss(d, d_zhi + 2 * k, d_lt + 2 * k, IDESC_G2, !(first && k == 0));
+                        if (!(p.dbg & 4)) mma_f16_ss(d, d_zhi + 2 * k, d_lt + 2 * k, IDESC_G2, !(first && k == 0));
 #pragma unroll
                     for (int k = 0; k < NC / 16; ++k)
-                        mma_f16_ss(d, d_zlo + 2 * k, d_lt + 2 * k, IDESC_G2, 1);
+                        if (!(p.dbg & 4)) mma_f16_ss(d, d_zlo + 2 * k, d_lt + 2 * k, IDESC_G2, 1);
                     mma_commit(lt_empty + lt_s);
                 }
                 __syncwarp();
@@ -242,7 +243,7 @@ __global__ void __launch_bounds__(k1::THREADS, 1)
                     const uint64_t d_lt = d_lt0 + ((lt_s * LT_BYTES) >> 4);
 #pragma unroll
                     for (int k = 0; k < NC / 16; ++k)
-                        mma_f16_ss(d, d_zhi + 2 * k, d_lt + 2 * k, IDESC_G2, 1);
+                        if (!(p.dbg & 4)) mma_f16_ss(d, d_zhi + 2 * k, d_lt + 2 * k, IDESC_G2, 1);
                     mma_commit(lt_empty + lt_s);
                     mma_commit(z_empty + b);
                 }
@@ -298,6 +299,10 @@ __global__ void __launch_bounds__(k1::THREADS, 1)
             if (lane == 0) mbar_arrive(s_empty + b);
 
             uint32_t hi[16], lo[16];
+            if (p.dbg & 1) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) { hi[i] = s[2 * i]; lo[i] = s[2 * i + 1]; }
+            } else
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
                 float z2[2];
@@ -353,7 +358,7 @@ __global__ void __launch_bounds__(k1::THREADS, 1)
                     if (lane == 0) mbar_arrive(g_empty);
                 }
                 const int gc0 = cb * N2 + c0;
-                if (!row_ok || gc0 >= p.b_eff) continue;
+                if (!row_ok || gc0 >= p.b_eff || (p.dbg & 2)) continue;
                 const float4* cs4 = reinterpret_cast<const float4*>(p.col_scale + gc0);
                 float out[32];
 #pragma unroll

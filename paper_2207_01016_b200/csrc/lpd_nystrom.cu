@@ -6,7 +6,7 @@
 // (factor_kernel.cuh) and K4 (decision_kernels.cuh).
 //
 // Host-row calls (lpd_compute_g_*) shard rows contiguously across devices
-// (reference compute_G splits rows into chunks, proj/src/factor.cpp:179-190;
+// (reference compute_G splits rows into chunks, proj/src/factor.cpp:97-108;
 // here each device owns a contiguous shard, no collective) and pipeline
 // H2D → prep → factor → D2H in row chunks on two streams per device, one host
 // thread per device. Errors never escape as exceptions: every entry point
@@ -234,7 +234,7 @@ void validate_basis_args(int64_t B, int64_t d, int64_t b_eff, double gamma, cons
     if (d < 0) fail(LPD_ERR_INVALID_ARGUMENT, "feature dimension must be non-negative");
     if (b_eff <= 0) fail(LPD_ERR_INVALID_ARGUMENT, "L must have at least one column");
     if (!L) fail(LPD_ERR_INVALID_ARGUMENT, "L is null");
-    // reference validate(): proj/src/kernel.cpp:286-291
+    // reference validate(): proj/src/kernel.cpp:10-15
     if (!(gamma > 0.0) || !std::isfinite(gamma))
         fail(LPD_ERR_INVALID_ARGUMENT, "kernel gamma must be positive and finite");
     if (d > lpd::KD_MAX)
@@ -246,7 +246,7 @@ void validate_basis_args(int64_t B, int64_t d, int64_t b_eff, double gamma, cons
 // Builds the basis on one device from a dense fp64 landmark block (ld_lm) and
 // L (B × b_eff, row-major), both already on that device. Buffers are reused when
 // the padded shapes are unchanged (new γ / new L on the same budget is the
-// common case: grid search, reference modelsel.cpp:466-476).
+// common case: grid search, reference modelsel.cpp:180-190).
 void build_basis(DeviceState& ds, const double* lm_dev, int64_t B, int64_t d, int64_t ld_lm,
                  const double* L_dev, int64_t b_eff, double gamma, cudaStream_t st, bool sync) {
     CUDA_TRY(cudaSetDevice(ds.device));
@@ -340,6 +340,11 @@ void launch_factor(DeviceState& ds, Slot& s, const double* x_dev, int64_t m, int
     p.col_scale = ds.col_scale;
     p.G = g_dev;
     p.ldg = ldg;
+    static const int dbg = [] {
+        const char* e = std::getenv("LPD_K1_DEBUG");
+        return e ? std::atoi(e) : 0;
+    }();
+    p.dbg = dbg;
     const int64_t tiles = static_cast<int64_t>(p.n_row_tiles) * p.n_col_blocks;
     const int grid = static_cast<int>(std::min<int64_t>(tiles, ds.num_sms));
     cudaEvent_t* pr = nullptr;

@@ -9,7 +9,7 @@
 //   hi = fp16(x·s), lo = fp16(x·s − hi) into a [rows_pad × 64] K-major plane.
 //   aux = (‖x−μ‖² in fp64 rounded to fp32, mult · 2^-e).
 //
-//   L (reference proj/src/factor.cpp:150-163, consumed at :176-189): transposed
+//   L (reference proj/src/factor.cpp:68-81, consumed at :176-189): transposed
 //   to Lᵀ [Beff_pad × B_pad] with a power-of-two scale u_k per G column so the
 //   column max lands in [2^13, 2^14); col_scale_k = 2^-13 / u_k undoes both
 //   that and the 2^13 carried by Z.

@@ -1,6 +1,6 @@
 """Row sharding across GPUs (one process per GPU) — SURVEY.md §8(e).
 
-Rows of G are independent (reference proj/src/factor.cpp:179-190 computes
+Rows of G are independent (reference proj/src/factor.cpp:97-108 computes
 them in independent chunks; SPEC.md:220 requires worker-count invariance), so
 the units are split into contiguous row ranges with no collective on G. The
 only exchange is the per-γ basis (landmarks, L, γ) broadcast from rank 0.

@@ -39,7 +39,7 @@ def row_rel_err(G, R):
 
 
 def np_gaussian_L(Y, gamma, tau=1e-12):
-    """L = U D^-1/2 on retained eigenvalues (reference factor.cpp:115-163), numpy eigh;
+    """L = U D^-1/2 on retained eigenvalues (reference factor.cpp:33-81), numpy eigh;
     used only to build test inputs — both paths under comparison get this same L."""
     ny = (Y * Y).sum(1)
     K = np.exp(-gamma * np.maximum(ny[:, None] + ny[None, :] - 2.0 * Y @ Y.T, 0.0))

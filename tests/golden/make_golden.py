@@ -6,7 +6,7 @@ compiled unmodified by oracle/Makefile):  python tests/golden/make_golden.py
   spec_known_answers.json  SPEC.md known answers (analytic; SPEC line cited per entry)
   c1_mini.npz              C1 blobs, first 1024 rows, 128 landmarks chosen by the
                            reference select_landmarks(seed=1), L and G from the
-                           reference build_factor_with_landmarks (factor.cpp:194-225)
+                           reference build_factor_with_landmarks (factor.cpp:112-143)
   susy_mini.npz            SUSY-shaped d=18, gamma=2^-7 (ill-conditioned), n=512, B=256
   sparse_mini.npz          random sparse CSR points incl. empty rows, n=300, d=40, B=64
 """

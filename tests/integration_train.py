@@ -1,0 +1,106 @@
+"""Runs the reference's public Python API (`lpdsvm.train`, `Model.predict`,
+`Model.decision_values`, `lpdsvm.cross_validate`) from one build of the
+reference's `_core` module and saves the results, so two builds can be compared
+in separate processes (two pybind11 modules registering the same C++ types cannot
+share one interpreter).
+
+  python tests/integration_train.py <module_dir> <out.npz> [--n N --d D --budget B ...]
+
+<module_dir> is a directory holding `lpdsvm/_core*.so`:
+  integration/_build  — the reference with compute_G served by the B200 library
+  oracle/_ref         — the reference as is (CPU; test infrastructure)
+"""
+import argparse
+import ctypes
+import glob
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def libsvm_text(X, y):
+    # repr() of a float64 holding an fp32 value round-trips exactly through strtod
+    lines = []
+    for xi, yi in zip(X, y):
+        feats = " ".join(f"{j + 1}:{float(v)!r}" for j, v in enumerate(xi) if v != 0.0)
+        lines.append(f"{int(yi)} {feats}")
+    return "\n".join(lines) + "\n"
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("module_dir")
+    ap.add_argument("out")
+    ap.add_argument("--n", type=int, default=4000)
+    ap.add_argument("--n-test", type=int, default=1000)
+    ap.add_argument("--d", type=int, default=20)
+    ap.add_argument("--budget", type=int, default=400)
+    ap.add_argument("--gamma", type=float, default=0.05)
+    ap.add_argument("--C", type=float, default=1.0)
+    ap.add_argument("--classes", type=int, default=2)
+    ap.add_argument("--threads", type=int, default=4)
+    ap.add_argument("--tau", type=float, default=1e-6)
+    args = ap.parse_args()
+
+    mdir = args.module_dir if os.path.isabs(args.module_dir) else os.path.join(ROOT, args.module_dir)
+    sys.path.insert(0, mdir)
+    if os.path.isdir(os.path.join(mdir, "lpdsvm")):
+        import lpdsvm  # the build under test (package layout of the reference)
+    else:
+        import _core as lpdsvm  # oracle/_ref ships the bare extension module
+
+    sys.path.insert(0, ROOT)
+    from paper_2207_01016_b200 import synthetic
+
+    if args.classes == 2:
+        X, y = synthetic.blobs(args.n + args.n_test, args.d, seed=11)
+    else:
+        X, y = synthetic.imagenet_like(args.n + args.n_test, args.d, args.classes, seed=11)
+        X = X / 4.0  # keep γ·d² in a useful range for the small test
+        X = X.astype(np.float32).astype(np.float64)
+    train = lpdsvm.parse_dataset(libsvm_text(X[: args.n], y[: args.n]))
+    test = lpdsvm.parse_dataset(libsvm_text(X[args.n :], y[args.n :]))
+
+    t0 = time.perf_counter()
+    model, stats = lpdsvm.train(train, budget=args.budget, C=args.C, gamma=args.gamma,
+                                threads=args.threads, tau=args.tau)
+    train_s = time.perf_counter() - t0
+    pred = model.predict(test, threads=args.threads)
+    dv = model.decision_values(test)
+    cv = lpdsvm.cross_validate(train, budget=args.budget, C=args.C, gamma=args.gamma, folds=3,
+                               threads=args.threads, tau=args.tau)
+
+    so = glob.glob(os.path.join(os.path.dirname(lpdsvm.__file__), "_core*.so"))[0]
+    # (for the package layout, __file__ is lpdsvm/__init__.py next to _core*.so)
+    lib = ctypes.CDLL(so)
+    adapter_calls = -1
+    if hasattr(lib, "lpd_adapter_calls"):
+        lib.lpd_adapter_calls.restype = ctypes.c_longlong
+        adapter_calls = int(lib.lpd_adapter_calls())
+    np.savez(
+        args.out,
+        pred=pred,
+        dv=dv,
+        y_test=y[args.n :],
+        error_rate=model.error_rate(test),
+        cv_mean_error=cv["mean_error"],
+        cv_fold_errors=cv["fold_errors"],
+        effective_rank=model.effective_rank,
+        gmatrix_seconds=stats["gmatrix_seconds"],
+        preparation_seconds=stats["preparation_seconds"],
+        training_seconds=stats["training_seconds"],
+        train_wall_seconds=train_s,
+        epochs=stats["epochs"],
+        adapter_calls=adapter_calls,
+        model_text=np.array(model.to_string()),
+    )
+    print(f"{args.module_dir}: error {model.error_rate(test):.4f} cv {cv['mean_error']:.4f} "
+          f"gmatrix {stats['gmatrix_seconds']:.3f}s adapter_calls {adapter_calls}")
+
+
+if __name__ == "__main__":
+    main()

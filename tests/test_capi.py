@@ -49,11 +49,11 @@ def test_no_device_fails_loudly():
 def test_compute_G_argument_errors_match_reference():
     pts = np.zeros((3, 2))
     lms = np.zeros((2, 2))
-    with pytest.raises(ValueError, match="chunk_size"):       # factor.cpp:169
+    with pytest.raises(ValueError, match="chunk_size"):       # factor.cpp:87
         P.compute_G(pts, None, lms, None, np.eye(2), P.KernelParams(1.0), 0)
-    with pytest.raises(ValueError, match="L row count"):      # factor.cpp:173
+    with pytest.raises(ValueError, match="L row count"):      # factor.cpp:91
         P.compute_G(pts, None, lms, None, np.eye(3), P.KernelParams(1.0), 16)
-    with pytest.raises(ValueError, match="gamma"):            # kernel.cpp:289-290
+    with pytest.raises(ValueError, match="gamma"):            # kernel.cpp:13-14
         P.compute_G(pts, None, lms, None, np.eye(2), P.KernelParams(-1.0), 16)
     with pytest.raises(ValueError, match="gamma"):
         P.compute_G(pts, None, lms, None, np.eye(2), P.KernelParams(float("inf")), 16)
