@@ -7,19 +7,26 @@
 // proj/src/factor.cpp:97-108 calling proj/src/kernel.cpp:31-57).
 //
 // Design (persistent, one CTA per SM, warp-specialised, 384 threads):
-//   warp 0     TMA producer A: X tile (once per tile) and landmark chunks
-//   warp 1     MMA issuer (one elected lane): GEMM1 S = X·Bᵀ and GEMM2 G += Z·L, both into TMEM
+//   warp 0     TMA producer: landmark chunks (64 landmarks, hi/lo planes)
+//   warp 1     MMA issuer (one elected lane)
 //   warp 2     TMEM allocator
-//   warp 3     TMA producer B: Lᵀ half-chunks (separate ring, so landmark loads never queue behind it)
-//   warps 4-11 epilogue: S (TMEM) → Z = exp(...) → fp16 hi/lo (SMEM, swizzled
-//              K-major, the A operand of GEMM2); at tile end G (TMEM) → global
+//   warp 3     TMA producer: Lᵀ half-chunks of this tile's 256-column block
+//   warps 4-11 epilogue: X tile → TMEM; S → Z (in place, TMEM); G (TMEM) → SMEM → TMA store
 //
-// Precision: every operand is carried as an unevaluated sum hi + lo of two
-// fp16 values after an exact power-of-two scaling (per X row, per landmark,
-// per G column, and 2^13 for Z), and each product uses three tcgen05 kind::f16
-// MMAs (hi·hi + hi·lo + lo·hi) with fp32 accumulation. That keeps 22 mantissa
-// bits per operand — the same as a 3×TF32 split — at twice the tensor rate of
-// kind::tf32. Z never leaves the SM (TMEM → registers → SMEM → tensor core).
+// Tensor memory (512 columns × 128 lanes × 32 bit):
+//   [0, 256)    G accumulator, fp32, row i of the tile in lane i
+//   [256, 448)  three S/Z buffers of 64 columns: GEMM1 writes S = X·B̃ᵀ (fp32), the
+//               epilogue reads it and writes Z·2^13 back in place as packed fp16
+//               hi/lo, which GEMM2 reads as its A operand (TS form)
+//   [448, 512)  X tile, fp16 hi [448, 480) and lo [480, 512): GEMM1's A operand
+// so neither X, S nor Z ever touches shared memory, and no K/Z block touches HBM.
+//
+// Precision: operands are unevaluated sums hi + lo of two fp16 values after exact
+// power-of-two scaling, and each product is three kind::f16 MMAs (hi·hi + hi·lo +
+// lo·hi) accumulating in fp32 — 22 mantissa bits per operand, like a 3×TF32 split,
+// at twice the tensor rate of kind::tf32. The landmark norm rides through GEMM1 as an
+// augmented column (prep_kernels.cuh), so the epilogue is t = R_i + acc·sx_i,
+// Z·2^13 = 2^min(t, 13).
 #pragma once
 
 #include "ptx.cuh"
@@ -32,14 +39,37 @@ struct FactorParams {
     int n_chunks;           // B_pad / 64
     int n_col_blocks;       // Beff_pad / 256
     int b_eff;              // valid G columns
-    int ksteps1;            // ceil(d / 16): K-steps of GEMM1 inside the 64-wide atom
-    float neg_gamma_log2e;  // −γ·log2(e)
-    const float2* row_aux;  // [n_pad] (‖x_i − μ‖², 2^-e_i = inverse of the X row scale)
-    const float2* lm_aux;   // [B_pad] (‖b_j − μ‖², −2·2^-e_j)
+    int ksteps1;            // ceil((d + 1) / 16): K-steps of GEMM1 (d features + norm column)
+    int tma_store;          // 1: G leaves through SMEM + TMA store (tensor map valid)
+    const float2* row_aux;  // [n_pad] (R_i, sx_i): t = R_i + acc*sx_i (prep_rows_kernel)
+    const __half* x_hi;     // [n_pad x 64] point planes (K-major)
+    const __half* x_lo;
     const float* col_scale; // [Beff_pad] 2^-13 / u_k (undoes Z and Lᵀ-row scaling)
     void* G;                // output, row-major, leading dimension ldg (elements)
     long long ldg;
     int dbg;                // profiling ablations (LPD_K1_DEBUG), 0 in production
+    unsigned long long* dbg_out;  // [2 roles x 8 phases] cycle sums when dbg & 16
+};
+
+// Phase-cycle probe for profiling builds (dbg & 16): accumulates clock64 deltas
+// per phase in registers, flushed once per warp at kernel end.
+struct PhaseProbe {
+    bool on;
+    unsigned long long last = 0, acc[8] = {};
+    __device__ explicit PhaseProbe(bool enabled) : on(enabled) {
+        if (on) last = clock64();
+    }
+    __device__ __forceinline__ void mark(int k) {
+        if (on) {
+            const unsigned long long t = clock64();
+            acc[k] += t - last;
+            last = t;
+        }
+    }
+    __device__ void flush(unsigned long long* out) {
+        if (on && out)
+            for (int k = 0; k < 8; ++k) atomicAdd(out + k, acc[k]);
+    }
 };
 
 namespace k1 {
@@ -47,42 +77,48 @@ constexpr int BM = 128;        // rows per tile (UMMA M)
 constexpr int NC = 64;         // landmarks per chunk: N of GEMM1, K of GEMM2
 constexpr int KD = 64;         // padded feature dim (one 128-byte swizzle atom of fp16)
 constexpr int N2 = 256;        // G columns per tile (UMMA N of GEMM2)
-constexpr int NS_LM = 2;       // landmark-chunk stages
-constexpr int NS_LT = 3;       // Lᵀ half-chunk stages (hi and lo travel separately)
+constexpr int NS_LM = 3;       // landmark-chunk stages
+constexpr int NS_LT = 4;       // Lᵀ half-chunk stages (hi and lo travel separately)
+constexpr int NSZ = 3;         // S/Z TMEM buffers
 constexpr int EPI_WARPS = 8;
 constexpr int THREADS = 128 + 32 * EPI_WARPS;
 constexpr int Z13 = 13;        // Z is carried as Z·2^13 in fp16
 
-constexpr uint32_t X_BYTES = BM * KD * 2;            // 16 KB per hi/lo
-constexpr uint32_t LM_BYTES = NC * KD * 2;           // 8 KB per hi/lo
+constexpr uint32_t LM_BYTES = NC * KD * 2;           // 8 KB per hi/lo plane
 constexpr uint32_t LT_BYTES = N2 * NC * 2;           // 32 KB per stage
-constexpr uint32_t Z_BYTES = BM * NC * 2;            // 16 KB per hi/lo
+constexpr uint32_t STG_BYTES = 32 * 128;             // 4 KB G staging per epilogue warp
 
-constexpr uint32_t OFF_XHI = 0;
-constexpr uint32_t OFF_XLO = OFF_XHI + X_BYTES;
-constexpr uint32_t OFF_LM = OFF_XLO + X_BYTES;                      // stage s: hi, lo
+constexpr uint32_t OFF_LM = 0;                                      // stage s: hi, lo
 constexpr uint32_t OFF_LT = OFF_LM + NS_LM * 2 * LM_BYTES;          // stage s
-constexpr uint32_t OFF_Z = OFF_LT + NS_LT * LT_BYTES;               // buf b: hi, lo
-constexpr uint32_t OFF_BAR = OFF_Z + 2 * 2 * Z_BYTES;
-constexpr uint32_t NUM_BARS = 2 + 2 * NS_LM + 2 * NS_LT + 2 * 2 + 2 * 2 + 2;
+constexpr uint32_t OFF_STG = OFF_LT + NS_LT * LT_BYTES;             // warp w
+constexpr uint32_t OFF_BAR = OFF_STG + EPI_WARPS * STG_BYTES;
+constexpr uint32_t NUM_BARS = 2 + 2 * NS_LM + 2 * NS_LT + 3 * NSZ + 2;
 constexpr uint32_t SMEM_BYTES = OFF_BAR + NUM_BARS * 8 + 16 + 1024;  // + alignment slack
 
 constexpr uint32_t TMEM_COLS = 512;
-constexpr uint32_t TM_G = 0;       // G accumulator: columns [0, 256)
-constexpr uint32_t TM_S = 256;     // S buffers: 256 + 64·b
+constexpr uint32_t TM_G = 0;
+constexpr uint32_t TM_SZ = 256;    // buffer b at 256 + 64·b
+constexpr uint32_t TM_XHI = 448;
+constexpr uint32_t TM_XLO = 480;
 
 constexpr uint32_t IDESC_G1 = idesc_f16_f32(BM, NC);
 constexpr uint32_t IDESC_G2 = idesc_f16_f32(BM, N2);
+
+// Column of K-step k (16 landmarks) of the Z hi / lo planes inside an S/Z buffer.
+// Epilogue warp `half` owns S columns [32·half, 32·half + 32) and writes its Z hi
+// into the first 16 and Z lo into the last 16 of them, so no warp overwrites S
+// columns another warp may still be reading.
+__device__ __forceinline__ uint32_t z_hi_col(uint32_t k) { return (k >> 1) * 32 + (k & 1) * 8; }
+__device__ __forceinline__ uint32_t z_lo_col(uint32_t k) { return z_hi_col(k) + 16; }
 }  // namespace k1
 
 template <typename OutT>
 __global__ void __launch_bounds__(k1::THREADS, 1)
-    nystrom_factor_kernel(const __grid_constant__ CUtensorMap tm_xhi,
-                          const __grid_constant__ CUtensorMap tm_xlo,
-                          const __grid_constant__ CUtensorMap tm_lmhi,
+    nystrom_factor_kernel(const __grid_constant__ CUtensorMap tm_lmhi,
                           const __grid_constant__ CUtensorMap tm_lmlo,
                           const __grid_constant__ CUtensorMap tm_lthi,
-                          const __grid_constant__ CUtensorMap tm_ltlo, const FactorParams p) {
+                          const __grid_constant__ CUtensorMap tm_ltlo,
+                          const __grid_constant__ CUtensorMap tm_g, const FactorParams p) {
     using namespace k1;
     extern __shared__ uint8_t smem_raw[];
     // 1024-byte alignment is required by the 128-byte swizzle atoms.
@@ -98,10 +134,9 @@ __global__ void __launch_bounds__(k1::THREADS, 1)
     uint64_t* lt_full = lm_empty + NS_LM;
     uint64_t* lt_empty = lt_full + NS_LT;
     uint64_t* s_full = lt_empty + NS_LT;
-    uint64_t* s_empty = s_full + 2;
-    uint64_t* z_full = s_empty + 2;
-    uint64_t* z_empty = z_full + 2;
-    uint64_t* g_full = z_empty + 2;
+    uint64_t* z_full = s_full + NSZ;
+    uint64_t* sz_empty = z_full + NSZ;
+    uint64_t* g_full = sz_empty + NSZ;
     uint64_t* g_empty = g_full + 1;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NUM_BARS);
 
@@ -110,24 +145,23 @@ __global__ void __launch_bounds__(k1::THREADS, 1)
     const int num_tiles = p.n_row_tiles * p.n_col_blocks;
 
     if (threadIdx.x == 0) {
-        mbar_init(x_full, 1);
+        mbar_init(x_full, EPI_WARPS);
         mbar_init(x_empty, 1);
         for (int s = 0; s < NS_LM; ++s) { mbar_init(lm_full + s, 1); mbar_init(lm_empty + s, 1); }
         for (int s = 0; s < NS_LT; ++s) { mbar_init(lt_full + s, 1); mbar_init(lt_empty + s, 1); }
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < NSZ; ++b) {
             mbar_init(s_full + b, 1);
-            mbar_init(s_empty + b, EPI_WARPS);
             mbar_init(z_full + b, EPI_WARPS);
-            mbar_init(z_empty + b, 1);
+            mbar_init(sz_empty + b, 1);
         }
         mbar_init(g_full, 1);
         mbar_init(g_empty, EPI_WARPS);
         fence_mbar_init();
     }
     if (warp == 0 && lane == 0) {
-        tma_prefetch_desc(&tm_xhi); tma_prefetch_desc(&tm_xlo);
         tma_prefetch_desc(&tm_lmhi); tma_prefetch_desc(&tm_lmlo);
         tma_prefetch_desc(&tm_lthi); tma_prefetch_desc(&tm_ltlo);
+        if (p.tma_store) tma_prefetch_desc(&tm_g);
     }
     if (warp == 2) tmem_alloc(tmem_slot, TMEM_COLS);
     tc_fence_before();
@@ -136,17 +170,11 @@ __global__ void __launch_bounds__(k1::THREADS, 1)
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
-        // ============ TMA producer A: X tile (once per tile) + landmark chunks ============
+        // ============ TMA producer: landmark chunks (hi, lo) ============
         if (lane == 0) {
             const uint64_t keep = policy_evict_last();    // landmarks: reused by every tile
-            const uint64_t stream = policy_evict_first(); // X: read once per tile
-            uint32_t lm_s = 0, lm_ph = 0, it = 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
-                const int rt = tile / p.n_col_blocks;
-                mbar_wait(x_empty, (it & 1) ^ 1);
-                mbar_arrive_expect_tx(x_full, 2 * X_BYTES);
-                tma_load_2d_hint(&tm_xhi, x_full, smem + OFF_XHI, 0, rt * BM, stream);
-                tma_load_2d_hint(&tm_xlo, x_full, smem + OFF_XLO, 0, rt * BM, stream);
+            uint32_t lm_s = 0, lm_ph = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
                 for (int j = 0; j < p.n_chunks; ++j) {
                     mbar_wait(lm_empty + lm_s, lm_ph ^ 1);
                     mbar_arrive_expect_tx(lm_full + lm_s, 2 * LM_BYTES);
@@ -158,13 +186,12 @@ __global__ void __launch_bounds__(k1::THREADS, 1)
             }
         }
     } else if (warp == 3) {
-        // ============ TMA producer B: Lᵀ half-chunks (hi, lo) of this tile's column block ============
+        // ============ TMA producer: Lᵀ half-chunks (hi, lo) of this tile's column block ============
         if (lane == 0) {
             const uint64_t keep = policy_evict_last();
             uint32_t lt_s = 0, lt_ph = 0;
             for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-                const int rt = tile / p.n_col_blocks;
-                const int cb = tile - rt * p.n_col_blocks;
+                const int cb = tile / p.n_row_tiles;
                 for (int j = 0; j < p.n_chunks; ++j) {
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
@@ -182,92 +209,103 @@ __global__ void __launch_bounds__(k1::THREADS, 1)
         // Descriptor for smem address a is kDescHi | (a >> 4); K-step k adds 2k (32 bytes).
         const uint64_t dbase = sdesc_kmajor_sw128(0);
         auto desc = [&](uint32_t addr) -> uint64_t { return dbase | static_cast<uint64_t>((addr >> 4) & 0x3FFF); };
-        const uint64_t d_xhi = desc(base_addr + OFF_XHI), d_xlo = desc(base_addr + OFF_XLO);
         const uint64_t d_lm0 = desc(base_addr + OFF_LM);
         const uint64_t d_lt0 = desc(base_addr + OFF_LT);
-        const uint64_t d_z0 = desc(base_addr + OFF_Z);
         uint32_t lm_s = 0, lm_ph = 0, lt_s = 0, lt_ph = 0, it = 0;
-        uint32_t s_cnt = 0, z_cnt = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
-            mbar_wait(x_full, it & 1);
-            tc_fence_after();
+        uint32_t c1 = 0, c2 = 0;  // chunk sequence numbers of GEMM1 / GEMM2 (S/Z ring)
+        PhaseProbe pr((p.dbg & 16) != 0);
 
-            auto gemm1 = [&]() {
-                const uint32_t b = s_cnt & 1, ph = (s_cnt >> 1) & 1;
-                mbar_wait(s_empty + b, ph ^ 1);
-                mbar_wait(lm_full + lm_s, lm_ph);
-                tc_fence_after();
-                if (elect_one()) {
-                    const uint64_t d_lmhi = d_lm0 + ((lm_s * 2 * LM_BYTES) >> 4);
-                    const uint64_t d_lmlo = d_lmhi + (LM_BYTES >> 4);
-                    const uint32_t d = tmem_base + TM_S + b * NC;
-#pragma unroll
-                    for (int pass = 0; pass < 3; ++pass) {
-                        const uint64_t a = (pass == 2) ? d_xlo : d_xhi;
-                        const uint64_t bb = (pass == 1) ? d_lmlo : d_lmhi;
-                        for (int k = 0; k < p.ksteps1; ++k)
-                            if (!(p.dbg & 8)) mma_f16_ss(d, a + 2 * k, bb + 2 * k, IDESC_G1, (pass | k) != 0);
-                    }
-                    mma_commit(lm_empty + lm_s);
-                    mma_commit(s_full + b);
-                }
-                __syncwarp();
-                if (++lm_s == NS_LM) { lm_s = 0; lm_ph ^= 1; }
-                ++s_cnt;
-            };
-            auto gemm2 = [&](bool first) {
-                const uint32_t b = z_cnt & 1, ph = (z_cnt >> 1) & 1;
-                const uint64_t d_zhi = d_z0 + ((b * 2 * Z_BYTES) >> 4);
-                const uint64_t d_zlo = d_zhi + (Z_BYTES >> 4);
-                const uint32_t d = tmem_base + TM_G;
-                mbar_wait(z_full + b, ph);
-                // Lᵀ hi stage: Z_hi·Lᵀ_hi + Z_lo·Lᵀ_hi
-                mbar_wait(lt_full + lt_s, lt_ph);
-                tc_fence_after();
-                if (elect_one()) {
-                    const uint64_t d_lt = d_lt0 + ((lt_s * LT_BYTES) >> 4);
-#pragma unroll
-                    for (int k = 0; k < NC / 16; ++k)
-                        if (!(p.dbg & 4)) mma_f16_ss(d, d_zhi + 2 * k, d_lt + 2 * k, IDESC_G2, !(first && k == 0));
-#pragma unroll
-                    for (int k = 0; k < NC / 16; ++k)
-                        if (!(p.dbg & 4)) mma_f16_ss(d, d_zlo + 2 * k, d_lt + 2 * k, IDESC_G2, 1);
-                    mma_commit(lt_empty + lt_s);
-                }
-                __syncwarp();
-                if (++lt_s == NS_LT) { lt_s = 0; lt_ph ^= 1; }
-                // Lᵀ lo stage: Z_hi·Lᵀ_lo
-                mbar_wait(lt_full + lt_s, lt_ph);
-                tc_fence_after();
-                if (elect_one()) {
-                    const uint64_t d_lt = d_lt0 + ((lt_s * LT_BYTES) >> 4);
-#pragma unroll
-                    for (int k = 0; k < NC / 16; ++k)
-                        if (!(p.dbg & 4)) mma_f16_ss(d, d_zhi + 2 * k, d_lt + 2 * k, IDESC_G2, 1);
-                    mma_commit(lt_empty + lt_s);
-                    mma_commit(z_empty + b);
-                }
-                __syncwarp();
-                if (++lt_s == NS_LT) { lt_s = 0; lt_ph ^= 1; }
-                ++z_cnt;
-            };
-
-            gemm1();
-            if (p.n_chunks == 1 && elect_one()) mma_commit(x_empty);
-            __syncwarp();
-            // G accumulator must have been drained by the epilogue (previous tile).
-            mbar_wait(g_empty, (it & 1) ^ 1);
+        // GEMM1 of chunk q: S(b) = X·B̃ᵀ, three split passes. The last one of a tile
+        // also releases the X tile.
+        auto gemm1 = [&](int q) {
+            const uint32_t b = c1 % NSZ, ph = (c1 / NSZ) & 1;
+            pr.mark(5);
+            mbar_wait(sz_empty + b, ph ^ 1);
+            pr.mark(0);
+            mbar_wait(lm_full + lm_s, lm_ph);
+            pr.mark(1);
             tc_fence_after();
-            for (int j = 1; j < p.n_chunks; ++j) {
-                gemm1();
-                if (j == p.n_chunks - 1 && elect_one()) mma_commit(x_empty);
-                __syncwarp();
-                gemm2(j == 1);
+            if (elect_one()) {
+                const uint64_t d_lmhi = d_lm0 + ((lm_s * 2 * LM_BYTES) >> 4);
+                const uint64_t d_lmlo = d_lmhi + (LM_BYTES >> 4);
+                const uint32_t d = tmem_base + TM_SZ + b * NC;
+#pragma unroll
+                for (int pass = 0; pass < 3; ++pass) {
+                    const uint32_t a = tmem_base + ((pass == 2) ? TM_XLO : TM_XHI);
+                    const uint64_t bb = (pass == 1) ? d_lmlo : d_lmhi;
+                    for (int k = 0; k < p.ksteps1; ++k)
+                        if (!(p.dbg & 8)) mma_f16_ts(d, a + 8 * k, bb + 2 * k, IDESC_G1, (pass | k) != 0);
+                }
+                mma_commit(lm_empty + lm_s);
+                mma_commit(s_full + b);
+                if (q == p.n_chunks - 1) mma_commit(x_empty);
             }
-            gemm2(p.n_chunks == 1);
+            __syncwarp();
+            if (++lm_s == NS_LM) { lm_s = 0; lm_ph ^= 1; }
+            ++c1;
+        };
+        // GEMM2 of a chunk: G += Z_hi·Lᵀ_hi + Z_lo·Lᵀ_hi + Z_hi·Lᵀ_lo, Z from TMEM.
+        auto gemm2 = [&](bool first) {
+            const uint32_t b = c2 % NSZ, ph = (c2 / NSZ) & 1;
+            const uint32_t zb = tmem_base + TM_SZ + b * NC;
+            const uint32_t d = tmem_base + TM_G;
+            pr.mark(5);
+            mbar_wait(z_full + b, ph);
+            pr.mark(2);
+            mbar_wait(lt_full + lt_s, lt_ph);
+            pr.mark(3);
+            tc_fence_after();
+            if (elect_one()) {
+                const uint64_t d_lt = d_lt0 + ((lt_s * LT_BYTES) >> 4);
+#pragma unroll
+                for (int k = 0; k < NC / 16; ++k)
+                    if (!(p.dbg & 4)) mma_f16_ts(d, zb + z_hi_col(k), d_lt + 2 * k, IDESC_G2, !(first && k == 0));
+#pragma unroll
+                for (int k = 0; k < NC / 16; ++k)
+                    if (!(p.dbg & 4)) mma_f16_ts(d, zb + z_lo_col(k), d_lt + 2 * k, IDESC_G2, 1);
+                mma_commit(lt_empty + lt_s);
+            }
+            __syncwarp();
+            if (++lt_s == NS_LT) { lt_s = 0; lt_ph ^= 1; }
+            pr.mark(5);
+            mbar_wait(lt_full + lt_s, lt_ph);
+            pr.mark(3);
+            tc_fence_after();
+            if (elect_one()) {
+                const uint64_t d_lt = d_lt0 + ((lt_s * LT_BYTES) >> 4);
+#pragma unroll
+                for (int k = 0; k < NC / 16; ++k)
+                    if (!(p.dbg & 4)) mma_f16_ts(d, zb + z_hi_col(k), d_lt + 2 * k, IDESC_G2, 1);
+                mma_commit(lt_empty + lt_s);
+                mma_commit(sz_empty + b);
+            }
+            __syncwarp();
+            if (++lt_s == NS_LT) { lt_s = 0; lt_ph ^= 1; }
+            ++c2;
+        };
+
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+            pr.mark(5);
+            mbar_wait(x_full, it & 1);
+            pr.mark(6);
+            tc_fence_after();
+            // GEMM1 runs two chunks ahead of GEMM2 (three S/Z buffers).
+            gemm1(0);
+            if (p.n_chunks > 1) gemm1(1);
+            // G accumulator must have been drained by the epilogue (previous tile).
+            pr.mark(5);
+            mbar_wait(g_empty, (it & 1) ^ 1);
+            pr.mark(4);
+            tc_fence_after();
+            for (int j = 0; j < p.n_chunks; ++j) {
+                gemm2(j == 0);
+                if (j + 2 < p.n_chunks) gemm1(j + 2);
+            }
             if (elect_one()) mma_commit(g_full);
             __syncwarp();
         }
+        pr.mark(5);
+        if (lane == 0) pr.flush(p.dbg_out);
     } else if (warp >= 4) {
         // ===================== epilogue warps =====================
         const int ew = warp - 4;
@@ -275,77 +313,99 @@ __global__ void __launch_bounds__(k1::THREADS, 1)
         const int half = ew >> 2;           // which 32 of the 64 chunk columns
         const int r = quad * 32 + lane;     // row within the tile
         const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
-        const float ngl2e = p.neg_gamma_log2e;
         uint32_t cnt = 0;
+        PhaseProbe pr((p.dbg & 16) != 0);
+        uint8_t* stg = smem + OFF_STG + ew * STG_BYTES;
+        const uint32_t stg_addr = base_addr + OFF_STG + ew * STG_BYTES;
 
-        // Z for chunk j of a tile: S (TMEM) -> exp -> fp16 hi/lo -> swizzled SMEM.
-        auto produce_z = [&](float nx, float xinv, int j) {
-            const uint32_t b = cnt & 1, ph = (cnt >> 1) & 1;
-            float2 aux[32];
-            const float4* a4 = reinterpret_cast<const float4*>(p.lm_aux + j * NC + half * 32);
+        // X tile rt: this thread's row of the hi (half 0) or lo (half 1) plane, loaded
+        // into registers a whole tile ahead, then written to TMEM once the previous
+        // tile's last GEMM1 has consumed X.
+        uint32_t xv[32];
+        auto load_x = [&](int rt) {
+            const uint4* src = reinterpret_cast<const uint4*>(
+                (half ? p.x_lo : p.x_hi) + (static_cast<long long>(rt) * BM + r) * KD);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const float4 v = __ldg(a4 + i);
-                aux[2 * i] = make_float2(v.x, v.y);
-                aux[2 * i + 1] = make_float2(v.z, v.w);
+            for (int i = 0; i < 8; ++i) {
+                const uint4 q = __ldg(src + i);
+                xv[4 * i] = q.x; xv[4 * i + 1] = q.y; xv[4 * i + 2] = q.z; xv[4 * i + 3] = q.w;
             }
-            uint32_t s[32];
-            mbar_wait(s_full + b, ph);
+        };
+        auto write_x = [&](uint32_t itx) {
+            const uint32_t (&v)[32] = xv;
+            mbar_wait(x_empty, (itx & 1) ^ 1);
             tc_fence_after();
-            tmem_ld_32x32b_x32(tmem_base + lane_off + TM_S + b * NC + half * 32, s);
-            tmem_wait_ld();
+            tmem_st_32x32b_x32(tmem_base + lane_off + (half ? TM_XLO : TM_XHI), v);
+            tmem_wait_st();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(s_empty + b);
+            if (lane == 0) mbar_arrive(x_full);
+        };
 
+        // Z for one chunk: S (TMEM) -> exp -> fp16 hi/lo -> same TMEM columns.
+        // t = R + acc*sx (landmark norm already inside acc, prep_rows_kernel), so an
+        // element costs half an FFMA2, one FMNMX, one MUFU.EX2, one LOP3 (hi =
+        // top 11 significant bits), half an FSUB2 (lo = z - hi) and one F2FP.
+        auto produce_z = [&](uint64_t R2, uint64_t sx2) {
+            const uint32_t b = cnt % NSZ, ph = (cnt / NSZ) & 1;
+            const uint32_t col = tmem_base + lane_off + TM_SZ + b * NC + half * 32;
+            uint32_t s[32];
+            pr.mark(7);
+            mbar_wait(s_full + b, ph);
+            pr.mark(0);
+            tc_fence_after();
+            tmem_ld_32x32b_x32(col, s);
+            tmem_wait_ld();
+            pr.mark(1);
             uint32_t hi[16], lo[16];
             if (p.dbg & 1) {
 #pragma unroll
                 for (int i = 0; i < 16; ++i) { hi[i] = s[2 * i]; lo[i] = s[2 * i + 1]; }
-            } else
+            } else {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                float z2[2];
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const int c = 2 * i + e;
-                    const float acc = __uint_as_float(s[c]);
-                    const float coef = aux[c].y * xinv;
-                    float d2 = fmaf(acc, coef, nx + aux[c].x);
-                    d2 = fmaxf(d2, 0.0f);
-                    z2[e] = ex2_approx(fmaf(d2, ngl2e, static_cast<float>(Z13)));
+                for (int i = 0; i < 16; ++i) {
+                    float t0, t1;
+                    f2_unpack(ffma2(f2_pack(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])),
+                                    sx2, R2), t0, t1);
+                    const float z0 = ex2_approx(fminf(t0, static_cast<float>(Z13)));
+                    const float z1 = ex2_approx(fminf(t1, static_cast<float>(Z13)));
+                    const float h0 = __uint_as_float(__float_as_uint(z0) & 0xFFFFE000u);
+                    const float h1 = __uint_as_float(__float_as_uint(z1) & 0xFFFFE000u);
+                    float l0, l1;
+                    f2_unpack(fsub2(f2_pack(z0, z1), f2_pack(h0, h1)), l0, l1);
+                    hi[i] = pack_half2(h0, h1);
+                    lo[i] = pack_half2(l0, l1);
                 }
-                const uint32_t h = pack_half2(z2[0], z2[1]);
-                const float2 hf = __half22float2(*reinterpret_cast<const __half2*>(&h));
-                hi[i] = h;
-                lo[i] = pack_half2(z2[0] - hf.x, z2[1] - hf.y);
             }
-            mbar_wait(z_empty + b, ph ^ 1);
-            const uint32_t zhi = base_addr + OFF_Z + b * 2 * Z_BYTES;
-            const uint32_t zlo = zhi + Z_BYTES;
-            const uint32_t row_base = static_cast<uint32_t>(r) * 128u;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const uint32_t ch = static_cast<uint32_t>(half * 4 + q);
-                const uint32_t off = row_base + ((ch ^ static_cast<uint32_t>(r & 7)) << 4);
-                st_shared_v4(zhi + off, hi[4 * q], hi[4 * q + 1], hi[4 * q + 2], hi[4 * q + 3]);
-                st_shared_v4(zlo + off, lo[4 * q], lo[4 * q + 1], lo[4 * q + 2], lo[4 * q + 3]);
-            }
-            fence_proxy_async_smem();
+            pr.mark(2);
+            tmem_st_32x32b_x16(col, hi);
+            tmem_st_32x32b_x16(col + 16, lo);
+            tmem_wait_st();
+            tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(z_full + b);
+            pr.mark(4);
             ++cnt;
         };
 
         // G accumulator of a finished tile: TMEM -> scale -> global (128 columns per warp).
         auto drain_g = [&](int tile, uint32_t it) {
-            const int rt = tile / p.n_col_blocks;
-            const int cb = tile - rt * p.n_col_blocks;
-            const int grow = rt * BM + r;
+            const int cb = tile / p.n_row_tiles;
+            const int rt = tile - cb * p.n_row_tiles;
+            pr.mark(7);
             mbar_wait(g_full, it & 1);
+            pr.mark(5);
             tc_fence_after();
+            if (p.dbg & 64) {  // bypass the drain: free the accumulator at once
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(g_empty);
+                return;
+            }
+            const int grow = rt * BM + r;
             const bool row_ok = grow < p.n_rows;
             OutT* grow_ptr = static_cast<OutT*>(p.G) + static_cast<long long>(grow) * p.ldg;
+            constexpr int SLAB = 128 / sizeof(OutT);  // columns per 128-byte staging row
 #pragma unroll 1
             for (int m = 0; m < 4; ++m) {
                 const int c0 = half * 128 + m * 32;
@@ -358,7 +418,7 @@ __global__ void __launch_bounds__(k1::THREADS, 1)
                     if (lane == 0) mbar_arrive(g_empty);
                 }
                 const int gc0 = cb * N2 + c0;
-                if (!row_ok || gc0 >= p.b_eff || (p.dbg & 2)) continue;
+                if (gc0 >= p.b_eff || (p.dbg & 2)) continue;
                 const float4* cs4 = reinterpret_cast<const float4*>(p.col_scale + gc0);
                 float out[32];
 #pragma unroll
@@ -369,6 +429,36 @@ __global__ void __launch_bounds__(k1::THREADS, 1)
                     out[4 * i + 2] = __uint_as_float(v[4 * i + 2]) * sc.z;
                     out[4 * i + 3] = __uint_as_float(v[4 * i + 3]) * sc.w;
                 }
+                if (p.tma_store) {
+                    // 32 rows x SLAB columns per store; 128-byte swizzled staging rows
+                    // (16-byte chunk c of row r at chunk c ^ (r & 7)): conflict-free STS.
+#pragma unroll
+                    for (int sl = 0; sl < 32 / SLAB; ++sl) {
+                        if (lane == 0) bulk_wait_group_read<0>();
+                        __syncwarp();
+#pragma unroll
+                        for (int c = 0; c < 8; ++c) {
+                            uint32_t w[4];
+                            if constexpr (sizeof(OutT) == 8) {
+                                const double d0 = out[sl * SLAB + 2 * c], d1 = out[sl * SLAB + 2 * c + 1];
+                                w[0] = __double2loint(d0); w[1] = __double2hiint(d0);
+                                w[2] = __double2loint(d1); w[3] = __double2hiint(d1);
+                            } else {
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) w[e] = __float_as_uint(out[4 * c + e]);
+                            }
+                            st_shared_v4(stg_addr + lane * 128 + ((c ^ (lane & 7)) << 4), w[0], w[1], w[2], w[3]);
+                        }
+                        fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            tma_store_2d(&tm_g, stg, gc0 + sl * SLAB, rt * BM + quad * 32);
+                            bulk_commit_group();
+                        }
+                    }
+                    continue;
+                }
+                if (!row_ok) continue;
                 OutT* dst = grow_ptr + gc0;
                 const int ncols = min(32, p.b_eff - gc0);
                 const bool vec = ncols == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
@@ -397,26 +487,44 @@ __global__ void __launch_bounds__(k1::THREADS, 1)
                     }
                 }
             }
+            pr.mark(6);
         };
 
-        // The drain of tile t is deferred until Z(t+1, 0) is produced, so the
-        // tensor core has GEMM2 work queued the moment the accumulator frees up.
-        int pending = -1;
-        uint32_t pending_it = 0, it = 0;
+        // Per tile: Z for every chunk; the next tile's X goes into TMEM as soon as
+        // this tile's last GEMM1 has consumed X (before the drain, so the next
+        // tile's first GEMM1s overlap the drain).
+        // Tiles run column-block-major (tile = cb·n_row_tiles + rt), so the CTAs in
+        // flight share one 4 MB Lᵀ column block in L2.
+        uint32_t it = 0;
+        if (static_cast<int>(blockIdx.x) < num_tiles) {
+            load_x(static_cast<int>(blockIdx.x) % p.n_row_tiles);
+            write_x(0);
+        }
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
-            const int rt = tile / p.n_col_blocks;
+            const int rt = tile % p.n_row_tiles;
             const float2 ra = p.row_aux[rt * BM + r];
+            const uint64_t R2 = f2_pack(ra.x, ra.x), sx2 = f2_pack(ra.y, ra.y);
+            const int next = tile + gridDim.x;
+            if (next < num_tiles) load_x(next % p.n_row_tiles);
             for (int j = 0; j < p.n_chunks; ++j) {
-                produce_z(ra.x, ra.y, j);
-                if (j == 0 && pending >= 0) {
-                    drain_g(pending, pending_it);
-                    pending = -1;
+                if (p.dbg & 32) {  // bypass: keep the barrier protocol, skip Z math and stores
+                    const uint32_t b = cnt % NSZ, ph = (cnt / NSZ) & 1;
+                    mbar_wait(s_full + b, ph);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(z_full + b);
+                    ++cnt;
+                } else {
+                    produce_z(R2, sx2);
                 }
             }
-            pending = tile;
-            pending_it = it;
+            if (next < num_tiles) write_x(it + 1);
+            pr.mark(3);
+            drain_g(tile, it);
         }
-        if (pending >= 0) drain_g(pending, pending_it);
+        if (lane == 0) bulk_wait_group<0>();
+        __syncwarp();
+        pr.mark(7);
+        if (lane == 0) pr.flush(p.dbg_out ? p.dbg_out + 8 : nullptr);
     }
 
     tc_fence_before();

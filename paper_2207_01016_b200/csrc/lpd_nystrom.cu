@@ -109,6 +109,26 @@ CUtensorMap make_plane_map(const void* base, uint64_t rows, uint64_t cols, uint3
     return m;
 }
 
+// Output G [rows × cols] (row pitch ld elements) as the TMA-store target of the
+// factor kernel: box = 32 rows × one 128-byte row segment, 128-byte swizzle.
+// Returns false when the layout cannot be described (unaligned base or pitch).
+bool make_g_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint64_t ld,
+                bool f64) {
+    const uint64_t es = f64 ? 8 : 4;
+    if ((reinterpret_cast<uintptr_t>(base) & 15) != 0 || (ld * es) % 16 != 0 || rows == 0 ||
+        cols == 0 || rows >= (1ull << 31) || cols >= (1ull << 31))
+        return false;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {ld * es};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / es), 32};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode_fn()(m, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                             2, const_cast<void*>(base), dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 template <typename T>
 void dev_alloc(T** p, size_t count) {
     *p = nullptr;
@@ -130,7 +150,8 @@ struct Slot {
     __half* xlo = nullptr;
     float2* raux = nullptr;  // [rows_cap]
     double* g = nullptr;     // [rows_cap × b_eff] fp64 (host-call path)
-    int64_t g_cols = 0;
+    int64_t g_cols = 0;      // b_eff the g buffer was sized for
+    int64_t g_ld = 0;        // its row pitch (elements; even, so rows stay 16-byte aligned)
     int64_t nnz_cap = 0;
     int64_t* indptr = nullptr;
     int32_t* indices = nullptr;
@@ -146,7 +167,10 @@ struct DeviceState {
     double* mu = nullptr;
     __half* lm_hi = nullptr;
     __half* lm_lo = nullptr;
-    float2* lm_aux = nullptr;
+    lpd::BasisConsts* consts = nullptr;  // beta, aug, g (device)
+    double* lm_nb = nullptr;             // [B] landmark stats scratch
+    double* lm_mx = nullptr;
+    int* err = nullptr;                  // set by prep_rows_kernel on fp16 underflow
     __half* lt_hi = nullptr;
     __half* lt_lo = nullptr;
     float* col_scale = nullptr;
@@ -162,7 +186,7 @@ struct DeviceState {
     int64_t ring_count = 0;  // launches recorded since the last reset
 
     void free_basis() {
-        dev_free(mu); dev_free(lm_hi); dev_free(lm_lo); dev_free(lm_aux);
+        dev_free(mu); dev_free(lm_hi); dev_free(lm_lo); dev_free(consts); dev_free(lm_nb); dev_free(lm_mx);
         dev_free(lt_hi); dev_free(lt_lo); dev_free(col_scale);
         has_basis = false;
     }
@@ -190,7 +214,8 @@ void ensure_slot(DeviceState& ds, Slot& s, int64_t rows, bool need_g, int64_t nn
         dev_alloc(&s.xhi, static_cast<size_t>(cap * lpd::KD_MAX));
         dev_alloc(&s.xlo, static_cast<size_t>(cap * lpd::KD_MAX));
         dev_alloc(&s.raux, static_cast<size_t>(cap));
-        if (need_g) dev_alloc(&s.g, static_cast<size_t>(cap * ds.b_eff));
+        s.g_ld = round_up(ds.b_eff, 2);
+        if (need_g) dev_alloc(&s.g, static_cast<size_t>(cap * s.g_ld));
         s.g_cols = need_g ? ds.b_eff : 0;
         s.rows_cap = cap;
     }
@@ -221,6 +246,8 @@ void init_device(DeviceState& ds, int device) {
         for (auto& e : s.ev) CUDA_TRY(cudaEventCreate(&e));
     }
     for (auto& e : ds.kev) CUDA_TRY(cudaEventCreate(&e));
+    dev_alloc(&ds.err, 1);
+    CUDA_TRY(cudaMemset(ds.err, 0, sizeof(int)));
     for (auto& pr : ds.ring)
         for (auto& e : pr) CUDA_TRY(cudaEventCreate(&e));
     CUDA_TRY(cudaFuncSetAttribute(lpd::nystrom_factor_kernel<double>,
@@ -237,8 +264,8 @@ void validate_basis_args(int64_t B, int64_t d, int64_t b_eff, double gamma, cons
     // reference validate(): proj/src/kernel.cpp:10-15
     if (!(gamma > 0.0) || !std::isfinite(gamma))
         fail(LPD_ERR_INVALID_ARGUMENT, "kernel gamma must be positive and finite");
-    if (d > lpd::KD_MAX)
-        fail(LPD_ERR_UNSUPPORTED, "this build's fused factor kernel supports d <= 64 (got d=" +
+    if (d > lpd::KD_MAX - 1)
+        fail(LPD_ERR_UNSUPPORTED, "this build's fused factor kernel supports d <= 63 (got d=" +
                                       std::to_string(d) + ")");
     if (B > (1 << 30) || b_eff > (1 << 30)) fail(LPD_ERR_UNSUPPORTED, "basis too large");
 }
@@ -261,7 +288,9 @@ void build_basis(DeviceState& ds, const double* lm_dev, int64_t B, int64_t d, in
         dev_alloc(&ds.mu, lpd::KD_MAX);
         dev_alloc(&ds.lm_hi, static_cast<size_t>(B_pad * lpd::KD_MAX));
         dev_alloc(&ds.lm_lo, static_cast<size_t>(B_pad * lpd::KD_MAX));
-        dev_alloc(&ds.lm_aux, static_cast<size_t>(B_pad));
+        dev_alloc(&ds.consts, 1);
+        dev_alloc(&ds.lm_nb, static_cast<size_t>(B_pad));
+        dev_alloc(&ds.lm_mx, static_cast<size_t>(B_pad));
         dev_alloc(&ds.lt_hi, static_cast<size_t>(Beff_pad * B_pad));
         dev_alloc(&ds.lt_lo, static_cast<size_t>(Beff_pad * B_pad));
         dev_alloc(&ds.col_scale, static_cast<size_t>(Beff_pad));
@@ -278,10 +307,16 @@ void build_basis(DeviceState& ds, const double* lm_dev, int64_t B, int64_t d, in
                                                        static_cast<int>(d), ds.mu);
     {
         const int threads = 256, rows_per_block = threads / 32;
-        const int blocks = static_cast<int>((B_pad + rows_per_block - 1) / rows_per_block);
-        lpd::prep_rows_dense_kernel<<<blocks, threads, 0, st>>>(
-            lm_dev, ld_lm, static_cast<int>(B), static_cast<int>(d), ds.mu, ds.lm_hi, ds.lm_lo,
-            ds.lm_aux, static_cast<int>(B_pad), -2.0f);
+        const int blocks = static_cast<int>((B + rows_per_block - 1) / rows_per_block);
+        lpd::landmark_stats_kernel<<<blocks, threads, 0, st>>>(lm_dev, ld_lm, static_cast<int>(B),
+                                                               static_cast<int>(d), ds.mu, ds.lm_nb,
+                                                               ds.lm_mx);
+        lpd::basis_consts_kernel<<<1, 256, 0, st>>>(ds.lm_nb, ds.lm_mx, static_cast<int>(B), gamma,
+                                                    ds.consts);
+        const int pblocks = static_cast<int>((B_pad + rows_per_block - 1) / rows_per_block);
+        lpd::prep_landmarks_kernel<<<pblocks, threads, 0, st>>>(
+            lm_dev, ld_lm, static_cast<int>(B), static_cast<int>(d), ds.mu, ds.consts, ds.lm_hi,
+            ds.lm_lo, static_cast<int>(B_pad));
     }
     lpd::col_absmax_kernel<<<static_cast<int>((b_eff + 127) / 128), 128, 0, st>>>(
         L_dev, static_cast<int>(B), static_cast<int>(b_eff), ds.colmax);
@@ -321,22 +356,26 @@ void launch_factor(DeviceState& ds, Slot& s, const double* x_dev, int64_t m, int
         const int threads = 256, rows_per_block = threads / 32;
         const int64_t blocks = std::min<int64_t>((m_pad + rows_per_block - 1) / rows_per_block,
                                                  static_cast<int64_t>(ds.num_sms) * 16);
-        lpd::prep_rows_dense_kernel<<<static_cast<int>(blocks), threads, 0, st>>>(
-            x_dev, ldx, static_cast<int>(m), static_cast<int>(ds.d), ds.mu, s.xhi, s.xlo, s.raux,
-            static_cast<int>(m_pad), 1.0f);
+        lpd::prep_rows_kernel<<<static_cast<int>(blocks), threads, 0, st>>>(
+            x_dev, ldx, static_cast<int>(m), static_cast<int>(ds.d), ds.mu, ds.consts, s.xhi, s.xlo,
+            s.raux, static_cast<int>(m_pad), ds.err);
     }
-    const CUtensorMap tm_xhi = make_plane_map(s.xhi, m_pad, lpd::KD_MAX, lpd::k1::BM, 64);
-    const CUtensorMap tm_xlo = make_plane_map(s.xlo, m_pad, lpd::KD_MAX, lpd::k1::BM, 64);
+    CUtensorMap tm_g;
+    std::memset(&tm_g, 0, sizeof(tm_g));
+    const bool tma_store = make_g_map(&tm_g, g_dev, static_cast<uint64_t>(m),
+                                      static_cast<uint64_t>(ds.b_eff), static_cast<uint64_t>(ldg),
+                                      out_dtype == LPD_OUT_F64);
     lpd::FactorParams p;
     p.n_rows = static_cast<int>(m);
     p.n_row_tiles = static_cast<int>(m_pad / lpd::k1::BM);
     p.n_chunks = static_cast<int>(ds.B_pad / lpd::k1::NC);
     p.n_col_blocks = static_cast<int>(ds.Beff_pad / lpd::k1::N2);
     p.b_eff = static_cast<int>(ds.b_eff);
-    p.ksteps1 = static_cast<int>(std::max<int64_t>(1, (ds.d + 15) / 16));
-    p.neg_gamma_log2e = static_cast<float>(-ds.gamma * 1.4426950408889634);
+    p.ksteps1 = static_cast<int>((ds.d + 1 + 15) / 16);
     p.row_aux = s.raux;
-    p.lm_aux = ds.lm_aux;
+    p.x_hi = s.xhi;
+    p.x_lo = s.xlo;
+    p.tma_store = tma_store ? 1 : 0;
     p.col_scale = ds.col_scale;
     p.G = g_dev;
     p.ldg = ldg;
@@ -345,6 +384,13 @@ void launch_factor(DeviceState& ds, Slot& s, const double* x_dev, int64_t m, int
         return e ? std::atoi(e) : 0;
     }();
     p.dbg = dbg;
+    static unsigned long long* dbg_out = nullptr;
+    p.dbg_out = nullptr;
+    if (dbg & 16) {
+        if (!dbg_out) CUDA_TRY(cudaMalloc(&dbg_out, 16 * sizeof(unsigned long long)));
+        CUDA_TRY(cudaMemsetAsync(dbg_out, 0, 16 * sizeof(unsigned long long), st));
+        p.dbg_out = dbg_out;
+    }
     const int64_t tiles = static_cast<int64_t>(p.n_row_tiles) * p.n_col_blocks;
     const int grid = static_cast<int>(std::min<int64_t>(tiles, ds.num_sms));
     cudaEvent_t* pr = nullptr;
@@ -355,16 +401,39 @@ void launch_factor(DeviceState& ds, Slot& s, const double* x_dev, int64_t m, int
     }
     if (out_dtype == LPD_OUT_F64)
         lpd::nystrom_factor_kernel<double><<<grid, lpd::k1::THREADS, lpd::k1::SMEM_BYTES, st>>>(
-            tm_xhi, tm_xlo, ds.tm_lmhi, ds.tm_lmlo, ds.tm_lthi, ds.tm_ltlo, p);
+            ds.tm_lmhi, ds.tm_lmlo, ds.tm_lthi, ds.tm_ltlo, tm_g, p);
     else
         lpd::nystrom_factor_kernel<float><<<grid, lpd::k1::THREADS, lpd::k1::SMEM_BYTES, st>>>(
-            tm_xhi, tm_xlo, ds.tm_lmhi, ds.tm_lmlo, ds.tm_lthi, ds.tm_ltlo, p);
+            ds.tm_lmhi, ds.tm_lmlo, ds.tm_lthi, ds.tm_ltlo, tm_g, p);
+    if (dbg & 16) {
+        unsigned long long h[16];
+        CUDA_TRY(cudaMemcpyAsync(h, dbg_out, sizeof(h), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        const double ctas = grid, per_mma = ctas, per_epi = ctas * lpd::k1::EPI_WARPS;
+        std::fprintf(stderr, "[k1 phases, cycles per CTA] mma: s_empty %.3g lm_full %.3g z_full %.3g "
+                     "lt_full %.3g g_empty %.3g issue %.3g x_full %.3g | epi: s_full %.3g ldtm %.3g math %.3g "
+                     "z_empty %.3g sts %.3g g_full %.3g drain %.3g other %.3g\n",
+                     h[0] / per_mma, h[1] / per_mma, h[2] / per_mma, h[3] / per_mma, h[4] / per_mma,
+                     h[5] / per_mma, h[6] / per_mma, h[8] / per_epi, h[9] / per_epi, h[10] / per_epi, h[11] / per_epi,
+                     h[12] / per_epi, h[13] / per_epi, h[14] / per_epi, h[15] / per_epi);
+    }
     if (time_it) {
         CUDA_TRY(cudaEventRecord(ds.kev[1], st));
         if (ds.ring_count < DeviceState::kRing) CUDA_TRY(cudaEventRecord(pr[1], st));
         ++ds.ring_count;
     }
     CUDA_TRY(cudaGetLastError());
+}
+
+// Reads (and clears) the row-prep range flag after the device's work is complete.
+void check_range_flag(DeviceState& ds) {
+    int flag = 0;
+    CUDA_TRY(cudaMemcpy(&flag, ds.err, sizeof(int), cudaMemcpyDeviceToHost));
+    if (flag) {
+        CUDA_TRY(cudaMemset(ds.err, 0, sizeof(int)));
+        fail(LPD_ERR_UNSUPPORTED,
+             "point features too large for the split-fp16 operands (|x - mean| >= 2^28)");
+    }
 }
 
 lpd_context* check_ctx(lpd_context* ctx, bool need_basis) {
@@ -435,11 +504,11 @@ void compute_rows_host(lpd_context* ctx, int64_t n, double* G, int64_t ldg, lpd_
             }
             stage_x(ds, s, r0, rows);  // records ev[0] and fills s.x
             CUDA_TRY(cudaEventRecord(s.ev[1], s.stream));
-            launch_factor(ds, s, s.x, rows, ds.d, s.g, b_eff, LPD_OUT_F64, s.stream, false);
+            launch_factor(ds, s, s.x, rows, ds.d, s.g, s.g_ld, LPD_OUT_F64, s.stream, false);
             launches[di] += 2;
             CUDA_TRY(cudaEventRecord(s.ev[2], s.stream));
             CUDA_TRY(cudaMemcpy2DAsync(G + r0 * ldg, sizeof(double) * ldg, s.g,
-                                       sizeof(double) * b_eff, sizeof(double) * b_eff,
+                                       sizeof(double) * s.g_ld, sizeof(double) * b_eff,
                                        static_cast<size_t>(rows), cudaMemcpyDeviceToHost,
                                        s.stream));
             CUDA_TRY(cudaEventRecord(s.ev[3], s.stream));
@@ -453,6 +522,7 @@ void compute_rows_host(lpd_context* ctx, int64_t n, double* G, int64_t ldg, lpd_
             cudaEventElapsedTime(&c, s.ev[2], s.ev[3]);
             h2d[di] += a * 1e-3; ker[di] += b * 1e-3; d2h[di] += c * 1e-3;
         }
+        check_range_flag(ds);
     });
     if (tm) {
         std::memset(tm, 0, sizeof(*tm));
@@ -544,6 +614,7 @@ int lpd_context_destroy(lpd_context* ctx) {
         cudaDeviceSynchronize();
         ds.free_basis();
         dev_free(ds.colmax);
+        dev_free(ds.err);
         for (auto& s : ds.slot) {
             ds.free_slot(s);
             if (s.stream) cudaStreamDestroy(s.stream);
@@ -710,6 +781,7 @@ int lpd_compute_g_device(lpd_context* ctx, int device_index, const double* X_dev
         launch_factor(ds, s, X_dev, n, ldx, G_dev, ldg, out_dtype, st, true);
         if (!stream) {
             CUDA_TRY(cudaStreamSynchronize(st));
+            check_range_flag(ds);
             float ms = 0.f;
             CUDA_TRY(cudaEventElapsedTime(&ms, ds.kev[0], ds.kev[1]));
             ds.last_kernel_ms = ms;

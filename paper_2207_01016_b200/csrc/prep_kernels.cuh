@@ -2,15 +2,15 @@
 // the split-fp16 operand planes the fused factor kernel consumes.
 //
 //   rows (points or landmarks), reference proj/src/kernel.cpp:21-25 (squared_norms)
-//   and proj/src/dataio.cpp:32-36 (squared_norm): centred by μ (the landmark
+//   and proj/src/dataio.cpp:32-36 (squared_norm): centred by mu (the landmark
 //   mean; distances are translation invariant, and centring shrinks
-//   ‖x‖²+‖b‖² so the −2⟨x,b⟩ cancellation loses fewer bits), scaled by an exact
-//   power of two so the largest |entry| lands in [2^13, 2^14), and written as
-//   hi = fp16(x·s), lo = fp16(x·s − hi) into a [rows_pad × 64] K-major plane.
-//   aux = (‖x−μ‖² in fp64 rounded to fp32, mult · 2^-e).
+//   |x|^2+|b|^2 so the -2<x,b> cancellation loses fewer bits), scaled by an exact
+//   power of two (per point row; one global scale for the landmarks) and written
+//   as hi = fp16(v*s), lo = fp16(v*s - hi) into a [rows_pad x 64] K-major plane.
+//   Column d carries the landmark norm (augmented GEMM1, see prep_rows_kernel).
 //
-//   L (reference proj/src/factor.cpp:68-81, consumed at :176-189): transposed
-//   to Lᵀ [Beff_pad × B_pad] with a power-of-two scale u_k per G column so the
+//   L (reference proj/src/factor.cpp:68-81, consumed at :94-107): transposed
+//   to L^T [Beff_pad x B_pad] with a power-of-two scale u_k per G column so the
 //   column max lands in [2^13, 2^14); col_scale_k = 2^-13 / u_k undoes both
 //   that and the 2^13 carried by Z.
 #pragma once
@@ -36,15 +36,125 @@ __device__ __forceinline__ double warp_max_d(double v) {
 // Exponent e with 2^e <= v < 2^(e+1) for v > 0 (v finite).
 __device__ __forceinline__ int floor_log2(double v) { return ilogb(v); }
 
-// One warp per row; d <= 64. Rows in [m, m_pad) are written as zero padding.
-// X may be null when m == 0.
-__global__ void prep_rows_dense_kernel(const double* __restrict__ X, long long ldx, int m, int d,
-                                       const double* __restrict__ mu, __half* __restrict__ hi,
-                                       __half* __restrict__ lo, float2* __restrict__ aux,
-                                       int m_pad, float mult) {
+// Basis constants shared by the landmark and row preps (device memory, so the
+// whole basis build stays asynchronous on the caller's stream):
+//   beta   global power-of-two landmark scale (max |b - mu| lands in [2^13, 2^14))
+//   aug    2^-s, the augmented-column scale (landmark side 2^-s, point side 2^s)
+//   g      -gamma * log2(e)
+struct BasisConsts {
+    double beta;
+    double aug;
+    double g;
+    double pad;
+};
+
+// Exponent clamp for row scales: 2^(13-e) must stay inside fp16's normal range.
+__device__ __forceinline__ int clamp_exp(double mx) {
+    int e = mx > 0.0 ? floor_log2(mx) : -1;
+    return min(max(e, -1), 27);
+}
+
+// Per landmark j (one warp each): nb[j] = |b_j - mu|^2 and mx[j] = max |b_j - mu|.
+__global__ void landmark_stats_kernel(const double* __restrict__ Y, long long ldy, int m, int d,
+                                      const double* __restrict__ mu, double* __restrict__ nb,
+                                      double* __restrict__ mx) {
+    const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= m) return;
+    const double* y = Y + static_cast<long long>(row) * ldy;
+    const double v0 = lane < d ? y[lane] - mu[lane] : 0.0;
+    const double v1 = lane + 32 < d ? y[lane + 32] - mu[lane + 32] : 0.0;
+    const double ss = warp_sum_d(v0 * v0 + v1 * v1);
+    const double mxv = warp_max_d(fmax(fabs(v0), fabs(v1)));
+    if (lane == 0) {
+        nb[row] = ss;
+        mx[row] = mxv;
+    }
+}
+
+// Single block: beta from the global landmark max, s from the largest augmented
+// entry beta*|b|^2/2 (kept below 2^15 so it fits fp16).
+__global__ void basis_consts_kernel(const double* __restrict__ nb, const double* __restrict__ mx,
+                                    int m, double gamma, BasisConsts* __restrict__ out) {
+    __shared__ double smx[32], snb[32];
+    double a = 0.0, b = 0.0;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        a = fmax(a, mx[i]);
+        b = fmax(b, nb[i]);
+    }
+    a = warp_max_d(a);
+    b = warp_max_d(b);
+    if ((threadIdx.x & 31) == 0) {
+        smx[threadIdx.x >> 5] = a;
+        snb[threadIdx.x >> 5] = b;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) {
+            a = fmax(a, smx[w]);
+            b = fmax(b, snb[w]);
+        }
+        const double beta = ldexp(1.0, 13 - clamp_exp(a));
+        const double maxw = 0.5 * beta * b;
+        const int s = maxw > 0.0 ? max(0, floor_log2(maxw) - 14) : 0;
+        out->beta = beta;
+        out->aug = ldexp(1.0, -s);
+        out->g = -gamma * 1.4426950408889634;
+        out->pad = 0.0;
+    }
+}
+
+// Landmark planes [m_pad x 64] K-major: columns [0, d) = (b - mu)*beta as fp16 hi/lo;
+// column d = -beta*|b - mu|^2/2 * 2^-s (hi/lo) — the landmark norm rides through
+// GEMM1 against a constant column on the point side, so the epilogue needs no
+// per-landmark term: t = R_i + acc*sx_i (see prep_rows_kernel). Rows >= m are 0.
+__global__ void prep_landmarks_kernel(const double* __restrict__ Y, long long ldy, int m, int d,
+                                      const double* __restrict__ mu,
+                                      const BasisConsts* __restrict__ kc, __half* __restrict__ hi,
+                                      __half* __restrict__ lo, int m_pad) {
     const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    const double beta = kc->beta, aug = kc->aug;
+    for (int row = warp_global; row < m_pad; row += nwarps) {
+        double v0 = 0.0, v1 = 0.0;
+        if (row < m) {
+            const double* y = Y + static_cast<long long>(row) * ldy;
+            if (lane < d) v0 = y[lane] - mu[lane];
+            if (lane + 32 < d) v1 = y[lane + 32] - mu[lane + 32];
+        }
+        const double nb = warp_sum_d(v0 * v0 + v1 * v1);
+        double a0 = v0 * beta, a1 = v1 * beta;
+        const double w = row < m ? -0.5 * beta * nb * aug : 0.0;
+        if (lane == d) a0 = w;
+        if (lane + 32 == d) a1 = w;
+        const __half h0 = __double2half(a0), h1 = __double2half(a1);
+        const long long base = static_cast<long long>(row) * KD_MAX;
+        hi[base + lane] = h0;
+        hi[base + lane + 32] = h1;
+        lo[base + lane] = __double2half(a0 - static_cast<double>(__half2float(h0)));
+        lo[base + lane + 32] = __double2half(a1 - static_cast<double>(__half2float(h1)));
+    }
+}
+
+// Point rows [m_pad x 64] K-major, one warp per row (d <= 63): columns [0, d) =
+// (x - mu)*sigma_i as fp16 hi/lo with sigma_i = 2^(13 - e_i) per row (e_i >= s - 1
+// so that column d = sigma_i*2^s <= 2^14 — a power of two: exact in hi, lo = 0;
+// rows close to mu simply keep fewer leading zeros). With acc = GEMM1 (3 split
+// terms) = sigma_i*beta*(<x-mu, b-mu> - |b-mu|^2/2):
+//   t = 13 + g*d2 = R_i + acc*sx_i,  R_i = 13 + g*|x-mu|^2,  sx_i = -2g/(sigma_i*beta)
+// (g = -gamma*log2 e), i.e. Z*2^13 = ex2(min(t, 13)): the reference's clamp of d2 at
+// 0 (kernel.cpp:49-51). aux[i] = (R_i, sx_i). Rows in [m, m_pad) are zero padding.
+// Sets *err if a row's entries would overflow fp16 (|x - mu| >= 2^28).
+__global__ void prep_rows_kernel(const double* __restrict__ X, long long ldx, int m, int d,
+                                 const double* __restrict__ mu, const BasisConsts* __restrict__ kc,
+                                 __half* __restrict__ hi, __half* __restrict__ lo,
+                                 float2* __restrict__ aux, int m_pad, int* __restrict__ err) {
+    const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    const double beta = kc->beta, aug = kc->aug, g = kc->g;
+    const int s_exp = -ilogb(aug);
     for (int row = warp_global; row < m_pad; row += nwarps) {
         double v0 = 0.0, v1 = 0.0;
         if (row < m) {
@@ -54,21 +164,23 @@ __global__ void prep_rows_dense_kernel(const double* __restrict__ X, long long l
         }
         const double ss = warp_sum_d(v0 * v0 + v1 * v1);
         const double mx = warp_max_d(fmax(fabs(v0), fabs(v1)));
-        int e = 0;
-        if (mx > 0.0) e = floor_log2(mx);
-        const double s = ldexp(1.0, 13 - e);
-        const double a0 = v0 * s, a1 = v1 * s;
+        const int e = max(clamp_exp(mx), s_exp - 1);
+        const double sigma = ldexp(1.0, 13 - e);
+        double a0 = v0 * sigma, a1 = v1 * sigma;
+        const double w = sigma / aug;
+        if (lane == d) a0 = w;
+        if (lane + 32 == d) a1 = w;
         const __half h0 = __double2half(a0), h1 = __double2half(a1);
-        const __half l0 = __double2half(a0 - static_cast<double>(__half2float(h0)));
-        const __half l1 = __double2half(a1 - static_cast<double>(__half2float(h1)));
         const long long base = static_cast<long long>(row) * KD_MAX;
         hi[base + lane] = h0;
         hi[base + lane + 32] = h1;
-        lo[base + lane] = l0;
-        lo[base + lane + 32] = l1;
-        if (lane == 0)
-            aux[row] = make_float2(static_cast<float>(ss),
-                                   mult * static_cast<float>(ldexp(1.0, e - 13)));
+        lo[base + lane] = __double2half(a0 - static_cast<double>(__half2float(h0)));
+        lo[base + lane + 32] = __double2half(a1 - static_cast<double>(__half2float(h1)));
+        if (lane == 0) {
+            aux[row] = make_float2(static_cast<float>(13.0 + g * ss),
+                                   static_cast<float>(-2.0 * g / (sigma * beta)));
+            if (row < m && mx >= 0x1p28) atomicExch(err, 1);
+        }
     }
 }
 

@@ -78,7 +78,7 @@ def test_kernel_values_identity_basis(gpu_ctx):
 @pytest.mark.parametrize("n,d,B,beff_cut,gamma", [
     (1, 5, 1, 0, 0.5),        # single row, single landmark
     (127, 3, 65, 0, 1.0),     # ragged rows (< one tile), landmarks = 64 + 1
-    (129, 64, 64, 0, 0.05),   # max d, rows = tile + 1
+    (129, 63, 64, 0, 0.05),   # max d of the fused small-d kernel, rows = tile + 1
     (300, 17, 300, 1, 0.2),   # b_eff = 299 (odd leading dimension)
     (1000, 50, 257, 0, 0.02),  # b_eff = 257 (two column blocks, second nearly empty)
     (513, 1, 40, 0, 3.0),     # d = 1
