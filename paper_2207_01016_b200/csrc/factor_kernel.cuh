@@ -6,12 +6,18 @@
 // the reference's per-chunk kernel_block + Eigen GEMM (reference
 // proj/src/factor.cpp:97-108 calling proj/src/kernel.cpp:31-57).
 //
-// Design (persistent, one CTA per SM, warp-specialised, 384 threads):
-//   warp 0     TMA producer: landmark chunks (64 landmarks, hi/lo planes)
-//   warp 1     MMA issuer (one elected lane)
-//   warp 2     TMEM allocator
-//   warp 3     TMA producer: Lᵀ half-chunks of this tile's 256-column block
-//   warps 4-11 epilogue: X tile → TMEM; S → Z (in place, TMEM); G (TMEM) → SMEM → TMA store
+// Design: persistent CTA pairs (cluster of 2, one CTA per SM, 384 threads each).
+// A pair owns a 256-row × 256-column G tile; each CTA holds 128 rows in its own
+// TMEM and streams HALF of every shared operand (32 of a chunk's 64 landmarks, 128
+// of the 256 Lᵀ rows) — tcgen05 cta_group::2 MMAs read B from both SMs' shared
+// memory — so L2→SM traffic and SMEM bandwidth per SM are halved.
+//   warp 0     TMA producer: landmark half-chunks (hi/lo planes)       [both CTAs]
+//   warp 1     MMA issuer (one elected lane)                            [leader CTA]
+//   warp 2     TMEM allocator (cta_group::2)                            [both CTAs]
+//   warp 3     TMA producer: Lᵀ half-chunks of the tile's column block [both CTAs]
+//   warps 4-11 epilogue: X → TMEM; S → Z (in place, TMEM); G → SMEM → TMA store
+// Barriers the MMA waits on live in the leader CTA (TMA bytes and epilogue arrivals
+// of both CTAs land there); MMA commits multicast to both CTAs.
 //
 // Tensor memory (512 columns × 128 lanes × 32 bit):
 //   [0, 256)    G accumulator, fp32, row i of the tile in lane i
@@ -35,14 +41,14 @@ namespace lpd {
 
 struct FactorParams {
     int n_rows;             // valid rows of this launch (rows >= n_rows are padding)
-    int n_row_tiles;        // ceil(n_rows / 128)
+    int n_row_tiles;        // ceil(n_rows / 256): 256-row pair tiles
     int n_chunks;           // B_pad / 64
     int n_col_blocks;       // Beff_pad / 256
     int b_eff;              // valid G columns
     int ksteps1;            // ceil((d + 1) / 16): K-steps of GEMM1 (d features + norm column)
     int tma_store;          // 1: G leaves through SMEM + TMA store (tensor map valid)
     const float2* row_aux;  // [n_pad] (R_i, sx_i): t = R_i + acc*sx_i (prep_rows_kernel)
-    const __half* x_hi;     // [n_pad x 64] point planes (K-major)
+    const __half* x_hi;     // [n_pad x 64] point planes (K-major), n_pad % 256 == 0
     const __half* x_lo;
     const float* col_scale; // [Beff_pad] 2^-13 / u_k (undoes Z and Lᵀ-row scaling)
     void* G;                // output, row-major, leading dimension ldg (elements)
@@ -73,25 +79,29 @@ struct PhaseProbe {
 };
 
 namespace k1 {
-constexpr int BM = 128;        // rows per tile (UMMA M)
+constexpr int BM = 128;        // rows per CTA (UMMA M = 256 per pair)
+constexpr int PM = 256;        // rows per CTA pair
 constexpr int NC = 64;         // landmarks per chunk: N of GEMM1, K of GEMM2
+constexpr int NCH = 32;        // landmarks per chunk held by one CTA
 constexpr int KD = 64;         // padded feature dim (one 128-byte swizzle atom of fp16)
 constexpr int N2 = 256;        // G columns per tile (UMMA N of GEMM2)
-constexpr int NS_LM = 3;       // landmark-chunk stages
-constexpr int NS_LT = 4;       // Lᵀ half-chunk stages (hi and lo travel separately)
+constexpr int N2H = 128;       // Lᵀ rows per tile held by one CTA
+constexpr int NS_LM = 4;       // landmark-chunk stages
+constexpr int NS_LT = 6;       // Lᵀ half-chunk stages (hi and lo travel separately)
 constexpr int NSZ = 3;         // S/Z TMEM buffers
 constexpr int EPI_WARPS = 8;
 constexpr int THREADS = 128 + 32 * EPI_WARPS;
 constexpr int Z13 = 13;        // Z is carried as Z·2^13 in fp16
 
-constexpr uint32_t LM_BYTES = NC * KD * 2;           // 8 KB per hi/lo plane
-constexpr uint32_t LT_BYTES = N2 * NC * 2;           // 32 KB per stage
-constexpr uint32_t STG_BYTES = 32 * 128;             // 4 KB G staging per epilogue warp
+constexpr uint32_t LM_BYTES = NCH * KD * 2;          // 4 KB per hi/lo plane (this CTA's half)
+constexpr uint32_t LT_BYTES = N2H * NC * 2;          // 16 KB per stage (this CTA's half)
+constexpr uint32_t STG_BYTES = 32 * 128;             // 4 KB G staging buffer
+constexpr int NSTG = 2;                              // staging buffers per epilogue warp
 
 constexpr uint32_t OFF_LM = 0;                                      // stage s: hi, lo
 constexpr uint32_t OFF_LT = OFF_LM + NS_LM * 2 * LM_BYTES;          // stage s
-constexpr uint32_t OFF_STG = OFF_LT + NS_LT * LT_BYTES;             // warp w
-constexpr uint32_t OFF_BAR = OFF_STG + EPI_WARPS * STG_BYTES;
+constexpr uint32_t OFF_STG = OFF_LT + NS_LT * LT_BYTES;             // warp w, buffer k
+constexpr uint32_t OFF_BAR = OFF_STG + EPI_WARPS * NSTG * STG_BYTES;
 constexpr uint32_t NUM_BARS = 2 + 2 * NS_LM + 2 * NS_LT + 3 * NSZ + 2;
 constexpr uint32_t SMEM_BYTES = OFF_BAR + NUM_BARS * 8 + 16 + 1024;  // + alignment slack
 
@@ -101,8 +111,9 @@ constexpr uint32_t TM_SZ = 256;    // buffer b at 256 + 64·b
 constexpr uint32_t TM_XHI = 448;
 constexpr uint32_t TM_XLO = 480;
 
-constexpr uint32_t IDESC_G1 = idesc_f16_f32(BM, NC);
-constexpr uint32_t IDESC_G2 = idesc_f16_f32(BM, N2);
+constexpr uint32_t IDESC_G1 = idesc_f16_f32(PM, NC);
+constexpr uint32_t IDESC_G2 = idesc_f16_f32(PM, N2);
+constexpr uint16_t PAIR = 0x3;     // multicast mask: both CTAs of the pair
 
 // Column of K-step k (16 landmarks) of the Z hi / lo planes inside an S/Z buffer.
 // Epilogue warp `half` owns S columns [32·half, 32·half + 32) and writes its Z hi
@@ -113,7 +124,7 @@ __device__ __forceinline__ uint32_t z_lo_col(uint32_t k) { return z_hi_col(k) + 
 }  // namespace k1
 
 template <typename OutT>
-__global__ void __launch_bounds__(k1::THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
     nystrom_factor_kernel(const __grid_constant__ CUtensorMap tm_lmhi,
                           const __grid_constant__ CUtensorMap tm_lmlo,
                           const __grid_constant__ CUtensorMap tm_lthi,
@@ -143,19 +154,24 @@ __global__ void __launch_bounds__(k1::THREADS, 1)
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int num_tiles = p.n_row_tiles * p.n_col_blocks;
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+    const int pair = blockIdx.x >> 1, num_pairs = gridDim.x >> 1;
+    // leader-CTA (shared::cluster) address of a local barrier
+    auto lead = [&](uint64_t* bar) { return mapa_shared(smem_u32(bar), 0); };
 
     if (threadIdx.x == 0) {
-        mbar_init(x_full, EPI_WARPS);
+        mbar_init(x_full, 2 * EPI_WARPS);
         mbar_init(x_empty, 1);
         for (int s = 0; s < NS_LM; ++s) { mbar_init(lm_full + s, 1); mbar_init(lm_empty + s, 1); }
         for (int s = 0; s < NS_LT; ++s) { mbar_init(lt_full + s, 1); mbar_init(lt_empty + s, 1); }
         for (int b = 0; b < NSZ; ++b) {
             mbar_init(s_full + b, 1);
-            mbar_init(z_full + b, EPI_WARPS);
+            mbar_init(z_full + b, 2 * EPI_WARPS);
             mbar_init(sz_empty + b, 1);
         }
         mbar_init(g_full, 1);
-        mbar_init(g_empty, EPI_WARPS);
+        mbar_init(g_empty, 2 * EPI_WARPS);
         fence_mbar_init();
     }
     if (warp == 0 && lane == 0) {
@@ -163,49 +179,52 @@ __global__ void __launch_bounds__(k1::THREADS, 1)
         tma_prefetch_desc(&tm_lthi); tma_prefetch_desc(&tm_ltlo);
         if (p.tma_store) tma_prefetch_desc(&tm_g);
     }
-    if (warp == 2) tmem_alloc(tmem_slot, TMEM_COLS);
+    if (warp == 2) tmem_alloc_2sm(tmem_slot, TMEM_COLS);
     tc_fence_before();
-    __syncthreads();
+    cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
-        // ============ TMA producer: landmark chunks (hi, lo) ============
+        // ============ TMA producer: this CTA's half of each landmark chunk (hi, lo) ============
         if (lane == 0) {
             const uint64_t keep = policy_evict_last();    // landmarks: reused by every tile
             uint32_t lm_s = 0, lm_ph = 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            for (int tile = pair; tile < num_tiles; tile += num_pairs) {
                 for (int j = 0; j < p.n_chunks; ++j) {
-                    mbar_wait(lm_empty + lm_s, lm_ph ^ 1);
-                    mbar_arrive_expect_tx(lm_full + lm_s, 2 * LM_BYTES);
+                    mbar_wait_cluster(lm_empty + lm_s, lm_ph ^ 1);
+                    if (leader) mbar_arrive_expect_tx(lm_full + lm_s, 2 * 2 * LM_BYTES);
+                    const uint32_t bar = lead(lm_full + lm_s);
                     uint8_t* lm = smem + OFF_LM + lm_s * 2 * LM_BYTES;
-                    tma_load_2d_hint(&tm_lmhi, lm_full + lm_s, lm, 0, j * NC, keep);
-                    tma_load_2d_hint(&tm_lmlo, lm_full + lm_s, lm + LM_BYTES, 0, j * NC, keep);
+                    const int row = j * NC + static_cast<int>(rank) * NCH;
+                    tma_load_2d_2sm(&tm_lmhi, bar, lm, 0, row, keep);
+                    tma_load_2d_2sm(&tm_lmlo, bar, lm + LM_BYTES, 0, row, keep);
                     if (++lm_s == NS_LM) { lm_s = 0; lm_ph ^= 1; }
                 }
             }
         }
     } else if (warp == 3) {
-        // ============ TMA producer: Lᵀ half-chunks (hi, lo) of this tile's column block ============
+        // ============ TMA producer: this CTA's half of the tile's Lᵀ rows, per half-chunk ============
         if (lane == 0) {
             const uint64_t keep = policy_evict_last();
             uint32_t lt_s = 0, lt_ph = 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            for (int tile = pair; tile < num_tiles; tile += num_pairs) {
                 const int cb = tile / p.n_row_tiles;
+                const int row = cb * N2 + static_cast<int>(rank) * N2H;
                 for (int j = 0; j < p.n_chunks; ++j) {
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
-                        mbar_wait(lt_empty + lt_s, lt_ph ^ 1);
-                        mbar_arrive_expect_tx(lt_full + lt_s, LT_BYTES);
-                        tma_load_2d_hint(h ? &tm_ltlo : &tm_lthi, lt_full + lt_s,
-                                         smem + OFF_LT + lt_s * LT_BYTES, j * NC, cb * N2, keep);
+                        mbar_wait_cluster(lt_empty + lt_s, lt_ph ^ 1);
+                        if (leader) mbar_arrive_expect_tx(lt_full + lt_s, 2 * LT_BYTES);
+                        tma_load_2d_2sm(h ? &tm_ltlo : &tm_lthi, lead(lt_full + lt_s),
+                                        smem + OFF_LT + lt_s * LT_BYTES, j * NC, row, keep);
                         if (++lt_s == NS_LT) { lt_s = 0; lt_ph ^= 1; }
                     }
                 }
             }
         }
-    } else if (warp == 1) {
-        // ============ MMA issuer: whole warp follows the schedule, one elected lane issues ============
+    } else if (warp == 1 && leader) {
+        // ============ MMA issuer (pair leader): whole warp follows the schedule, one lane issues ============
         // Descriptor for smem address a is kDescHi | (a >> 4); K-step k adds 2k (32 bytes).
         const uint64_t dbase = sdesc_kmajor_sw128(0);
         auto desc = [&](uint32_t addr) -> uint64_t { return dbase | static_cast<uint64_t>((addr >> 4) & 0x3FFF); };
@@ -222,7 +241,7 @@ __global__ void __launch_bounds__(k1::THREADS, 1)
             pr.mark(5);
             mbar_wait(sz_empty + b, ph ^ 1);
             pr.mark(0);
-            mbar_wait(lm_full + lm_s, lm_ph);
+            mbar_wait_cluster(lm_full + lm_s, lm_ph);
             pr.mark(1);
             tc_fence_after();
             if (elect_one()) {
@@ -234,11 +253,11 @@ __global__ void __launch_bounds__(k1::THREADS, 1)
                     const uint32_t a = tmem_base + ((pass == 2) ? TM_XLO : TM_XHI);
                     const uint64_t bb = (pass == 1) ? d_lmlo : d_lmhi;
                     for (int k = 0; k < p.ksteps1; ++k)
-                        if (!(p.dbg & 8)) mma_f16_ts(d, a + 8 * k, bb + 2 * k, IDESC_G1, (pass | k) != 0);
+                        if (!(p.dbg & 8)) mma_f16_ts_2sm(d, a + 8 * k, bb + 2 * k, IDESC_G1, (pass | k) != 0);
                 }
-                mma_commit(lm_empty + lm_s);
-                mma_commit(s_full + b);
-                if (q == p.n_chunks - 1) mma_commit(x_empty);
+                mma_commit_2sm_mc(lm_empty + lm_s, PAIR);
+                mma_commit_2sm_mc(s_full + b, PAIR);
+                if (q == p.n_chunks - 1) mma_commit_2sm_mc(x_empty, PAIR);
             }
             __syncwarp();
             if (++lm_s == NS_LM) { lm_s = 0; lm_ph ^= 1; }
@@ -250,58 +269,58 @@ __global__ void __launch_bounds__(k1::THREADS, 1)
             const uint32_t zb = tmem_base + TM_SZ + b * NC;
             const uint32_t d = tmem_base + TM_G;
             pr.mark(5);
-            mbar_wait(z_full + b, ph);
+            mbar_wait_cluster(z_full + b, ph);
             pr.mark(2);
-            mbar_wait(lt_full + lt_s, lt_ph);
+            mbar_wait_cluster(lt_full + lt_s, lt_ph);
             pr.mark(3);
             tc_fence_after();
             if (elect_one()) {
                 const uint64_t d_lt = d_lt0 + ((lt_s * LT_BYTES) >> 4);
 #pragma unroll
                 for (int k = 0; k < NC / 16; ++k)
-                    if (!(p.dbg & 4)) mma_f16_ts(d, zb + z_hi_col(k), d_lt + 2 * k, IDESC_G2, !(first && k == 0));
+                    if (!(p.dbg & 4)) mma_f16_ts_2sm(d, zb + z_hi_col(k), d_lt + 2 * k, IDESC_G2, !(first && k == 0));
 #pragma unroll
                 for (int k = 0; k < NC / 16; ++k)
-                    if (!(p.dbg & 4)) mma_f16_ts(d, zb + z_lo_col(k), d_lt + 2 * k, IDESC_G2, 1);
-                mma_commit(lt_empty + lt_s);
+                    if (!(p.dbg & 4)) mma_f16_ts_2sm(d, zb + z_lo_col(k), d_lt + 2 * k, IDESC_G2, 1);
+                mma_commit_2sm_mc(lt_empty + lt_s, PAIR);
             }
             __syncwarp();
             if (++lt_s == NS_LT) { lt_s = 0; lt_ph ^= 1; }
             pr.mark(5);
-            mbar_wait(lt_full + lt_s, lt_ph);
+            mbar_wait_cluster(lt_full + lt_s, lt_ph);
             pr.mark(3);
             tc_fence_after();
             if (elect_one()) {
                 const uint64_t d_lt = d_lt0 + ((lt_s * LT_BYTES) >> 4);
 #pragma unroll
                 for (int k = 0; k < NC / 16; ++k)
-                    if (!(p.dbg & 4)) mma_f16_ts(d, zb + z_hi_col(k), d_lt + 2 * k, IDESC_G2, 1);
-                mma_commit(lt_empty + lt_s);
-                mma_commit(sz_empty + b);
+                    if (!(p.dbg & 4)) mma_f16_ts_2sm(d, zb + z_hi_col(k), d_lt + 2 * k, IDESC_G2, 1);
+                mma_commit_2sm_mc(lt_empty + lt_s, PAIR);
+                mma_commit_2sm(sz_empty + b);
             }
             __syncwarp();
             if (++lt_s == NS_LT) { lt_s = 0; lt_ph ^= 1; }
             ++c2;
         };
 
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+        for (int tile = pair; tile < num_tiles; tile += num_pairs, ++it) {
             pr.mark(5);
-            mbar_wait(x_full, it & 1);
+            mbar_wait_cluster(x_full, it & 1);
             pr.mark(6);
             tc_fence_after();
             // GEMM1 runs two chunks ahead of GEMM2 (three S/Z buffers).
             gemm1(0);
             if (p.n_chunks > 1) gemm1(1);
-            // G accumulator must have been drained by the epilogue (previous tile).
+            // G accumulators (both CTAs) must have been drained (previous tile).
             pr.mark(5);
-            mbar_wait(g_empty, (it & 1) ^ 1);
+            mbar_wait_cluster(g_empty, (it & 1) ^ 1);
             pr.mark(4);
             tc_fence_after();
             for (int j = 0; j < p.n_chunks; ++j) {
                 gemm2(j == 0);
                 if (j + 2 < p.n_chunks) gemm1(j + 2);
             }
-            if (elect_one()) mma_commit(g_full);
+            if (elect_one()) mma_commit_2sm_mc(g_full, PAIR);
             __syncwarp();
         }
         pr.mark(5);
@@ -311,12 +330,12 @@ __global__ void __launch_bounds__(k1::THREADS, 1)
         const int ew = warp - 4;
         const int quad = warp & 3;          // TMEM lane quadrant this warp may access
         const int half = ew >> 2;           // which 32 of the 64 chunk columns
-        const int r = quad * 32 + lane;     // row within the tile
+        const int r = quad * 32 + lane;     // row within this CTA's 128 rows of the tile
+        const int r_pair = static_cast<int>(rank) * BM + r;  // row within the 256-row pair tile
         const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
-        uint32_t cnt = 0;
+        uint32_t cnt = 0, stg_k = 0;
         PhaseProbe pr((p.dbg & 16) != 0);
-        uint8_t* stg = smem + OFF_STG + ew * STG_BYTES;
-        const uint32_t stg_addr = base_addr + OFF_STG + ew * STG_BYTES;
+        const uint32_t x_full_l = lead(x_full), g_empty_l = lead(g_empty), z_full_l = lead(z_full);
 
         // X tile rt: this thread's row of the hi (half 0) or lo (half 1) plane, loaded
         // into registers a whole tile ahead, then written to TMEM once the previous
@@ -324,7 +343,7 @@ __global__ void __launch_bounds__(k1::THREADS, 1)
         uint32_t xv[32];
         auto load_x = [&](int rt) {
             const uint4* src = reinterpret_cast<const uint4*>(
-                (half ? p.x_lo : p.x_hi) + (static_cast<long long>(rt) * BM + r) * KD);
+                (half ? p.x_lo : p.x_hi) + (static_cast<long long>(rt) * PM + r_pair) * KD);
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 const uint4 q = __ldg(src + i);
@@ -333,13 +352,13 @@ __global__ void __launch_bounds__(k1::THREADS, 1)
         };
         auto write_x = [&](uint32_t itx) {
             const uint32_t (&v)[32] = xv;
-            mbar_wait(x_empty, (itx & 1) ^ 1);
+            mbar_wait_cluster(x_empty, (itx & 1) ^ 1);
             tc_fence_after();
             tmem_st_32x32b_x32(tmem_base + lane_off + (half ? TM_XLO : TM_XHI), v);
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(x_full);
+            if (lane == 0) mbar_arrive_cluster(x_full_l);
         };
 
         // Z for one chunk: S (TMEM) -> exp -> fp16 hi/lo -> same TMEM columns.
@@ -351,7 +370,7 @@ __global__ void __launch_bounds__(k1::THREADS, 1)
             const uint32_t col = tmem_base + lane_off + TM_SZ + b * NC + half * 32;
             uint32_t s[32];
             pr.mark(7);
-            mbar_wait(s_full + b, ph);
+            mbar_wait_cluster(s_full + b, ph);
             pr.mark(0);
             tc_fence_after();
             tmem_ld_32x32b_x32(col, s);
@@ -383,7 +402,7 @@ __global__ void __launch_bounds__(k1::THREADS, 1)
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(z_full + b);
+            if (lane == 0) mbar_arrive_cluster(z_full_l + 8 * b);
             pr.mark(4);
             ++cnt;
         };
@@ -393,16 +412,16 @@ __global__ void __launch_bounds__(k1::THREADS, 1)
             const int cb = tile / p.n_row_tiles;
             const int rt = tile - cb * p.n_row_tiles;
             pr.mark(7);
-            mbar_wait(g_full, it & 1);
+            mbar_wait_cluster(g_full, it & 1);
             pr.mark(5);
             tc_fence_after();
             if (p.dbg & 64) {  // bypass the drain: free the accumulator at once
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(g_empty);
+                if (lane == 0) mbar_arrive_cluster(g_empty_l);
                 return;
             }
-            const int grow = rt * BM + r;
+            const int grow = rt * PM + r_pair;
             const bool row_ok = grow < p.n_rows;
             OutT* grow_ptr = static_cast<OutT*>(p.G) + static_cast<long long>(grow) * p.ldg;
             constexpr int SLAB = 128 / sizeof(OutT);  // columns per 128-byte staging row
@@ -415,7 +434,7 @@ __global__ void __launch_bounds__(k1::THREADS, 1)
                 if (m == 3) {
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(g_empty);
+                    if (lane == 0) mbar_arrive_cluster(g_empty_l);
                 }
                 const int gc0 = cb * N2 + c0;
                 if (gc0 >= p.b_eff || (p.dbg & 2)) continue;
@@ -434,8 +453,12 @@ __global__ void __launch_bounds__(k1::THREADS, 1)
                     // (16-byte chunk c of row r at chunk c ^ (r & 7)): conflict-free STS.
 #pragma unroll
                     for (int sl = 0; sl < 32 / SLAB; ++sl) {
-                        if (lane == 0) bulk_wait_group_read<0>();
+                        // double-buffered staging: the store issued two slabs ago has
+                        // finished reading this buffer once at most one group is pending
+                        if (lane == 0) bulk_wait_group_read<NSTG - 1>();
                         __syncwarp();
+                        const uint32_t sbuf = OFF_STG + (ew * NSTG + stg_k) * STG_BYTES;
+                        stg_k = (stg_k + 1) % NSTG;
 #pragma unroll
                         for (int c = 0; c < 8; ++c) {
                             uint32_t w[4];
@@ -447,12 +470,12 @@ __global__ void __launch_bounds__(k1::THREADS, 1)
 #pragma unroll
                                 for (int e = 0; e < 4; ++e) w[e] = __float_as_uint(out[4 * c + e]);
                             }
-                            st_shared_v4(stg_addr + lane * 128 + ((c ^ (lane & 7)) << 4), w[0], w[1], w[2], w[3]);
+                            st_shared_v4(base_addr + sbuf + lane * 128 + ((c ^ (lane & 7)) << 4), w[0], w[1], w[2], w[3]);
                         }
                         fence_proxy_async_smem();
                         __syncwarp();
                         if (lane == 0) {
-                            tma_store_2d(&tm_g, stg, gc0 + sl * SLAB, rt * BM + quad * 32);
+                            tma_store_2d(&tm_g, smem + sbuf, gc0 + sl * SLAB, rt * PM + static_cast<int>(rank) * BM + quad * 32);
                             bulk_commit_group();
                         }
                     }
@@ -496,22 +519,22 @@ __global__ void __launch_bounds__(k1::THREADS, 1)
         // Tiles run column-block-major (tile = cb·n_row_tiles + rt), so the CTAs in
         // flight share one 4 MB Lᵀ column block in L2.
         uint32_t it = 0;
-        if (static_cast<int>(blockIdx.x) < num_tiles) {
-            load_x(static_cast<int>(blockIdx.x) % p.n_row_tiles);
+        if (pair < num_tiles) {
+            load_x(pair % p.n_row_tiles);
             write_x(0);
         }
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+        for (int tile = pair; tile < num_tiles; tile += num_pairs, ++it) {
             const int rt = tile % p.n_row_tiles;
-            const float2 ra = p.row_aux[rt * BM + r];
+            const float2 ra = p.row_aux[rt * PM + r_pair];
             const uint64_t R2 = f2_pack(ra.x, ra.x), sx2 = f2_pack(ra.y, ra.y);
-            const int next = tile + gridDim.x;
+            const int next = tile + num_pairs;
             if (next < num_tiles) load_x(next % p.n_row_tiles);
             for (int j = 0; j < p.n_chunks; ++j) {
                 if (p.dbg & 32) {  // bypass: keep the barrier protocol, skip Z math and stores
                     const uint32_t b = cnt % NSZ, ph = (cnt / NSZ) & 1;
-                    mbar_wait(s_full + b, ph);
+                    mbar_wait_cluster(s_full + b, ph);
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(z_full + b);
+                    if (lane == 0) mbar_arrive_cluster(z_full_l + 8 * b);
                     ++cnt;
                 } else {
                     produce_z(R2, sx2);
@@ -527,10 +550,12 @@ __global__ void __launch_bounds__(k1::THREADS, 1)
         if (lane == 0) pr.flush(p.dbg_out ? p.dbg_out + 8 : nullptr);
     }
 
+    // Neither CTA may leave while the leader's MMAs still read the peer's TMEM /
+    // shared memory or multicast commits into it.
     tc_fence_before();
-    __syncthreads();
+    cluster_sync();
     tc_fence_after();
-    if (warp == 2) tmem_dealloc(tmem_base, TMEM_COLS);
+    if (warp == 2) tmem_dealloc_2sm(tmem_base, TMEM_COLS);
 }
 
 }  // namespace lpd

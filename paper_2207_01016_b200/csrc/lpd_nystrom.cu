@@ -206,7 +206,7 @@ struct lpd_context {
 namespace {
 
 void ensure_slot(DeviceState& ds, Slot& s, int64_t rows, bool need_g, int64_t nnz) {
-    const int64_t rows_pad = round_up(std::max<int64_t>(rows, 1), 128);
+    const int64_t rows_pad = round_up(std::max<int64_t>(rows, 1), lpd::k1::PM);
     if (rows_pad > s.rows_cap || (need_g && s.g_cols != ds.b_eff)) {
         dev_free(s.x); dev_free(s.xhi); dev_free(s.xlo); dev_free(s.raux); dev_free(s.g);
         const int64_t cap = std::max(rows_pad, s.rows_cap);
@@ -295,10 +295,11 @@ void build_basis(DeviceState& ds, const double* lm_dev, int64_t B, int64_t d, in
         dev_alloc(&ds.lt_lo, static_cast<size_t>(Beff_pad * B_pad));
         dev_alloc(&ds.col_scale, static_cast<size_t>(Beff_pad));
         dev_alloc(&ds.colmax, static_cast<size_t>(Beff_pad));
-        ds.tm_lmhi = make_plane_map(ds.lm_hi, B_pad, lpd::KD_MAX, lpd::k1::NC, 64);
-        ds.tm_lmlo = make_plane_map(ds.lm_lo, B_pad, lpd::KD_MAX, lpd::k1::NC, 64);
-        ds.tm_lthi = make_plane_map(ds.lt_hi, Beff_pad, B_pad, lpd::k1::N2, 64);
-        ds.tm_ltlo = make_plane_map(ds.lt_lo, Beff_pad, B_pad, lpd::k1::N2, 64);
+        // per-CTA halves: 32 landmark rows, 128 Lᵀ rows (the pair splits N)
+        ds.tm_lmhi = make_plane_map(ds.lm_hi, B_pad, lpd::KD_MAX, lpd::k1::NCH, 64);
+        ds.tm_lmlo = make_plane_map(ds.lm_lo, B_pad, lpd::KD_MAX, lpd::k1::NCH, 64);
+        ds.tm_lthi = make_plane_map(ds.lt_hi, Beff_pad, B_pad, lpd::k1::N2H, 64);
+        ds.tm_ltlo = make_plane_map(ds.lt_lo, Beff_pad, B_pad, lpd::k1::N2H, 64);
     }
     ds.has_basis = false;
     ds.B = B; ds.d = d; ds.b_eff = b_eff; ds.gamma = gamma;
@@ -351,7 +352,7 @@ void build_basis_host_L(DeviceState& ds, const double* lm_dev, int64_t B, int64_
 void launch_factor(DeviceState& ds, Slot& s, const double* x_dev, int64_t m, int64_t ldx,
                    void* g_dev, int64_t ldg, int out_dtype, cudaStream_t st, bool time_it) {
     if (m <= 0) return;
-    const int64_t m_pad = round_up(m, 128);
+    const int64_t m_pad = round_up(m, lpd::k1::PM);
     {
         const int threads = 256, rows_per_block = threads / 32;
         const int64_t blocks = std::min<int64_t>((m_pad + rows_per_block - 1) / rows_per_block,
@@ -367,7 +368,7 @@ void launch_factor(DeviceState& ds, Slot& s, const double* x_dev, int64_t m, int
                                       out_dtype == LPD_OUT_F64);
     lpd::FactorParams p;
     p.n_rows = static_cast<int>(m);
-    p.n_row_tiles = static_cast<int>(m_pad / lpd::k1::BM);
+    p.n_row_tiles = static_cast<int>(m_pad / lpd::k1::PM);
     p.n_chunks = static_cast<int>(ds.B_pad / lpd::k1::NC);
     p.n_col_blocks = static_cast<int>(ds.Beff_pad / lpd::k1::N2);
     p.b_eff = static_cast<int>(ds.b_eff);
@@ -392,7 +393,8 @@ void launch_factor(DeviceState& ds, Slot& s, const double* x_dev, int64_t m, int
         p.dbg_out = dbg_out;
     }
     const int64_t tiles = static_cast<int64_t>(p.n_row_tiles) * p.n_col_blocks;
-    const int grid = static_cast<int>(std::min<int64_t>(tiles, ds.num_sms));
+    // CTA pairs (cluster of 2): one pair per two SMs, persistent over the tiles
+    const int grid = 2 * static_cast<int>(std::min<int64_t>(tiles, ds.num_sms / 2));
     cudaEvent_t* pr = nullptr;
     if (time_it) {
         pr = ds.ring[ds.ring_count % DeviceState::kRing];

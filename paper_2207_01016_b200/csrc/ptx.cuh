@@ -49,13 +49,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     }
 }
 
-// Cluster-scope variant for barriers that receive arrivals (or TMA transaction
-// bytes) from the peer CTA of a pair.
+// Wait on a barrier that receives arrivals (or TMA transaction bytes) from the peer
+// CTA of a pair. Same instruction as mbar_wait (CUTLASS's ClusterBarrier uses the
+// default acquire.cta form too); kept separate to mark the cross-CTA waits.
 __device__ __forceinline__ bool mbar_try_wait_cluster(uint64_t* bar, uint32_t parity) {
     uint32_t ok;
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(ok)
         : "r"(smem_u32(bar)), "r"(parity)
@@ -83,9 +84,11 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t local_addr, uint32_t ra
     return r;
 }
 // Arrive (release, cluster scope) on an mbarrier given by its shared::cluster address.
+// Default (CTA-scope release) semantics, as CUTLASS's 2-SM arrivals: the data these
+// arrivals publish is TMEM, ordered by tcgen05.wait::st + tcgen05.fence, so no
+// cluster-scope memory fence is needed (and .release.cluster costs ~1k cycles).
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
-                 : "memory");
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive_expect_tx_cluster(uint32_t cluster_addr, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(
