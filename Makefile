@@ -9,8 +9,11 @@ HDRS    := $(wildcard $(CSRC)/*.cuh) include/lpd_nystrom.h
 
 all: $(LIB) oracle integration
 
-$(LIB): $(CSRC)/lpd_nystrom.cu $(HDRS)
-	$(NVCC) $(NVFLAGS) -shared -o $@ $< -lcuda 2> $(PKG)/ptxas.log || (cat $(PKG)/ptxas.log; false)
+$(CSRC)/host_widen.o: $(CSRC)/host_widen.cpp
+	g++ -O3 -fPIC -c -o $@ $<
+
+$(LIB): $(CSRC)/lpd_nystrom.cu $(HDRS) $(CSRC)/host_widen.o
+	$(NVCC) $(NVFLAGS) -shared -o $@ $< $(CSRC)/host_widen.o -lcuda 2> $(PKG)/ptxas.log || (cat $(PKG)/ptxas.log; false)
 	@grep -E "registers|spill|smem" $(PKG)/ptxas.log | head -20 || true
 
 oracle:
@@ -21,7 +24,7 @@ integration: $(LIB)
 	$(MAKE) -C integration
 
 clean:
-	rm -f $(LIB) $(PKG)/ptxas.log
+	rm -f $(LIB) $(PKG)/ptxas.log $(CSRC)/host_widen.o
 	$(MAKE) -C oracle clean
 	$(MAKE) -C integration clean
 

@@ -300,30 +300,40 @@ def main():
         g_bytes = n * b_eff * 8
         if psutil.virtual_memory().available > 2.5 * g_bytes * max(1, torch.cuda.device_count() if world > 1 else 1):
             Xh = torch.from_numpy(X).pin_memory()
-            Gh = torch.empty((n, b_eff), dtype=torch.float64).pin_memory()
             Yh = lm_dev.cpu().numpy()
             Lh = L_dev.cpu().numpy()
-            Xn, Gn = Xh.numpy(), Gh.numpy()
-            ctx.set_basis_dense(Yh, Lh, cfg.gamma)
-            ctx.compute_g_dense(Xn, out=Gn)  # warm-up
-            ts = []
-            for _ in range(args.e2e_steps):
-                if dist:
-                    dist.barrier()
-                t0 = time.perf_counter()
+            Xn = Xh.numpy()
+
+            def run_e2e(Gout):
                 ctx.set_basis_dense(Yh, Lh, cfg.gamma)
-                ctx.compute_g_dense(Xn, out=Gn)
-                dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
-                if dist:
-                    dist.all_reduce(dt, op=dist.ReduceOp.MAX)
-                ts.append(float(dt.item()))
-            e2e = {"value": N * n / statistics.mean(ts), "unit": UNIT,
+                ctx.compute_g_dense(Xn, out=Gout)  # warm-up (also first-touches Gout)
+                ts = []
+                for _ in range(args.e2e_steps):
+                    if dist:
+                        dist.barrier()
+                    t0 = time.perf_counter()
+                    ctx.set_basis_dense(Yh, Lh, cfg.gamma)
+                    ctx.compute_g_dense(Xn, out=Gout)
+                    dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+                    if dist:
+                        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+                    ts.append(float(dt.item()))
+                # spot-check the host result against the device-path result
+                assert np.array_equal(Gout[:1000], G_dev[:1000].cpu().numpy())
+                return statistics.mean(ts)
+
+            # the caller's G is ordinary pageable, pre-touched memory, like the
+            # reference's zero-filled Matrix (matrix.hpp:15-16)
+            Gn = np.zeros((n, b_eff), dtype=np.float64)
+            t_e2e = run_e2e(Gn)
+            e2e = {"value": N * n / t_e2e, "unit": UNIT,
                    "h2d_bytes_per_step": int(X.nbytes + Yh.nbytes + Lh.nbytes),
-                   "d2h_bytes_per_step": int(g_bytes), "seconds_per_step": statistics.mean(ts),
-                   "path": "lpd_set_basis_dense + lpd_compute_g_dense, pinned host X -> host fp64 G"}
-            # spot-check the e2e result against the device result
-            assert np.array_equal(Gn[:1000], G_dev[:1000].cpu().numpy())
-            del Xh, Gh
+                   "d2h_bytes_per_step": int(n * (-(-b_eff // 4) * 4) * 4),
+                   "seconds_per_step": t_e2e,
+                   "path": "lpd_set_basis_dense + lpd_compute_g_dense: pinned host X -> device; fp32 G -> "
+                           "pinned staging -> host threads widen (AVX-512 streaming stores) into the "
+                           "caller's pageable fp64 G"}
+            del Xh, Gn
         else:
             e2e = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                    "skipped": "host RAM too small for a pinned fp64 G of this workload"}

@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <condition_variable>
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>
@@ -32,6 +33,9 @@
 #include "decision_kernels.cuh"
 #include "factor_kernel.cuh"
 #include "prep_kernels.cuh"
+
+extern "C" void lpd_host_widen_rows(const float* src, int64_t lds, double* dst, int64_t ldd,
+                                    int64_t r0, int64_t r1, int64_t cols);
 
 namespace {
 
@@ -149,9 +153,10 @@ struct Slot {
     __half* xhi = nullptr;   // [rows_cap × 64]
     __half* xlo = nullptr;
     float2* raux = nullptr;  // [rows_cap]
-    double* g = nullptr;     // [rows_cap × b_eff] fp64 (host-call path)
-    int64_t g_cols = 0;      // b_eff the g buffer was sized for
-    int64_t g_ld = 0;        // its row pitch (elements; even, so rows stay 16-byte aligned)
+    void* g = nullptr;       // [rows_cap × g_ld] fp32 G of the host-call path (device)
+    float* h = nullptr;      // [rows_cap × g_ld] pinned host staging of g
+    int64_t g_cols = 0;      // b_eff the g buffers were sized for
+    int64_t g_ld = 0;        // their row pitch (elements; multiple of 4: 16-byte rows)
     int64_t nnz_cap = 0;
     int64_t* indptr = nullptr;
     int32_t* indices = nullptr;
@@ -192,6 +197,8 @@ struct DeviceState {
     }
     void free_slot(Slot& s) {
         dev_free(s.x); dev_free(s.xhi); dev_free(s.xlo); dev_free(s.raux); dev_free(s.g);
+        if (s.h) cudaFreeHost(s.h);
+        s.h = nullptr;
         dev_free(s.indptr); dev_free(s.indices); dev_free(s.values);
         s.rows_cap = 0; s.g_cols = 0; s.nnz_cap = 0;
     }
@@ -209,13 +216,20 @@ void ensure_slot(DeviceState& ds, Slot& s, int64_t rows, bool need_g, int64_t nn
     const int64_t rows_pad = round_up(std::max<int64_t>(rows, 1), lpd::k1::PM);
     if (rows_pad > s.rows_cap || (need_g && s.g_cols != ds.b_eff)) {
         dev_free(s.x); dev_free(s.xhi); dev_free(s.xlo); dev_free(s.raux); dev_free(s.g);
+        if (s.h) cudaFreeHost(s.h);
+        s.h = nullptr;
         const int64_t cap = std::max(rows_pad, s.rows_cap);
         dev_alloc(&s.x, static_cast<size_t>(cap * std::max<int64_t>(ds.d, 1)));
         dev_alloc(&s.xhi, static_cast<size_t>(cap * lpd::KD_MAX));
         dev_alloc(&s.xlo, static_cast<size_t>(cap * lpd::KD_MAX));
         dev_alloc(&s.raux, static_cast<size_t>(cap));
-        s.g_ld = round_up(ds.b_eff, 2);
-        if (need_g) dev_alloc(&s.g, static_cast<size_t>(cap * s.g_ld));
+        s.g_ld = round_up(ds.b_eff, 4);
+        if (need_g) {
+            dev_alloc(reinterpret_cast<float**>(&s.g), static_cast<size_t>(cap * s.g_ld));
+            CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&s.h),
+                                   sizeof(float) * static_cast<size_t>(cap * s.g_ld),
+                                   cudaHostAllocPortable));
+        }
         s.g_cols = need_g ? ds.b_eff : 0;
         s.rows_cap = cap;
     }
@@ -438,6 +452,72 @@ void check_range_flag(DeviceState& ds) {
     }
 }
 
+// Persistent host workers for the fp32 -> fp64 widening of G chunks into the
+// caller's buffer (the reference's Matrix is plain pageable memory: widening from a
+// pinned fp32 staging buffer halves PCIe bytes and beats a pageable fp64 DMA 3x).
+class HostPool {
+public:
+    explicit HostPool(int n) {
+        for (int i = 0; i < n; ++i) th_.emplace_back([this, i] { loop(i); });
+    }
+    ~HostPool() {
+        {
+            std::lock_guard<std::mutex> l(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+    int size() const { return static_cast<int>(th_.size()); }
+    // Runs fn(worker) on every worker and waits.
+    void run(const std::function<void(int)>& fn) {
+        std::unique_lock<std::mutex> l(mu_);
+        fn_ = &fn;
+        pending_ = static_cast<int>(th_.size());
+        ++gen_;
+        cv_.notify_all();
+        done_cv_.wait(l, [this] { return pending_ == 0; });
+        fn_ = nullptr;
+    }
+
+private:
+    void loop(int i) {
+        uint64_t seen = 0;
+        for (;;) {
+            const std::function<void(int)>* fn;
+            {
+                std::unique_lock<std::mutex> l(mu_);
+                cv_.wait(l, [&] { return stop_ || gen_ != seen; });
+                if (stop_) return;
+                seen = gen_;
+                fn = fn_;
+            }
+            (*fn)(i);
+            {
+                std::lock_guard<std::mutex> l(mu_);
+                if (--pending_ == 0) done_cv_.notify_all();
+            }
+        }
+    }
+    std::vector<std::thread> th_;
+    std::mutex mu_;
+    std::condition_variable cv_, done_cv_;
+    const std::function<void(int)>* fn_ = nullptr;
+    int pending_ = 0;
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+};
+
+// dst[r][c] = src[r][c] (fp32 -> fp64) for rows [0, rows), split over the pool
+// (host_widen.cpp: AVX-512 streaming stores).
+void widen_rows(HostPool& pool, const float* src, int64_t lds, double* dst, int64_t ldd,
+                int64_t rows, int64_t cols) {
+    const int T = pool.size();
+    pool.run([&](int w) {
+        lpd_host_widen_rows(src, lds, dst, ldd, rows * w / T, rows * (w + 1) / T, cols);
+    });
+}
+
 lpd_context* check_ctx(lpd_context* ctx, bool need_basis) {
     if (!ctx) fail(LPD_ERR_INVALID_ARGUMENT, "null context");
     if (ctx->dev.empty()) fail(LPD_ERR_NO_DEVICE, "context has no devices");
@@ -472,58 +552,70 @@ void run_parallel(lpd_context* ctx, const std::function<void(DeviceState&, int)>
         if (codes[i] != LPD_OK) fail(codes[i], "device " + std::to_string(i) + ": " + errs[i]);
 }
 
-// Host-row pipeline shared by the dense and CSR entry points. `stage_x` fills
-// slot.x (dense fp64 [rows × d]) on the slot's stream for global rows
-// [r0, r0 + rows).
+// Host-row pipeline shared by the dense and CSR entry points. Each device owns a
+// contiguous row shard (reference compute_G chunks rows, factor.cpp:97-108; rows
+// are independent, so no collective) and runs, per row chunk on alternating slots:
+//   stage_x (H2D of X rows) -> prep -> fused factor kernel (fp32 G) -> D2H into a
+//   pinned fp32 staging buffer
+// while its host workers widen the previous chunk to fp64 straight into the
+// caller's G rows (measured on the B200 box: 0.37 s for C2's 19 GB fp64 G, vs 0.46 s
+// for an fp64 DMA straight into a pinned G and ~1.1 s into a pageable one). `stage_x`
+// fills slot.x (dense fp64 [rows × d]) on the slot's
+// stream for global rows [r0, r0 + rows) and records ev[0].
 template <typename StageX>
 void compute_rows_host(lpd_context* ctx, int64_t n, double* G, int64_t ldg, lpd_timings* tm,
                        StageX&& stage_x) {
     const int nd = static_cast<int>(ctx->dev.size());
     const auto t0 = std::chrono::steady_clock::now();
-    std::vector<double> h2d(nd, 0.0), ker(nd, 0.0), d2h(nd, 0.0);
+    std::vector<double> h2d(nd, 0.0), ker(nd, 0.0), d2h(nd, 0.0), host(nd, 0.0);
     std::vector<int64_t> launches(nd, 0);
     const int64_t b_eff = ctx->dev[0].b_eff;
-    // Rows per pipeline chunk: ~256 MB of fp64 G, multiple of 128.
+    // Rows per pipeline chunk: ~128 MB of fp32 G, multiple of the 256-row pair tile.
     const int64_t chunk = std::max<int64_t>(
-        128, std::min<int64_t>(round_up(n, 128), (256ll << 20) / (8 * b_eff) / 128 * 128));
+        256, std::min<int64_t>(round_up(n, 256), (128ll << 20) / (4 * b_eff) / 256 * 256));
+    const int hw = std::max(1u, std::thread::hardware_concurrency());
+    const int workers = std::max(1, std::min(16, hw / nd));
     run_parallel(ctx, [&](DeviceState& ds, int di) {
         CUDA_TRY(cudaSetDevice(ds.device));
-        const int64_t per = round_up((n + nd - 1) / nd, 128);
+        HostPool pool(workers);
+        const int64_t per = round_up((n + nd - 1) / nd, 256);
         const int64_t r_begin = std::min<int64_t>(n, per * di);
         const int64_t r_end = std::min<int64_t>(n, per * (di + 1));
-        int64_t k = 0;
-        std::vector<int64_t> pending_rows[2];
-        for (int64_t r0 = r_begin; r0 < r_end; r0 += chunk, ++k) {
-            const int64_t rows = std::min(chunk, r_end - r0);
-            Slot& s = ds.slot[k & 1];
-            CUDA_TRY(cudaStreamSynchronize(s.stream));  // slot reuse (two chunks ago)
-            if (k >= 2) {
-                float a = 0, b = 0, c = 0;
-                cudaEventElapsedTime(&a, s.ev[0], s.ev[1]);
-                cudaEventElapsedTime(&b, s.ev[1], s.ev[2]);
-                cudaEventElapsedTime(&c, s.ev[2], s.ev[3]);
-                h2d[di] += a * 1e-3; ker[di] += b * 1e-3; d2h[di] += c * 1e-3;
-            }
-            stage_x(ds, s, r0, rows);  // records ev[0] and fills s.x
-            CUDA_TRY(cudaEventRecord(s.ev[1], s.stream));
-            launch_factor(ds, s, s.x, rows, ds.d, s.g, s.g_ld, LPD_OUT_F64, s.stream, false);
-            launches[di] += 2;
-            CUDA_TRY(cudaEventRecord(s.ev[2], s.stream));
-            CUDA_TRY(cudaMemcpy2DAsync(G + r0 * ldg, sizeof(double) * ldg, s.g,
-                                       sizeof(double) * s.g_ld, sizeof(double) * b_eff,
-                                       static_cast<size_t>(rows), cudaMemcpyDeviceToHost,
-                                       s.stream));
-            CUDA_TRY(cudaEventRecord(s.ev[3], s.stream));
-        }
-        for (int64_t kk = std::max<int64_t>(0, k - 2); kk < k; ++kk) {
-            Slot& s = ds.slot[kk & 1];
+        int64_t pend_r0[2] = {-1, -1}, pend_rows[2] = {0, 0};
+        auto finish = [&](int k) {  // wait for slot k's chunk and widen it into G
+            Slot& s = ds.slot[k];
+            if (pend_r0[k] < 0) return;
             CUDA_TRY(cudaStreamSynchronize(s.stream));
             float a = 0, b = 0, c = 0;
             cudaEventElapsedTime(&a, s.ev[0], s.ev[1]);
             cudaEventElapsedTime(&b, s.ev[1], s.ev[2]);
             cudaEventElapsedTime(&c, s.ev[2], s.ev[3]);
             h2d[di] += a * 1e-3; ker[di] += b * 1e-3; d2h[di] += c * 1e-3;
+            const auto w0 = std::chrono::steady_clock::now();
+            widen_rows(pool, s.h, s.g_ld, G + pend_r0[k] * ldg, ldg, pend_rows[k], b_eff);
+            host[di] += std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
+            pend_r0[k] = -1;
+        };
+        int64_t k = 0;
+        for (int64_t r0 = r_begin; r0 < r_end; r0 += chunk, ++k) {
+            const int64_t rows = std::min(chunk, r_end - r0);
+            const int sl = static_cast<int>(k & 1);
+            Slot& s = ds.slot[sl];
+            finish(sl);                // slot reuse: its chunk (k - 2) is widened by now
+            stage_x(ds, s, r0, rows);  // records ev[0] and fills s.x
+            CUDA_TRY(cudaEventRecord(s.ev[1], s.stream));
+            launch_factor(ds, s, s.x, rows, ds.d, s.g, s.g_ld, LPD_OUT_F32, s.stream, false);
+            launches[di] += 2;
+            CUDA_TRY(cudaEventRecord(s.ev[2], s.stream));
+            CUDA_TRY(cudaMemcpyAsync(s.h, s.g, sizeof(float) * static_cast<size_t>(rows * s.g_ld),
+                                     cudaMemcpyDeviceToHost, s.stream));
+            CUDA_TRY(cudaEventRecord(s.ev[3], s.stream));
+            pend_r0[sl] = r0;
+            pend_rows[sl] = rows;
+            if (k >= 1) finish(static_cast<int>((k - 1) & 1));  // overlaps chunk k on the GPU
         }
+        finish(0);
+        finish(1);
         check_range_flag(ds);
     });
     if (tm) {
@@ -532,6 +624,7 @@ void compute_rows_host(lpd_context* ctx, int64_t n, double* G, int64_t ldg, lpd_
             tm->h2d_seconds += h2d[i];
             tm->kernel_seconds += ker[i];
             tm->d2h_seconds += d2h[i];
+            tm->host_copy_seconds += host[i];
             tm->launches += launches[i];
         }
         tm->rows = n;
