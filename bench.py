@@ -36,7 +36,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "Nyström factor rows/s"
 UNIT = "rows/s"
-LAUNCHES_PER_STEP = 6  # K2: column_mean, prep_rows(landmarks), col_absmax, lt_split; K3 prep_rows; K1
+LAUNCHES_PER_STEP = 8  # K2: column_mean, landmark_stats, basis_consts, prep_landmarks, col_absmax, lt_split; K3 prep_rows; K1
 
 
 def parse():
@@ -288,8 +288,8 @@ def main():
     achieved = F / (k_ms / 1e3) / 1e12
     traffic = load_traffic()
     # issued tensor work (3-term split, padded shapes, GEMM1 recomputed per 256-column block)
-    npad, bpad, epad = -(-n // 128) * 128, -(-B // 64) * 64, -(-b_eff // 256) * 256
-    k1 = -(-cfg.d // 16) * 16
+    npad, bpad, epad = -(-n // 256) * 256, -(-B // 64) * 64, -(-b_eff // 256) * 256
+    k1 = -(-(cfg.d + 1) // 16) * 16  # d features + the augmented norm column
     issued = 3 * (2.0 * npad * bpad * k1 * (epad // 256) + 2.0 * npad * bpad * epad)
 
     # ---------------- end to end through the C ABI with host buffers ----------------

@@ -13,12 +13,12 @@ import numpy as np
 
 __all__ = ["row_shard", "broadcast_basis"]
 
-ROW_ALIGN = 128  # one UMMA M tile
+ROW_ALIGN = 256  # one CTA-pair tile (2 x 128-row UMMA M halves)
 
 
 def row_shard(n: int, world_size: int, rank: int, align: int = ROW_ALIGN) -> Tuple[int, int]:
     """Contiguous [begin, end) of rank's rows; boundaries are multiples of `align`
-    (so no 128-row tile straddles two GPUs) and the union over ranks is [0, n)."""
+    (so no 256-row pair tile straddles two GPUs) and the union over ranks is [0, n)."""
     if world_size < 1 or not (0 <= rank < world_size):
         raise ValueError("invalid rank / world size")
     if n < 0:
