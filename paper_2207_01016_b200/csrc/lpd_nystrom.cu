@@ -32,6 +32,7 @@
 #include "../../include/lpd_nystrom.h"
 #include "decision_kernels.cuh"
 #include "factor_kernel.cuh"
+#include "panel_kernels.cuh"
 #include "prep_kernels.cuh"
 
 extern "C" void lpd_host_widen_rows(const float* src, int64_t lds, double* dst, int64_t ldd,
@@ -157,6 +158,8 @@ struct Slot {
     float* h = nullptr;      // [rows_cap × g_ld] pinned host staging of g
     int64_t g_cols = 0;      // b_eff the g buffers were sized for
     int64_t g_ld = 0;        // their row pitch (elements; multiple of 4: 16-byte rows)
+    int64_t kd = 0;          // plane width the x planes were sized for
+    int64_t d_cap = 0;       // columns the fp64 x buffer was sized for
     int64_t nnz_cap = 0;
     int64_t* indptr = nullptr;
     int32_t* indices = nullptr;
@@ -168,6 +171,11 @@ struct DeviceState {
     int num_sms = 0;
     bool has_basis = false;
     int64_t B = 0, d = 0, b_eff = 0, B_pad = 0, Beff_pad = 0;
+    int64_t kd = lpd::KD_MAX;  // plane width: 64 (fused path, d <= 63) or round_up(d + 1, 64)
+    bool large = false;        // d >= 64: two-launch panel path (panel_kernels.cuh)
+    __half* z_hi = nullptr;    // large path: Z panel scratch [z_rows × B_pad]
+    __half* z_lo = nullptr;
+    int64_t z_rows = 0;
     double gamma = 1.0;
     double* mu = nullptr;
     __half* lm_hi = nullptr;
@@ -193,6 +201,8 @@ struct DeviceState {
     void free_basis() {
         dev_free(mu); dev_free(lm_hi); dev_free(lm_lo); dev_free(consts); dev_free(lm_nb); dev_free(lm_mx);
         dev_free(lt_hi); dev_free(lt_lo); dev_free(col_scale);
+        dev_free(z_hi); dev_free(z_lo);
+        z_rows = 0;
         has_basis = false;
     }
     void free_slot(Slot& s) {
@@ -214,14 +224,17 @@ namespace {
 
 void ensure_slot(DeviceState& ds, Slot& s, int64_t rows, bool need_g, int64_t nnz) {
     const int64_t rows_pad = round_up(std::max<int64_t>(rows, 1), lpd::k1::PM);
-    if (rows_pad > s.rows_cap || (need_g && s.g_cols != ds.b_eff)) {
+    if (rows_pad > s.rows_cap || (need_g && s.g_cols != ds.b_eff) || s.kd != ds.kd ||
+        s.d_cap < ds.d) {
         dev_free(s.x); dev_free(s.xhi); dev_free(s.xlo); dev_free(s.raux); dev_free(s.g);
         if (s.h) cudaFreeHost(s.h);
         s.h = nullptr;
         const int64_t cap = std::max(rows_pad, s.rows_cap);
         dev_alloc(&s.x, static_cast<size_t>(cap * std::max<int64_t>(ds.d, 1)));
-        dev_alloc(&s.xhi, static_cast<size_t>(cap * lpd::KD_MAX));
-        dev_alloc(&s.xlo, static_cast<size_t>(cap * lpd::KD_MAX));
+        dev_alloc(&s.xhi, static_cast<size_t>(cap * ds.kd));
+        dev_alloc(&s.xlo, static_cast<size_t>(cap * ds.kd));
+        s.kd = ds.kd;
+        s.d_cap = std::max<int64_t>(ds.d, 1);
         dev_alloc(&s.raux, static_cast<size_t>(cap));
         s.g_ld = round_up(ds.b_eff, 4);
         if (need_g) {
@@ -268,6 +281,12 @@ void init_device(DeviceState& ds, int device) {
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, lpd::k1::SMEM_BYTES));
     CUDA_TRY(cudaFuncSetAttribute(lpd::nystrom_factor_kernel<float>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, lpd::k1::SMEM_BYTES));
+    CUDA_TRY(cudaFuncSetAttribute(lpd::panel_gemm_kernel<lpd::PANEL_Z, float>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, lpd::kp::SMEM_BYTES));
+    CUDA_TRY(cudaFuncSetAttribute(lpd::panel_gemm_kernel<lpd::PANEL_G, float>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, lpd::kp::SMEM_BYTES));
+    CUDA_TRY(cudaFuncSetAttribute(lpd::panel_gemm_kernel<lpd::PANEL_G, double>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, lpd::kp::SMEM_BYTES));
 }
 
 void validate_basis_args(int64_t B, int64_t d, int64_t b_eff, double gamma, const double* L) {
@@ -278,9 +297,7 @@ void validate_basis_args(int64_t B, int64_t d, int64_t b_eff, double gamma, cons
     // reference validate(): proj/src/kernel.cpp:10-15
     if (!(gamma > 0.0) || !std::isfinite(gamma))
         fail(LPD_ERR_INVALID_ARGUMENT, "kernel gamma must be positive and finite");
-    if (d > lpd::KD_MAX - 1)
-        fail(LPD_ERR_UNSUPPORTED, "this build's fused factor kernel supports d <= 63 (got d=" +
-                                      std::to_string(d) + ")");
+    if (d > 65536) fail(LPD_ERR_UNSUPPORTED, "feature dimension above 65536");
     if (B > (1 << 30) || b_eff > (1 << 30)) fail(LPD_ERR_UNSUPPORTED, "basis too large");
 }
 
@@ -291,17 +308,23 @@ void validate_basis_args(int64_t B, int64_t d, int64_t b_eff, double gamma, cons
 void build_basis(DeviceState& ds, const double* lm_dev, int64_t B, int64_t d, int64_t ld_lm,
                  const double* L_dev, int64_t b_eff, double gamma, cudaStream_t st, bool sync) {
     CUDA_TRY(cudaSetDevice(ds.device));
-    const int64_t B_pad = round_up(B, lpd::k1::NC);
+    // d <= 63: the fused kernel (features + norm column in one 64-wide atom);
+    // otherwise the panel path, whose Z GEMM tiles the landmarks 256 at a time.
+    const bool large = d > lpd::KD_MAX - 1;
+    const int64_t kd = large ? round_up(d + 1, lpd::kp::BK) : lpd::KD_MAX;
+    const int64_t B_pad = round_up(B, large ? lpd::kp::BN : lpd::k1::NC);
     const int64_t Beff_pad = round_up(b_eff, lpd::k1::N2);
-    if (!ds.lt_hi || B_pad != ds.B_pad || Beff_pad != ds.Beff_pad) {
+    if (!ds.lt_hi || B_pad != ds.B_pad || Beff_pad != ds.Beff_pad || kd != ds.kd || large != ds.large) {
         CUDA_TRY(cudaDeviceSynchronize());
         ds.free_basis();
         dev_free(ds.colmax);
         ds.B_pad = B_pad;
         ds.Beff_pad = Beff_pad;
-        dev_alloc(&ds.mu, lpd::KD_MAX);
-        dev_alloc(&ds.lm_hi, static_cast<size_t>(B_pad * lpd::KD_MAX));
-        dev_alloc(&ds.lm_lo, static_cast<size_t>(B_pad * lpd::KD_MAX));
+        ds.kd = kd;
+        ds.large = large;
+        dev_alloc(&ds.mu, static_cast<size_t>(kd));
+        dev_alloc(&ds.lm_hi, static_cast<size_t>(B_pad * kd));
+        dev_alloc(&ds.lm_lo, static_cast<size_t>(B_pad * kd));
         dev_alloc(&ds.consts, 1);
         dev_alloc(&ds.lm_nb, static_cast<size_t>(B_pad));
         dev_alloc(&ds.lm_mx, static_cast<size_t>(B_pad));
@@ -309,17 +332,19 @@ void build_basis(DeviceState& ds, const double* lm_dev, int64_t B, int64_t d, in
         dev_alloc(&ds.lt_lo, static_cast<size_t>(Beff_pad * B_pad));
         dev_alloc(&ds.col_scale, static_cast<size_t>(Beff_pad));
         dev_alloc(&ds.colmax, static_cast<size_t>(Beff_pad));
-        // per-CTA halves: 32 landmark rows, 128 Lᵀ rows (the pair splits N)
-        ds.tm_lmhi = make_plane_map(ds.lm_hi, B_pad, lpd::KD_MAX, lpd::k1::NCH, 64);
-        ds.tm_lmlo = make_plane_map(ds.lm_lo, B_pad, lpd::KD_MAX, lpd::k1::NCH, 64);
+        // per-CTA halves of N: 32 landmark rows (fused kernel) or 128 (panel Z GEMM),
+        // 128 Lᵀ rows (both)
+        const uint32_t lm_box = large ? lpd::kp::BNH : lpd::k1::NCH;
+        ds.tm_lmhi = make_plane_map(ds.lm_hi, B_pad, kd, lm_box, 64);
+        ds.tm_lmlo = make_plane_map(ds.lm_lo, B_pad, kd, lm_box, 64);
         ds.tm_lthi = make_plane_map(ds.lt_hi, Beff_pad, B_pad, lpd::k1::N2H, 64);
         ds.tm_ltlo = make_plane_map(ds.lt_lo, Beff_pad, B_pad, lpd::k1::N2H, 64);
     }
     ds.has_basis = false;
     ds.B = B; ds.d = d; ds.b_eff = b_eff; ds.gamma = gamma;
 
-    lpd::column_mean_kernel<<<1, lpd::KD_MAX, 0, st>>>(lm_dev, ld_lm, static_cast<int>(B),
-                                                       static_cast<int>(d), ds.mu);
+    lpd::column_mean_kernel<<<static_cast<int>(kd / 32), dim3(32, 8), 0, st>>>(
+        lm_dev, ld_lm, static_cast<int>(B), static_cast<int>(d), static_cast<int>(kd), ds.mu);
     {
         const int threads = 256, rows_per_block = threads / 32;
         const int blocks = static_cast<int>((B + rows_per_block - 1) / rows_per_block);
@@ -330,8 +355,8 @@ void build_basis(DeviceState& ds, const double* lm_dev, int64_t B, int64_t d, in
                                                     ds.consts);
         const int pblocks = static_cast<int>((B_pad + rows_per_block - 1) / rows_per_block);
         lpd::prep_landmarks_kernel<<<pblocks, threads, 0, st>>>(
-            lm_dev, ld_lm, static_cast<int>(B), static_cast<int>(d), ds.mu, ds.consts, ds.lm_hi,
-            ds.lm_lo, static_cast<int>(B_pad));
+            lm_dev, ld_lm, static_cast<int>(B), static_cast<int>(d), static_cast<int>(kd), ds.mu,
+            ds.consts, ds.lm_hi, ds.lm_lo, static_cast<int>(B_pad));
     }
     lpd::col_absmax_kernel<<<static_cast<int>((b_eff + 127) / 128), 128, 0, st>>>(
         L_dev, static_cast<int>(B), static_cast<int>(b_eff), ds.colmax);
@@ -362,6 +387,76 @@ void build_basis_host_L(DeviceState& ds, const double* lm_dev, int64_t B, int64_
     dev_free(L_dev);
 }
 
+// Large-d factor (d >= 64) for m prepped rows in slot s: per row panel, the Z GEMM
+// (MODE_Z, exp epilogue, fp16 hi/lo planes in a device scratch) and the projection
+// GEMM (MODE_G). The scratch holds at most ~2 GB of Z planes.
+void launch_factor_panels(DeviceState& ds, Slot& s, int64_t m, void* g_dev, int64_t ldg,
+                          int out_dtype, cudaStream_t st, bool time_it) {
+    const int64_t m_pad = round_up(m, lpd::kp::PM);
+    const int64_t panel = std::min<int64_t>(
+        m_pad, std::max<int64_t>(lpd::kp::PM, ((2ll << 30) / (4 * ds.B_pad)) / lpd::kp::PM * lpd::kp::PM));
+    if (ds.z_rows < panel) {
+        CUDA_TRY(cudaStreamSynchronize(st));
+        dev_free(ds.z_hi);
+        dev_free(ds.z_lo);
+        dev_alloc(&ds.z_hi, static_cast<size_t>(panel * ds.B_pad));
+        dev_alloc(&ds.z_lo, static_cast<size_t>(panel * ds.B_pad));
+        ds.z_rows = panel;
+    }
+    cudaEvent_t* pr = nullptr;
+    if (time_it) {
+        pr = ds.ring[ds.ring_count % DeviceState::kRing];
+        CUDA_TRY(cudaEventRecord(ds.kev[0], st));
+        if (ds.ring_count < DeviceState::kRing) CUDA_TRY(cudaEventRecord(pr[0], st));
+    }
+    const CUtensorMap tm_zhi = make_plane_map(ds.z_hi, panel, ds.B_pad, lpd::kp::BM, 64);
+    const CUtensorMap tm_zlo = make_plane_map(ds.z_lo, panel, ds.B_pad, lpd::kp::BM, 64);
+    for (int64_t r0 = 0; r0 < m; r0 += panel) {
+        const int64_t rows = std::min(panel, m - r0);
+        const int64_t rows_pad = round_up(rows, lpd::kp::PM);
+        const CUtensorMap tm_xhi = make_plane_map(s.xhi + r0 * ds.kd, rows_pad, ds.kd, lpd::kp::BM, 64);
+        const CUtensorMap tm_xlo = make_plane_map(s.xlo + r0 * ds.kd, rows_pad, ds.kd, lpd::kp::BM, 64);
+        lpd::PanelParams pz{};
+        pz.n_row_pairs = static_cast<int>(rows_pad / lpd::kp::PM);
+        pz.n_col_blocks = static_cast<int>(ds.B_pad / lpd::kp::BN);
+        pz.n_kchunks = static_cast<int>(ds.kd / lpd::kp::BK);
+        pz.n_rows = static_cast<int>(rows);
+        pz.n_cols = static_cast<int>(ds.B_pad);
+        pz.row_aux = s.raux + r0;
+        pz.z_hi = ds.z_hi;
+        pz.z_lo = ds.z_lo;
+        pz.ldz = ds.B_pad;
+        const int64_t tz = static_cast<int64_t>(pz.n_row_pairs) * pz.n_col_blocks;
+        const int gz = 2 * static_cast<int>(std::min<int64_t>(tz, ds.num_sms / 2));
+        lpd::panel_gemm_kernel<lpd::PANEL_Z, float><<<gz, lpd::kp::THREADS, lpd::kp::SMEM_BYTES, st>>>(
+            tm_xhi, tm_xlo, ds.tm_lmhi, ds.tm_lmlo, pz);
+        lpd::PanelParams pg{};
+        pg.n_row_pairs = pz.n_row_pairs;
+        pg.n_col_blocks = static_cast<int>(ds.Beff_pad / lpd::kp::BN);
+        pg.n_kchunks = static_cast<int>(ds.B_pad / lpd::kp::BK);
+        pg.n_rows = static_cast<int>(rows);
+        pg.n_cols = static_cast<int>(ds.b_eff);
+        pg.col_scale = ds.col_scale;
+        const size_t es = out_dtype == LPD_OUT_F64 ? 8 : 4;
+        pg.G = static_cast<char*>(g_dev) + static_cast<size_t>(r0) * ldg * es;
+        pg.ldg = ldg;
+        const int64_t tg = static_cast<int64_t>(pg.n_row_pairs) * pg.n_col_blocks;
+        const int gg = 2 * static_cast<int>(std::min<int64_t>(tg, ds.num_sms / 2));
+        if (out_dtype == LPD_OUT_F64)
+            lpd::panel_gemm_kernel<lpd::PANEL_G, double><<<gg, lpd::kp::THREADS, lpd::kp::SMEM_BYTES, st>>>(
+                tm_zhi, tm_zlo, ds.tm_lthi, ds.tm_ltlo, pg);
+        else
+            lpd::panel_gemm_kernel<lpd::PANEL_G, float><<<gg, lpd::kp::THREADS, lpd::kp::SMEM_BYTES, st>>>(
+                tm_zhi, tm_zlo, ds.tm_lthi, ds.tm_ltlo, pg);
+        CUDA_TRY(cudaGetLastError());
+    }
+    if (time_it) {
+        CUDA_TRY(cudaEventRecord(ds.kev[1], st));
+        if (ds.ring_count < DeviceState::kRing) CUDA_TRY(cudaEventRecord(pr[1], st));
+        ++ds.ring_count;
+    }
+}
+
 // prep + fused factor kernel for m rows of dense fp64 X already on the device.
 void launch_factor(DeviceState& ds, Slot& s, const double* x_dev, int64_t m, int64_t ldx,
                    void* g_dev, int64_t ldg, int out_dtype, cudaStream_t st, bool time_it) {
@@ -372,8 +467,12 @@ void launch_factor(DeviceState& ds, Slot& s, const double* x_dev, int64_t m, int
         const int64_t blocks = std::min<int64_t>((m_pad + rows_per_block - 1) / rows_per_block,
                                                  static_cast<int64_t>(ds.num_sms) * 16);
         lpd::prep_rows_kernel<<<static_cast<int>(blocks), threads, 0, st>>>(
-            x_dev, ldx, static_cast<int>(m), static_cast<int>(ds.d), ds.mu, ds.consts, s.xhi, s.xlo,
-            s.raux, static_cast<int>(m_pad), ds.err);
+            x_dev, ldx, static_cast<int>(m), static_cast<int>(ds.d), static_cast<int>(ds.kd), ds.mu,
+            ds.consts, s.xhi, s.xlo, s.raux, static_cast<int>(m_pad), ds.err);
+    }
+    if (ds.large) {
+        launch_factor_panels(ds, s, m, g_dev, ldg, out_dtype, st, time_it);
+        return;
     }
     CUtensorMap tm_g;
     std::memset(&tm_g, 0, sizeof(tm_g));

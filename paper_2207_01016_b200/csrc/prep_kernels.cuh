@@ -20,7 +20,7 @@
 
 namespace lpd {
 
-constexpr int KD_MAX = 64;
+constexpr int KD_MAX = 64;  // plane width of the fused small-d kernel (d <= 63)
 
 __device__ __forceinline__ double warp_sum_d(double v) {
 #pragma unroll
@@ -62,10 +62,14 @@ __global__ void landmark_stats_kernel(const double* __restrict__ Y, long long ld
     const int lane = threadIdx.x & 31;
     if (row >= m) return;
     const double* y = Y + static_cast<long long>(row) * ldy;
-    const double v0 = lane < d ? y[lane] - mu[lane] : 0.0;
-    const double v1 = lane + 32 < d ? y[lane + 32] - mu[lane + 32] : 0.0;
-    const double ss = warp_sum_d(v0 * v0 + v1 * v1);
-    const double mxv = warp_max_d(fmax(fabs(v0), fabs(v1)));
+    double ss = 0.0, mxv = 0.0;
+    for (int c = lane; c < d; c += 32) {
+        const double v = y[c] - mu[c];
+        ss += v * v;
+        mxv = fmax(mxv, fabs(v));
+    }
+    ss = warp_sum_d(ss);
+    mxv = warp_max_d(mxv);
     if (lane == 0) {
         nb[row] = ss;
         mx[row] = mxv;
@@ -104,12 +108,19 @@ __global__ void basis_consts_kernel(const double* __restrict__ nb, const double*
     }
 }
 
-// Landmark planes [m_pad x 64] K-major: columns [0, d) = (b - mu)*beta as fp16 hi/lo;
-// column d = -beta*|b - mu|^2/2 * 2^-s (hi/lo) — the landmark norm rides through
-// GEMM1 against a constant column on the point side, so the epilogue needs no
-// per-landmark term: t = R_i + acc*sx_i (see prep_rows_kernel). Rows >= m are 0.
+__device__ __forceinline__ void split_store(__half* hi, __half* lo, long long o, double a) {
+    const __half h = __double2half(a);
+    hi[o] = h;
+    lo[o] = __double2half(a - static_cast<double>(__half2float(h)));
+}
+
+// Landmark planes [m_pad x kd] K-major (kd % 64 == 0, kd > d): columns [0, d) =
+// (b - mu)*beta as fp16 hi/lo; column d = -beta*|b - mu|^2/2 * 2^-s (hi/lo) — the
+// landmark norm rides through GEMM1 against a constant column on the point side, so
+// the epilogue needs no per-landmark term: t = R_i + acc*sx_i (see prep_rows_kernel).
+// Columns (d, kd) and rows >= m are 0.
 __global__ void prep_landmarks_kernel(const double* __restrict__ Y, long long ldy, int m, int d,
-                                      const double* __restrict__ mu,
+                                      int kd, const double* __restrict__ mu,
                                       const BasisConsts* __restrict__ kc, __half* __restrict__ hi,
                                       __half* __restrict__ lo, int m_pad) {
     const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -117,36 +128,29 @@ __global__ void prep_landmarks_kernel(const double* __restrict__ Y, long long ld
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
     const double beta = kc->beta, aug = kc->aug;
     for (int row = warp_global; row < m_pad; row += nwarps) {
-        double v0 = 0.0, v1 = 0.0;
-        if (row < m) {
-            const double* y = Y + static_cast<long long>(row) * ldy;
-            if (lane < d) v0 = y[lane] - mu[lane];
-            if (lane + 32 < d) v1 = y[lane + 32] - mu[lane + 32];
+        const double* y = Y + static_cast<long long>(row) * ldy;
+        const long long base = static_cast<long long>(row) * kd;
+        double nb = 0.0;
+        for (int c = lane; c < kd; c += 32) {
+            const double v = (row < m && c < d) ? y[c] - mu[c] : 0.0;
+            nb += v * v;
+            if (c != d) split_store(hi, lo, base + c, v * beta);
         }
-        const double nb = warp_sum_d(v0 * v0 + v1 * v1);
-        double a0 = v0 * beta, a1 = v1 * beta;
-        const double w = row < m ? -0.5 * beta * nb * aug : 0.0;
-        if (lane == d) a0 = w;
-        if (lane + 32 == d) a1 = w;
-        const __half h0 = __double2half(a0), h1 = __double2half(a1);
-        const long long base = static_cast<long long>(row) * KD_MAX;
-        hi[base + lane] = h0;
-        hi[base + lane + 32] = h1;
-        lo[base + lane] = __double2half(a0 - static_cast<double>(__half2float(h0)));
-        lo[base + lane + 32] = __double2half(a1 - static_cast<double>(__half2float(h1)));
+        nb = warp_sum_d(nb);
+        if (lane == 0) split_store(hi, lo, base + d, row < m ? -0.5 * beta * nb * aug : 0.0);
     }
 }
 
-// Point rows [m_pad x 64] K-major, one warp per row (d <= 63): columns [0, d) =
-// (x - mu)*sigma_i as fp16 hi/lo with sigma_i = 2^(13 - e_i) per row (e_i >= s - 1
-// so that column d = sigma_i*2^s <= 2^14 — a power of two: exact in hi, lo = 0;
-// rows close to mu simply keep fewer leading zeros). With acc = GEMM1 (3 split
-// terms) = sigma_i*beta*(<x-mu, b-mu> - |b-mu|^2/2):
+// Point rows [m_pad x kd] K-major, one warp per row (kd % 64 == 0, kd > d): columns
+// [0, d) = (x - mu)*sigma_i as fp16 hi/lo with sigma_i = 2^(13 - e_i) per row (e_i >=
+// s - 1 so that column d = sigma_i*2^s <= 2^14 — a power of two: exact in hi, lo = 0;
+// rows close to mu simply keep fewer leading zeros). With acc = GEMM1 (3 split terms)
+// = sigma_i*beta*(<x-mu, b-mu> - |b-mu|^2/2):
 //   t = 13 + g*d2 = R_i + acc*sx_i,  R_i = 13 + g*|x-mu|^2,  sx_i = -2g/(sigma_i*beta)
 // (g = -gamma*log2 e), i.e. Z*2^13 = ex2(min(t, 13)): the reference's clamp of d2 at
 // 0 (kernel.cpp:49-51). aux[i] = (R_i, sx_i). Rows in [m, m_pad) are zero padding.
 // Sets *err if a row's entries would overflow fp16 (|x - mu| >= 2^28).
-__global__ void prep_rows_kernel(const double* __restrict__ X, long long ldx, int m, int d,
+__global__ void prep_rows_kernel(const double* __restrict__ X, long long ldx, int m, int d, int kd,
                                  const double* __restrict__ mu, const BasisConsts* __restrict__ kc,
                                  __half* __restrict__ hi, __half* __restrict__ lo,
                                  float2* __restrict__ aux, int m_pad, int* __restrict__ err) {
@@ -156,26 +160,23 @@ __global__ void prep_rows_kernel(const double* __restrict__ X, long long ldx, in
     const double beta = kc->beta, aug = kc->aug, g = kc->g;
     const int s_exp = -ilogb(aug);
     for (int row = warp_global; row < m_pad; row += nwarps) {
-        double v0 = 0.0, v1 = 0.0;
-        if (row < m) {
-            const double* x = X + static_cast<long long>(row) * ldx;
-            if (lane < d) v0 = x[lane] - mu[lane];
-            if (lane + 32 < d) v1 = x[lane + 32] - mu[lane + 32];
-        }
-        const double ss = warp_sum_d(v0 * v0 + v1 * v1);
-        const double mx = warp_max_d(fmax(fabs(v0), fabs(v1)));
+        const double* x = X + static_cast<long long>(row) * ldx;
+        const long long base = static_cast<long long>(row) * kd;
+        double ss = 0.0, mx = 0.0;
+        if (row < m)
+            for (int c = lane; c < d; c += 32) {
+                const double v = x[c] - mu[c];
+                ss += v * v;
+                mx = fmax(mx, fabs(v));
+            }
+        ss = warp_sum_d(ss);
+        mx = warp_max_d(mx);
         const int e = max(clamp_exp(mx), s_exp - 1);
         const double sigma = ldexp(1.0, 13 - e);
-        double a0 = v0 * sigma, a1 = v1 * sigma;
-        const double w = sigma / aug;
-        if (lane == d) a0 = w;
-        if (lane + 32 == d) a1 = w;
-        const __half h0 = __double2half(a0), h1 = __double2half(a1);
-        const long long base = static_cast<long long>(row) * KD_MAX;
-        hi[base + lane] = h0;
-        hi[base + lane + 32] = h1;
-        lo[base + lane] = __double2half(a0 - static_cast<double>(__half2float(h0)));
-        lo[base + lane + 32] = __double2half(a1 - static_cast<double>(__half2float(h1)));
+        for (int c = lane; c < kd; c += 32) {
+            const double v = (row < m && c < d) ? x[c] - mu[c] : 0.0;
+            split_store(hi, lo, base + c, c == d ? sigma / aug : v * sigma);
+        }
         if (lane == 0) {
             aux[row] = make_float2(static_cast<float>(13.0 + g * ss),
                                    static_cast<float>(-2.0 * g / (sigma * beta)));
@@ -202,15 +203,22 @@ __global__ void csr_to_dense_kernel(const int64_t* __restrict__ indptr,
     }
 }
 
-// μ = column mean of the landmark rows (fp64). One thread per column.
+// mu = column mean of the landmark rows (fp64), mu[c] = 0 for c in [d, kd).
+// Block (32, 8) per 32 columns: coalesced row reads, shared-memory reduction.
 __global__ void column_mean_kernel(const double* __restrict__ Y, long long ldy, int m, int d,
-                                   double* __restrict__ mu) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= KD_MAX) return;
+                                   int kd, double* __restrict__ mu) {
+    __shared__ double part[8][33];
+    const int c = blockIdx.x * 32 + threadIdx.x;
     double s = 0.0;
     if (c < d)
-        for (int r = 0; r < m; ++r) s += Y[static_cast<long long>(r) * ldy + c];
-    mu[c] = (c < d && m > 0) ? s / m : 0.0;
+        for (int r = threadIdx.y; r < m; r += 8) s += Y[static_cast<long long>(r) * ldy + c];
+    part[threadIdx.y][threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.y == 0 && c < kd) {
+        double t = 0.0;
+        for (int k = 0; k < 8; ++k) t += part[k][threadIdx.x];
+        mu[c] = (c < d && m > 0) ? t / m : 0.0;
+    }
 }
 
 // Column max |L[:, k]| over the B rows (fp64), L row-major [B × b_eff].

@@ -95,6 +95,46 @@ def test_edge_shapes(gpu_ctx, n, d, B, beff_cut, gamma):
     assert_conditioned_parity(G, X, Y, L, gamma)
 
 
+@pytest.mark.parametrize("n,d,B,gamma,kind", [
+    (300, 64, 100, 0.05, "normal"),       # first d on the two-launch panel path
+    (700, 200, 300, 0.01, "normal"),      # B_pad = 512: two landmark blocks, b_eff > 256
+    (513, 130, 257, 0.02, "normal"),      # ragged rows / landmarks / columns
+    (1, 100, 1, 0.1, "normal"),           # single row, single landmark
+    (600, 2048, 512, 1.0 / 2048, "imagenet"),  # C4 feature shape: non-negative, non-centred
+])
+def test_large_d_panel_path(gpu_ctx, n, d, B, gamma, kind):
+    """d >= 64 runs the Z-panel GEMM + projection GEMM (panel_kernels.cuh)."""
+    rng = np.random.default_rng(n + d)
+    if kind == "imagenet":
+        from paper_2207_01016_b200 import synthetic
+
+        X, _ = synthetic.imagenet_like(n, d, 10, seed=4)
+    else:
+        X = rng.standard_normal((n, d)).astype(np.float32).astype(np.float64)
+    Y = X[rng.choice(n, min(B, n), replace=False)] if B <= n else rng.standard_normal((B, d))
+    L = np_gaussian_L(Y, gamma, 1e-10)
+    gpu_ctx.set_basis_dense(Y, L, gamma)
+    G = gpu_ctx.compute_g_dense(X)
+    assert G.shape == (n, L.shape[1]) and np.all(np.isfinite(G))
+    assert_conditioned_parity(G, X, Y, L, gamma)
+
+
+def test_large_d_device_entry_matches_host_entry(gpu_ctx):
+    """Device-resident path (panels, fp64 out) == host path (fp32 widened) bitwise."""
+    import torch
+
+    rng = np.random.default_rng(8)
+    X = rng.standard_normal((1000, 96)).astype(np.float32).astype(np.float64)
+    Y = X[:200]
+    L = np_gaussian_L(Y, 0.02, 1e-10)
+    gpu_ctx.set_basis_dense(Y, L, 0.02)
+    G_host = gpu_ctx.compute_g_dense(X)
+    Xd = torch.from_numpy(X).cuda()
+    Gd = torch.empty((1000, L.shape[1]), dtype=torch.float64, device="cuda")
+    gpu_ctx.compute_g_device(Xd, Gd)
+    assert np.array_equal(Gd.cpu().numpy(), G_host)
+
+
 def test_empty_and_duplicate_points(gpu_ctx):
     rng = np.random.default_rng(4)
     X = rng.standard_normal((260, 12))
@@ -151,8 +191,13 @@ def test_error_behaviour(gpu_ctx):
     gpu_ctx.set_basis_dense(Y, np.eye(10), 1.0)
     with pytest.raises(ValueError, match="dimension"):
         gpu_ctx.compute_g_dense(np.zeros((3, 6)))
-    with pytest.raises(P.LpdError):
-        gpu_ctx.set_basis_dense(np.zeros((4, 65)), np.eye(4), 1.0)  # d > 64: outside this kernel's envelope
+    with pytest.raises(P.LpdError):  # outside the envelope: d > 65536
+        gpu_ctx.set_basis_dense(np.zeros((1, 65537)), np.eye(1), 1.0)
+    with pytest.raises(P.LpdError):  # features beyond the split-fp16 range (|x - mean| >= 2^28)
+        gpu_ctx.set_basis_dense(Y, np.eye(10), 1.0)
+        X = np.zeros((3, 5))
+        X[1, 2] = 2.0**29
+        gpu_ctx.compute_g_dense(X)
 
 
 def test_decision_values(gpu_ctx):
