@@ -63,12 +63,12 @@ def load_peaks():
         return {"tflops": 1590.0, "hbm": 6650.0, "src": "fallback"}
 
 
-def load_traffic():
-    """dram read+write bytes per K1 launch on this workload from the committed ncu
-    summary (profiles/), or None."""
+def load_traffic(workload):
+    """dram read+write bytes per launch of this workload's dominant kernel, from the
+    committed ncu --set full summaries (profiles/traffic.json), or None."""
     try:
-        with open(os.path.join(ROOT, "profiles", "k1_c2_traffic.json")) as f:
-            return json.load(f)
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f)[workload]["bytes"]
     except Exception:
         return None
 
@@ -129,20 +129,31 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def make_basis(X0, cfg, seed=1):
+def make_basis(X0, cfg, seed=1, device=None):
     """Landmarks: B rows of rank 0's data drawn uniformly without replacement
     (as the reference's select_landmarks does, factor.cpp:27-31; numpy's seeded
-    generator here); L from the eigendecomposition of K (factor.cpp:33-81;
-    numpy LAPACK, setup only, outside the timed region)."""
+    generator here); L from the eigendecomposition of K (factor.cpp:33-81).
+    Setup only, outside the timed region: numpy LAPACK for B <= 8192, cuSOLVER
+    through torch on the GPU for larger bases (C4: B = 16384)."""
     ids = np.random.default_rng(seed).choice(X0.shape[0], cfg.budget, replace=False)
     Y = np.ascontiguousarray(X0[ids])
-    ny = (Y * Y).sum(1)
-    K = np.exp(-cfg.gamma * np.maximum(ny[:, None] + ny[None, :] - 2.0 * Y @ Y.T, 0.0))
-    w, U = np.linalg.eigh(0.5 * (K + K.T))
-    w, U = w[::-1], U[:, ::-1]
+    if cfg.budget <= 8192 or device is None:
+        ny = (Y * Y).sum(1)
+        K = np.exp(-cfg.gamma * np.maximum(ny[:, None] + ny[None, :] - 2.0 * Y @ Y.T, 0.0))
+        w, U = np.linalg.eigh(0.5 * (K + K.T))
+        w, U = w[::-1], U[:, ::-1]
+        keep = w > 1e-12 * w[0]
+        return Y, np.ascontiguousarray(U[:, keep] / np.sqrt(w[keep]))
+    import torch
+
+    Yt = torch.from_numpy(Y).to(device)
+    ny = (Yt * Yt).sum(1)
+    K = torch.exp(-cfg.gamma * torch.clamp(ny[:, None] + ny[None, :] - 2.0 * Yt @ Yt.T, min=0.0))
+    w, U = torch.linalg.eigh(0.5 * (K + K.T))
+    w, U = torch.flip(w, [0]), torch.flip(U, [1])
     keep = w > 1e-12 * w[0]
-    L = np.ascontiguousarray(U[:, keep] / np.sqrt(w[keep]))
-    return Y, L
+    L = (U[:, keep] / torch.sqrt(w[keep])).contiguous()
+    return Y, L.cpu().numpy()
 
 
 def cpu_reference_rate(X, Y, L, gamma, target_s, threads, max_rows):
@@ -167,11 +178,13 @@ def run_reference(args, cfg, rank):
         return
     from oracle import oracle as O
 
-    n = args.rows or cfg.n
     from paper_2207_01016_b200 import synthetic
 
-    X, _ = synthetic.blobs(n, cfg.d, cfg.seed)
-    Y, L = make_basis(X, cfg)
+    n = args.rows or synthetic.rows_per_gpu(cfg)
+    X, _ = synthetic.make(cfg, rows=slice(0, n), n=max(n, cfg.n))
+    import torch
+
+    Y, L = make_basis(X, cfg, device="cuda" if torch.cuda.is_available() else None)
     threads = O.ref_lib().ref_hardware_threads()
     # size each step so warmup + steps stay within a few minutes
     per_step = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
@@ -227,12 +240,12 @@ def main():
 
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    n = args.rows or cfg.n
+    n = args.rows or synthetic.rows_per_gpu(cfg)
     N = world
     # weak scaling: this rank's rows of an N·n-row dataset
-    X, _ = synthetic.blobs(N * n, cfg.d, cfg.seed, rows=slice(rank * n, (rank + 1) * n))
+    X, _ = synthetic.make(cfg, rows=slice(rank * n, (rank + 1) * n), n=N * n)
     if rank == 0:
-        Y, L = make_basis(X, cfg)
+        Y, L = make_basis(X, cfg, device=dev)
         meta = torch.tensor([Y.shape[0], L.shape[1]], dtype=torch.int64, device=dev)
     else:
         meta = torch.zeros(2, dtype=torch.int64, device=dev)
@@ -286,11 +299,17 @@ def main():
     F = 2.0 * n * B * cfg.d + 2.0 * n * B * b_eff
     peaks = load_peaks()
     achieved = F / (k_ms / 1e3) / 1e12
-    traffic = load_traffic()
+    traffic = load_traffic(cfg.name)
     # issued tensor work (3-term split, padded shapes, GEMM1 recomputed per 256-column block)
-    npad, bpad, epad = -(-n // 256) * 256, -(-B // 64) * 64, -(-b_eff // 256) * 256
-    k1 = -(-(cfg.d + 1) // 16) * 16  # d features + the augmented norm column
-    issued = 3 * (2.0 * npad * bpad * k1 * (epad // 256) + 2.0 * npad * bpad * epad)
+    npad, epad = -(-n // 256) * 256, -(-b_eff // 256) * 256
+    if cfg.d <= 63:  # fused kernel: GEMM1 (d + norm column, 16-wide K steps) per 256-column block
+        bpad = -(-B // 64) * 64
+        k1 = -(-(cfg.d + 1) // 16) * 16
+        issued = 3 * (2.0 * npad * bpad * k1 * (epad // 256) + 2.0 * npad * bpad * epad)
+    else:  # panel path: Z GEMM once (K = d + norm column, 64-wide chunks), then the projection
+        bpad = -(-B // 256) * 256
+        kd = -(-(cfg.d + 1) // 64) * 64
+        issued = 3 * (2.0 * npad * bpad * kd + 2.0 * npad * bpad * epad)
 
     # ---------------- end to end through the C ABI with host buffers ----------------
     e2e = None
@@ -356,10 +375,13 @@ def main():
             "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None,
             "dtype": "f16x3 split operands, f32 accumulate, f64 G",
-            "data": "synthetic (covtype-shaped two-class blobs, seed 2; landmarks = reference select_landmarks)",
+            "data": (f"synthetic ({'1000-class non-negative ImageNet-feature-shaped' if cfg.classes > 2 else 'two-class Gaussian blobs'}"
+                     f", seed {cfg.seed}; landmarks drawn like the reference select_landmarks, L from eigh(K))"),
             "config": {"workload": cfg.name, "n_per_gpu": n, "d": cfg.d, "B": B, "b_eff": b_eff,
                        "gamma": cfg.gamma, "parallelism": f"rows sharded over {N} GPU(s), basis broadcast",
-                       "l2": "inputs larger than L2 (G 19 GB/step per GPU written, X 0.25 GB read)"},
+                       "path": "fused K1 (d <= 63)" if cfg.d <= 63 else "panel path: Z GEMM + projection GEMM (d >= 64)",
+                       "l2": f"inputs larger than L2 (G {n * b_eff * 8 / 1e9:.1f} GB/step per GPU written, "
+                             f"X {X.nbytes / 1e9:.2f} GB read)"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peaks["tflops"], "unit": "TFLOP/s",
                          "frac": achieved / peaks["tflops"], "traffic": traffic,
                          "kernel_ms": k_ms, "flops_per_launch": F, "issued_tensor_flops_per_launch": issued,

@@ -18,7 +18,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-__all__ = ["Config", "CONFIGS", "blobs", "imagenet_like", "make"]
+__all__ = ["Config", "CONFIGS", "blobs", "imagenet_like", "make", "rows_per_gpu"]
 
 
 @dataclass(frozen=True)
@@ -31,13 +31,20 @@ class Config:
     C: float
     seed: int
     classes: int = 2
+    rows_per_gpu: int = 0  # bench: rows per GPU (weak scaling); 0 = n
+
+
+def rows_per_gpu(cfg: "Config") -> int:
+    return cfg.rows_per_gpu or cfg.n
 
 
 CONFIGS = {
     "c1": Config("c1_blobs", 20_000, 50, 1_000, 0.02, 1.0, 1),
     "c2": Config("c2_covtype_shaped", 581_012, 54, 4_096, 1.0 / 54, 1.0, 2),
-    "c3": Config("c3_susy_shaped", 5_000_000, 18, 8_192, 1.0 / 18, 1.0, 3),
-    "c4": Config("c4_imagenet_shaped", 1_281_167, 2048, 16_384, 1.0 / 2048, 1.0, 4, classes=1000),
+    # C3/C4 are row-sharded over 8 GPUs in BASELINE.json: a GPU owns n/8 rows
+    "c3": Config("c3_susy_shaped", 5_000_000, 18, 8_192, 1.0 / 18, 1.0, 3, rows_per_gpu=625_000),
+    "c4": Config("c4_imagenet_shaped", 1_281_167, 2048, 16_384, 1.0 / 2048, 1.0, 4, classes=1000,
+                 rows_per_gpu=160_146),
 }
 
 
@@ -85,7 +92,9 @@ def imagenet_like(n: int, d: int, classes: int, seed: int, rows: slice | None = 
     return X, y
 
 
-def make(cfg: Config, rows: slice | None = None):
+def make(cfg: Config, rows: slice | None = None, n: int | None = None):
+    """Rows `rows` of the config's n-row (or `n`-row) dataset."""
+    n = cfg.n if n is None else n
     if cfg.classes > 2:
-        return imagenet_like(cfg.n, cfg.d, cfg.classes, cfg.seed, rows)
-    return blobs(cfg.n, cfg.d, cfg.seed, rows)
+        return imagenet_like(n, cfg.d, cfg.classes, cfg.seed, rows)
+    return blobs(n, cfg.d, cfg.seed, rows)
