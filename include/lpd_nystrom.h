@@ -116,6 +116,19 @@ int lpd_decision_values_device(lpd_context* ctx, int device_index, const void* G
 int lpd_decision_values(lpd_context* ctx, const double* G, int64_t n, int64_t b_eff, int64_t ldg,
                         const double* W, int64_t P, double* D, int64_t ldd);
 
+/* One-vs-one prediction (K5): the basis must have been set with L := betasᵀ
+ * (B x P, P = num_classes*(num_classes-1)/2, the reference's OvoModel::betas
+ * transposed, proj/include/lpdsvm/multiclass.hpp:57-68). Computes the decision values
+ * Z(x, landmarks)·betasᵀ on the device and the majority vote
+ * (proj/src/multiclass.cpp:153-168); classes[i] receives the winning class INDEX
+ * (into the model's LabelMap) for row i. Replaces lpdsvm::ovo_predict
+ * (multiclass.cpp:170-200). num_classes <= 2048. */
+int lpd_predict_ovo_dense(lpd_context* ctx, const double* X, int64_t n, int64_t d, int64_t ldx,
+                          int64_t num_classes, int32_t* classes);
+int lpd_predict_ovo_csr(lpd_context* ctx, int64_t n, int64_t d, const int64_t* indptr,
+                        const int32_t* indices, const double* values, int64_t num_classes,
+                        int32_t* classes);
+
 /* Last kernel timing of the fused factor kernel on device_index (milliseconds,
  * CUDA events around the launch on its stream), for benchmarks. */
 double lpd_last_factor_kernel_ms(const lpd_context* ctx, int device_index);

@@ -66,6 +66,8 @@ EXPORTED_SYMBOLS = (
     "lpd_last_factor_kernel_ms",
     "lpd_set_basis_device",
     "lpd_factor_kernel_stats",
+    "lpd_predict_ovo_dense",
+    "lpd_predict_ovo_csr",
 )
 
 
@@ -144,6 +146,8 @@ def load_library(path: Optional[str] = None) -> ctypes.CDLL:
     lib.lpd_set_basis_device.argtypes = [vp, ctypes.c_int, vp, i64, i64, i64, vp, i64, ctypes.c_double, vp]
     lib.lpd_factor_kernel_stats.argtypes = [vp, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
                                             ctypes.POINTER(ctypes.c_int64), ctypes.c_int]
+    lib.lpd_predict_ovo_dense.argtypes = [vp, _c_dbl_p, i64, i64, i64, i64, _c_i32_p]
+    lib.lpd_predict_ovo_csr.argtypes = [vp, i64, i64, _c_i64_p, _c_i32_p, _c_dbl_p, i64, _c_i32_p]
     if path is None:
         _lib = lib
     return lib
@@ -341,6 +345,26 @@ class Context:
         return float(self._lib.lpd_last_factor_kernel_ms(self._h, device_index))
 
     # ---------------------------------------------------------------- decision values
+    def predict_ovo_dense(self, X: np.ndarray, num_classes: int) -> np.ndarray:
+        """Class indices of the one-vs-one vote for dense rows X; the basis must
+        have been set with L := betas.T (reference ovo_predict, multiclass.cpp:170-200)."""
+        x = _f64(X)
+        out = np.empty(x.shape[0], dtype=np.int32)
+        _check(self._lib.lpd_predict_ovo_dense(self._h, _ptr(x), x.shape[0], x.shape[1], x.shape[1],
+                                               num_classes, _ptr(out, ctypes.c_int32)))
+        return out
+
+    def predict_ovo_csr(self, indptr, indices, values, num_classes: int) -> np.ndarray:
+        ip = np.ascontiguousarray(indptr, dtype=np.int64)
+        ix = np.ascontiguousarray(indices, dtype=np.int32)
+        vv = _f64(values)
+        n = ip.shape[0] - 1
+        out = np.empty(n, dtype=np.int32)
+        _check(self._lib.lpd_predict_ovo_csr(self._h, n, self.dim, _ptr(ip, ctypes.c_int64),
+                                             _ptr(ix, ctypes.c_int32), _ptr(vv), num_classes,
+                                             _ptr(out, ctypes.c_int32)))
+        return out
+
     def decision_values(self, G: np.ndarray, W: np.ndarray) -> np.ndarray:
         g = _f64(G)
         w = _f64(W)

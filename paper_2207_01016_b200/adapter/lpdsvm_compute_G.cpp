@@ -1,4 +1,5 @@
-// lpdsvm_compute_G.cpp — the drop-in: a strong definition of
+// lpdsvm_compute_G.cpp — the drop-in: strong definitions of lpdsvm::ovo_predict (below)
+// and
 //
 //   lpdsvm::Matrix lpdsvm::compute_G(std::span<const SparseVector> points,
 //                                    std::span<const double> norms,
@@ -41,6 +42,7 @@
 #include "lpdsvm/factor.hpp"
 #include "lpdsvm/kernel.hpp"
 #include "lpdsvm/matrix.hpp"
+#include "lpdsvm/multiclass.hpp"
 #include "lpd_nystrom.h"
 
 namespace {
@@ -48,6 +50,7 @@ namespace {
 std::mutex g_mu;
 lpd_context* g_ctx = nullptr;
 std::atomic<long long> g_calls{0};
+std::atomic<long long> g_predict_calls{0};
 lpd_timings g_last{};
 
 [[noreturn]] void rethrow_status(int status, const char* what) {
@@ -153,11 +156,59 @@ Matrix compute_G(std::span<const SparseVector> points, std::span<const double> /
     return G;
 }
 
+// Strong definition of
+//   std::vector<double> lpdsvm::ovo_predict(const OvoModel&, std::span<const SparseVector>, int)
+// (reference proj/include/lpdsvm/multiclass.hpp:80-82, proj/src/multiclass.cpp:170-200),
+// which integration/Makefile weakens in multiclass.o: the decision values
+// Z(points, landmarks)·betasᵀ are the factor kernel with L := betasᵀ (B × P), and the
+// vote (multiclass.cpp:153-168) runs on the device (lpd_predict_ovo_csr). Reached from
+// Model.predict / Model.error_rate (module.cpp:136-156) and predict_file
+// (model_io.cpp:245-260).
+std::vector<double> ovo_predict(const OvoModel& model, std::span<const SparseVector> points,
+                                int num_threads) {
+    const std::size_t n = points.size();
+    const std::size_t c = model.num_classes();
+    const std::size_t P = model.num_pairs();
+    const std::size_t b = model.landmarks.size();
+    std::vector<double> predictions(n);
+    if (n == 0) return predictions;
+    if (P == 0) {  // one class: the reference's empty vote picks class 0
+        for (double& v : predictions) v = model.label_map.classes[0];
+        return predictions;
+    }
+    validate(model.kernel);
+    std::lock_guard<std::mutex> lock(g_mu);
+    ++g_predict_calls;
+    const int threads = std::max(1, num_threads);
+    Csr xs = flatten(points, threads);
+    Csr ls = flatten(model.landmarks, threads);
+    const int64_t d = std::max<int64_t>(1, 1 + std::max(xs.max_index, ls.max_index));
+    // betas is P × B (multiclass.hpp:63): the projection operand is its transpose
+    Matrix bt(b, P);
+    for (std::size_t p = 0; p < P; ++p)
+        for (std::size_t j = 0; j < b; ++j) bt(j, p) = model.betas(p, j);
+    lpd_context* ctx = context();
+    int rc = lpd_set_basis_csr(ctx, static_cast<int64_t>(b), d, ls.indptr.data(), ls.indices.data(),
+                               ls.values.data(), bt.data(), static_cast<int64_t>(P),
+                               model.kernel.gamma);
+    if (rc != LPD_OK) rethrow_status(rc, "lpd_set_basis_csr");
+    std::vector<int32_t> cls(n);
+    rc = lpd_predict_ovo_csr(ctx, static_cast<int64_t>(n), d, xs.indptr.data(), xs.indices.data(),
+                             xs.values.data(), static_cast<int64_t>(c), cls.data());
+    if (rc != LPD_OK) rethrow_status(rc, "lpd_predict_ovo_csr");
+    for (std::size_t i = 0; i < n; ++i)
+        predictions[i] = model.label_map.classes[static_cast<std::size_t>(cls[i])];
+    return predictions;
+}
+
 }  // namespace lpdsvm
 
 // Introspection for the integration tests: proves the reference's call went here.
 extern "C" __attribute__((visibility("default"))) long long lpd_adapter_calls(void) {
     return g_calls.load();
+}
+extern "C" __attribute__((visibility("default"))) long long lpd_adapter_predict_calls(void) {
+    return g_predict_calls.load();
 }
 extern "C" __attribute__((visibility("default"))) void lpd_adapter_last_timings(lpd_timings* out) {
     std::lock_guard<std::mutex> lock(g_mu);

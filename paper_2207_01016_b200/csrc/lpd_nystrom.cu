@@ -173,6 +173,10 @@ struct DeviceState {
     int64_t B = 0, d = 0, b_eff = 0, B_pad = 0, Beff_pad = 0;
     int64_t kd = lpd::KD_MAX;  // plane width: 64 (fused path, d <= 63) or round_up(d + 1, 64)
     bool large = false;        // d >= 64: two-launch panel path (panel_kernels.cuh)
+    int2* pairs = nullptr;     // OVO pair table for the vote (K5)
+    int pairs_classes = 0;
+    int32_t* votes = nullptr;  // per-chunk predicted class indices
+    int64_t votes_cap = 0;
     __half* z_hi = nullptr;    // large path: Z panel scratch [z_rows × B_pad]
     __half* z_lo = nullptr;
     int64_t z_rows = 0;
@@ -245,6 +249,9 @@ void ensure_slot(DeviceState& ds, Slot& s, int64_t rows, bool need_g, int64_t nn
         }
         s.g_cols = need_g ? ds.b_eff : 0;
         s.rows_cap = cap;
+        // indptr is sized by rows_cap: re-create the CSR staging with the new capacity
+        dev_free(s.indptr); dev_free(s.indices); dev_free(s.values);
+        s.nnz_cap = 0;
     }
     if (nnz > s.nnz_cap) {
         dev_free(s.indptr); dev_free(s.indices); dev_free(s.values);
@@ -733,6 +740,93 @@ void compute_rows_host(lpd_context* ctx, int64_t n, double* G, int64_t ldg, lpd_
     }
 }
 
+// Stages CSR rows [r0, r0 + rows) into slot.x as dense fp64 (H2D of the chunk's
+// CSR arrays + device densify), recording ev[0]. Zeros are implicit, as in the
+// reference's SparseVector (dataio.hpp:23-24).
+void stage_csr_rows(DeviceState& ds, Slot& s, int64_t r0, int64_t rows, int64_t d,
+                    const int64_t* indptr, const int32_t* indices, const double* values) {
+    const int64_t e0 = indptr[r0], e1 = indptr[r0 + rows];
+    ensure_slot(ds, s, rows, true, e1 - e0);
+    // rebase indptr for this chunk on the host (small), then densify on device
+    std::vector<int64_t> ip(static_cast<size_t>(rows + 1));
+    for (int64_t i = 0; i <= rows; ++i) ip[i] = indptr[r0 + i] - e0;
+    CUDA_TRY(cudaEventRecord(s.ev[0], s.stream));
+    CUDA_TRY(cudaMemcpyAsync(s.indptr, ip.data(), sizeof(int64_t) * (rows + 1), cudaMemcpyHostToDevice,
+                             s.stream));
+    if (e1 > e0) {
+        CUDA_TRY(cudaMemcpyAsync(s.indices, indices + e0, sizeof(int32_t) * (e1 - e0),
+                                 cudaMemcpyHostToDevice, s.stream));
+        CUDA_TRY(cudaMemcpyAsync(s.values, values + e0, sizeof(double) * (e1 - e0),
+                                 cudaMemcpyHostToDevice, s.stream));
+    }
+    if (d > 0)
+        lpd::csr_to_dense_kernel<<<static_cast<int>((rows + 7) / 8), 256, 0, s.stream>>>(
+            s.indptr, s.indices, s.values, static_cast<int>(rows), static_cast<int>(d), s.x);
+    CUDA_TRY(cudaGetLastError());
+    // ip must outlive the async copy: synchronise the H2D before returning
+    CUDA_TRY(cudaStreamSynchronize(s.stream));
+}
+
+// Prediction (K5 = K1 with L := betasᵀ, then the OVO vote) for host rows: per
+// device shard and row chunk, stage_x -> prep -> factor kernel writing the fp32
+// decision values D (n × P) into the slot's G buffer -> vote kernel -> class
+// indices D2H. Reference: ovo_predict (multiclass.cpp:170-200), vote (:153-168).
+template <typename StageX>
+void predict_rows_host(lpd_context* ctx, int64_t n, int64_t num_classes, int32_t* out,
+                       StageX&& stage_x) {
+    const int nd = static_cast<int>(ctx->dev.size());
+    const int64_t P = ctx->dev[0].b_eff;
+    const int64_t chunk = std::max<int64_t>(
+        256, std::min<int64_t>(round_up(n, 256), (128ll << 20) / (4 * P) / 256 * 256));
+    run_parallel(ctx, [&](DeviceState& ds, int di) {
+        CUDA_TRY(cudaSetDevice(ds.device));
+        const int64_t per = round_up((n + nd - 1) / nd, 256);
+        const int64_t r_begin = std::min<int64_t>(n, per * di);
+        const int64_t r_end = std::min<int64_t>(n, per * (di + 1));
+        Slot& s = ds.slot[0];
+        if (ds.pairs_classes != num_classes) {
+            dev_free(ds.pairs);
+            dev_alloc(&ds.pairs, static_cast<size_t>(P));
+            lpd::ovo_pair_table_kernel<<<static_cast<int>(num_classes), 128, 0, s.stream>>>(
+                static_cast<int>(num_classes), ds.pairs);
+            CUDA_TRY(cudaGetLastError());
+            ds.pairs_classes = static_cast<int>(num_classes);
+        }
+        if (ds.votes_cap < chunk) {
+            dev_free(ds.votes);
+            dev_alloc(&ds.votes, static_cast<size_t>(chunk));
+            ds.votes_cap = chunk;
+        }
+        for (int64_t r0 = r_begin; r0 < r_end; r0 += chunk) {
+            const int64_t rows = std::min(chunk, r_end - r0);
+            stage_x(ds, s, r0, rows);
+            launch_factor(ds, s, s.x, rows, ds.d, s.g, s.g_ld, LPD_OUT_F32, s.stream, false);
+            const int blocks = static_cast<int>(std::min<int64_t>((rows + lpd::VOTE_WARPS - 1) / lpd::VOTE_WARPS,
+                                                                  static_cast<int64_t>(ds.num_sms) * 8));
+            lpd::ovo_vote_kernel<float><<<blocks, 32 * lpd::VOTE_WARPS,
+                                          sizeof(int) * lpd::VOTE_WARPS * num_classes, s.stream>>>(
+                static_cast<const float*>(s.g), s.g_ld, static_cast<int>(rows),
+                static_cast<int>(num_classes), ds.pairs, static_cast<int>(P), ds.votes);
+            CUDA_TRY(cudaGetLastError());
+            CUDA_TRY(cudaMemcpyAsync(out + r0, ds.votes, sizeof(int32_t) * rows, cudaMemcpyDeviceToHost,
+                                     s.stream));
+            CUDA_TRY(cudaStreamSynchronize(s.stream));
+        }
+        check_range_flag(ds);
+    });
+}
+
+void check_predict_args(lpd_context* ctx, int64_t n, int64_t num_classes, const int32_t* out) {
+    if (n < 0) fail(LPD_ERR_INVALID_ARGUMENT, "negative row count");
+    if (num_classes < 2 || num_classes > lpd::VOTE_MAX_CLASSES)
+        fail(num_classes < 2 ? LPD_ERR_INVALID_ARGUMENT : LPD_ERR_UNSUPPORTED,
+             "num_classes must be in [2, " + std::to_string(lpd::VOTE_MAX_CLASSES) + "]");
+    if (ctx->dev[0].b_eff != num_classes * (num_classes - 1) / 2)
+        fail(LPD_ERR_INVALID_ARGUMENT,
+             "basis projection must have num_classes*(num_classes-1)/2 columns (betas transposed)");
+    if (n > 0 && !out) fail(LPD_ERR_INVALID_ARGUMENT, "null output");
+}
+
 }  // namespace
 
 // =================================================================== C ABI
@@ -809,6 +903,8 @@ int lpd_context_destroy(lpd_context* ctx) {
         ds.free_basis();
         dev_free(ds.colmax);
         dev_free(ds.err);
+        dev_free(ds.pairs);
+        dev_free(ds.votes);
         for (auto& s : ds.slot) {
             ds.free_slot(s);
             if (s.stream) cudaStreamDestroy(s.stream);
@@ -931,26 +1027,7 @@ int lpd_compute_g_csr(lpd_context* ctx, int64_t n, int64_t d, const int64_t* ind
         if (ldg < b_eff) fail(LPD_ERR_INVALID_ARGUMENT, "ldg < b_eff");
         if (n > 0 && (!G || !indptr)) fail(LPD_ERR_INVALID_ARGUMENT, "null buffer");
         compute_rows_host(ctx, n, G, ldg, timings, [&](DeviceState& ds, Slot& s, int64_t r0, int64_t rows) {
-            const int64_t e0 = indptr[r0], e1 = indptr[r0 + rows];
-            ensure_slot(ds, s, rows, true, e1 - e0);
-            // rebase indptr for this chunk on the host (small), then densify on device
-            std::vector<int64_t> ip(static_cast<size_t>(rows + 1));
-            for (int64_t i = 0; i <= rows; ++i) ip[i] = indptr[r0 + i] - e0;
-            CUDA_TRY(cudaEventRecord(s.ev[0], s.stream));
-            CUDA_TRY(cudaMemcpyAsync(s.indptr, ip.data(), sizeof(int64_t) * (rows + 1),
-                                     cudaMemcpyHostToDevice, s.stream));
-            if (e1 > e0) {
-                CUDA_TRY(cudaMemcpyAsync(s.indices, indices + e0, sizeof(int32_t) * (e1 - e0),
-                                         cudaMemcpyHostToDevice, s.stream));
-                CUDA_TRY(cudaMemcpyAsync(s.values, values + e0, sizeof(double) * (e1 - e0),
-                                         cudaMemcpyHostToDevice, s.stream));
-            }
-            if (d > 0)
-                lpd::csr_to_dense_kernel<<<static_cast<int>((rows + 7) / 8), 256, 0, s.stream>>>(
-                    s.indptr, s.indices, s.values, static_cast<int>(rows), static_cast<int>(d), s.x);
-            CUDA_TRY(cudaGetLastError());
-            // ip must outlive the async copy: synchronise the H2D before returning
-            CUDA_TRY(cudaStreamSynchronize(s.stream));
+            stage_csr_rows(ds, s, r0, rows, d, indptr, indices, values);
         });
     });
 }
@@ -1091,6 +1168,39 @@ int lpd_decision_values(lpd_context* ctx, const double* G, int64_t n, int64_t b_
             throw;
         }
         cleanup();
+    });
+}
+
+int lpd_predict_ovo_dense(lpd_context* ctx, const double* X, int64_t n, int64_t d, int64_t ldx,
+                          int64_t num_classes, int32_t* classes) {
+    return guarded([&] {
+        check_ctx(ctx, true);
+        check_predict_args(ctx, n, num_classes, classes);
+        if (d != ctx->dev[0].d) fail(LPD_ERR_INVALID_ARGUMENT, "point dimension does not match the basis");
+        if (ldx < d) fail(LPD_ERR_INVALID_ARGUMENT, "ldx < d");
+        if (n > 0 && !X && d > 0) fail(LPD_ERR_INVALID_ARGUMENT, "null buffer");
+        predict_rows_host(ctx, n, num_classes, classes, [&](DeviceState& ds, Slot& s, int64_t r0, int64_t rows) {
+            ensure_slot(ds, s, rows, true, 0);
+            CUDA_TRY(cudaEventRecord(s.ev[0], s.stream));
+            if (d > 0)
+                CUDA_TRY(cudaMemcpy2DAsync(s.x, sizeof(double) * d, X + r0 * ldx, sizeof(double) * ldx,
+                                           sizeof(double) * d, static_cast<size_t>(rows),
+                                           cudaMemcpyHostToDevice, s.stream));
+        });
+    });
+}
+
+int lpd_predict_ovo_csr(lpd_context* ctx, int64_t n, int64_t d, const int64_t* indptr,
+                        const int32_t* indices, const double* values, int64_t num_classes,
+                        int32_t* classes) {
+    return guarded([&] {
+        check_ctx(ctx, true);
+        check_predict_args(ctx, n, num_classes, classes);
+        if (d != ctx->dev[0].d) fail(LPD_ERR_INVALID_ARGUMENT, "point dimension does not match the basis");
+        if (n > 0 && !indptr) fail(LPD_ERR_INVALID_ARGUMENT, "null buffer");
+        predict_rows_host(ctx, n, num_classes, classes, [&](DeviceState& ds, Slot& s, int64_t r0, int64_t rows) {
+            stage_csr_rows(ds, s, r0, rows, d, indptr, indices, values);
+        });
     });
 }
 

@@ -249,3 +249,38 @@ def test_compute_G_mirror_sparse_points():
     G = P.compute_G(pts, None, lms, None, L, P.KernelParams(0.4), 4096)
     R = O.ora_compute_g((ip, ix, vv), (lp, li, lv), L, 0.4, 4096)
     assert row_rel_err(G, R) <= TOL_G
+
+
+@pytest.mark.parametrize("c,d,B", [(2, 20, 150), (5, 30, 200), (12, 90, 300)])
+def test_predict_ovo_matches_oracle(gpu_ctx, c, d, B):
+    """K5: decision values Z·betasᵀ on the device + the reference vote
+    (multiclass.cpp:153-168, 170-200). Classes agree with the oracle except on rows
+    whose smallest |decision| is within fp32-level rounding of 0."""
+    rng = np.random.default_rng(c * 7 + d)
+    n, gamma = 1500, 1.0 / d
+    X = rng.standard_normal((n, d)).astype(np.float32).astype(np.float64)
+    Y = X[rng.choice(n, B, replace=False)]
+    P_ = c * (c - 1) // 2
+    betas = rng.standard_normal((P_, B))
+    gpu_ctx.set_basis_dense(Y, np.ascontiguousarray(betas.T), gamma)
+    got = gpu_ctx.predict_ovo_dense(X, c)
+    Z = O.ora_kernel_block(O.dense_to_csr(X), O.dense_to_csr(Y), gamma)
+    D = Z @ betas.T
+    want = np.array([O.ora_vote(D[i], c) for i in range(n)])
+    margin = np.min(np.abs(D), axis=1) / np.max(np.abs(D))
+    clear = margin > 1e-4
+    assert clear.mean() > 0.9
+    assert np.array_equal(got[clear], want[clear])
+    # the CSR entry gives the same classes
+    ip, ix, vv, _ = P.sparse_to_csr(list(X))
+    assert np.array_equal(gpu_ctx.predict_ovo_csr(ip, ix, vv, c), got)
+
+
+def test_predict_ovo_argument_errors(gpu_ctx):
+    Y = np.eye(6)
+    gpu_ctx.set_basis_dense(Y, np.ones((6, 3)), 0.5)  # P = 3 <-> 3 classes
+    with pytest.raises(ValueError):
+        gpu_ctx.predict_ovo_dense(np.zeros((2, 6)), 4)  # 4 classes need 6 pairs
+    with pytest.raises(ValueError):
+        gpu_ctx.predict_ovo_dense(np.zeros((2, 6)), 1)
+    assert gpu_ctx.predict_ovo_dense(np.zeros((0, 6)), 3).shape == (0,)

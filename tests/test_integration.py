@@ -1,5 +1,5 @@
 """The drop-in: the reference's own Python API (`lpdsvm.train`, `cross_validate`,
-`Model.predict`) with lpdsvm::compute_G served by the B200 library
+`Model.predict`) with lpdsvm::compute_G and lpdsvm::ovo_predict served by the B200 library
 (integration/Makefile links paper_2207_01016_b200/adapter over the C ABI and
 weakens the reference definition). Compared against the unmodified reference
 build (oracle/_ref) on identical data, landmarks and host eig."""
@@ -14,6 +14,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 INTEG = os.path.join(ROOT, "integration", "_build")
 REF = os.path.join(ROOT, "oracle", "_ref")
 RUNNER = os.path.join(ROOT, "tests", "integration_train.py")
+OVO_PREDICT = ("_ZN6lpdsvm11ovo_predictERKNS_8OvoModelESt4spanIKSt6vectorINS_7FeatureESaIS5_EELm"
+               "18446744073709551615EEi")
 COMPUTE_G = ("_ZN6lpdsvm9compute_GESt4spanIKSt6vectorINS_7FeatureESaIS2_EELm18446744073709551615EES0_"
              "IKdLm18446744073709551615EES6_S8_RKNS_6MatrixERKNS_12KernelParamsEmi")
 
@@ -44,7 +46,8 @@ def test_override_is_linked():
     so = _core_so(INTEG)
     syms = subprocess.run(["nm", "-D", so], capture_output=True, text=True).stdout
     assert f"T {COMPUTE_G}" in syms
-    for s in ("lpd_set_basis_csr", "lpd_compute_g_csr", "lpd_context_create"):
+    assert f"T {OVO_PREDICT}" in syms
+    for s in ("lpd_set_basis_csr", "lpd_compute_g_csr", "lpd_context_create", "lpd_predict_ovo_csr"):
         assert f"U {s}" in syms
     weak = os.path.join(INTEG, "obj", "factor_weak.o")
     if os.path.exists(weak):
@@ -80,6 +83,8 @@ def test_reference_api_on_gpu_matches_reference(tmp_path, classes):
     r = np.load(tmp_path / "ref.npz")
     # train + cross_validate each build one factor through compute_G
     assert int(g["adapter_calls"]) >= 2
+    # Model.predict ran ovo_predict on the device (counter read right after it)
+    assert int(g["predict_calls"]) >= 1
     assert int(g["effective_rank"]) == int(r["effective_rank"])
     agree = float(np.mean(g["pred"] == r["pred"]))
     assert agree >= 0.99, agree
