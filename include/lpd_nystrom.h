@@ -129,6 +129,18 @@ int lpd_predict_ovo_csr(lpd_context* ctx, int64_t n, int64_t d, const int64_t* i
                         const int32_t* indices, const double* values, int64_t num_classes,
                         int32_t* classes);
 
+/* Kernel block K[i][j] = exp(-gamma * max(0, norms_a[i] + norms_b[j] - 2<a_i, b_j>)) in fp64
+ * with the reference's operation order (K7; replaces lpdsvm::kernel_block,
+ * proj/include/lpdsvm/kernel.hpp:26-32, proj/src/kernel.cpp:31-57, whose main caller is
+ * the landmark Gram matrix of build_factor_with_landmarks, factor.cpp:121-126). Rows are
+ * CSR; pass a_indptr / b_indptr = NULL to give dense row-major fp64 rows (ld = d) in
+ * a_values / b_values. out is m x n row-major (ld = ldo), host memory. Runs on the
+ * context's first device. */
+int lpd_kernel_block(lpd_context* ctx, int64_t m, const int64_t* a_indptr, const int32_t* a_indices,
+                     const double* a_values, const double* norms_a, int64_t n,
+                     const int64_t* b_indptr, const int32_t* b_indices, const double* b_values,
+                     const double* norms_b, int64_t d, double gamma, double* out, int64_t ldo);
+
 /* Last kernel timing of the fused factor kernel on device_index (milliseconds,
  * CUDA events around the launch on its stream), for benchmarks. */
 double lpd_last_factor_kernel_ms(const lpd_context* ctx, int device_index);

@@ -68,6 +68,7 @@ EXPORTED_SYMBOLS = (
     "lpd_factor_kernel_stats",
     "lpd_predict_ovo_dense",
     "lpd_predict_ovo_csr",
+    "lpd_kernel_block",
 )
 
 
@@ -146,6 +147,8 @@ def load_library(path: Optional[str] = None) -> ctypes.CDLL:
     lib.lpd_set_basis_device.argtypes = [vp, ctypes.c_int, vp, i64, i64, i64, vp, i64, ctypes.c_double, vp]
     lib.lpd_factor_kernel_stats.argtypes = [vp, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
                                             ctypes.POINTER(ctypes.c_int64), ctypes.c_int]
+    lib.lpd_kernel_block.argtypes = [vp, i64, _c_i64_p, _c_i32_p, _c_dbl_p, _c_dbl_p, i64, _c_i64_p,
+                                     _c_i32_p, _c_dbl_p, _c_dbl_p, i64, ctypes.c_double, _c_dbl_p, i64]
     lib.lpd_predict_ovo_dense.argtypes = [vp, _c_dbl_p, i64, i64, i64, i64, _c_i32_p]
     lib.lpd_predict_ovo_csr.argtypes = [vp, i64, i64, _c_i64_p, _c_i32_p, _c_dbl_p, i64, _c_i32_p]
     if path is None:
@@ -363,6 +366,21 @@ class Context:
         _check(self._lib.lpd_predict_ovo_csr(self._h, n, self.dim, _ptr(ip, ctypes.c_int64),
                                              _ptr(ix, ctypes.c_int32), _ptr(vv), num_classes,
                                              _ptr(out, ctypes.c_int32)))
+        return out
+
+    def kernel_block(self, A: np.ndarray, B: np.ndarray, gamma: float, norms_a=None,
+                     norms_b=None) -> np.ndarray:
+        """fp64 kernel block of dense rows (reference kernel_block, kernel.cpp:31-57);
+        norms default to the rows' squared norms (kernel.cpp:59-65)."""
+        a, b = _f64(A), _f64(B)
+        if a.ndim != 2 or b.ndim != 2 or a.shape[1] != b.shape[1]:
+            raise ValueError("A and B must be 2-D with the same number of columns")
+        na = _f64((a * a).sum(1) if norms_a is None else norms_a)
+        nb = _f64((b * b).sum(1) if norms_b is None else norms_b)
+        out = np.zeros((a.shape[0], b.shape[0]))
+        _check(self._lib.lpd_kernel_block(self._h, a.shape[0], None, None, _ptr(a), _ptr(na), b.shape[0],
+                                          None, None, _ptr(b), _ptr(nb), a.shape[1], float(gamma),
+                                          _ptr(out), b.shape[0]))
         return out
 
     def decision_values(self, G: np.ndarray, W: np.ndarray) -> np.ndarray:

@@ -1,5 +1,5 @@
-// lpdsvm_compute_G.cpp — the drop-in: strong definitions of lpdsvm::ovo_predict (below)
-// and
+// lpdsvm_compute_G.cpp — the drop-in: strong definitions of lpdsvm::kernel_block,
+// squared_norms and ovo_predict (below) and
 //
 //   lpdsvm::Matrix lpdsvm::compute_G(std::span<const SparseVector> points,
 //                                    std::span<const double> norms,
@@ -51,6 +51,7 @@ std::mutex g_mu;
 lpd_context* g_ctx = nullptr;
 std::atomic<long long> g_calls{0};
 std::atomic<long long> g_predict_calls{0};
+std::atomic<long long> g_block_calls{0};
 lpd_timings g_last{};
 
 [[noreturn]] void rethrow_status(int status, const char* what) {
@@ -156,6 +157,58 @@ Matrix compute_G(std::span<const SparseVector> points, std::span<const double> /
     return G;
 }
 
+// Strong definition of lpdsvm::kernel_block (kernel.hpp:26-32, kernel.cpp:31-57),
+// weakened in kernel.o by integration/Makefile. The remaining callers after the
+// compute_G / ovo_predict overrides are the landmark Gram matrix of
+// build_factor_with_landmarks (factor.cpp:121-126) and the convenience overload
+// (kernel.cpp:59-65). K7 computes it in fp64 with the reference's operation order
+// (gram_kernels.cuh), so L is unchanged.
+Matrix kernel_block(std::span<const SparseVector> rows_a, std::span<const double> norms_a,
+                    std::span<const SparseVector> rows_b, std::span<const double> norms_b,
+                    const KernelParams& params, int num_threads) {
+    validate(params);
+    const std::size_t m = rows_a.size(), n = rows_b.size();
+    Matrix block(m, n);
+    if (m == 0 || n == 0) return block;
+    std::lock_guard<std::mutex> lock(g_mu);
+    ++g_block_calls;
+    const int threads = std::max(1, num_threads);
+    Csr as = flatten(rows_a, threads);
+    Csr bs = flatten(rows_b, threads);
+    const int64_t d = std::max<int64_t>(1, 1 + std::max(as.max_index, bs.max_index));
+    const int rc = lpd_kernel_block(context(), static_cast<int64_t>(m), as.indptr.data(), as.indices.data(),
+                                    as.values.data(), norms_a.data(), static_cast<int64_t>(n),
+                                    bs.indptr.data(), bs.indices.data(), bs.values.data(),
+                                    norms_b.data(), d, params.gamma, block.data(),
+                                    static_cast<int64_t>(n));
+    if (rc != LPD_OK) rethrow_status(rc, "lpd_kernel_block");
+    return block;
+}
+
+// Strong definition of squared_norms (kernel.hpp:21-24, kernel.cpp:21-25), weakened in
+// kernel.o: the same per-point sequential sum (dataio.cpp:32-36, bitwise identical),
+// spread over the host's threads. The reference runs it serially over all n points
+// inside the gmatrix timer (factor.cpp:130).
+std::vector<double> squared_norms(std::span<const SparseVector> points) {
+    const std::size_t n = points.size();
+    std::vector<double> norms(n);
+    const int T = static_cast<int>(std::max<std::size_t>(
+        1, std::min<std::size_t>(std::max(1u, std::thread::hardware_concurrency()), n / 16384)));
+    auto work = [&](int t) {
+        const std::size_t b = n * static_cast<std::size_t>(t) / static_cast<std::size_t>(T);
+        const std::size_t e = n * static_cast<std::size_t>(t + 1) / static_cast<std::size_t>(T);
+        for (std::size_t i = b; i < e; ++i) norms[i] = squared_norm(points[i]);
+    };
+    if (T == 1) {
+        work(0);
+    } else {
+        std::vector<std::thread> th;
+        for (int t = 0; t < T; ++t) th.emplace_back(work, t);
+        for (auto& x : th) x.join();
+    }
+    return norms;
+}
+
 // Strong definition of
 //   std::vector<double> lpdsvm::ovo_predict(const OvoModel&, std::span<const SparseVector>, int)
 // (reference proj/include/lpdsvm/multiclass.hpp:80-82, proj/src/multiclass.cpp:170-200),
@@ -206,6 +259,9 @@ std::vector<double> ovo_predict(const OvoModel& model, std::span<const SparseVec
 // Introspection for the integration tests: proves the reference's call went here.
 extern "C" __attribute__((visibility("default"))) long long lpd_adapter_calls(void) {
     return g_calls.load();
+}
+extern "C" __attribute__((visibility("default"))) long long lpd_adapter_block_calls(void) {
+    return g_block_calls.load();
 }
 extern "C" __attribute__((visibility("default"))) long long lpd_adapter_predict_calls(void) {
     return g_predict_calls.load();

@@ -32,6 +32,7 @@
 #include "../../include/lpd_nystrom.h"
 #include "decision_kernels.cuh"
 #include "factor_kernel.cuh"
+#include "gram_kernels.cuh"
 #include "panel_kernels.cuh"
 #include "prep_kernels.cuh"
 
@@ -1201,6 +1202,83 @@ int lpd_predict_ovo_csr(lpd_context* ctx, int64_t n, int64_t d, const int64_t* i
         predict_rows_host(ctx, n, num_classes, classes, [&](DeviceState& ds, Slot& s, int64_t r0, int64_t rows) {
             stage_csr_rows(ds, s, r0, rows, d, indptr, indices, values);
         });
+    });
+}
+
+// K7: fp64 kernel block on the context's first device (reference kernel_block,
+// kernel.cpp:31-57). Rows are CSR (dense rows: pass indptr = NULL and the dense fp64
+// row-major arrays as `values`, ld = d).
+int lpd_kernel_block(lpd_context* ctx, int64_t m, const int64_t* a_indptr, const int32_t* a_indices,
+                     const double* a_values, const double* norms_a, int64_t n,
+                     const int64_t* b_indptr, const int32_t* b_indices, const double* b_values,
+                     const double* norms_b, int64_t d, double gamma, double* out, int64_t ldo) {
+    return guarded([&] {
+        check_ctx(ctx, false);
+        if (m < 0 || n < 0 || d < 0) fail(LPD_ERR_INVALID_ARGUMENT, "negative size");
+        if (!(gamma > 0.0) || !std::isfinite(gamma))
+            fail(LPD_ERR_INVALID_ARGUMENT, "kernel gamma must be positive and finite");
+        if (ldo < n) fail(LPD_ERR_INVALID_ARGUMENT, "ldo < n");
+        if (m == 0 || n == 0) return;
+        if (!out || !norms_a || !norms_b) fail(LPD_ERR_INVALID_ARGUMENT, "null buffer");
+        if (m > (1 << 30) || n > (1 << 30) || d > (1 << 30)) fail(LPD_ERR_UNSUPPORTED, "block too large");
+        DeviceState& ds = ctx->dev[0];
+        CUDA_TRY(cudaSetDevice(ds.device));
+        cudaStream_t st = ds.slot[0].stream;
+        const int64_t dd = std::max<int64_t>(d, 1);
+        std::vector<void*> tmp;
+        auto alloc = [&](size_t bytes) {
+            void* p = nullptr;
+            CUDA_TRY(cudaMalloc(&p, std::max<size_t>(bytes, 8)));
+            tmp.push_back(p);
+            return p;
+        };
+        auto cleanup = [&] { for (void* p : tmp) cudaFree(p); };
+        try {
+            // rows -> dense fp64 [rows × d] on the device
+            auto stage = [&](int64_t rows, const int64_t* ip, const int32_t* ix, const double* vv) {
+                double* dense = static_cast<double*>(alloc(sizeof(double) * rows * dd));
+                if (!ip) {
+                    if (d > 0)
+                        CUDA_TRY(cudaMemcpyAsync(dense, vv, sizeof(double) * rows * d, cudaMemcpyHostToDevice, st));
+                    return dense;
+                }
+                const int64_t e0 = ip[0], nnz = ip[rows] - ip[0];
+                std::vector<int64_t> rb(static_cast<size_t>(rows + 1));
+                for (int64_t i = 0; i <= rows; ++i) rb[i] = ip[i] - e0;
+                int64_t* dip = static_cast<int64_t*>(alloc(sizeof(int64_t) * (rows + 1)));
+                int32_t* dix = static_cast<int32_t*>(alloc(sizeof(int32_t) * nnz));
+                double* dvv = static_cast<double*>(alloc(sizeof(double) * nnz));
+                CUDA_TRY(cudaMemcpyAsync(dip, rb.data(), sizeof(int64_t) * (rows + 1), cudaMemcpyHostToDevice, st));
+                if (nnz > 0) {
+                    CUDA_TRY(cudaMemcpyAsync(dix, ix + e0, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, st));
+                    CUDA_TRY(cudaMemcpyAsync(dvv, vv + e0, sizeof(double) * nnz, cudaMemcpyHostToDevice, st));
+                }
+                if (d > 0)
+                    lpd::csr_to_dense_kernel<<<static_cast<int>((rows + 7) / 8), 256, 0, st>>>(
+                        dip, dix, dvv, static_cast<int>(rows), static_cast<int>(d), dense);
+                CUDA_TRY(cudaGetLastError());
+                CUDA_TRY(cudaStreamSynchronize(st));  // rb must outlive its copy
+                return dense;
+            };
+            double* A = stage(m, a_indptr, a_indices, a_values);
+            double* Bd = stage(n, b_indptr, b_indices, b_values);
+            double* dna = static_cast<double*>(alloc(sizeof(double) * m));
+            double* dnb = static_cast<double*>(alloc(sizeof(double) * n));
+            double* dout = static_cast<double*>(alloc(sizeof(double) * m * n));
+            CUDA_TRY(cudaMemcpyAsync(dna, norms_a, sizeof(double) * m, cudaMemcpyHostToDevice, st));
+            CUDA_TRY(cudaMemcpyAsync(dnb, norms_b, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+            dim3 grid(static_cast<unsigned>((n + lpd::GT - 1) / lpd::GT), static_cast<unsigned>((m + lpd::GT - 1) / lpd::GT));
+            lpd::gram_f64_kernel<<<grid, 256, 0, st>>>(A, dd, static_cast<int>(m), Bd, dd, static_cast<int>(n),
+                                                      static_cast<int>(d), dna, dnb, gamma, dout, n);
+            CUDA_TRY(cudaGetLastError());
+            CUDA_TRY(cudaMemcpy2DAsync(out, sizeof(double) * ldo, dout, sizeof(double) * n, sizeof(double) * n,
+                                       static_cast<size_t>(m), cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaStreamSynchronize(st));
+        } catch (...) {
+            cleanup();
+            throw;
+        }
+        cleanup();
     });
 }
 

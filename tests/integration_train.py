@@ -77,12 +77,14 @@ def main():
     so = glob.glob(os.path.join(os.path.dirname(lpdsvm.__file__), "_core*.so"))[0]
     # (for the package layout, __file__ is lpdsvm/__init__.py next to _core*.so)
     lib = ctypes.CDLL(so)
-    adapter_calls = predict_calls = -1
+    adapter_calls = predict_calls = block_calls = -1
     if hasattr(lib, "lpd_adapter_calls"):
         lib.lpd_adapter_calls.restype = ctypes.c_longlong
         lib.lpd_adapter_predict_calls.restype = ctypes.c_longlong
         adapter_calls = int(lib.lpd_adapter_calls())
         predict_calls = int(lib.lpd_adapter_predict_calls())
+        lib.lpd_adapter_block_calls.restype = ctypes.c_longlong
+        block_calls = int(lib.lpd_adapter_block_calls())
     np.savez(
         args.out,
         pred=pred,
@@ -99,6 +101,7 @@ def main():
         epochs=stats["epochs"],
         adapter_calls=adapter_calls,
         predict_calls=predict_calls,
+        block_calls=block_calls,
         model_text=np.array(model.to_string()),
     )
     print(f"{args.module_dir}: error {model.error_rate(test):.4f} cv {cv['mean_error']:.4f} "

@@ -284,3 +284,25 @@ def test_predict_ovo_argument_errors(gpu_ctx):
     with pytest.raises(ValueError):
         gpu_ctx.predict_ovo_dense(np.zeros((2, 6)), 1)
     assert gpu_ctx.predict_ovo_dense(np.zeros((0, 6)), 3).shape == (0,)
+
+
+@pytest.mark.parametrize("m,n,d,gamma", [(300, 300, 50, 0.02), (257, 65, 2048, 1.0 / 2048), (1, 7, 3, 1.0)])
+def test_kernel_block_fp64_matches_reference(gpu_ctx, m, n, d, gamma):
+    """K7 (landmark Gram): fp64 with the reference's operation order, so it agrees
+    with the reference's own kernel_block (oracle/_ref) up to the last ulps of exp."""
+    rng = np.random.default_rng(m + d)
+    A = rng.standard_normal((m, d)).astype(np.float32).astype(np.float64)
+    B = A[:n] if n <= m else rng.standard_normal((n, d))
+    if O.ref_available():
+        Kref = O.ref_kernel_block(O.dense_to_csr(A), O.dense_to_csr(B), gamma)
+        na, nb = O.ref_squared_norms(O.dense_to_csr(A)), O.ref_squared_norms(O.dense_to_csr(B))
+    else:
+        Kref = O.ora_kernel_block(O.dense_to_csr(A), O.dense_to_csr(B), gamma)
+        na, nb = (A * A).sum(1), (B * B).sum(1)
+    K = gpu_ctx.kernel_block(A, B, gamma, na, nb)
+    rel = np.abs(K - Kref) / np.maximum(np.abs(Kref), 1e-300)
+    # dot products and d2 are bitwise the reference's; exp differs from glibc's by
+    # at most an ulp or two (CUDA exp is not correctly rounded)
+    assert float(rel.max()) <= 5e-16, float(rel.max())
+    if n == m:
+        assert np.all(np.diag(K) == 1.0)

@@ -85,6 +85,8 @@ def test_reference_api_on_gpu_matches_reference(tmp_path, classes):
     assert int(g["adapter_calls"]) >= 2
     # Model.predict ran ovo_predict on the device (counter read right after it)
     assert int(g["predict_calls"]) >= 1
+    # the landmark Gram matrices (train + cross_validate) ran on the device in fp64
+    assert int(g["block_calls"]) >= 2
     assert int(g["effective_rank"]) == int(r["effective_rank"])
     agree = float(np.mean(g["pred"] == r["pred"]))
     assert agree >= 0.99, agree
