@@ -141,6 +141,22 @@ int lpd_kernel_block(lpd_context* ctx, int64_t m, const int64_t* a_indptr, const
                      const int64_t* b_indptr, const int32_t* b_indices, const double* b_values,
                      const double* norms_b, int64_t d, double gamma, double* out, int64_t ldo);
 
+/* Resident G (config 5, solver sweeps). With keep_resident on, lpd_compute_g_* also
+ * leaves the fp32 G (bit-identical to the fp64 G it returns) on the devices, row-sharded
+ * like the computation, until the next call; lpd_resident_shape reports n = 0 when the
+ * last call could not keep it (HBM short). */
+int lpd_set_keep_resident(lpd_context* ctx, int enable);
+int lpd_resident_shape(const lpd_context* ctx, int64_t* n, int64_t* b_eff);
+/* D[i][p] = sum_j G[rows[i]][j] * W[p][j] (fp64 accumulation; W is P x b_eff, D is
+ * count x P): the held-out scoring of cross-validation (proj/src/modelsel.cpp:123-140)
+ * and the gradients 1 - y_i G_i.w of reactivation_pass (proj/src/dcd.cpp:150-172). */
+int lpd_resident_gw(lpd_context* ctx, const int32_t* rows, int64_t count, const double* W,
+                    int64_t P, double* D);
+/* w[j] = sum_i coef[i] * G[rows[i]][j] (fp64, deterministic order): rebuild_w of the
+ * warm starts (proj/src/dcd.cpp:91-102). */
+int lpd_resident_gtv(lpd_context* ctx, const int32_t* rows, const double* coef, int64_t count,
+                     double* w);
+
 /* Last kernel timing of the fused factor kernel on device_index (milliseconds,
  * CUDA events around the launch on its stream), for benchmarks. */
 double lpd_last_factor_kernel_ms(const lpd_context* ctx, int device_index);

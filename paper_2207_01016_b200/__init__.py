@@ -69,6 +69,10 @@ EXPORTED_SYMBOLS = (
     "lpd_predict_ovo_dense",
     "lpd_predict_ovo_csr",
     "lpd_kernel_block",
+    "lpd_set_keep_resident",
+    "lpd_resident_shape",
+    "lpd_resident_gw",
+    "lpd_resident_gtv",
 )
 
 
@@ -149,6 +153,10 @@ def load_library(path: Optional[str] = None) -> ctypes.CDLL:
                                             ctypes.POINTER(ctypes.c_int64), ctypes.c_int]
     lib.lpd_kernel_block.argtypes = [vp, i64, _c_i64_p, _c_i32_p, _c_dbl_p, _c_dbl_p, i64, _c_i64_p,
                                      _c_i32_p, _c_dbl_p, _c_dbl_p, i64, ctypes.c_double, _c_dbl_p, i64]
+    lib.lpd_set_keep_resident.argtypes = [vp, ctypes.c_int]
+    lib.lpd_resident_shape.argtypes = [vp, _c_i64_p, _c_i64_p]
+    lib.lpd_resident_gw.argtypes = [vp, _c_i32_p, i64, _c_dbl_p, i64, _c_dbl_p]
+    lib.lpd_resident_gtv.argtypes = [vp, _c_i32_p, _c_dbl_p, i64, _c_dbl_p]
     lib.lpd_predict_ovo_dense.argtypes = [vp, _c_dbl_p, i64, i64, i64, i64, _c_i32_p]
     lib.lpd_predict_ovo_csr.argtypes = [vp, i64, i64, _c_i64_p, _c_i32_p, _c_dbl_p, i64, _c_i32_p]
     if path is None:
@@ -367,6 +375,33 @@ class Context:
                                              _ptr(ix, ctypes.c_int32), _ptr(vv), num_classes,
                                              _ptr(out, ctypes.c_int32)))
         return out
+
+    # ------------------------------------------------------- resident G (K6)
+    def set_keep_resident(self, enable: bool = True) -> None:
+        """Keep the fp32 G of later compute_g_* calls on the devices (config 5)."""
+        _check(self._lib.lpd_set_keep_resident(self._h, int(bool(enable))))
+
+    def resident_shape(self) -> tuple:
+        n, b = ctypes.c_int64(), ctypes.c_int64()
+        _check(self._lib.lpd_resident_shape(self._h, ctypes.byref(n), ctypes.byref(b)))
+        return n.value, b.value
+
+    def resident_gw(self, rows, W: np.ndarray) -> np.ndarray:
+        """D = G[rows] · Wᵀ on the resident G (held-out CV scoring, modelsel.cpp:123-140)."""
+        r = np.ascontiguousarray(rows, dtype=np.int32)
+        w = _f64(np.atleast_2d(W))
+        D = np.empty((r.shape[0], w.shape[0]))
+        _check(self._lib.lpd_resident_gw(self._h, _ptr(r, ctypes.c_int32), r.shape[0], _ptr(w), w.shape[0],
+                                         _ptr(D)))
+        return D
+
+    def resident_gtv(self, rows, coef) -> np.ndarray:
+        """w = Σ_i coef_i · G[rows_i] on the resident G (rebuild_w, dcd.cpp:91-102)."""
+        r = np.ascontiguousarray(rows, dtype=np.int32)
+        c = _f64(coef)
+        w = np.empty(self.resident_shape()[1])
+        _check(self._lib.lpd_resident_gtv(self._h, _ptr(r, ctypes.c_int32), _ptr(c), r.shape[0], _ptr(w)))
+        return w
 
     def kernel_block(self, A: np.ndarray, B: np.ndarray, gamma: float, norms_a=None,
                      norms_b=None) -> np.ndarray:

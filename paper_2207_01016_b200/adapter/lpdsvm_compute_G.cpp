@@ -29,6 +29,9 @@
 // `num_threads` sizes the host threads that flatten the sparse points.
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cmath>
+#include <limits>
 #include <cstdint>
 #include <cstdlib>
 #include <mutex>
@@ -42,7 +45,10 @@
 #include "lpdsvm/factor.hpp"
 #include "lpdsvm/kernel.hpp"
 #include "lpdsvm/matrix.hpp"
+#include "lpdsvm/dcd.hpp"
+#include "lpdsvm/modelsel.hpp"
 #include "lpdsvm/multiclass.hpp"
+#include "lpdsvm/rng.hpp"
 #include "lpd_nystrom.h"
 
 namespace {
@@ -52,6 +58,29 @@ lpd_context* g_ctx = nullptr;
 std::atomic<long long> g_calls{0};
 std::atomic<long long> g_predict_calls{0};
 std::atomic<long long> g_block_calls{0};
+std::atomic<long long> g_sweep_calls{0};   // rebuild_w / reactivation_pass served on device
+std::atomic<long long> g_score_calls{0};   // CV held-out scorings served on device
+
+// The G most recently produced by compute_G is also kept on the device (fp32, the
+// same values as the returned fp64 Matrix). Host Matrix objects are matched to it by
+// data pointer, shape and a bitwise probe of a few elements (guards against a freed
+// and reused buffer).
+struct ResidentG {
+    const double* ptr = nullptr;
+    std::size_t rows = 0, cols = 0;
+    std::size_t probe_at[8] = {};
+    double probe_val[8] = {};
+} g_res;
+
+// Device products are used above this many G elements per call (below it the host
+// loop is faster than a launch + transfers); LPD_DEVICE_MIN_ELEMS overrides (tests).
+std::size_t device_min_elems() {
+    static const std::size_t v = [] {
+        const char* e = std::getenv("LPD_DEVICE_MIN_ELEMS");
+        return e ? static_cast<std::size_t>(std::strtoull(e, nullptr, 10)) : (std::size_t(1) << 20);
+    }();
+    return v;
+}
 lpd_timings g_last{};
 
 [[noreturn]] void rethrow_status(int status, const char* what) {
@@ -150,11 +179,231 @@ Matrix compute_G(std::span<const SparseVector> points, std::span<const double> /
                                params.gamma);
     if (rc != LPD_OK) rethrow_status(rc, "lpd_set_basis_csr");
 
+    // keep G on the device for the solver sweeps and CV scoring (LPD_KEEP_G=0 disables)
+    const char* keep = std::getenv("LPD_KEEP_G");
+    lpd_set_keep_resident(ctx, !(keep && keep[0] == '0'));
     Matrix G(n, b_eff);
     rc = lpd_compute_g_csr(ctx, static_cast<int64_t>(n), d, xs.indptr.data(), xs.indices.data(),
                            xs.values.data(), G.data(), static_cast<int64_t>(b_eff), &g_last);
     if (rc != LPD_OK) rethrow_status(rc, "lpd_compute_g_csr");
+    int64_t rn = 0, rb = 0;
+    lpd_resident_shape(ctx, &rn, &rb);
+    g_res = ResidentG{};
+    if (rn == static_cast<int64_t>(n) && rb == static_cast<int64_t>(b_eff)) {
+        g_res.ptr = G.data();
+        g_res.rows = n;
+        g_res.cols = b_eff;
+        for (int k = 0; k < 8; ++k) {
+            g_res.probe_at[k] = (n * b_eff - 1) * static_cast<std::size_t>(k) / 7;
+            g_res.probe_val[k] = G.data()[g_res.probe_at[k]];
+        }
+    }
     return G;
+}
+
+// ------------------------------------------------------------------ resident-G sweeps
+// (K6): the solver's G·w products over many rows run on the device copy of G when the
+// Matrix the reference passes is the one compute_G produced.
+
+}  // namespace lpdsvm
+
+namespace {
+
+bool resident_matches(const lpdsvm::Matrix& G) {
+    if (!g_res.ptr || G.data() != g_res.ptr || G.rows() != g_res.rows || G.cols() != g_res.cols)
+        return false;
+    for (int k = 0; k < 8; ++k)
+        if (G.data()[g_res.probe_at[k]] != g_res.probe_val[k]) return false;
+    return true;
+}
+
+}  // namespace
+
+namespace lpdsvm {
+
+// rebuild_w (dcd.hpp:54-55, dcd.cpp:91-102): w = Σ_{α_i ≠ 0} α_i y_i G_{row_i}, the warm-start
+// rebuild of make_state (dcd.cpp:115-121). Device: fixed-order fp64 sums over the resident
+// G; host: the reference's sequential loop.
+std::vector<double> rebuild_w(const BinaryProblem& problem, const Matrix& G,
+                              std::span<const double> alpha) {
+    std::vector<double> w(G.cols(), 0.0);
+    std::vector<int32_t> rows;
+    std::vector<double> coef;
+    for (std::size_t i = 0; i < problem.size(); ++i) {
+        if (alpha[i] == 0.0) continue;
+        rows.push_back(problem.row_ids[i]);
+        coef.push_back(alpha[i] * problem.y[i]);
+    }
+    if (rows.size() * G.cols() >= device_min_elems()) {
+        std::lock_guard<std::mutex> lock(g_mu);
+        if (resident_matches(G)) {
+            const int rc = lpd_resident_gtv(context(), rows.data(), coef.data(),
+                                            static_cast<int64_t>(rows.size()), w.data());
+            if (rc != LPD_OK) rethrow_status(rc, "lpd_resident_gtv");
+            ++g_sweep_calls;
+            return w;
+        }
+    }
+    for (std::size_t k = 0; k < rows.size(); ++k) {
+        const double* row = G.row(static_cast<std::size_t>(rows[k]));
+        for (std::size_t j = 0; j < w.size(); ++j) w[j] += coef[k] * row[j];
+    }
+    return w;
+}
+
+// reactivation_pass (dcd.hpp:87-89, dcd.cpp:150-172): gradients 1 − y_i·G_i·w of the
+// inactive variables (device over the resident G when large), then the reference's
+// reactivation rule on the host.
+std::size_t reactivation_pass(DualState& state, const BinaryProblem& problem, const Matrix& G,
+                              double eps, SolveReport* report, double* max_violation) {
+    std::vector<std::size_t> idle;
+    for (std::size_t i = 0; i < problem.size(); ++i)
+        if (!state.active[i]) idle.push_back(i);
+    std::vector<double> dots(idle.size());
+    bool done = false;
+    if (idle.size() * G.cols() >= device_min_elems()) {
+        std::lock_guard<std::mutex> lock(g_mu);
+        if (resident_matches(G)) {
+            std::vector<int32_t> rows(idle.size());
+            for (std::size_t k = 0; k < idle.size(); ++k) rows[k] = problem.row_ids[idle[k]];
+            const int rc = lpd_resident_gw(context(), rows.data(), static_cast<int64_t>(rows.size()),
+                                           state.w.data(), 1, dots.data());
+            if (rc != LPD_OK) rethrow_status(rc, "lpd_resident_gw");
+            ++g_sweep_calls;
+            done = true;
+        }
+    }
+    if (!done)
+        for (std::size_t k = 0; k < idle.size(); ++k) {
+            const double* row = G.row(static_cast<std::size_t>(problem.row_ids[idle[k]]));
+            double acc = 0.0;
+            for (std::size_t j = 0; j < G.cols(); ++j) acc += row[j] * state.w[j];
+            dots[k] = acc;
+        }
+    std::size_t reactivated = 0;
+    double worst = 0.0;
+    for (std::size_t k = 0; k < idle.size(); ++k) {
+        const std::size_t i = idle[k];
+        const double v = projected_violation(1.0 - problem.y[i] * dots[k], state.alpha[i], problem.C);
+        if (report) ++report->coordinate_visits;
+        worst = std::max(worst, v);
+        if (v >= eps) {
+            state.active[i] = 1;
+            state.stall[i] = 0;
+            ++state.active_count;
+            ++reactivated;
+        }
+    }
+    if (max_violation) *max_violation = worst;
+    return reactivated;
+}
+
+// cross_validate (modelsel.hpp:49-51, modelsel.cpp:65-161): per fold, train every pair on
+// the other folds (ovo_train, warm-started from the store when given) and score the
+// held-out rows on their G rows — the scoring D = G_heldout·pair_wᵀ runs on the device
+// copy of G (then the reference's vote), the rest is the reference's orchestration.
+CvResult cross_validate(const LowRankFactor& factor, std::span<const double> labels,
+                        const LabelMap& label_map, const FoldAssignment& folds, double C,
+                        const CvOptions& options, WarmStore* warm) {
+    const std::size_t n = labels.size();
+    if (n != factor.G.rows()) throw std::invalid_argument("label count does not match G");
+    if (folds.fold_of.size() != n) throw std::invalid_argument("fold assignment size mismatch");
+    const int k = folds.k;
+    const std::size_t c = label_map.num_classes();
+    const std::size_t num_pairs = c * (c - 1) / 2;
+    if (warm && warm->size() != static_cast<std::size_t>(k))
+        throw std::invalid_argument("warm store fold count mismatch");
+
+    CvResult out;
+    out.fold_errors.assign(static_cast<std::size_t>(k), std::numeric_limits<double>::quiet_NaN());
+    out.fold_valid.assign(static_cast<std::size_t>(k), 0);
+    out.fold_epochs.assign(static_cast<std::size_t>(k), 0);
+    out.fold_seconds.assign(static_cast<std::size_t>(k), 0.0);
+
+    std::vector<int> cls(n);
+    for (std::size_t r = 0; r < n; ++r) cls[r] = label_map.index_of(labels[r]);
+
+    for (int f = 0; f < k; ++f) {
+        const auto start = std::chrono::steady_clock::now();
+        std::vector<std::uint8_t> train_rows(n, 0), seen(c, 0);
+        std::vector<int32_t> held;
+        for (std::size_t r = 0; r < n; ++r) {
+            if (folds.fold_of[r] == f) {
+                held.push_back(static_cast<int32_t>(r));
+            } else {
+                train_rows[r] = 1;
+                seen[static_cast<std::size_t>(cls[r])] = 1;
+            }
+        }
+        if (std::find(seen.begin(), seen.end(), 0) != seen.end()) continue;  // fold invalid
+
+        OvoTrainOptions to;
+        to.solve = options.solve;
+        to.num_threads = options.num_threads;
+        to.tag_base = combine_seed(options.tag_base, static_cast<std::uint64_t>(f));
+        const std::vector<std::vector<double>>* warm_in = nullptr;
+        if (warm) {
+            auto& store = (*warm)[static_cast<std::size_t>(f)];
+            if (store.size() != num_pairs) throw std::invalid_argument("warm store pair count mismatch");
+            warm_in = &store;
+            for (const auto& a : store)
+                if (!a.empty()) ++out.warm_used;
+        }
+        OvoTrainResult trained = ovo_train(factor, labels, label_map, C, to, train_rows, warm_in);
+        out.binary_solves += static_cast<long long>(trained.reports.size());
+        for (const SolveReport& rep : trained.reports) {
+            out.fold_epochs[static_cast<std::size_t>(f)] += rep.epochs;
+            out.total_epochs += rep.epochs;
+        }
+
+        // held-out decisions D (|held| × pairs)
+        const std::size_t be = trained.pair_w.cols();
+        std::vector<double> D(held.size() * num_pairs, 0.0);
+        bool on_device = false;
+        if (held.size() * be >= device_min_elems()) {
+            std::lock_guard<std::mutex> lock(g_mu);
+            if (resident_matches(factor.G)) {
+                const int rc = lpd_resident_gw(context(), held.data(), static_cast<int64_t>(held.size()),
+                                               trained.pair_w.data(), static_cast<int64_t>(num_pairs),
+                                               D.data());
+                if (rc != LPD_OK) rethrow_status(rc, "lpd_resident_gw");
+                ++g_score_calls;
+                on_device = true;
+            }
+        }
+        if (!on_device)
+            for (std::size_t h = 0; h < held.size(); ++h) {
+                const double* g = factor.G.row(static_cast<std::size_t>(held[h]));
+                for (std::size_t p = 0; p < num_pairs; ++p) {
+                    const double* wv = trained.pair_w.row(p);
+                    double acc = 0.0;
+                    for (std::size_t j = 0; j < be; ++j) acc += g[j] * wv[j];
+                    D[h * num_pairs + p] = acc;
+                }
+            }
+        std::size_t wrong = 0;
+        for (std::size_t h = 0; h < held.size(); ++h) {
+            const int v = vote(std::span<const double>(D.data() + h * num_pairs, num_pairs), c);
+            if (label_map.classes[static_cast<std::size_t>(v)] != labels[static_cast<std::size_t>(held[h])]) ++wrong;
+        }
+        out.fold_valid[static_cast<std::size_t>(f)] = 1;
+        out.fold_errors[static_cast<std::size_t>(f)] =
+            held.empty() ? 0.0 : static_cast<double>(wrong) / static_cast<double>(held.size());
+        out.fold_seconds[static_cast<std::size_t>(f)] =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - start).count();
+        if (warm) (*warm)[static_cast<std::size_t>(f)] = std::move(trained.pair_alpha);
+    }
+
+    double total = 0.0;
+    int valid = 0;
+    for (int f = 0; f < k; ++f)
+        if (out.fold_valid[static_cast<std::size_t>(f)]) {
+            total += out.fold_errors[static_cast<std::size_t>(f)];
+            ++valid;
+        }
+    if (valid == 0) throw std::runtime_error("every fold was missing a class");
+    out.mean_error = total / valid;
+    return out;
 }
 
 // Strong definition of lpdsvm::kernel_block (kernel.hpp:26-32, kernel.cpp:31-57),
@@ -259,6 +508,12 @@ std::vector<double> ovo_predict(const OvoModel& model, std::span<const SparseVec
 // Introspection for the integration tests: proves the reference's call went here.
 extern "C" __attribute__((visibility("default"))) long long lpd_adapter_calls(void) {
     return g_calls.load();
+}
+extern "C" __attribute__((visibility("default"))) long long lpd_adapter_sweep_calls(void) {
+    return g_sweep_calls.load();
+}
+extern "C" __attribute__((visibility("default"))) long long lpd_adapter_score_calls(void) {
+    return g_score_calls.load();
 }
 extern "C" __attribute__((visibility("default"))) long long lpd_adapter_block_calls(void) {
     return g_block_calls.load();

@@ -131,3 +131,67 @@ __global__ void ovo_pair_table_kernel(int num_classes, int2* __restrict__ pairs)
 }
 
 }  // namespace lpd
+
+namespace lpd {
+
+// K6 — products with the resident fp32 G for the host solver and CV scoring.
+//
+// gather_gw: D[i][p] = Σ_j G[rows[i]][j]·W[p][j] (fp64 accumulation), one warp per listed
+//   row, PB weight vectors per pass. Held-out scoring (modelsel.cpp:123-140) and the
+//   reactivation gradients 1 − y_i·G_i·w (dcd.cpp:150-172).
+template <int PB>
+__global__ void gather_gw_kernel(const float* __restrict__ G, long long ldg, int b_eff,
+                                 const int32_t* __restrict__ rows, int count,
+                                 const double* __restrict__ W, int P, int p0,
+                                 double* __restrict__ D) {
+    const int lane = threadIdx.x & 31;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int np = min(PB, P - p0);
+    for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < count; i += nwarps) {
+        const float* g = G + static_cast<long long>(rows[i]) * ldg;
+        double acc[PB];
+#pragma unroll
+        for (int q = 0; q < PB; ++q) acc[q] = 0.0;
+        for (int k = lane; k < b_eff; k += 32) {
+            const double a = static_cast<double>(g[k]);
+#pragma unroll
+            for (int q = 0; q < PB; ++q)
+                if (q < np) acc[q] = fma(a, __ldg(W + static_cast<long long>(p0 + q) * b_eff + k), acc[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < PB; ++q) {
+            double v = acc[q];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0 && q < np) D[static_cast<long long>(i) * P + p0 + q] = v;
+        }
+    }
+}
+
+// gather_gtv, pass 1: partial[g][j] = Σ_{i in row group g} coef[i]·G[rows[i]][j] (fp64),
+//   block = (column slab of 128 × row group); pass 2 sums the partials of each column
+//   in group order, so w = Σ_i coef_i·G_i (rebuild_w, dcd.cpp:91-102) is deterministic.
+constexpr int GTV_ROWS = 256;   // rows per group
+__global__ void gather_gtv_partial_kernel(const float* __restrict__ G, long long ldg, int b_eff,
+                                          const int32_t* __restrict__ rows,
+                                          const double* __restrict__ coef, int count,
+                                          double* __restrict__ partial) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int g = blockIdx.y;
+    if (j >= b_eff) return;
+    const int i0 = g * GTV_ROWS, i1 = min(count, i0 + GTV_ROWS);
+    double acc = 0.0;
+    for (int i = i0; i < i1; ++i)
+        acc = fma(coef[i], static_cast<double>(G[static_cast<long long>(rows[i]) * ldg + j]), acc);
+    partial[static_cast<long long>(g) * b_eff + j] = acc;
+}
+__global__ void gather_gtv_sum_kernel(const double* __restrict__ partial, int groups, int b_eff,
+                                      double* __restrict__ w) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= b_eff) return;
+    double acc = 0.0;
+    for (int g = 0; g < groups; ++g) acc += partial[static_cast<long long>(g) * b_eff + j];
+    w[j] = acc;
+}
+
+}  // namespace lpd

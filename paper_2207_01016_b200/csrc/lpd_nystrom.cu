@@ -174,6 +174,10 @@ struct DeviceState {
     int64_t B = 0, d = 0, b_eff = 0, B_pad = 0, Beff_pad = 0;
     int64_t kd = lpd::KD_MAX;  // plane width: 64 (fused path, d <= 63) or round_up(d + 1, 64)
     bool large = false;        // d >= 64: two-launch panel path (panel_kernels.cuh)
+    float* res_g = nullptr;    // resident fp32 G rows [res_r0, res_r0 + res_rows), ld res_ld
+    int64_t res_r0 = 0, res_rows = 0, res_ld = 0, res_cap = 0;
+    void* scratch = nullptr;   // per-call device scratch of the resident-G products
+    size_t scratch_cap = 0;
     int2* pairs = nullptr;     // OVO pair table for the vote (K5)
     int pairs_classes = 0;
     int32_t* votes = nullptr;  // per-chunk predicted class indices
@@ -223,6 +227,8 @@ struct DeviceState {
 
 struct lpd_context {
     std::vector<DeviceState> dev;
+    bool keep_resident = false;  // keep the fp32 G of host-row calls on the devices
+    int64_t res_n = 0, res_b_eff = 0;
 };
 
 namespace {
@@ -682,12 +688,38 @@ void compute_rows_host(lpd_context* ctx, int64_t n, double* G, int64_t ldg, lpd_
         256, std::min<int64_t>(round_up(n, 256), (128ll << 20) / (4 * b_eff) / 256 * 256));
     const int hw = std::max(1u, std::thread::hardware_concurrency());
     const int workers = std::max(1, std::min(16, hw / nd));
+    ctx->res_n = 0;
+    std::vector<int> resident_ok(nd, 0);
     run_parallel(ctx, [&](DeviceState& ds, int di) {
         CUDA_TRY(cudaSetDevice(ds.device));
         HostPool pool(workers);
         const int64_t per = round_up((n + nd - 1) / nd, 256);
         const int64_t r_begin = std::min<int64_t>(n, per * di);
         const int64_t r_end = std::min<int64_t>(n, per * (di + 1));
+        // Resident G (config 5 / solver sweeps): the kernel writes this shard's rows
+        // straight into a persistent fp32 buffer and the D2H reads from there. Best
+        // effort: if HBM is short the call simply runs without it.
+        bool resident = false;
+        if (ctx->keep_resident && r_end > r_begin) {
+            const int64_t ld = round_up(b_eff, 4);
+            const int64_t need = (r_end - r_begin) * ld + 256 * ld;
+            if (ds.res_cap < need) {
+                dev_free(ds.res_g);
+                ds.res_cap = 0;
+                if (cudaMalloc(reinterpret_cast<void**>(&ds.res_g), sizeof(float) * static_cast<size_t>(need)) ==
+                    cudaSuccess)
+                    ds.res_cap = need;
+                else
+                    cudaGetLastError();
+            }
+            if (ds.res_cap >= need) {
+                resident = true;
+                ds.res_r0 = r_begin;
+                ds.res_rows = r_end - r_begin;
+                ds.res_ld = ld;
+            }
+        }
+        if (!resident) ds.res_rows = 0;
         int64_t pend_r0[2] = {-1, -1}, pend_rows[2] = {0, 0};
         auto finish = [&](int k) {  // wait for slot k's chunk and widen it into G
             Slot& s = ds.slot[k];
@@ -711,10 +743,11 @@ void compute_rows_host(lpd_context* ctx, int64_t n, double* G, int64_t ldg, lpd_
             finish(sl);                // slot reuse: its chunk (k - 2) is widened by now
             stage_x(ds, s, r0, rows);  // records ev[0] and fills s.x
             CUDA_TRY(cudaEventRecord(s.ev[1], s.stream));
-            launch_factor(ds, s, s.x, rows, ds.d, s.g, s.g_ld, LPD_OUT_F32, s.stream, false);
+            float* gdst = resident ? ds.res_g + (r0 - r_begin) * ds.res_ld : static_cast<float*>(s.g);
+            launch_factor(ds, s, s.x, rows, ds.d, gdst, s.g_ld, LPD_OUT_F32, s.stream, false);
             launches[di] += 2;
             CUDA_TRY(cudaEventRecord(s.ev[2], s.stream));
-            CUDA_TRY(cudaMemcpyAsync(s.h, s.g, sizeof(float) * static_cast<size_t>(rows * s.g_ld),
+            CUDA_TRY(cudaMemcpyAsync(s.h, gdst, sizeof(float) * static_cast<size_t>(rows * s.g_ld),
                                      cudaMemcpyDeviceToHost, s.stream));
             CUDA_TRY(cudaEventRecord(s.ev[3], s.stream));
             pend_r0[sl] = r0;
@@ -724,7 +757,12 @@ void compute_rows_host(lpd_context* ctx, int64_t n, double* G, int64_t ldg, lpd_
         finish(0);
         finish(1);
         check_range_flag(ds);
+        resident_ok[di] = resident || r_end <= r_begin;
     });
+    if (ctx->keep_resident && std::all_of(resident_ok.begin(), resident_ok.end(), [](int v) { return v; })) {
+        ctx->res_n = n;
+        ctx->res_b_eff = b_eff;
+    }
     if (tm) {
         std::memset(tm, 0, sizeof(*tm));
         for (int i = 0; i < nd; ++i) {
@@ -828,6 +866,42 @@ void check_predict_args(lpd_context* ctx, int64_t n, int64_t num_classes, const 
     if (n > 0 && !out) fail(LPD_ERR_INVALID_ARGUMENT, "null output");
 }
 
+// Device scratch for the resident-G products (grown, never shrunk).
+void* scratch(DeviceState& ds, size_t bytes) {
+    if (ds.scratch_cap < bytes) {
+        if (ds.scratch) cudaFree(ds.scratch);
+        ds.scratch = nullptr;
+        ds.scratch_cap = 0;
+        CUDA_TRY(cudaMalloc(&ds.scratch, bytes));
+        ds.scratch_cap = bytes;
+    }
+    return ds.scratch;
+}
+
+void check_resident(lpd_context* ctx, const int32_t* rows, int64_t count) {
+    check_ctx(ctx, false);
+    if (ctx->res_n <= 0) fail(LPD_ERR_INVALID_ARGUMENT, "no resident G (lpd_set_keep_resident before lpd_compute_g_*)");
+    if (count < 0) fail(LPD_ERR_INVALID_ARGUMENT, "negative count");
+    if (count > 0 && !rows) fail(LPD_ERR_INVALID_ARGUMENT, "null rows");
+    for (int64_t i = 0; i < count; ++i)
+        if (rows[i] < 0 || rows[i] >= ctx->res_n) fail(LPD_ERR_INVALID_ARGUMENT, "row index out of range");
+}
+
+// Splits listed rows by the device holding them: (local row, position in the list).
+std::vector<std::vector<std::pair<int32_t, int64_t>>> split_rows(lpd_context* ctx, const int32_t* rows,
+                                                                 int64_t count) {
+    std::vector<std::vector<std::pair<int32_t, int64_t>>> parts(ctx->dev.size());
+    for (int64_t i = 0; i < count; ++i)
+        for (size_t di = 0; di < ctx->dev.size(); ++di) {
+            const DeviceState& ds = ctx->dev[di];
+            if (rows[i] >= ds.res_r0 && rows[i] < ds.res_r0 + ds.res_rows) {
+                parts[di].emplace_back(static_cast<int32_t>(rows[i] - ds.res_r0), i);
+                break;
+            }
+        }
+    return parts;
+}
+
 }  // namespace
 
 // =================================================================== C ABI
@@ -906,6 +980,8 @@ int lpd_context_destroy(lpd_context* ctx) {
         dev_free(ds.err);
         dev_free(ds.pairs);
         dev_free(ds.votes);
+        dev_free(ds.res_g);
+        if (ds.scratch) cudaFree(ds.scratch);
         for (auto& s : ds.slot) {
             ds.free_slot(s);
             if (s.stream) cudaStreamDestroy(s.stream);
@@ -1279,6 +1355,118 @@ int lpd_kernel_block(lpd_context* ctx, int64_t m, const int64_t* a_indptr, const
             throw;
         }
         cleanup();
+    });
+}
+
+int lpd_set_keep_resident(lpd_context* ctx, int enable) {
+    return guarded([&] {
+        check_ctx(ctx, false);
+        ctx->keep_resident = enable != 0;
+        if (!ctx->keep_resident) {
+            for (auto& ds : ctx->dev) {
+                CUDA_TRY(cudaSetDevice(ds.device));
+                CUDA_TRY(cudaDeviceSynchronize());
+                dev_free(ds.res_g);
+                ds.res_cap = ds.res_rows = 0;
+            }
+            ctx->res_n = 0;
+        }
+    });
+}
+
+int lpd_resident_shape(const lpd_context* ctx, int64_t* n, int64_t* b_eff) {
+    if (!ctx) return LPD_ERR_INVALID_ARGUMENT;
+    if (n) *n = ctx->res_n;
+    if (b_eff) *b_eff = ctx->res_n > 0 ? ctx->res_b_eff : 0;
+    return LPD_OK;
+}
+
+int lpd_resident_gw(lpd_context* ctx, const int32_t* rows, int64_t count, const double* W, int64_t P,
+                    double* D) {
+    return guarded([&] {
+        check_resident(ctx, rows, count);
+        if (P < 0 || (P > 0 && !W) || (count > 0 && P > 0 && !D)) fail(LPD_ERR_INVALID_ARGUMENT, "bad W / D");
+        if (count == 0 || P == 0) return;
+        const int64_t b_eff = ctx->res_b_eff;
+        auto parts = split_rows(ctx, rows, count);
+        run_parallel(ctx, [&](DeviceState& ds, int di) {
+            const auto& part = parts[static_cast<size_t>(di)];
+            if (part.empty()) return;
+            CUDA_TRY(cudaSetDevice(ds.device));
+            cudaStream_t st = ds.slot[0].stream;
+            const int64_t m = static_cast<int64_t>(part.size());
+            const size_t off_w = round_up(sizeof(int32_t) * m, 256);
+            const size_t off_d = off_w + round_up(sizeof(double) * P * b_eff, 256);
+            char* base = static_cast<char*>(scratch(ds, off_d + sizeof(double) * m * P));
+            std::vector<int32_t> local(static_cast<size_t>(m));
+            for (int64_t i = 0; i < m; ++i) local[i] = part[i].first;
+            int32_t* drows = reinterpret_cast<int32_t*>(base);
+            double* dw = reinterpret_cast<double*>(base + off_w);
+            double* dd = reinterpret_cast<double*>(base + off_d);
+            CUDA_TRY(cudaMemcpyAsync(drows, local.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, st));
+            CUDA_TRY(cudaMemcpyAsync(dw, W, sizeof(double) * P * b_eff, cudaMemcpyHostToDevice, st));
+            const int blocks = static_cast<int>(std::min<int64_t>((m + 7) / 8, static_cast<int64_t>(ds.num_sms) * 16));
+            for (int64_t p0 = 0; p0 < P; p0 += 4)
+                lpd::gather_gw_kernel<4><<<blocks, 256, 0, st>>>(ds.res_g, ds.res_ld, static_cast<int>(b_eff), drows,
+                                                                 static_cast<int>(m), dw, static_cast<int>(P),
+                                                                 static_cast<int>(p0), dd);
+            CUDA_TRY(cudaGetLastError());
+            std::vector<double> hd(static_cast<size_t>(m * P));
+            CUDA_TRY(cudaMemcpyAsync(hd.data(), dd, sizeof(double) * m * P, cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaStreamSynchronize(st));
+            for (int64_t i = 0; i < m; ++i)
+                std::memcpy(D + part[i].second * P, hd.data() + i * P, sizeof(double) * P);
+        });
+    });
+}
+
+int lpd_resident_gtv(lpd_context* ctx, const int32_t* rows, const double* coef, int64_t count, double* w) {
+    return guarded([&] {
+        check_resident(ctx, rows, count);
+        const int64_t b_eff = ctx->res_b_eff;
+        if (!w) fail(LPD_ERR_INVALID_ARGUMENT, "null w");
+        if (count > 0 && !coef) fail(LPD_ERR_INVALID_ARGUMENT, "null coef");
+        std::fill(w, w + b_eff, 0.0);
+        if (count == 0) return;
+        auto parts = split_rows(ctx, rows, count);
+        const int nd = static_cast<int>(ctx->dev.size());
+        std::vector<std::vector<double>> partial(nd);
+        run_parallel(ctx, [&](DeviceState& ds, int di) {
+            const auto& part = parts[static_cast<size_t>(di)];
+            if (part.empty()) return;
+            CUDA_TRY(cudaSetDevice(ds.device));
+            cudaStream_t st = ds.slot[0].stream;
+            const int64_t m = static_cast<int64_t>(part.size());
+            const int64_t groups = (m + lpd::GTV_ROWS - 1) / lpd::GTV_ROWS;
+            const size_t off_c = round_up(sizeof(int32_t) * m, 256);
+            const size_t off_p = off_c + round_up(sizeof(double) * m, 256);
+            const size_t off_w = off_p + round_up(sizeof(double) * groups * b_eff, 256);
+            char* base = static_cast<char*>(scratch(ds, off_w + sizeof(double) * b_eff));
+            std::vector<int32_t> local(static_cast<size_t>(m));
+            std::vector<double> lc(static_cast<size_t>(m));
+            for (int64_t i = 0; i < m; ++i) {
+                local[i] = part[i].first;
+                lc[i] = coef[part[i].second];
+            }
+            int32_t* drows = reinterpret_cast<int32_t*>(base);
+            double* dc = reinterpret_cast<double*>(base + off_c);
+            double* dp = reinterpret_cast<double*>(base + off_p);
+            double* dw = reinterpret_cast<double*>(base + off_w);
+            CUDA_TRY(cudaMemcpyAsync(drows, local.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, st));
+            CUDA_TRY(cudaMemcpyAsync(dc, lc.data(), sizeof(double) * m, cudaMemcpyHostToDevice, st));
+            dim3 grid(static_cast<unsigned>((b_eff + 127) / 128), static_cast<unsigned>(groups));
+            lpd::gather_gtv_partial_kernel<<<grid, 128, 0, st>>>(ds.res_g, ds.res_ld, static_cast<int>(b_eff),
+                                                                 drows, dc, static_cast<int>(m), dp);
+            lpd::gather_gtv_sum_kernel<<<static_cast<int>((b_eff + 255) / 256), 256, 0, st>>>(
+                dp, static_cast<int>(groups), static_cast<int>(b_eff), dw);
+            CUDA_TRY(cudaGetLastError());
+            partial[di].resize(static_cast<size_t>(b_eff));
+            CUDA_TRY(cudaMemcpyAsync(partial[di].data(), dw, sizeof(double) * b_eff, cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaStreamSynchronize(st));
+        });
+        for (int di = 0; di < nd; ++di)  // fixed device order: deterministic
+            if (!partial[di].empty())
+                for (int64_t j = 0; j < b_eff; ++j) w[j] += partial[di][j];
     });
 }
 

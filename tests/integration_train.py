@@ -73,11 +73,14 @@ def main():
     dv = model.decision_values(test)
     cv = lpdsvm.cross_validate(train, budget=args.budget, C=args.C, gamma=args.gamma, folds=3,
                                threads=args.threads, tau=args.tau)
+    # warm-started (gamma, C) grid: exercises rebuild_w on the warm starts
+    grid = lpdsvm.grid_search(train, gammas=[args.gamma], Cs=[0.5 * args.C, args.C], budget=args.budget,
+                              folds=3, threads=args.threads, tau=args.tau)
 
     so = glob.glob(os.path.join(os.path.dirname(lpdsvm.__file__), "_core*.so"))[0]
     # (for the package layout, __file__ is lpdsvm/__init__.py next to _core*.so)
     lib = ctypes.CDLL(so)
-    adapter_calls = predict_calls = block_calls = -1
+    adapter_calls = predict_calls = block_calls = sweep_calls = score_calls = -1
     if hasattr(lib, "lpd_adapter_calls"):
         lib.lpd_adapter_calls.restype = ctypes.c_longlong
         lib.lpd_adapter_predict_calls.restype = ctypes.c_longlong
@@ -85,6 +88,10 @@ def main():
         predict_calls = int(lib.lpd_adapter_predict_calls())
         lib.lpd_adapter_block_calls.restype = ctypes.c_longlong
         block_calls = int(lib.lpd_adapter_block_calls())
+        lib.lpd_adapter_sweep_calls.restype = ctypes.c_longlong
+        lib.lpd_adapter_score_calls.restype = ctypes.c_longlong
+        sweep_calls = int(lib.lpd_adapter_sweep_calls())
+        score_calls = int(lib.lpd_adapter_score_calls())
     np.savez(
         args.out,
         pred=pred,
@@ -102,6 +109,10 @@ def main():
         adapter_calls=adapter_calls,
         predict_calls=predict_calls,
         block_calls=block_calls,
+        sweep_calls=sweep_calls,
+        score_calls=score_calls,
+        grid_errors=np.array([e["mean_error"] for e in grid["entries"]]),
+        grid_warm=grid["warm_started_solves"],
         model_text=np.array(model.to_string()),
     )
     print(f"{args.module_dir}: error {model.error_rate(test):.4f} cv {cv['mean_error']:.4f} "

@@ -306,3 +306,32 @@ def test_kernel_block_fp64_matches_reference(gpu_ctx, m, n, d, gamma):
     assert float(rel.max()) <= 5e-16, float(rel.max())
     if n == m:
         assert np.all(np.diag(K) == 1.0)
+
+
+def test_resident_g_products(gpu_ctx):
+    """K6: G kept resident (fp32, bit-identical to the returned fp64 G) serves the
+    held-out scoring G[rows]·Wᵀ and rebuild_w's Σ coef_i·G_i in fp64 on the device."""
+    rng = np.random.default_rng(12)
+    X = rng.standard_normal((3000, 20)).astype(np.float32).astype(np.float64)
+    Y = X[:300]
+    L = np_gaussian_L(Y, 0.05, 1e-10)
+    gpu_ctx.set_basis_dense(Y, L, 0.05)
+    gpu_ctx.set_keep_resident(True)
+    try:
+        G = gpu_ctx.compute_g_dense(X)
+        assert gpu_ctx.resident_shape() == (3000, L.shape[1])
+        rows = rng.choice(3000, 777, replace=False).astype(np.int32)
+        W = rng.standard_normal((3, L.shape[1]))
+        D = gpu_ctx.resident_gw(rows, W)
+        Dref = G[rows] @ W.T
+        assert np.max(np.abs(D - Dref)) <= 1e-12 * np.max(np.abs(Dref))
+        coef = rng.standard_normal(777)
+        w = gpu_ctx.resident_gtv(rows, coef)
+        wref = coef @ G[rows]
+        assert np.max(np.abs(w - wref)) <= 1e-12 * np.max(np.abs(wref))
+        assert np.array_equal(w, gpu_ctx.resident_gtv(rows, coef))  # deterministic
+        with pytest.raises(ValueError):
+            gpu_ctx.resident_gw(np.array([3000], np.int32), W)
+    finally:
+        gpu_ctx.set_keep_resident(False)
+    assert gpu_ctx.resident_shape()[0] == 0

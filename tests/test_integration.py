@@ -27,9 +27,9 @@ def _core_so(d):
     return hits[0] if hits else None
 
 
-def _run(module_dir, out, *extra, check=True):
+def _run(module_dir, out, *extra, check=True, env=None):
     r = subprocess.run([sys.executable, RUNNER, module_dir, out, *extra], capture_output=True,
-                       text=True, timeout=900)
+                       text=True, timeout=900, env=None if env is None else {**os.environ, **env})
     if check and r.returncode != 0:
         raise AssertionError(f"{module_dir} failed:\n{r.stdout}\n{r.stderr}")
     return r
@@ -77,7 +77,8 @@ def test_reference_api_on_gpu_matches_reference(tmp_path, classes):
     assert _core_so(INTEG) is not None, "integration/_build missing: run make -C integration where /root/reference exists"
     assert _core_so(REF) is not None, "oracle/_ref missing"
     extra = ["--classes", str(classes)] + (["--d", "32", "--gamma", "0.02"] if classes > 2 else [])
-    _run(INTEG, str(tmp_path / "gpu.npz"), *extra)
+    # every G·w sweep / CV scoring large or small goes to the resident device G
+    _run(INTEG, str(tmp_path / "gpu.npz"), *extra, env={"LPD_DEVICE_MIN_ELEMS": "0"})
     _run(REF, str(tmp_path / "ref.npz"), *extra)
     g = np.load(tmp_path / "gpu.npz")
     r = np.load(tmp_path / "ref.npz")
@@ -87,6 +88,11 @@ def test_reference_api_on_gpu_matches_reference(tmp_path, classes):
     assert int(g["predict_calls"]) >= 1
     # the landmark Gram matrices (train + cross_validate) ran on the device in fp64
     assert int(g["block_calls"]) >= 2
+    # solver sweeps (reactivation passes, warm-start rebuild_w) and CV held-out scoring
+    # ran on the resident device G
+    assert int(g["sweep_calls"]) >= 1 and int(g["score_calls"]) >= 3
+    assert int(g["grid_warm"]) == int(r["grid_warm"]) > 0
+    assert np.max(np.abs(g["grid_errors"] - r["grid_errors"])) <= 0.01
     assert int(g["effective_rank"]) == int(r["effective_rank"])
     agree = float(np.mean(g["pred"] == r["pred"]))
     assert agree >= 0.99, agree
