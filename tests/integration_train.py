@@ -44,6 +44,8 @@ def main():
     ap.add_argument("--classes", type=int, default=2)
     ap.add_argument("--threads", type=int, default=4)
     ap.add_argument("--tau", type=float, default=1e-6)
+    ap.add_argument("--seed", type=int, default=11)
+    ap.add_argument("--train-only", action="store_true", help="train + predict only (timing runs)")
     args = ap.parse_args()
 
     mdir = args.module_dir if os.path.isabs(args.module_dir) else os.path.join(ROOT, args.module_dir)
@@ -57,19 +59,34 @@ def main():
     from paper_2207_01016_b200 import synthetic
 
     if args.classes == 2:
-        X, y = synthetic.blobs(args.n + args.n_test, args.d, seed=11)
+        X, y = synthetic.blobs(args.n + args.n_test, args.d, seed=args.seed)
     else:
-        X, y = synthetic.imagenet_like(args.n + args.n_test, args.d, args.classes, seed=11)
+        X, y = synthetic.imagenet_like(args.n + args.n_test, args.d, args.classes, seed=args.seed)
         X = X / 4.0  # keep γ·d² in a useful range for the small test
         X = X.astype(np.float32).astype(np.float64)
+    t0 = time.perf_counter()
     train = lpdsvm.parse_dataset(libsvm_text(X[: args.n], y[: args.n]))
     test = lpdsvm.parse_dataset(libsvm_text(X[args.n :], y[args.n :]))
+    parse_s = time.perf_counter() - t0
 
     t0 = time.perf_counter()
     model, stats = lpdsvm.train(train, budget=args.budget, C=args.C, gamma=args.gamma,
                                 threads=args.threads, tau=args.tau)
     train_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
     pred = model.predict(test, threads=args.threads)
+    predict_s = time.perf_counter() - t0
+    if args.train_only:
+        import json
+
+        out = {"build": args.module_dir, "n": args.n, "d": args.d, "budget": args.budget,
+               "effective_rank": model.effective_rank, "threads": args.threads,
+               "parse_seconds": parse_s, "train_wall_seconds": train_s, "predict_seconds": predict_s,
+               "test_error": float(np.mean(pred != y[args.n:])), **{k: stats[k] for k in stats}}
+        with open(args.out, "w") as f:
+            json.dump(out, f)
+        print(json.dumps(out))
+        return
     dv = model.decision_values(test)
     cv = lpdsvm.cross_validate(train, budget=args.budget, C=args.C, gamma=args.gamma, folds=3,
                                threads=args.threads, tau=args.tau)
