@@ -36,7 +36,16 @@ sys.path.insert(0, ROOT)
 
 METRIC = "Nyström factor rows/s"
 UNIT = "rows/s"
-LAUNCHES_PER_STEP = 8  # K2: column_mean, landmark_stats, basis_consts, prep_landmarks, col_absmax, lt_split; K3 prep_rows; K1
+# per step: K2 (column_mean, landmark_stats, basis_consts, prep_landmarks, col_absmax,
+# lt_split) + K3 prep_rows + the factor: one fused K1 launch (d <= 63) or, on the panel
+# path, a Z GEMM and a projection GEMM per <= 2 GB Z panel
+def launches_per_step(n, d, B):
+    if d <= 63:
+        return 8
+    bpad = -(-B // 256) * 256
+    panel = max(256, (2 * 2**30 // (4 * bpad)) // 256 * 256)
+    npad = -(-n // 256) * 256
+    return 7 + 2 * (-(-npad // panel))
 
 
 def parse():
@@ -389,7 +398,7 @@ def main():
                          "peak_source": f"MEASURED_PEAKS.json bf16_tflops ({peaks['src']}; kind::f16 runs at the bf16 rate)"},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": LAUNCHES_PER_STEP * args.steps,
+            "gpu_launches": launches_per_step(n, cfg.d, B) * args.steps,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -90,9 +90,36 @@ lpd_timings g_last{};
 }
 
 // One process-wide context over LPD_NUM_GPUS (or all visible) devices; the
-// reference's FactorOptions has no device field (factor.hpp:57-63).
+// reference's FactorOptions has no device field (factor.hpp:57-63). CUDA context
+// creation (~0.7 s) starts in the background when the module is loaded, so the first
+// train/predict call does not pay it; context() waits for it (or re-raises its error).
+struct EagerContext {
+    std::thread th;
+    int rc = LPD_OK;
+    std::string err;
+    lpd_context* ctx = nullptr;
+    EagerContext() {
+        const char* e = std::getenv("LPD_EAGER_INIT");
+        if (e && e[0] == '0') return;
+        th = std::thread([this] {
+            rc = lpd_context_create(&ctx, 0);
+            if (rc != LPD_OK) err = lpd_last_error();
+        });
+    }
+    ~EagerContext() {
+        if (th.joinable()) th.join();
+    }
+} g_eager;
+
 lpd_context* context() {
     if (!g_ctx) {
+        if (g_eager.th.joinable()) {
+            g_eager.th.join();
+            if (g_eager.rc == LPD_OK) {
+                g_ctx = g_eager.ctx;
+                return g_ctx;
+            }
+        }
         int rc = lpd_context_create(&g_ctx, 0);
         if (rc != LPD_OK) rethrow_status(rc, "lpd_context_create");
     }

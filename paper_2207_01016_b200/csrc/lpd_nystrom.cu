@@ -157,7 +157,8 @@ struct Slot {
     float2* raux = nullptr;  // [rows_cap]
     void* g = nullptr;       // [rows_cap × g_ld] fp32 G of the host-call path (device)
     float* h = nullptr;      // [rows_cap × g_ld] pinned host staging of g
-    int64_t g_cols = 0;      // b_eff the g buffers were sized for
+    int64_t g_cols = 0;      // b_eff of the current layout
+    int64_t g_elems = 0;     // capacity of g / h in elements
     int64_t g_ld = 0;        // their row pitch (elements; multiple of 4: 16-byte rows)
     int64_t kd = 0;          // plane width the x planes were sized for
     int64_t d_cap = 0;       // columns the fp64 x buffer was sized for
@@ -207,10 +208,15 @@ struct DeviceState {
     cudaEvent_t ring[kRing][2] = {};
     int64_t ring_count = 0;  // launches recorded since the last reset
 
+    struct {
+        size_t mu = 0, lm_hi = 0, lm_lo = 0, consts = 0, lm_nb = 0, lm_mx = 0, lt_hi = 0, lt_lo = 0,
+               col_scale = 0, colmax = 0;
+    } cap;  // basis buffer capacities (elements)
     void free_basis() {
         dev_free(mu); dev_free(lm_hi); dev_free(lm_lo); dev_free(consts); dev_free(lm_nb); dev_free(lm_mx);
         dev_free(lt_hi); dev_free(lt_lo); dev_free(col_scale);
         dev_free(z_hi); dev_free(z_lo);
+        cap = {};
         z_rows = 0;
         has_basis = false;
     }
@@ -219,7 +225,7 @@ struct DeviceState {
         if (s.h) cudaFreeHost(s.h);
         s.h = nullptr;
         dev_free(s.indptr); dev_free(s.indices); dev_free(s.values);
-        s.rows_cap = 0; s.g_cols = 0; s.nnz_cap = 0;
+        s.rows_cap = 0; s.g_cols = 0; s.g_elems = 0; s.nnz_cap = 0;
     }
 };
 
@@ -235,8 +241,9 @@ namespace {
 
 void ensure_slot(DeviceState& ds, Slot& s, int64_t rows, bool need_g, int64_t nnz) {
     const int64_t rows_pad = round_up(std::max<int64_t>(rows, 1), lpd::k1::PM);
-    if (rows_pad > s.rows_cap || (need_g && s.g_cols != ds.b_eff) || s.kd != ds.kd ||
-        s.d_cap < ds.d) {
+    const int64_t g_ld = round_up(ds.b_eff, 4);
+    if (rows_pad > s.rows_cap || (need_g && std::max(rows_pad, s.rows_cap) * g_ld > s.g_elems) ||
+        s.kd != ds.kd || s.d_cap < ds.d) {
         dev_free(s.x); dev_free(s.xhi); dev_free(s.xlo); dev_free(s.raux); dev_free(s.g);
         if (s.h) cudaFreeHost(s.h);
         s.h = nullptr;
@@ -247,19 +254,22 @@ void ensure_slot(DeviceState& ds, Slot& s, int64_t rows, bool need_g, int64_t nn
         s.kd = ds.kd;
         s.d_cap = std::max<int64_t>(ds.d, 1);
         dev_alloc(&s.raux, static_cast<size_t>(cap));
-        s.g_ld = round_up(ds.b_eff, 4);
         if (need_g) {
-            dev_alloc(reinterpret_cast<float**>(&s.g), static_cast<size_t>(cap * s.g_ld));
+            dev_alloc(reinterpret_cast<float**>(&s.g), static_cast<size_t>(cap * g_ld));
             CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&s.h),
-                                   sizeof(float) * static_cast<size_t>(cap * s.g_ld),
+                                   sizeof(float) * static_cast<size_t>(cap * g_ld),
                                    cudaHostAllocPortable));
+            s.g_elems = cap * g_ld;
+        } else {
+            s.g_elems = 0;
         }
-        s.g_cols = need_g ? ds.b_eff : 0;
         s.rows_cap = cap;
         // indptr is sized by rows_cap: re-create the CSR staging with the new capacity
         dev_free(s.indptr); dev_free(s.indices); dev_free(s.values);
         s.nnz_cap = 0;
     }
+    s.g_ld = g_ld;
+    s.g_cols = ds.b_eff;
     if (nnz > s.nnz_cap) {
         dev_free(s.indptr); dev_free(s.indices); dev_free(s.values);
         dev_alloc(&s.indptr, static_cast<size_t>(s.rows_cap + 1));
@@ -295,6 +305,28 @@ void init_device(DeviceState& ds, int device) {
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, lpd::k1::SMEM_BYTES));
     CUDA_TRY(cudaFuncSetAttribute(lpd::nystrom_factor_kernel<float>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, lpd::k1::SMEM_BYTES));
+    // Load every kernel now (CUDA lazy loading would otherwise charge the first call of
+    // each one): context creation runs in the background when the adapter loads.
+    {
+        cudaFuncAttributes fa;
+        const void* fns[] = {
+            reinterpret_cast<const void*>(lpd::prep_rows_kernel),
+            reinterpret_cast<const void*>(lpd::prep_landmarks_kernel),
+            reinterpret_cast<const void*>(lpd::landmark_stats_kernel),
+            reinterpret_cast<const void*>(lpd::basis_consts_kernel),
+            reinterpret_cast<const void*>(lpd::column_mean_kernel),
+            reinterpret_cast<const void*>(lpd::col_absmax_kernel),
+            reinterpret_cast<const void*>(lpd::lt_split_kernel),
+            reinterpret_cast<const void*>(lpd::csr_to_dense_kernel),
+            reinterpret_cast<const void*>(lpd::gram_f64_kernel),
+            reinterpret_cast<const void*>(lpd::ovo_vote_kernel<float>),
+            reinterpret_cast<const void*>(lpd::ovo_pair_table_kernel),
+            reinterpret_cast<const void*>(lpd::gather_gw_kernel<4>),
+            reinterpret_cast<const void*>(lpd::gather_gtv_partial_kernel),
+            reinterpret_cast<const void*>(lpd::gather_gtv_sum_kernel),
+        };
+        for (const void* f : fns) CUDA_TRY(cudaFuncGetAttributes(&fa, f));
+    }
     CUDA_TRY(cudaFuncSetAttribute(lpd::panel_gemm_kernel<lpd::PANEL_Z, float>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, lpd::kp::SMEM_BYTES));
     CUDA_TRY(cudaFuncSetAttribute(lpd::panel_gemm_kernel<lpd::PANEL_G, float>,
@@ -329,23 +361,36 @@ void build_basis(DeviceState& ds, const double* lm_dev, int64_t B, int64_t d, in
     const int64_t B_pad = round_up(B, large ? lpd::kp::BN : lpd::k1::NC);
     const int64_t Beff_pad = round_up(b_eff, lpd::k1::N2);
     if (!ds.lt_hi || B_pad != ds.B_pad || Beff_pad != ds.Beff_pad || kd != ds.kd || large != ds.large) {
-        CUDA_TRY(cudaDeviceSynchronize());
-        ds.free_basis();
-        dev_free(ds.colmax);
+        // Buffers only grow: alternating shapes (the factor basis, then the prediction
+        // basis L := betasᵀ, then the next γ's factor) reuse them without reallocating.
+        auto grow = [&](auto*& ptr, size_t& cap, size_t need) {
+            if (need > cap) {
+                CUDA_TRY(cudaDeviceSynchronize());
+                dev_free(ptr);
+                dev_alloc(&ptr, need);
+                cap = need;
+            }
+        };
+        if (large != ds.large || kd != ds.kd || B_pad != ds.B_pad) {  // Z scratch is shaped by these
+            CUDA_TRY(cudaDeviceSynchronize());
+            dev_free(ds.z_hi);
+            dev_free(ds.z_lo);
+            ds.z_rows = 0;
+        }
         ds.B_pad = B_pad;
         ds.Beff_pad = Beff_pad;
         ds.kd = kd;
         ds.large = large;
-        dev_alloc(&ds.mu, static_cast<size_t>(kd));
-        dev_alloc(&ds.lm_hi, static_cast<size_t>(B_pad * kd));
-        dev_alloc(&ds.lm_lo, static_cast<size_t>(B_pad * kd));
-        dev_alloc(&ds.consts, 1);
-        dev_alloc(&ds.lm_nb, static_cast<size_t>(B_pad));
-        dev_alloc(&ds.lm_mx, static_cast<size_t>(B_pad));
-        dev_alloc(&ds.lt_hi, static_cast<size_t>(Beff_pad * B_pad));
-        dev_alloc(&ds.lt_lo, static_cast<size_t>(Beff_pad * B_pad));
-        dev_alloc(&ds.col_scale, static_cast<size_t>(Beff_pad));
-        dev_alloc(&ds.colmax, static_cast<size_t>(Beff_pad));
+        grow(ds.mu, ds.cap.mu, static_cast<size_t>(kd));
+        grow(ds.lm_hi, ds.cap.lm_hi, static_cast<size_t>(B_pad * kd));
+        grow(ds.lm_lo, ds.cap.lm_lo, static_cast<size_t>(B_pad * kd));
+        grow(ds.consts, ds.cap.consts, 1);
+        grow(ds.lm_nb, ds.cap.lm_nb, static_cast<size_t>(B_pad));
+        grow(ds.lm_mx, ds.cap.lm_mx, static_cast<size_t>(B_pad));
+        grow(ds.lt_hi, ds.cap.lt_hi, static_cast<size_t>(Beff_pad * B_pad));
+        grow(ds.lt_lo, ds.cap.lt_lo, static_cast<size_t>(Beff_pad * B_pad));
+        grow(ds.col_scale, ds.cap.col_scale, static_cast<size_t>(Beff_pad));
+        grow(ds.colmax, ds.cap.colmax, static_cast<size_t>(Beff_pad));
         // per-CTA halves of N: 32 landmark rows (fused kernel) or 128 (panel Z GEMM),
         // 128 Lᵀ rows (both)
         const uint32_t lm_box = large ? lpd::kp::BNH : lpd::k1::NCH;

@@ -1,0 +1,95 @@
+"""Config 5 (BASELINE.json): the C2 factor (n=581,012, B=4,096) kept resident in HBM and
+the products the CV grid needs on it — held-out scoring D = G_heldout·Wᵀ (reference
+modelsel.cpp:123-140) and the warm-start rebuild w = Σ coef_i·G_i (dcd.cpp:91-102) — timed
+through the C ABI (host arguments in, host results out; wall clock per call, which
+includes the row-index / W uploads and the result download), next to the reference's own
+single-threaded scoring loop restated in C (oracle, test infrastructure) on the host G.
+
+  python scripts/bench_c5.py [--reps 20]     (prints one JSON object)
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--folds", type=int, default=5)
+    args = ap.parse_args()
+
+    import bench
+    import paper_2207_01016_b200 as P
+    from oracle import oracle as O
+    from paper_2207_01016_b200 import synthetic
+
+    cfg = synthetic.CONFIGS["c2"]
+    X, y = synthetic.make(cfg)
+    Y, L = bench.make_basis(X, cfg)
+    n, b_eff = X.shape[0], L.shape[1]
+    peaks = bench.load_peaks()
+    out = {"config": "c5: C2 factor resident in HBM, CV scoring + warm-start rebuild on device",
+           "n": n, "B": Y.shape[0], "b_eff": b_eff, "hbm_peak_gbs": peaks["hbm"], "peak_source": peaks["src"]}
+    with P.Context(1) as ctx:
+        ctx.set_basis_dense(Y, L, cfg.gamma)
+        ctx.set_keep_resident(True)
+        G = np.zeros((n, b_eff))
+        t0 = time.perf_counter()
+        ctx.compute_g_dense(X, out=G)
+        out["factor_seconds"] = time.perf_counter() - t0
+        assert ctx.resident_shape() == (n, b_eff)
+        fold = np.random.default_rng(5).permutation(n) % args.folds
+        held = np.flatnonzero(fold == 0).astype(np.int32)
+        train = np.flatnonzero(fold != 0).astype(np.int32)
+        rng = np.random.default_rng(0)
+        for P_ in (1, 45):  # binary, 10-class one-vs-one
+            W = rng.standard_normal((P_, b_eff))
+            D = ctx.resident_gw(held, W)
+            ts = []
+            for _ in range(args.reps):
+                t0 = time.perf_counter()
+                ctx.resident_gw(held, W)
+                ts.append(time.perf_counter() - t0)
+            t = float(np.median(ts))
+            byts = held.size * b_eff * 4  # fp32 resident G rows, read once per pass of <= 4 vectors
+            passes = -(-P_ // 4)
+            out[f"score_P{P_}"] = {"rows": int(held.size), "seconds": t, "rows_per_s": held.size / t,
+                                   "algorithmic_gbs": byts * passes / t / 1e9,
+                                   "frac_of_hbm": byts * passes / t / 1e9 / peaks["hbm"]}
+            if P_ == 1:
+                sub = held[:20000]
+                t0 = time.perf_counter()
+                Dc = O.ora_decision_values(G, W, rows=sub)
+                tc = time.perf_counter() - t0
+                out["score_P1"]["reference_loop_rows_per_s"] = sub.size / tc
+                out["score_P1"]["reference_loop_sample"] = f"{sub.size} held-out rows, 1 thread (modelsel.cpp:123-140 restated)"
+                err = np.max(np.abs(D[: sub.size] - Dc)) / np.max(np.abs(Dc))
+                out["score_P1"]["max_rel_diff_vs_reference_loop"] = float(err)
+        coef = rng.standard_normal(train.size)
+        w = ctx.resident_gtv(train, coef)
+        ts = []
+        for _ in range(args.reps):
+            t0 = time.perf_counter()
+            ctx.resident_gtv(train, coef)
+            ts.append(time.perf_counter() - t0)
+        t = float(np.median(ts))
+        out["rebuild_w"] = {"rows": int(train.size), "seconds": t,
+                            "algorithmic_gbs": train.size * b_eff * 4 / t / 1e9,
+                            "frac_of_hbm": train.size * b_eff * 4 / t / 1e9 / peaks["hbm"]}
+        sub = train[:20000]
+        t0 = time.perf_counter()
+        wref = coef[:20000] @ G[sub]
+        out["rebuild_w"]["numpy_host_rows_per_s"] = sub.size / (time.perf_counter() - t0)
+        ctx.set_keep_resident(False)
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

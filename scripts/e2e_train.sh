@@ -11,3 +11,4 @@ run() {  # n d budget gamma
 }
 run ${N1:-20000} 50 1000 0.02
 run ${N2:-200000} 54 2048 0.0185
+run ${N3:-581012} 54 4096 0.0185

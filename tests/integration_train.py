@@ -79,10 +79,22 @@ def main():
     if args.train_only:
         import json
 
+        # second, steady-state run in the same process (the first one also pays one-time
+        # CUDA driver/context initialisation on the GPU build)
+        t0 = time.perf_counter()
+        model2, stats2 = lpdsvm.train(train, budget=args.budget, C=args.C, gamma=args.gamma,
+                                      threads=args.threads, tau=args.tau)
+        train2_s = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        pred2 = model2.predict(test, threads=args.threads)
+        predict2_s = time.perf_counter() - t0
         out = {"build": args.module_dir, "n": args.n, "d": args.d, "budget": args.budget,
                "effective_rank": model.effective_rank, "threads": args.threads,
-               "parse_seconds": parse_s, "train_wall_seconds": train_s, "predict_seconds": predict_s,
-               "test_error": float(np.mean(pred != y[args.n:])), **{k: stats[k] for k in stats}}
+               "parse_seconds": parse_s,
+               "cold": {"train_wall_seconds": train_s, "predict_seconds": predict_s,
+                        **{k: stats[k] for k in ("preparation_seconds", "gmatrix_seconds", "training_seconds")}},
+               "train_wall_seconds": train2_s, "predict_seconds": predict2_s,
+               "test_error": float(np.mean(pred2 != y[args.n:])), **{k: stats2[k] for k in stats2}}
         with open(args.out, "w") as f:
             json.dump(out, f)
         print(json.dumps(out))
