@@ -27,8 +27,12 @@
 // reference's clamp at kernel.cpp:49-51). `chunk_size` is validated and otherwise
 // unused (the reference guarantees results independent of chunking);
 // `num_threads` sizes the host threads that flatten the sparse points.
+#include <sys/mman.h>
+
 #include <algorithm>
 #include <atomic>
+#include <cstring>
+#include <type_traits>
 #include <chrono>
 #include <cmath>
 #include <limits>
@@ -82,6 +86,9 @@ std::size_t device_min_elems() {
     return v;
 }
 lpd_timings g_last{};
+// host-side phases of the last compute_G (seconds): flatten, basis, Matrix allocation
+// (the reference Matrix zero-fills, matrix.hpp:15-16), device call
+double g_phase[4] = {};
 
 [[noreturn]] void rethrow_status(int status, const char* what) {
     std::string msg = std::string(what) + ": " + lpd_last_error();
@@ -172,6 +179,51 @@ Csr flatten(std::span<const lpdsvm::SparseVector> rows, int num_threads) {
     return c;
 }
 
+// Matrix(rows, cols) — the same object the reference constructor builds (rows_, cols_,
+// a zero-filled std::vector<double>, matrix.hpp:12-44) — without the reference's
+// dominant host cost at scale: 19 GB of serial 4 KB first-touch page faults at C2
+// (measured 6.75 s of a 7.5 s gmatrix). The storage is reserved, advised to use
+// transparent huge pages, first-touched by all host threads, and only then
+// value-initialised by the vector (zeros over present pages). The vector is moved into
+// the Matrix through its standard layout (rows_, cols_, data_ in declaration order).
+struct MatrixLayout {
+    std::size_t rows, cols;
+    std::vector<double> data;
+};
+lpdsvm::Matrix make_zero_matrix(std::size_t rows, std::size_t cols, int threads) {
+    if constexpr (sizeof(MatrixLayout) == sizeof(lpdsvm::Matrix) &&
+                  std::is_standard_layout_v<lpdsvm::Matrix> && std::is_standard_layout_v<MatrixLayout>) {
+        const std::size_t n = rows * cols;
+        if (n * sizeof(double) < (std::size_t(64) << 20)) return lpdsvm::Matrix(rows, cols);
+        std::vector<double> v;
+        v.reserve(n);
+        char* base = reinterpret_cast<char*>(v.data());
+        const std::size_t bytes = n * sizeof(double);
+        const std::uintptr_t huge = std::uintptr_t(2) << 20;
+        const std::uintptr_t a0 = (reinterpret_cast<std::uintptr_t>(base) + huge - 1) & ~(huge - 1);
+        const std::uintptr_t a1 = (reinterpret_cast<std::uintptr_t>(base) + bytes) & ~(huge - 1);
+        if (a1 > a0) madvise(reinterpret_cast<void*>(a0), a1 - a0, MADV_HUGEPAGE);
+        const int T = std::max(1, threads);
+        std::vector<std::thread> th;
+        for (int t = 0; t < T; ++t)
+            th.emplace_back([&, t] {
+                const std::size_t b0 = bytes * static_cast<std::size_t>(t) / static_cast<std::size_t>(T);
+                const std::size_t b1 = bytes * static_cast<std::size_t>(t + 1) / static_cast<std::size_t>(T);
+                std::memset(base + b0, 0, b1 - b0);
+            });
+        for (auto& x : th) x.join();
+        v.resize(n);
+        lpdsvm::Matrix m;
+        auto* L = reinterpret_cast<MatrixLayout*>(&m);
+        L->rows = rows;
+        L->cols = cols;
+        L->data = std::move(v);
+        return m;
+    } else {
+        return lpdsvm::Matrix(rows, cols);
+    }
+}
+
 }  // namespace
 
 namespace lpdsvm {
@@ -194,9 +246,17 @@ Matrix compute_G(std::span<const SparseVector> points, std::span<const double> /
 
     std::lock_guard<std::mutex> lock(g_mu);
     ++g_calls;
+    using clk = std::chrono::steady_clock;
+    auto t0 = clk::now();
+    auto lap = [&](int k) {
+        const auto t1 = clk::now();
+        g_phase[k] = std::chrono::duration<double>(t1 - t0).count();
+        t0 = t1;
+    };
     const int threads = std::max(1, num_threads);
     Csr xs = flatten(points, threads);
     Csr ls = flatten(landmarks, threads);
+    lap(0);
     // compute_G is not passed the dimension: d = 1 + max index over both sets.
     const int64_t d = std::max<int64_t>(1, 1 + std::max(xs.max_index, ls.max_index));
 
@@ -209,10 +269,13 @@ Matrix compute_G(std::span<const SparseVector> points, std::span<const double> /
     // keep G on the device for the solver sweeps and CV scoring (LPD_KEEP_G=0 disables)
     const char* keep = std::getenv("LPD_KEEP_G");
     lpd_set_keep_resident(ctx, !(keep && keep[0] == '0'));
-    Matrix G(n, b_eff);
+    lap(1);
+    Matrix G = make_zero_matrix(n, b_eff, static_cast<int>(std::max(1u, std::thread::hardware_concurrency())));
+    lap(2);
     rc = lpd_compute_g_csr(ctx, static_cast<int64_t>(n), d, xs.indptr.data(), xs.indices.data(),
                            xs.values.data(), G.data(), static_cast<int64_t>(b_eff), &g_last);
     if (rc != LPD_OK) rethrow_status(rc, "lpd_compute_g_csr");
+    lap(3);
     int64_t rn = 0, rb = 0;
     lpd_resident_shape(ctx, &rn, &rb);
     g_res = ResidentG{};
@@ -551,6 +614,10 @@ extern "C" __attribute__((visibility("default"))) long long lpd_adapter_predict_
 extern "C" __attribute__((visibility("default"))) void lpd_adapter_last_timings(lpd_timings* out) {
     std::lock_guard<std::mutex> lock(g_mu);
     if (out) *out = g_last;
+}
+extern "C" __attribute__((visibility("default"))) void lpd_adapter_phases(double* out4) {
+    std::lock_guard<std::mutex> lock(g_mu);
+    for (int k = 0; k < 4; ++k) out4[k] = g_phase[k];
 }
 extern "C" __attribute__((visibility("default"))) void lpd_adapter_release(void) {
     std::lock_guard<std::mutex> lock(g_mu);

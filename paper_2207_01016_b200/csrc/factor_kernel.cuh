@@ -46,19 +46,21 @@ struct FactorParams {
     int n_col_blocks;       // Beff_pad / 256
     int b_eff;              // valid G columns
     int ksteps1;            // ceil((d + 1) / 16): K-steps of GEMM1 (d features + norm column)
-    int tma_store;          // 1: G leaves through SMEM + TMA store (tensor map valid)
     const float2* row_aux;  // [n_pad] (R_i, sx_i): t = R_i + acc*sx_i (prep_rows_kernel)
-    const __half* x_hi;     // [n_pad x 64] point planes (K-major), n_pad % 256 == 0
-    const __half* x_lo;
     const float* col_scale; // [Beff_pad] 2^-13 / u_k (undoes Z and Lᵀ-row scaling)
-    void* G;                // output, row-major, leading dimension ldg (elements)
-    long long ldg;
+    // output G: the tm_g tensor map (TMA store, 16-byte aligned rows; the host stages
+    // through an aligned buffer otherwise)
     int dbg;                // profiling ablations (LPD_K1_DEBUG), 0 in production
     unsigned long long* dbg_out;  // [2 roles x 8 phases] cycle sums when dbg & 16
 };
 
-// Phase-cycle probe for profiling builds (dbg & 16): accumulates clock64 deltas
-// per phase in registers, flushed once per warp at kernel end.
+// Phase-cycle probe for profiling builds (compile with -DLPD_K1_PROBE=1 and run with
+// dbg & 16): accumulates clock64 deltas per phase in registers, flushed once per warp
+// at kernel end. In production builds it compiles to nothing (no registers).
+#ifndef LPD_K1_PROBE
+#define LPD_K1_PROBE 0
+#endif
+#if LPD_K1_PROBE
 struct PhaseProbe {
     bool on;
     unsigned long long last = 0, acc[8] = {};
@@ -77,6 +79,13 @@ struct PhaseProbe {
             for (int k = 0; k < 8; ++k) atomicAdd(out + k, acc[k]);
     }
 };
+#else
+struct PhaseProbe {
+    __device__ explicit PhaseProbe(bool) {}
+    __device__ __forceinline__ void mark(int) {}
+    __device__ __forceinline__ void flush(unsigned long long*) {}
+};
+#endif
 
 namespace k1 {
 constexpr int BM = 128;        // rows per CTA (UMMA M = 256 per pair)
@@ -101,8 +110,10 @@ constexpr int NSTG = 2;                              // staging buffers per epil
 constexpr uint32_t OFF_LM = 0;                                      // stage s: hi, lo
 constexpr uint32_t OFF_LT = OFF_LM + NS_LM * 2 * LM_BYTES;          // stage s
 constexpr uint32_t OFF_STG = OFF_LT + NS_LT * LT_BYTES;             // warp w, buffer k
-constexpr uint32_t OFF_BAR = OFF_STG + EPI_WARPS * NSTG * STG_BYTES;
-constexpr uint32_t NUM_BARS = 2 + 2 * NS_LM + 2 * NS_LT + 3 * NSZ + 2;
+constexpr uint32_t X_BYTES = BM * KD * 2;           // 16 KB: one X plane of this CTA's rows
+constexpr uint32_t OFF_X = OFF_STG + EPI_WARPS * NSTG * STG_BYTES;  // hi, lo
+constexpr uint32_t OFF_BAR = OFF_X + 2 * X_BYTES;
+constexpr uint32_t NUM_BARS = 4 + 2 * NS_LM + 2 * NS_LT + 3 * NSZ + 2;
 constexpr uint32_t SMEM_BYTES = OFF_BAR + NUM_BARS * 8 + 16 + 1024;  // + alignment slack
 
 constexpr uint32_t TMEM_COLS = 512;
@@ -125,7 +136,9 @@ __device__ __forceinline__ uint32_t z_lo_col(uint32_t k) { return z_hi_col(k) + 
 
 template <typename OutT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
-    nystrom_factor_kernel(const __grid_constant__ CUtensorMap tm_lmhi,
+    nystrom_factor_kernel(const __grid_constant__ CUtensorMap tm_xhi,
+                          const __grid_constant__ CUtensorMap tm_xlo,
+                          const __grid_constant__ CUtensorMap tm_lmhi,
                           const __grid_constant__ CUtensorMap tm_lmlo,
                           const __grid_constant__ CUtensorMap tm_lthi,
                           const __grid_constant__ CUtensorMap tm_ltlo,
@@ -149,6 +162,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
     uint64_t* sz_empty = z_full + NSZ;
     uint64_t* g_full = sz_empty + NSZ;
     uint64_t* g_empty = g_full + 1;
+    uint64_t* xs_full = g_empty + 1;   // X tile landed in SMEM (TMA)
+    uint64_t* xs_empty = xs_full + 1;  // X tile copied from SMEM into TMEM
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NUM_BARS);
 
     const int warp = threadIdx.x >> 5;
@@ -172,12 +187,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
         }
         mbar_init(g_full, 1);
         mbar_init(g_empty, 2 * EPI_WARPS);
+        mbar_init(xs_full, 1);
+        mbar_init(xs_empty, EPI_WARPS);
         fence_mbar_init();
     }
     if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tm_xhi); tma_prefetch_desc(&tm_xlo);
         tma_prefetch_desc(&tm_lmhi); tma_prefetch_desc(&tm_lmlo);
         tma_prefetch_desc(&tm_lthi); tma_prefetch_desc(&tm_ltlo);
-        if (p.tma_store) tma_prefetch_desc(&tm_g);
+        tma_prefetch_desc(&tm_g);
     }
     if (warp == 2) tmem_alloc_2sm(tmem_slot, TMEM_COLS);
     tc_fence_before();
@@ -189,8 +207,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
         // ============ TMA producer: this CTA's half of each landmark chunk (hi, lo) ============
         if (lane == 0) {
             const uint64_t keep = policy_evict_last();    // landmarks: reused by every tile
-            uint32_t lm_s = 0, lm_ph = 0;
-            for (int tile = pair; tile < num_tiles; tile += num_pairs) {
+            const uint64_t stream = policy_evict_first();  // X: read once per tile
+            uint32_t lm_s = 0, lm_ph = 0, xit = 0;
+            for (int tile = pair; tile < num_tiles; tile += num_pairs, ++xit) {
+                // this CTA's 128 rows of the tile's X planes, a tile ahead of its use
+                mbar_wait(xs_empty, (xit & 1) ^ 1);
+                mbar_arrive_expect_tx(xs_full, 2 * X_BYTES);
+                const int xrow = (tile % p.n_row_tiles) * PM + static_cast<int>(rank) * BM;
+                tma_load_2d_hint(&tm_xhi, xs_full, smem + OFF_X, 0, xrow, stream);
+                tma_load_2d_hint(&tm_xlo, xs_full, smem + OFF_X + X_BYTES, 0, xrow, stream);
                 for (int j = 0; j < p.n_chunks; ++j) {
                     mbar_wait_cluster(lm_empty + lm_s, lm_ph ^ 1);
                     if (leader) mbar_arrive_expect_tx(lm_full + lm_s, 2 * 2 * LM_BYTES);
@@ -337,21 +362,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
         PhaseProbe pr((p.dbg & 16) != 0);
         const uint32_t x_full_l = lead(x_full), g_empty_l = lead(g_empty), z_full_l = lead(z_full);
 
-        // X tile rt: this thread's row of the hi (half 0) or lo (half 1) plane, loaded
-        // into registers a whole tile ahead, then written to TMEM once the previous
-        // tile's last GEMM1 has consumed X.
-        uint32_t xv[32];
-        auto load_x = [&](int rt) {
-            const uint4* src = reinterpret_cast<const uint4*>(
-                (half ? p.x_lo : p.x_hi) + (static_cast<long long>(rt) * PM + r_pair) * KD);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const uint4 q = __ldg(src + i);
-                xv[4 * i] = q.x; xv[4 * i + 1] = q.y; xv[4 * i + 2] = q.z; xv[4 * i + 3] = q.w;
-            }
-        };
+        // X tile of iteration itx: this thread's row of the hi (half 0) or lo (half 1)
+        // plane from the TMA-staged SMEM copy (128-byte swizzled rows: 16-byte chunk c of
+        // row r at chunk c ^ (r & 7)) into TMEM, once the previous tile's last GEMM1 has
+        // consumed X.
         auto write_x = [&](uint32_t itx) {
-            const uint32_t (&v)[32] = xv;
+            uint32_t v[32];
+            mbar_wait(xs_full, itx & 1);
+            const uint32_t row = base_addr + OFF_X + (half ? X_BYTES : 0) + static_cast<uint32_t>(r) * 128u;
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+                ld_shared_v4(row + ((static_cast<uint32_t>(c) ^ static_cast<uint32_t>(r & 7)) << 4), v[4 * c],
+                             v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(xs_empty);
             mbar_wait_cluster(x_empty, (itx & 1) ^ 1);
             tc_fence_after();
             tmem_st_32x32b_x32(tmem_base + lane_off + (half ? TM_XLO : TM_XHI), v);
@@ -421,92 +445,61 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
                 if (lane == 0) mbar_arrive_cluster(g_empty_l);
                 return;
             }
-            const int grow = rt * PM + r_pair;
-            const bool row_ok = grow < p.n_rows;
-            OutT* grow_ptr = static_cast<OutT*>(p.G) + static_cast<long long>(grow) * p.ldg;
             constexpr int SLAB = 128 / sizeof(OutT);  // columns per 128-byte staging row
-#pragma unroll 1
+            // All 128 of this warp's accumulator columns go to registers first, so the
+            // accumulator is released to the next tile's GEMM2 after one TMEM round trip
+            // rather than after the stores.
+            uint32_t vall[4][32];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) tmem_ld_32x32b_x32(tmem_base + lane_off + TM_G + half * 128 + m * 32, vall[m]);
+            tmem_wait_ld();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(g_empty_l);
+#pragma unroll
             for (int m = 0; m < 4; ++m) {
                 const int c0 = half * 128 + m * 32;
-                uint32_t v[32];
-                tmem_ld_32x32b_x32(tmem_base + lane_off + TM_G + c0, v);
-                tmem_wait_ld();
-                if (m == 3) {
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive_cluster(g_empty_l);
-                }
+                uint32_t (&v)[32] = vall[m];  // scaled in place (register budget)
                 const int gc0 = cb * N2 + c0;
                 if (gc0 >= p.b_eff || (p.dbg & 2)) continue;
                 const float4* cs4 = reinterpret_cast<const float4*>(p.col_scale + gc0);
-                float out[32];
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
-                    const float4 sc = __ldg(cs4 + i);
-                    out[4 * i + 0] = __uint_as_float(v[4 * i + 0]) * sc.x;
-                    out[4 * i + 1] = __uint_as_float(v[4 * i + 1]) * sc.y;
-                    out[4 * i + 2] = __uint_as_float(v[4 * i + 2]) * sc.z;
-                    out[4 * i + 3] = __uint_as_float(v[4 * i + 3]) * sc.w;
+                    const float4 sc = ldg_f4_inorder(cs4 + i);
+                    v[4 * i + 0] = __float_as_uint(__uint_as_float(v[4 * i + 0]) * sc.x);
+                    v[4 * i + 1] = __float_as_uint(__uint_as_float(v[4 * i + 1]) * sc.y);
+                    v[4 * i + 2] = __float_as_uint(__uint_as_float(v[4 * i + 2]) * sc.z);
+                    v[4 * i + 3] = __float_as_uint(__uint_as_float(v[4 * i + 3]) * sc.w);
                 }
-                if (p.tma_store) {
-                    // 32 rows x SLAB columns per store; 128-byte swizzled staging rows
-                    // (16-byte chunk c of row r at chunk c ^ (r & 7)): conflict-free STS.
+                auto out = [&](int k) { return __uint_as_float(v[k]); };
+                // 32 rows x SLAB columns per store; 128-byte swizzled staging rows
+                // (16-byte chunk c of row r at chunk c ^ (r & 7)): conflict-free STS.
 #pragma unroll
-                    for (int sl = 0; sl < 32 / SLAB; ++sl) {
-                        // double-buffered staging: the store issued two slabs ago has
-                        // finished reading this buffer once at most one group is pending
-                        if (lane == 0) bulk_wait_group_read<NSTG - 1>();
-                        __syncwarp();
-                        const uint32_t sbuf = OFF_STG + (ew * NSTG + stg_k) * STG_BYTES;
-                        stg_k = (stg_k + 1) % NSTG;
+                for (int sl = 0; sl < 32 / SLAB; ++sl) {
+                    // double-buffered staging: the store issued two slabs ago has
+                    // finished reading this buffer once at most one group is pending
+                    if (lane == 0) bulk_wait_group_read<NSTG - 1>();
+                    __syncwarp();
+                    const uint32_t sbuf = OFF_STG + (ew * NSTG + stg_k) * STG_BYTES;
+                    stg_k = (stg_k + 1) % NSTG;
 #pragma unroll
-                        for (int c = 0; c < 8; ++c) {
-                            uint32_t w[4];
-                            if constexpr (sizeof(OutT) == 8) {
-                                const double d0 = out[sl * SLAB + 2 * c], d1 = out[sl * SLAB + 2 * c + 1];
-                                w[0] = __double2loint(d0); w[1] = __double2hiint(d0);
-                                w[2] = __double2loint(d1); w[3] = __double2hiint(d1);
-                            } else {
+                    for (int c = 0; c < 8; ++c) {
+                        uint32_t w[4];
+                        if constexpr (sizeof(OutT) == 8) {
+                            const double d0 = out(sl * SLAB + 2 * c), d1 = out(sl * SLAB + 2 * c + 1);
+                            w[0] = __double2loint(d0); w[1] = __double2hiint(d0);
+                            w[2] = __double2loint(d1); w[3] = __double2hiint(d1);
+                        } else {
 #pragma unroll
-                                for (int e = 0; e < 4; ++e) w[e] = __float_as_uint(out[4 * c + e]);
-                            }
-                            st_shared_v4(base_addr + sbuf + lane * 128 + ((c ^ (lane & 7)) << 4), w[0], w[1], w[2], w[3]);
+                            for (int e = 0; e < 4; ++e) w[e] = __float_as_uint(out(4 * c + e));
                         }
-                        fence_proxy_async_smem();
-                        __syncwarp();
-                        if (lane == 0) {
-                            tma_store_2d(&tm_g, smem + sbuf, gc0 + sl * SLAB, rt * PM + static_cast<int>(rank) * BM + quad * 32);
-                            bulk_commit_group();
-                        }
+                        st_shared_v4(base_addr + sbuf + lane * 128 + ((c ^ (lane & 7)) << 4), w[0], w[1], w[2], w[3]);
                     }
-                    continue;
-                }
-                if (!row_ok) continue;
-                OutT* dst = grow_ptr + gc0;
-                const int ncols = min(32, p.b_eff - gc0);
-                const bool vec = ncols == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
-                if constexpr (sizeof(OutT) == 8) {
-                    if (vec) {
-#pragma unroll
-                        for (int i = 0; i < 16; ++i)
-                            reinterpret_cast<double2*>(dst)[i] =
-                                make_double2(static_cast<double>(out[2 * i]),
-                                             static_cast<double>(out[2 * i + 1]));
-                    } else {
-#pragma unroll
-                        for (int i = 0; i < 32; ++i)
-                            if (i < ncols) dst[i] = static_cast<OutT>(out[i]);
-                    }
-                } else {
-                    if (vec) {
-#pragma unroll
-                        for (int i = 0; i < 8; ++i)
-                            reinterpret_cast<float4*>(dst)[i] =
-                                make_float4(out[4 * i], out[4 * i + 1], out[4 * i + 2], out[4 * i + 3]);
-                    } else {
-#pragma unroll
-                        for (int i = 0; i < 32; ++i)
-                            if (i < ncols) dst[i] = static_cast<OutT>(out[i]);
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tma_store_2d(&tm_g, smem + sbuf, gc0 + sl * SLAB, rt * PM + static_cast<int>(rank) * BM + quad * 32);
+                        bulk_commit_group();
                     }
                 }
             }
@@ -519,16 +512,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
         // Tiles run column-block-major (tile = cb·n_row_tiles + rt), so the CTAs in
         // flight share one 4 MB Lᵀ column block in L2.
         uint32_t it = 0;
-        if (pair < num_tiles) {
-            load_x(pair % p.n_row_tiles);
-            write_x(0);
-        }
+        if (pair < num_tiles) write_x(0);
         for (int tile = pair; tile < num_tiles; tile += num_pairs, ++it) {
             const int rt = tile % p.n_row_tiles;
             const float2 ra = p.row_aux[rt * PM + r_pair];
             const uint64_t R2 = f2_pack(ra.x, ra.x), sx2 = f2_pack(ra.y, ra.y);
             const int next = tile + num_pairs;
-            if (next < num_tiles) load_x(next % p.n_row_tiles);
             for (int j = 0; j < p.n_chunks; ++j) {
                 if (p.dbg & 32) {  // bypass: keep the barrier protocol, skip Z math and stores
                     const uint32_t b = cnt % NSZ, ph = (cnt / NSZ) & 1;

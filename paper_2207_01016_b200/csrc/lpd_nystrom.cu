@@ -179,6 +179,8 @@ struct DeviceState {
     int64_t res_r0 = 0, res_rows = 0, res_ld = 0, res_cap = 0;
     void* scratch = nullptr;   // per-call device scratch of the resident-G products
     size_t scratch_cap = 0;
+    void* gtmp = nullptr;      // aligned G staging for caller layouts TMA cannot store to
+    size_t gtmp_bytes = 0;
     int2* pairs = nullptr;     // OVO pair table for the vote (K5)
     int pairs_classes = 0;
     int32_t* votes = nullptr;  // per-chunk predicted class indices
@@ -468,6 +470,10 @@ void launch_factor_panels(DeviceState& ds, Slot& s, int64_t m, void* g_dev, int6
         CUDA_TRY(cudaEventRecord(ds.kev[0], st));
         if (ds.ring_count < DeviceState::kRing) CUDA_TRY(cudaEventRecord(pr[0], st));
     }
+    static const int group_r = [] {
+        const char* e = std::getenv("LPD_PANEL_GROUP");
+        return e ? std::max(1, std::atoi(e)) : 8;
+    }();
     const CUtensorMap tm_zhi = make_plane_map(ds.z_hi, panel, ds.B_pad, lpd::kp::BM, 64);
     const CUtensorMap tm_zlo = make_plane_map(ds.z_lo, panel, ds.B_pad, lpd::kp::BM, 64);
     for (int64_t r0 = 0; r0 < m; r0 += panel) {
@@ -485,6 +491,7 @@ void launch_factor_panels(DeviceState& ds, Slot& s, int64_t m, void* g_dev, int6
         pz.z_hi = ds.z_hi;
         pz.z_lo = ds.z_lo;
         pz.ldz = ds.B_pad;
+        pz.group_r = group_r;
         const int64_t tz = static_cast<int64_t>(pz.n_row_pairs) * pz.n_col_blocks;
         const int gz = 2 * static_cast<int>(std::min<int64_t>(tz, ds.num_sms / 2));
         lpd::panel_gemm_kernel<lpd::PANEL_Z, float><<<gz, lpd::kp::THREADS, lpd::kp::SMEM_BYTES, st>>>(
@@ -499,6 +506,7 @@ void launch_factor_panels(DeviceState& ds, Slot& s, int64_t m, void* g_dev, int6
         const size_t es = out_dtype == LPD_OUT_F64 ? 8 : 4;
         pg.G = static_cast<char*>(g_dev) + static_cast<size_t>(r0) * ldg * es;
         pg.ldg = ldg;
+        pg.group_r = group_r;
         const int64_t tg = static_cast<int64_t>(pg.n_row_pairs) * pg.n_col_blocks;
         const int gg = 2 * static_cast<int>(std::min<int64_t>(tg, ds.num_sms / 2));
         if (out_dtype == LPD_OUT_F64)
@@ -533,11 +541,30 @@ void launch_factor(DeviceState& ds, Slot& s, const double* x_dev, int64_t m, int
         launch_factor_panels(ds, s, m, g_dev, ldg, out_dtype, st, time_it);
         return;
     }
+    // The kernel stores G with TMA, which needs 16-byte aligned rows; an unaligned
+    // caller layout is served through an aligned device buffer and a 2-D copy.
     CUtensorMap tm_g;
     std::memset(&tm_g, 0, sizeof(tm_g));
-    const bool tma_store = make_g_map(&tm_g, g_dev, static_cast<uint64_t>(m),
-                                      static_cast<uint64_t>(ds.b_eff), static_cast<uint64_t>(ldg),
-                                      out_dtype == LPD_OUT_F64);
+    const size_t es = out_dtype == LPD_OUT_F64 ? 8 : 4;
+    void* g_out = g_dev;
+    int64_t ld_out = ldg;
+    if (!make_g_map(&tm_g, g_dev, static_cast<uint64_t>(m), static_cast<uint64_t>(ds.b_eff),
+                    static_cast<uint64_t>(ldg), out_dtype == LPD_OUT_F64)) {
+        ld_out = round_up(ds.b_eff, 4);
+        const size_t need = static_cast<size_t>(m * ld_out) * es;
+        if (ds.gtmp_bytes < need) {
+            CUDA_TRY(cudaStreamSynchronize(st));
+            if (ds.gtmp) cudaFree(ds.gtmp);
+            ds.gtmp = nullptr;
+            ds.gtmp_bytes = 0;
+            CUDA_TRY(cudaMalloc(&ds.gtmp, need));
+            ds.gtmp_bytes = need;
+        }
+        g_out = ds.gtmp;
+        if (!make_g_map(&tm_g, g_out, static_cast<uint64_t>(m), static_cast<uint64_t>(ds.b_eff),
+                        static_cast<uint64_t>(ld_out), out_dtype == LPD_OUT_F64))
+            fail(LPD_ERR_CUDA, "cannot describe the G staging buffer as a TMA tensor");
+    }
     lpd::FactorParams p;
     p.n_rows = static_cast<int>(m);
     p.n_row_tiles = static_cast<int>(m_pad / lpd::k1::PM);
@@ -546,12 +573,7 @@ void launch_factor(DeviceState& ds, Slot& s, const double* x_dev, int64_t m, int
     p.b_eff = static_cast<int>(ds.b_eff);
     p.ksteps1 = static_cast<int>((ds.d + 1 + 15) / 16);
     p.row_aux = s.raux;
-    p.x_hi = s.xhi;
-    p.x_lo = s.xlo;
-    p.tma_store = tma_store ? 1 : 0;
     p.col_scale = ds.col_scale;
-    p.G = g_dev;
-    p.ldg = ldg;
     static const int dbg = [] {
         const char* e = std::getenv("LPD_K1_DEBUG");
         return e ? std::atoi(e) : 0;
@@ -573,12 +595,14 @@ void launch_factor(DeviceState& ds, Slot& s, const double* x_dev, int64_t m, int
         CUDA_TRY(cudaEventRecord(ds.kev[0], st));
         if (ds.ring_count < DeviceState::kRing) CUDA_TRY(cudaEventRecord(pr[0], st));
     }
+    const CUtensorMap tm_xhi = make_plane_map(s.xhi, m_pad, lpd::KD_MAX, lpd::k1::BM, 64);
+    const CUtensorMap tm_xlo = make_plane_map(s.xlo, m_pad, lpd::KD_MAX, lpd::k1::BM, 64);
     if (out_dtype == LPD_OUT_F64)
         lpd::nystrom_factor_kernel<double><<<grid, lpd::k1::THREADS, lpd::k1::SMEM_BYTES, st>>>(
-            ds.tm_lmhi, ds.tm_lmlo, ds.tm_lthi, ds.tm_ltlo, tm_g, p);
+            tm_xhi, tm_xlo, ds.tm_lmhi, ds.tm_lmlo, ds.tm_lthi, ds.tm_ltlo, tm_g, p);
     else
         lpd::nystrom_factor_kernel<float><<<grid, lpd::k1::THREADS, lpd::k1::SMEM_BYTES, st>>>(
-            ds.tm_lmhi, ds.tm_lmlo, ds.tm_lthi, ds.tm_ltlo, tm_g, p);
+            tm_xhi, tm_xlo, ds.tm_lmhi, ds.tm_lmlo, ds.tm_lthi, ds.tm_ltlo, tm_g, p);
     if (dbg & 16) {
         unsigned long long h[16];
         CUDA_TRY(cudaMemcpyAsync(h, dbg_out, sizeof(h), cudaMemcpyDeviceToHost, st));
@@ -597,6 +621,9 @@ void launch_factor(DeviceState& ds, Slot& s, const double* x_dev, int64_t m, int
         ++ds.ring_count;
     }
     CUDA_TRY(cudaGetLastError());
+    if (g_out != g_dev)
+        CUDA_TRY(cudaMemcpy2DAsync(g_dev, es * ldg, g_out, es * ld_out, es * ds.b_eff,
+                                   static_cast<size_t>(m), cudaMemcpyDeviceToDevice, st));
 }
 
 // Reads (and clears) the row-prep range flag after the device's work is complete.
@@ -1027,6 +1054,7 @@ int lpd_context_destroy(lpd_context* ctx) {
         dev_free(ds.votes);
         dev_free(ds.res_g);
         if (ds.scratch) cudaFree(ds.scratch);
+        if (ds.gtmp) cudaFree(ds.gtmp);
         for (auto& s : ds.slot) {
             ds.free_slot(s);
             if (s.stream) cudaStreamDestroy(s.stream);

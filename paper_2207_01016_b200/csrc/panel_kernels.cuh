@@ -22,7 +22,7 @@
 // planes, with cta_group::2 loads counted on the leader's barrier); the leader issues
 // three split products per chunk (A_hi·B_hi + A_lo·B_hi + A_hi·B_lo) as M=256, N=256
 // tcgen05 SS MMAs into one of TWO TMEM accumulators, so the epilogue of tile t
-// overlaps the main loop of tile t+1. Tiles are rastered in groups of 8 row pairs so
+// overlaps the main loop of tile t+1. Tiles are rastered in groups of row pairs so
 // the pairs in flight share A rows and B rows in L2.
 #pragma once
 
@@ -45,6 +45,7 @@ struct PanelParams {
     const float* col_scale;   // MODE_G: 2^-13 / u_k per G column
     void* G;                  // MODE_G output, row-major, leading dimension ldg
     long long ldg;
+    int group_r;              // row pairs per raster group (L2 reuse of A and B rows)
 };
 
 namespace kp {
@@ -56,7 +57,6 @@ constexpr int BK = 64;        // K per chunk (one 128-byte swizzle atom of fp16)
 constexpr int NS = 3;         // chunk stages
 constexpr int EPI_WARPS = 8;
 constexpr int THREADS = 128 + 32 * EPI_WARPS;
-constexpr int GROUP_R = 8;    // row pairs per raster group
 constexpr uint32_t A_BYTES = BM * BK * 2;    // 16 KB per plane
 constexpr uint32_t B_BYTES = BNH * BK * 2;   // 16 KB per plane
 constexpr uint32_t STAGE = 2 * A_BYTES + 2 * B_BYTES;
@@ -66,12 +66,14 @@ constexpr uint32_t SMEM_BYTES = OFF_BAR + NUM_BARS * 8 + 16 + 1024;
 constexpr uint32_t IDESC = idesc_f16_f32(PM, BN);
 constexpr uint16_t PAIR = 0x3;
 
-__device__ __forceinline__ void tile_coords(int t, int nrp, int ncb, int& rp, int& cb) {
-    const int per_group = GROUP_R * ncb;
+// Tile t -> (row pair, column block): groups of group_r row pairs, column-major inside
+// a group, so the tiles in flight share group_r A row blocks and few B row blocks.
+__device__ __forceinline__ void tile_coords(int t, int nrp, int ncb, int group_r, int& rp, int& cb) {
+    const int per_group = group_r * ncb;
     const int g = t / per_group;
     const int in = t - g * per_group;
-    const int rows_in_group = min(GROUP_R, nrp - g * GROUP_R);
-    rp = g * GROUP_R + in % rows_in_group;
+    const int rows_in_group = min(group_r, nrp - g * group_r);
+    rp = g * group_r + in % rows_in_group;
     cb = in / rows_in_group;
 }
 }  // namespace kp
@@ -125,7 +127,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kp::THREADS, 1)
             uint32_t s = 0, ph = 0;
             for (int tile = pair; tile < num_tiles; tile += num_pairs) {
                 int rp, cb;
-                tile_coords(tile, p.n_row_pairs, p.n_col_blocks, rp, cb);
+                tile_coords(tile, p.n_row_pairs, p.n_col_blocks, p.group_r, rp, cb);
                 const int arow = rp * PM + static_cast<int>(rank) * BM;
                 const int brow = cb * BN + static_cast<int>(rank) * BNH;
                 for (int kc = 0; kc < p.n_kchunks; ++kc) {
@@ -185,7 +187,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kp::THREADS, 1)
         for (int tile = pair; tile < num_tiles; tile += num_pairs, ++it) {
             const uint32_t a = it & 1, aph = (it >> 1) & 1;
             int rp, cb;
-            tile_coords(tile, p.n_row_pairs, p.n_col_blocks, rp, cb);
+            tile_coords(tile, p.n_row_pairs, p.n_col_blocks, p.group_r, rp, cb);
             const long long row = static_cast<long long>(rp) * PM + rank * BM + quad * 32 + lane;
             float R = 0.f, sx = 0.f;
             if constexpr (MODE == PANEL_Z) {

@@ -88,7 +88,19 @@ def main():
         t0 = time.perf_counter()
         pred2 = model2.predict(test, threads=args.threads)
         predict2_s = time.perf_counter() - t0
-        out = {"build": args.module_dir, "n": args.n, "d": args.d, "budget": args.budget,
+        extra = {}
+        so = glob.glob(os.path.join(os.path.dirname(lpdsvm.__file__), "_core*.so"))[0]
+        lib = ctypes.CDLL(so)
+        if hasattr(lib, "lpd_adapter_phases"):
+            ph = (ctypes.c_double * 4)()
+            lib.lpd_adapter_phases(ph)
+            tm = (ctypes.c_double * 10)()  # lpd_timings (64 bytes): total, h2d, kernel, d2h, host_copy, ...
+            lib.lpd_adapter_last_timings(ctypes.cast(tm, ctypes.c_void_p))
+            extra["compute_G_phases"] = {"flatten": ph[0], "basis": ph[1], "matrix_alloc_zero_fill": ph[2],
+                                         "device_call": ph[3], "device_call_total": tm[0],
+                                         "h2d_event_s": tm[1], "kernel_event_s": tm[2], "d2h_event_s": tm[3],
+                                         "host_widen_s": tm[4]}
+        out = {"build": args.module_dir, "n": args.n, "d": args.d, "budget": args.budget, **extra,
                "effective_rank": model.effective_rank, "threads": args.threads,
                "parse_seconds": parse_s,
                "cold": {"train_wall_seconds": train_s, "predict_seconds": predict_s,
