@@ -138,7 +138,7 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def make_basis(X0, cfg, seed=1, device=None):
+def make_basis(X0, cfg, seed=1, device=None, return_ids=False):
     """Landmarks: B rows of rank 0's data drawn uniformly without replacement
     (as the reference's select_landmarks does, factor.cpp:27-31; numpy's seeded
     generator here); L from the eigendecomposition of K (factor.cpp:33-81).
@@ -152,7 +152,8 @@ def make_basis(X0, cfg, seed=1, device=None):
         w, U = np.linalg.eigh(0.5 * (K + K.T))
         w, U = w[::-1], U[:, ::-1]
         keep = w > 1e-12 * w[0]
-        return Y, np.ascontiguousarray(U[:, keep] / np.sqrt(w[keep]))
+        L = np.ascontiguousarray(U[:, keep] / np.sqrt(w[keep]))
+        return (Y, L, ids) if return_ids else (Y, L)
     import torch
 
     Yt = torch.from_numpy(Y).to(device)
@@ -161,8 +162,8 @@ def make_basis(X0, cfg, seed=1, device=None):
     w, U = torch.linalg.eigh(0.5 * (K + K.T))
     w, U = torch.flip(w, [0]), torch.flip(U, [1])
     keep = w > 1e-12 * w[0]
-    L = (U[:, keep] / torch.sqrt(w[keep])).contiguous()
-    return Y, L.cpu().numpy()
+    L = (U[:, keep] / torch.sqrt(w[keep])).contiguous().cpu().numpy()
+    return (Y, L, ids) if return_ids else (Y, L)
 
 
 def cpu_reference_rate(X, Y, L, gamma, target_s, threads, max_rows):

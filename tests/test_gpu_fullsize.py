@@ -1,0 +1,105 @@
+"""Parity at BASELINE.json's full sizes (one GPU's row shard of C2, C3 and C4).
+
+The whole shard is computed on the device through the C ABI (lpd_set_basis_device +
+lpd_compute_g_device, fp32 G so C3's 625,000 × 8,192 shard fits beside its inputs),
+then checked with properties that do not need a full CPU factor:
+
+  * sampled rows (tile edges, shard ends, random rows, landmark rows) against the
+    reference's own compute_G (oracle/_ref, all host threads), same landmarks and L:
+    max row-normwise relative error ≤ 1e-4 (tests/test_gpu_parity.py tolerance);
+  * the Nyström bound on every row: ‖G_i‖² = z_iᵀ·U·D⁻¹·Uᵀ·z_i ≤ k(x_i, x_i) = 1
+    (a Schur complement of the PSD kernel matrix; SPEC.md:207-221 identities);
+  * the Nyström identity on the landmark rows (they are rows of the shard):
+    G_S·G_Sᵀ = K_SS and diag = 1 when no eigenvalue is truncated;
+  * row-batching invariance: a sub-range recomputed on its own is bitwise equal.
+"""
+import numpy as np
+import pytest
+
+import paper_2207_01016_b200 as P
+from conftest import row_rel_err
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TOL_G = 1e-4
+TOL_NORM = 2e-3   # ‖G_i‖² − 1 on landmark rows / excess over 1 anywhere (fp32-level G, κ(K) amplification)
+TOL_GRAM = 2e-3   # |G_S G_Sᵀ − K_SS| on sampled landmark pairs
+
+
+def _setup(workload):
+    import torch
+
+    import bench
+    from paper_2207_01016_b200 import synthetic
+
+    cfg = synthetic.CONFIGS[workload]
+    n = synthetic.rows_per_gpu(cfg)
+    X, _ = synthetic.make(cfg, rows=slice(0, n))
+    dev = torch.device("cuda", 0)
+    Y, L, ids = bench.make_basis(X, cfg, device=dev, return_ids=True)
+    return cfg, n, X, Y, L, np.asarray(ids), dev
+
+
+def _reference_rows(X, rows, Y, L, gamma):
+    if not O.ref_available():
+        pytest.fail("reference build oracle/_ref missing on this box")
+    threads = O.ref_lib().ref_hardware_threads()
+    xs = O.dense_to_csr(np.ascontiguousarray(X[rows]))
+    chunk = max(1, -(-len(rows) // threads))
+    return O.ref_compute_g(xs, O.dense_to_csr(Y), L, gamma, chunk, threads)
+
+
+@pytest.mark.parametrize("workload,n_sample", [("c2", 384), ("c3", 384), ("c4", 48)])
+def test_full_shard_properties(workload, n_sample):
+    import torch
+
+    cfg, n, X, Y, L, ids, dev = _setup(workload)
+    b_eff = L.shape[1]
+    X_dev = torch.from_numpy(X).to(dev)
+    lm_dev = torch.from_numpy(Y).to(dev)
+    L_dev = torch.from_numpy(L).to(dev)
+    G_dev = torch.empty((n, b_eff), dtype=torch.float32, device=dev)
+    with P.Context(device_ids=[0]) as ctx:
+        ctx.set_basis_device(lm_dev, L_dev, cfg.gamma)
+        ctx.compute_g_device(X_dev, G_dev)
+        torch.cuda.synchronize(dev)
+
+        # Nyström bound on every row of the shard, and finiteness
+        sq = torch.empty(n, dtype=torch.float64, device=dev)
+        for r0 in range(0, n, 65536):
+            g = G_dev[r0:r0 + 65536].double()
+            sq[r0:r0 + 65536] = (g * g).sum(1)
+        assert bool(torch.isfinite(sq).all())
+        assert float(sq.max()) <= 1.0 + TOL_NORM, float(sq.max())
+
+        # landmark rows: diag(G_S G_Sᵀ) = 1 and G_S G_Sᵀ = K_SS (full rank basis)
+        ids_t = torch.from_numpy(ids).to(dev)
+        if b_eff == Y.shape[0]:
+            dsq = sq[ids_t]
+            assert float((dsq - 1.0).abs().max()) <= TOL_NORM
+        pick = np.random.default_rng(0).choice(len(ids), min(512, len(ids)), replace=False)
+        GS = G_dev[ids_t[torch.from_numpy(pick).to(dev)]].double()
+        Ys = Y[pick]
+        ny = (Ys * Ys).sum(1)
+        K = np.exp(-cfg.gamma * np.maximum(ny[:, None] + ny[None, :] - 2.0 * Ys @ Ys.T, 0.0))
+        assert np.abs((GS @ GS.T).cpu().numpy() - K).max() <= TOL_GRAM
+
+        # sampled rows against the reference compute_G: shard ends, 256-row pair-tile
+        # edges, random rows and a few landmark rows
+        rng = np.random.default_rng(1)
+        edges = [0, 1, 255, 256, 257, n // 2, n - 257, n - 256, n - 1]
+        rows = np.unique(np.concatenate([edges, rng.choice(n, n_sample, replace=False), ids[:8]]))
+        R = _reference_rows(X, rows, Y, L, cfg.gamma)
+        Gs = G_dev[torch.from_numpy(rows).to(dev)].double().cpu().numpy()
+        err = row_rel_err(Gs, R)
+        assert err <= TOL_G, err
+
+        # batching invariance: an unaligned sub-range recomputed alone is bitwise equal
+        a, b = n // 3 + 17, n // 3 + 17 + 5000
+        G_sub = torch.empty((b - a, b_eff), dtype=torch.float32, device=dev)
+        ctx.compute_g_device(X_dev[a:b].contiguous(), G_sub)
+        torch.cuda.synchronize(dev)
+        assert torch.equal(G_sub, G_dev[a:b])
+    del G_dev, X_dev
+    torch.cuda.empty_cache()
