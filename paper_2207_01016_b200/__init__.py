@@ -36,7 +36,8 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblpd_nystrom.so")
+# LPD_LIBRARY: an alternative in-tree build of the same library (profiling variants)
+LIB_PATH = os.environ.get("LPD_LIBRARY") or os.path.join(_HERE, "liblpd_nystrom.so")
 
 LPD_OK = 0
 LPD_ERR_INVALID_ARGUMENT = 1

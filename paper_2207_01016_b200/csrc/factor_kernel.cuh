@@ -15,7 +15,8 @@
 //   warp 1     MMA issuer (one elected lane)                            [leader CTA]
 //   warp 2     TMEM allocator (cta_group::2)                            [both CTAs]
 //   warp 3     TMA producer: Lᵀ half-chunks of the tile's column block [both CTAs]
-//   warps 4-11 epilogue: X → TMEM; S → Z (in place, TMEM); G → SMEM → TMA store
+//   warps 4-11 epilogue: X → TMEM; S → Z (in place, TMEM); G segments → fp32
+//              running sums in registers; G → SMEM → TMA store
 // Barriers the MMA waits on live in the leader CTA (TMA bytes and epilogue arrivals
 // of both CTAs land there); MMA commits multicast to both CTAs.
 //
@@ -26,6 +27,17 @@
 //               hi/lo, which GEMM2 reads as its A operand (TS form)
 //   [448, 512)  X tile, fp16 hi [448, 480) and lo [480, 512): GEMM1's A operand
 // so neither X, S nor Z ever touches shared memory, and no K/Z block touches HBM.
+//
+// Segmented G accumulation. The tensor core adds every MMA into the fp32 TMEM
+// accumulator with round-toward-zero; over C2's 768 K-steps per tile that bias alone
+// costs ~2e-4 relative error in G (C3: ~3e-3). GEMM2 is therefore
+// issued as two N=128 halves (TMEM columns [0,128) and [128,256)), and each half's
+// K range is cut into segments of `seg_chunks` chunks: at a segment end the epilogue
+// warps owning that half (they own exactly those 128 TMEM columns) add it into an
+// fp32 round-to-nearest running sum held in registers and release it; the next
+// segment restarts the accumulator from zero. The two halves' segment boundaries are
+// staggered by half a segment, and the MMA issues the other half first at a boundary,
+// so the tensor pipe keeps working while one half is read out.
 //
 // Precision: operands are unevaluated sums hi + lo of two fp16 values after exact
 // power-of-two scaling, and each product is three kind::f16 MMAs (hi·hi + hi·lo +
@@ -50,6 +62,8 @@ struct FactorParams {
     const float* col_scale; // [Beff_pad] 2^-13 / u_k (undoes Z and Lᵀ-row scaling)
     // output G: the tm_g tensor map (TMA store, 16-byte aligned rows; the host stages
     // through an aligned buffer otherwise)
+    int seg_chunks;         // chunks per G accumulator segment (>= 1)
+    int split_n;            // 1: GEMM2 as two N=128 halves with staggered segments; 0: one N=256 MMA
     int dbg;                // profiling ablations (LPD_K1_DEBUG), 0 in production
     unsigned long long* dbg_out;  // [2 roles x 8 phases] cycle sums when dbg & 16
 };
@@ -59,6 +73,14 @@ struct FactorParams {
 // at kernel end. In production builds it compiles to nothing (no registers).
 #ifndef LPD_K1_PROBE
 #define LPD_K1_PROBE 0
+#endif
+// Profiling builds only: LPD_K1_NOSEG=1 drops the mid-tile segment flushes (one
+// accumulator segment per tile), LPD_K1_NOREG=1 drops the register reallocation.
+#ifndef LPD_K1_NOSEG
+#define LPD_K1_NOSEG 0
+#endif
+#ifndef LPD_K1_NOREG
+#define LPD_K1_NOREG 0
 #endif
 #if LPD_K1_PROBE
 struct PhaseProbe {
@@ -113,7 +135,7 @@ constexpr uint32_t OFF_STG = OFF_LT + NS_LT * LT_BYTES;             // warp w, b
 constexpr uint32_t X_BYTES = BM * KD * 2;           // 16 KB: one X plane of this CTA's rows
 constexpr uint32_t OFF_X = OFF_STG + EPI_WARPS * NSTG * STG_BYTES;  // hi, lo
 constexpr uint32_t OFF_BAR = OFF_X + 2 * X_BYTES;
-constexpr uint32_t NUM_BARS = 4 + 2 * NS_LM + 2 * NS_LT + 3 * NSZ + 2;
+constexpr uint32_t NUM_BARS = 6 + 2 * NS_LM + 2 * NS_LT + 3 * NSZ + 2;
 constexpr uint32_t SMEM_BYTES = OFF_BAR + NUM_BARS * 8 + 16 + 1024;  // + alignment slack
 
 constexpr uint32_t TMEM_COLS = 512;
@@ -123,7 +145,9 @@ constexpr uint32_t TM_XHI = 448;
 constexpr uint32_t TM_XLO = 480;
 
 constexpr uint32_t IDESC_G1 = idesc_f16_f32(PM, NC);
-constexpr uint32_t IDESC_G2 = idesc_f16_f32(PM, N2);
+constexpr uint32_t IDESC_G2H = idesc_f16_f32(PM, N2 / 2);  // one half of the G tile
+constexpr uint32_t IDESC_G2 = idesc_f16_f32(PM, N2);        // the whole G tile
+constexpr uint32_t LT_HALF = (N2H / 2) * 128;               // bytes of 64 Lᵀ rows (8 swizzle atoms)
 constexpr uint16_t PAIR = 0x3;     // multicast mask: both CTAs of the pair
 
 // Column of K-step k (16 landmarks) of the Z hi / lo planes inside an S/Z buffer.
@@ -132,6 +156,20 @@ constexpr uint16_t PAIR = 0x3;     // multicast mask: both CTAs of the pair
 // columns another warp may still be reading.
 __device__ __forceinline__ uint32_t z_hi_col(uint32_t k) { return (k >> 1) * 32 + (k & 1) * 8; }
 __device__ __forceinline__ uint32_t z_lo_col(uint32_t k) { return z_hi_col(k) + 16; }
+
+// Segment boundaries of G half h (with split halves, staggered by half a segment).
+__device__ __forceinline__ bool seg_end(int h, int j, int n, int S, int split) {
+    return j == n - 1 || ((j + 1 + h * split * (S >> 1)) % S) == 0;
+}
+__device__ __forceinline__ bool seg_start(int h, int j, int n, int S, int split) {
+    return j == 0 || seg_end(h, j - 1, n, S, split);
+}
+// Tile column of running-sum entry e (0..127) of G half h. One N=256 MMA: TMEM
+// columns are tile columns. Split halves: TMEM half h holds 64 Lᵀ rows of each CTA of
+// the pair (CTA r holds tile columns [128r, 128r + 128)).
+__device__ __forceinline__ int half_col(int h, int e, int split) {
+    return split ? (e < 64 ? 0 : 64) + 64 * h + e : 128 * h + e;
+}
 }  // namespace k1
 
 template <typename OutT>
@@ -160,9 +198,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
     uint64_t* s_full = lt_empty + NS_LT;
     uint64_t* z_full = s_full + NSZ;
     uint64_t* sz_empty = z_full + NSZ;
-    uint64_t* g_full = sz_empty + NSZ;
-    uint64_t* g_empty = g_full + 1;
-    uint64_t* xs_full = g_empty + 1;   // X tile landed in SMEM (TMA)
+    uint64_t* acc_full = sz_empty + NSZ;  // [2] G half h: segment complete (MMA commit)
+    uint64_t* acc_empty = acc_full + 2;   // [2] G half h: segment read into the running sums
+    uint64_t* xs_full = acc_empty + 2;    // X tile landed in SMEM (TMA)
     uint64_t* xs_empty = xs_full + 1;  // X tile copied from SMEM into TMEM
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NUM_BARS);
 
@@ -185,8 +223,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
             mbar_init(z_full + b, 2 * EPI_WARPS);
             mbar_init(sz_empty + b, 1);
         }
-        mbar_init(g_full, 1);
-        mbar_init(g_empty, 2 * EPI_WARPS);
+        for (int h = 0; h < 2; ++h) { mbar_init(acc_full + h, 1); mbar_init(acc_empty + h, EPI_WARPS); }
         mbar_init(xs_full, 1);
         mbar_init(xs_empty, EPI_WARPS);
         fence_mbar_init();
@@ -203,7 +240,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    if (warp == 0) {
+    if (warp < 4) {
+      // producer / MMA warpgroup: registers go to the epilogue's running sums
+#if !LPD_K1_NOREG
+      reg_dealloc<56>();
+#endif
+      if (warp == 0) {
         // ============ TMA producer: this CTA's half of each landmark chunk (hi, lo) ============
         if (lane == 0) {
             const uint64_t keep = policy_evict_last();    // landmarks: reused by every tile
@@ -228,7 +270,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
                 }
             }
         }
-    } else if (warp == 3) {
+      } else if (warp == 3) {
         // ============ TMA producer: this CTA's half of the tile's Lᵀ rows, per half-chunk ============
         if (lane == 0) {
             const uint64_t keep = policy_evict_last();
@@ -248,7 +290,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
                 }
             }
         }
-    } else if (warp == 1 && leader) {
+      } else if (warp == 1 && leader) {
         // ============ MMA issuer (pair leader): whole warp follows the schedule, one lane issues ============
         // Descriptor for smem address a is kDescHi | (a >> 4); K-step k adds 2k (32 bytes).
         const uint64_t dbase = sdesc_kmajor_sw128(0);
@@ -288,27 +330,69 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
             if (++lm_s == NS_LM) { lm_s = 0; lm_ph ^= 1; }
             ++c1;
         };
-        // GEMM2 of a chunk: G += Z_hi·Lᵀ_hi + Z_lo·Lᵀ_hi + Z_hi·Lᵀ_lo, Z from TMEM.
-        auto gemm2 = [&](bool first) {
+        // GEMM2 of chunk j: G += Z_hi·Lᵀ_hi + Z_lo·Lᵀ_hi + Z_hi·Lᵀ_lo, Z from TMEM, as two
+        // N=128 halves. A half starting a new segment first waits until the epilogue
+        // has read its previous segment, and restarts from zero; the other half is
+        // issued first so the tensor pipe stays busy meanwhile.
+        const int S = p.seg_chunks, n = p.n_chunks, SP = p.split_n;
+        uint32_t hseg[2] = {0, 0};  // segments started per half (acc_empty parity)
+        auto gemm2 = [&](int j) {
             const uint32_t b = c2 % NSZ, ph = (c2 / NSZ) & 1;
             const uint32_t zb = tmem_base + TM_SZ + b * NC;
-            const uint32_t d = tmem_base + TM_G;
+            const bool st0 = seg_start(0, j, n, S, SP), st1 = seg_start(1, j, n, S, SP);
+            const int h0 = (st0 && !st1) ? 1 : 0;  // issue order of the halves
             pr.mark(5);
             mbar_wait_cluster(z_full + b, ph);
             pr.mark(2);
             mbar_wait_cluster(lt_full + lt_s, lt_ph);
             pr.mark(3);
             tc_fence_after();
-            if (elect_one()) {
-                const uint64_t d_lt = d_lt0 + ((lt_s * LT_BYTES) >> 4);
+            const uint64_t d_lt = d_lt0 + ((lt_s * LT_BYTES) >> 4);
+            if (!SP) {  // one N=256 MMA per K-step: both halves restart together
+                if (st0) {
+                    pr.mark(5);
+                    mbar_wait_cluster(acc_empty + 0, (hseg[0] & 1) ^ 1);
+                    mbar_wait_cluster(acc_empty + 1, (hseg[1] & 1) ^ 1);
+                    pr.mark(4);
+                    ++hseg[0];
+                    ++hseg[1];
+                    tc_fence_after();
+                }
+                if (elect_one()) {
+                    const uint32_t d = tmem_base + TM_G;
 #pragma unroll
-                for (int k = 0; k < NC / 16; ++k)
-                    if (!(p.dbg & 4)) mma_f16_ts_2sm(d, zb + z_hi_col(k), d_lt + 2 * k, IDESC_G2, !(first && k == 0));
+                    for (int k = 0; k < NC / 16; ++k)
+                        if (!(p.dbg & 4)) mma_f16_ts_2sm(d, zb + z_hi_col(k), d_lt + 2 * k, IDESC_G2, !(st0 && k == 0));
 #pragma unroll
-                for (int k = 0; k < NC / 16; ++k)
-                    if (!(p.dbg & 4)) mma_f16_ts_2sm(d, zb + z_lo_col(k), d_lt + 2 * k, IDESC_G2, 1);
-                mma_commit_2sm_mc(lt_empty + lt_s, PAIR);
+                    for (int k = 0; k < NC / 16; ++k)
+                        if (!(p.dbg & 4)) mma_f16_ts_2sm(d, zb + z_lo_col(k), d_lt + 2 * k, IDESC_G2, 1);
+                }
+                __syncwarp();
             }
+#pragma unroll
+            for (int q = 0; q < 2 * SP; ++q) {
+                const int h = h0 ^ q;
+                const bool fresh = h ? st1 : st0;
+                if (fresh) {
+                    pr.mark(5);
+                    mbar_wait_cluster(acc_empty + h, (hseg[h] & 1) ^ 1);
+                    pr.mark(4);
+                    ++hseg[h];
+                    tc_fence_after();
+                }
+                if (elect_one()) {
+                    const uint32_t d = tmem_base + TM_G + h * (N2 / 2);
+                    const uint64_t bh = d_lt + ((h * LT_HALF) >> 4);
+#pragma unroll
+                    for (int k = 0; k < NC / 16; ++k)
+                        if (!(p.dbg & 4)) mma_f16_ts_2sm(d, zb + z_hi_col(k), bh + 2 * k, IDESC_G2H, !(fresh && k == 0));
+#pragma unroll
+                    for (int k = 0; k < NC / 16; ++k)
+                        if (!(p.dbg & 4)) mma_f16_ts_2sm(d, zb + z_lo_col(k), bh + 2 * k, IDESC_G2H, 1);
+                }
+                __syncwarp();
+            }
+            if (elect_one()) mma_commit_2sm_mc(lt_empty + lt_s, PAIR);
             __syncwarp();
             if (++lt_s == NS_LT) { lt_s = 0; lt_ph ^= 1; }
             pr.mark(5);
@@ -316,12 +400,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
             pr.mark(3);
             tc_fence_after();
             if (elect_one()) {
-                const uint64_t d_lt = d_lt0 + ((lt_s * LT_BYTES) >> 4);
+                const uint64_t d_lt2 = d_lt0 + ((lt_s * LT_BYTES) >> 4);
+                if (SP) {
 #pragma unroll
-                for (int k = 0; k < NC / 16; ++k)
-                    if (!(p.dbg & 4)) mma_f16_ts_2sm(d, zb + z_hi_col(k), d_lt + 2 * k, IDESC_G2, 1);
+                    for (int q = 0; q < 2; ++q) {
+                        const int h = h0 ^ q;
+                        const uint32_t d = tmem_base + TM_G + h * (N2 / 2);
+                        const uint64_t bh = d_lt2 + ((h * LT_HALF) >> 4);
+#pragma unroll
+                        for (int k = 0; k < NC / 16; ++k)
+                            if (!(p.dbg & 4)) mma_f16_ts_2sm(d, zb + z_hi_col(k), bh + 2 * k, IDESC_G2H, 1);
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < NC / 16; ++k)
+                        if (!(p.dbg & 4)) mma_f16_ts_2sm(tmem_base + TM_G, zb + z_hi_col(k), d_lt2 + 2 * k, IDESC_G2, 1);
+                }
                 mma_commit_2sm_mc(lt_empty + lt_s, PAIR);
                 mma_commit_2sm(sz_empty + b);
+                if (seg_end(0, j, n, S, SP)) mma_commit_2sm_mc(acc_full + 0, PAIR);
+                if (seg_end(1, j, n, S, SP)) mma_commit_2sm_mc(acc_full + 1, PAIR);
             }
             __syncwarp();
             if (++lt_s == NS_LT) { lt_s = 0; lt_ph ^= 1; }
@@ -336,21 +434,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
             // GEMM1 runs two chunks ahead of GEMM2 (three S/Z buffers).
             gemm1(0);
             if (p.n_chunks > 1) gemm1(1);
-            // G accumulators (both CTAs) must have been drained (previous tile).
-            pr.mark(5);
-            mbar_wait_cluster(g_empty, (it & 1) ^ 1);
-            pr.mark(4);
-            tc_fence_after();
             for (int j = 0; j < p.n_chunks; ++j) {
-                gemm2(j == 0);
+                gemm2(j);
                 if (j + 2 < p.n_chunks) gemm1(j + 2);
             }
-            if (elect_one()) mma_commit_2sm_mc(g_full, PAIR);
-            __syncwarp();
         }
         pr.mark(5);
         if (lane == 0) pr.flush(p.dbg_out);
-    } else if (warp >= 4) {
+      }
+    } else {
+#if !LPD_K1_NOREG
+        reg_alloc<216>();
+#endif
         // ===================== epilogue warps =====================
         const int ew = warp - 4;
         const int quad = warp & 3;          // TMEM lane quadrant this warp may access
@@ -360,7 +455,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
         const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
         uint32_t cnt = 0, stg_k = 0;
         PhaseProbe pr((p.dbg & 16) != 0);
-        const uint32_t x_full_l = lead(x_full), g_empty_l = lead(g_empty), z_full_l = lead(z_full);
+        const uint32_t x_full_l = lead(x_full), acc_empty_l = lead(acc_empty + half), z_full_l = lead(z_full);
+        const int S = p.seg_chunks, n = p.n_chunks, SP = p.split_n;
+        float rs[128];      // fp32 round-to-nearest running sum of this thread's G row, TMEM half `half`
+        uint32_t fseg = 0;  // segments of this half read so far (acc_full parity)
+
+        // One finished segment of this warp's G half: TMEM -> registers, added into the
+        // running sums (the first segment of a tile initialises them), then released.
+        auto flush = [&](bool first) {
+            pr.mark(7);
+            mbar_wait_cluster(acc_full + half, fseg & 1);
+            pr.mark(5);
+            tc_fence_after();
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                uint32_t v[32];
+                tmem_ld_32x32b_x32(tmem_base + lane_off + TM_G + half * 128 + m * 32, v);
+                tmem_wait_ld();
+                if (first) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) rs[m * 32 + i] = __uint_as_float(v[i]);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) rs[m * 32 + i] += __uint_as_float(v[i]);
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(acc_empty_l);
+            ++fseg;
+        };
 
         // X tile of iteration itx: this thread's row of the hi (half 0) or lo (half 1)
         // plane from the TMA-staged SMEM copy (128-byte swizzled rows: 16-byte chunk c of
@@ -432,46 +556,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
         };
 
         // G accumulator of a finished tile: TMEM -> scale -> global (128 columns per warp).
-        auto drain_g = [&](int tile, uint32_t it) {
+        // G of a finished tile: last segment -> running sums -> ×col_scale -> global
+        // (128 columns per warp: two runs of 64 contiguous tile columns, half_col).
+        auto drain_g = [&](int tile, bool first) {
             const int cb = tile / p.n_row_tiles;
             const int rt = tile - cb * p.n_row_tiles;
-            pr.mark(7);
-            mbar_wait_cluster(g_full, it & 1);
-            pr.mark(5);
-            tc_fence_after();
-            if (p.dbg & 64) {  // bypass the drain: free the accumulator at once
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive_cluster(g_empty_l);
-                return;
-            }
+            flush(first);
+            if (p.dbg & 64) return;  // bypass the stores
             constexpr int SLAB = 128 / sizeof(OutT);  // columns per 128-byte staging row
-            // All 128 of this warp's accumulator columns go to registers first, so the
-            // accumulator is released to the next tile's GEMM2 after one TMEM round trip
-            // rather than after the stores.
-            uint32_t vall[4][32];
-#pragma unroll
-            for (int m = 0; m < 4; ++m) tmem_ld_32x32b_x32(tmem_base + lane_off + TM_G + half * 128 + m * 32, vall[m]);
-            tmem_wait_ld();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(g_empty_l);
 #pragma unroll
             for (int m = 0; m < 4; ++m) {
-                const int c0 = half * 128 + m * 32;
-                uint32_t (&v)[32] = vall[m];  // scaled in place (register budget)
+                const int c0 = half_col(half, m * 32, SP);
                 const int gc0 = cb * N2 + c0;
                 if (gc0 >= p.b_eff || (p.dbg & 2)) continue;
                 const float4* cs4 = reinterpret_cast<const float4*>(p.col_scale + gc0);
+                float v[32];
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
                     const float4 sc = ldg_f4_inorder(cs4 + i);
-                    v[4 * i + 0] = __float_as_uint(__uint_as_float(v[4 * i + 0]) * sc.x);
-                    v[4 * i + 1] = __float_as_uint(__uint_as_float(v[4 * i + 1]) * sc.y);
-                    v[4 * i + 2] = __float_as_uint(__uint_as_float(v[4 * i + 2]) * sc.z);
-                    v[4 * i + 3] = __float_as_uint(__uint_as_float(v[4 * i + 3]) * sc.w);
+                    v[4 * i + 0] = rs[m * 32 + 4 * i + 0] * sc.x;
+                    v[4 * i + 1] = rs[m * 32 + 4 * i + 1] * sc.y;
+                    v[4 * i + 2] = rs[m * 32 + 4 * i + 2] * sc.z;
+                    v[4 * i + 3] = rs[m * 32 + 4 * i + 3] * sc.w;
                 }
-                auto out = [&](int k) { return __uint_as_float(v[k]); };
                 // 32 rows x SLAB columns per store; 128-byte swizzled staging rows
                 // (16-byte chunk c of row r at chunk c ^ (r & 7)): conflict-free STS.
 #pragma unroll
@@ -486,12 +593,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
                     for (int c = 0; c < 8; ++c) {
                         uint32_t w[4];
                         if constexpr (sizeof(OutT) == 8) {
-                            const double d0 = out(sl * SLAB + 2 * c), d1 = out(sl * SLAB + 2 * c + 1);
+                            const double d0 = v[sl * SLAB + 2 * c], d1 = v[sl * SLAB + 2 * c + 1];
                             w[0] = __double2loint(d0); w[1] = __double2hiint(d0);
                             w[2] = __double2loint(d1); w[3] = __double2hiint(d1);
                         } else {
 #pragma unroll
-                            for (int e = 0; e < 4; ++e) w[e] = __float_as_uint(out(4 * c + e));
+                            for (int e = 0; e < 4; ++e) w[e] = __float_as_uint(v[4 * c + e]);
                         }
                         st_shared_v4(base_addr + sbuf + lane * 128 + ((c ^ (lane & 7)) << 4), w[0], w[1], w[2], w[3]);
                     }
@@ -518,7 +625,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
             const float2 ra = p.row_aux[rt * PM + r_pair];
             const uint64_t R2 = f2_pack(ra.x, ra.x), sx2 = f2_pack(ra.y, ra.y);
             const int next = tile + num_pairs;
-            for (int j = 0; j < p.n_chunks; ++j) {
+            bool first = true;  // no segment of this tile read yet
+            for (int j = 0; j < n; ++j) {
+                // the segment that ended with GEMM2(j - 2) is complete by the time
+                // GEMM1(j) (issued after it) has produced S(j)
+                if (!LPD_K1_NOSEG && j >= 2 && seg_end(half, j - 2, n, S, SP)) { flush(first); first = false; }
                 if (p.dbg & 32) {  // bypass: keep the barrier protocol, skip Z math and stores
                     const uint32_t b = cnt % NSZ, ph = (cnt / NSZ) & 1;
                     mbar_wait_cluster(s_full + b, ph);
@@ -529,9 +640,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
                     produce_z(R2, sx2);
                 }
             }
+            if (!LPD_K1_NOSEG && n >= 2 && seg_end(half, n - 2, n, S, SP)) { flush(first); first = false; }
             if (next < num_tiles) write_x(it + 1);
             pr.mark(3);
-            drain_g(tile, it);
+            drain_g(tile, first);
         }
         if (lane == 0) bulk_wait_group<0>();
         __syncwarp();

@@ -149,14 +149,13 @@ void dev_free(T*& p) {
 
 struct Slot {
     cudaStream_t stream = nullptr;
-    cudaEvent_t ev[4] = {};  // h2d start, kernels start, d2h start, d2h end
+    cudaEvent_t ev[6] = {};  // h2d start, kernels start, kernels end, d2h start, d2h end, delivered
     int64_t rows_cap = 0;    // capacity in rows (multiple of 128)
     double* x = nullptr;     // [rows_cap × d] fp64
     __half* xhi = nullptr;   // [rows_cap × 64]
     __half* xlo = nullptr;
     float2* raux = nullptr;  // [rows_cap]
     void* g = nullptr;       // [rows_cap × g_ld] fp32 G of the host-call path (device)
-    float* h = nullptr;      // [rows_cap × g_ld] pinned host staging of g
     int64_t g_cols = 0;      // b_eff of the current layout
     int64_t g_elems = 0;     // capacity of g / h in elements
     int64_t g_ld = 0;        // their row pitch (elements; multiple of 4: 16-byte rows)
@@ -202,6 +201,13 @@ struct DeviceState {
     double* colmax = nullptr;
     CUtensorMap tm_lmhi, tm_lmlo, tm_lthi, tm_ltlo;
     Slot slot[2];
+    // G delivery ring (host-row calls): small pinned fp32 buffers the D2H copies land
+    // in, each widened into the caller's fp64 G right after it lands (still in the
+    // CPU's last-level cache), on their own stream
+    cudaStream_t dstream = nullptr;
+    std::vector<float*> dring;
+    std::vector<cudaEvent_t> dring_ev;
+    size_t dring_bytes = 0;
     cudaEvent_t kev[2] = {};
     float last_kernel_ms = 0.f;
     // ring of (start, stop) event pairs around every timed factor-kernel launch,
@@ -224,8 +230,6 @@ struct DeviceState {
     }
     void free_slot(Slot& s) {
         dev_free(s.x); dev_free(s.xhi); dev_free(s.xlo); dev_free(s.raux); dev_free(s.g);
-        if (s.h) cudaFreeHost(s.h);
-        s.h = nullptr;
         dev_free(s.indptr); dev_free(s.indices); dev_free(s.values);
         s.rows_cap = 0; s.g_cols = 0; s.g_elems = 0; s.nnz_cap = 0;
     }
@@ -247,8 +251,6 @@ void ensure_slot(DeviceState& ds, Slot& s, int64_t rows, bool need_g, int64_t nn
     if (rows_pad > s.rows_cap || (need_g && std::max(rows_pad, s.rows_cap) * g_ld > s.g_elems) ||
         s.kd != ds.kd || s.d_cap < ds.d) {
         dev_free(s.x); dev_free(s.xhi); dev_free(s.xlo); dev_free(s.raux); dev_free(s.g);
-        if (s.h) cudaFreeHost(s.h);
-        s.h = nullptr;
         const int64_t cap = std::max(rows_pad, s.rows_cap);
         dev_alloc(&s.x, static_cast<size_t>(cap * std::max<int64_t>(ds.d, 1)));
         dev_alloc(&s.xhi, static_cast<size_t>(cap * ds.kd));
@@ -258,9 +260,6 @@ void ensure_slot(DeviceState& ds, Slot& s, int64_t rows, bool need_g, int64_t nn
         dev_alloc(&s.raux, static_cast<size_t>(cap));
         if (need_g) {
             dev_alloc(reinterpret_cast<float**>(&s.g), static_cast<size_t>(cap * g_ld));
-            CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&s.h),
-                                   sizeof(float) * static_cast<size_t>(cap * g_ld),
-                                   cudaHostAllocPortable));
             s.g_elems = cap * g_ld;
         } else {
             s.g_elems = 0;
@@ -448,6 +447,18 @@ void build_basis_host_L(DeviceState& ds, const double* lm_dev, int64_t B, int64_
     dev_free(L_dev);
 }
 
+// K chunks (of 64) per fp32 accumulator segment: each segment's tensor-core sum
+// (round-toward-zero accumulation) is added into a round-to-nearest running sum, so
+// the accumulation bias is bounded by one segment. LPD_SEG_CHUNKS
+// overrides (accuracy studies).
+int seg_chunks() {
+    static const int v = [] {
+        const char* e = std::getenv("LPD_SEG_CHUNKS");
+        return e ? std::max(1, std::atoi(e)) : 4;
+    }();
+    return v;
+}
+
 // Large-d factor (d >= 64) for m prepped rows in slot s: per row panel, the Z GEMM
 // (MODE_Z, exp epilogue, fp16 hi/lo planes in a device scratch) and the projection
 // GEMM (MODE_G). The scratch holds at most ~2 GB of Z planes.
@@ -474,6 +485,7 @@ void launch_factor_panels(DeviceState& ds, Slot& s, int64_t m, void* g_dev, int6
         const char* e = std::getenv("LPD_PANEL_GROUP");
         return e ? std::max(1, std::atoi(e)) : 8;
     }();
+    const int seg = seg_chunks();
     const CUtensorMap tm_zhi = make_plane_map(ds.z_hi, panel, ds.B_pad, lpd::kp::BM, 64);
     const CUtensorMap tm_zlo = make_plane_map(ds.z_lo, panel, ds.B_pad, lpd::kp::BM, 64);
     for (int64_t r0 = 0; r0 < m; r0 += panel) {
@@ -492,6 +504,7 @@ void launch_factor_panels(DeviceState& ds, Slot& s, int64_t m, void* g_dev, int6
         pz.z_lo = ds.z_lo;
         pz.ldz = ds.B_pad;
         pz.group_r = group_r;
+        pz.seg_chunks = seg;
         const int64_t tz = static_cast<int64_t>(pz.n_row_pairs) * pz.n_col_blocks;
         const int gz = 2 * static_cast<int>(std::min<int64_t>(tz, ds.num_sms / 2));
         lpd::panel_gemm_kernel<lpd::PANEL_Z, float><<<gz, lpd::kp::THREADS, lpd::kp::SMEM_BYTES, st>>>(
@@ -507,6 +520,7 @@ void launch_factor_panels(DeviceState& ds, Slot& s, int64_t m, void* g_dev, int6
         pg.G = static_cast<char*>(g_dev) + static_cast<size_t>(r0) * ldg * es;
         pg.ldg = ldg;
         pg.group_r = group_r;
+        pg.seg_chunks = seg;
         const int64_t tg = static_cast<int64_t>(pg.n_row_pairs) * pg.n_col_blocks;
         const int gg = 2 * static_cast<int>(std::min<int64_t>(tg, ds.num_sms / 2));
         if (out_dtype == LPD_OUT_F64)
@@ -574,6 +588,12 @@ void launch_factor(DeviceState& ds, Slot& s, const double* x_dev, int64_t m, int
     p.ksteps1 = static_cast<int>((ds.d + 1 + 15) / 16);
     p.row_aux = s.raux;
     p.col_scale = ds.col_scale;
+    p.seg_chunks = seg_chunks();
+    static const int split_n = [] {
+        const char* e = std::getenv("LPD_K1_SPLIT");
+        return e ? (std::atoi(e) != 0) : 0;
+    }();
+    p.split_n = split_n;
     static const int dbg = [] {
         const char* e = std::getenv("LPD_K1_DEBUG");
         return e ? std::atoi(e) : 0;
@@ -637,70 +657,95 @@ void check_range_flag(DeviceState& ds) {
     }
 }
 
-// Persistent host workers for the fp32 -> fp64 widening of G chunks into the
-// caller's buffer (the reference's Matrix is plain pageable memory: widening from a
-// pinned fp32 staging buffer halves PCIe bytes and beats a pageable fp64 DMA 3x).
-class HostPool {
+// Host workers for the fp32 -> fp64 widening of delivered G rows into the caller's
+// buffer (the reference's Matrix is plain pageable memory: widening from pinned fp32
+// buffers halves PCIe bytes and beats a pageable fp64 DMA 3x). The team spins
+// between work items: a delivery hands it one small buffer every ~0.1 ms, so a
+// condition-variable wake-up per item would cost more than the copy.
+class SpinTeam {
 public:
-    explicit HostPool(int n) {
-        for (int i = 0; i < n; ++i) th_.emplace_back([this, i] { loop(i); });
+    explicit SpinTeam(int n) : n_(std::max(1, n)) {
+        for (int i = 1; i < n_; ++i) th_.emplace_back([this, i] { loop(i); });
     }
-    ~HostPool() {
-        {
-            std::lock_guard<std::mutex> l(mu_);
-            stop_ = true;
-        }
-        cv_.notify_all();
+    ~SpinTeam() {
+        stop_.store(true, std::memory_order_relaxed);
         for (auto& t : th_) t.join();
     }
-    int size() const { return static_cast<int>(th_.size()); }
-    // Runs fn(worker) on every worker and waits.
+    int size() const { return n_; }
+    // Runs fn(worker) on every worker (the caller is worker 0) and waits.
     void run(const std::function<void(int)>& fn) {
-        std::unique_lock<std::mutex> l(mu_);
         fn_ = &fn;
-        pending_ = static_cast<int>(th_.size());
-        ++gen_;
-        cv_.notify_all();
-        done_cv_.wait(l, [this] { return pending_ == 0; });
-        fn_ = nullptr;
+        done_.store(0, std::memory_order_relaxed);
+        gen_.fetch_add(1, std::memory_order_release);
+        fn(0);
+        while (done_.load(std::memory_order_acquire) != n_ - 1) cpu_relax();
     }
 
 private:
+    static void cpu_relax() {
+#if defined(__x86_64__)
+        __builtin_ia32_pause();
+#endif
+    }
     void loop(int i) {
         uint64_t seen = 0;
         for (;;) {
-            const std::function<void(int)>* fn;
-            {
-                std::unique_lock<std::mutex> l(mu_);
-                cv_.wait(l, [&] { return stop_ || gen_ != seen; });
-                if (stop_) return;
-                seen = gen_;
-                fn = fn_;
+            uint64_t g;
+            while ((g = gen_.load(std::memory_order_acquire)) == seen) {
+                if (stop_.load(std::memory_order_relaxed)) return;
+                cpu_relax();
             }
-            (*fn)(i);
-            {
-                std::lock_guard<std::mutex> l(mu_);
-                if (--pending_ == 0) done_cv_.notify_all();
-            }
+            seen = g;
+            (*fn_)(i);
+            done_.fetch_add(1, std::memory_order_acq_rel);
         }
     }
+    int n_;
     std::vector<std::thread> th_;
-    std::mutex mu_;
-    std::condition_variable cv_, done_cv_;
     const std::function<void(int)>* fn_ = nullptr;
-    int pending_ = 0;
-    uint64_t gen_ = 0;
-    bool stop_ = false;
+    std::atomic<uint64_t> gen_{0};
+    std::atomic<int> done_{0};
+    std::atomic<bool> stop_{false};
 };
 
-// dst[r][c] = src[r][c] (fp32 -> fp64) for rows [0, rows), split over the pool
+// dst[r][c] = src[r][c] (fp32 -> fp64) for rows [0, rows), split over the team
 // (host_widen.cpp: AVX-512 streaming stores).
-void widen_rows(HostPool& pool, const float* src, int64_t lds, double* dst, int64_t ldd,
+void widen_rows(SpinTeam& team, const float* src, int64_t lds, double* dst, int64_t ldd,
                 int64_t rows, int64_t cols) {
-    const int T = pool.size();
-    pool.run([&](int w) {
+    const int T = team.size();
+    team.run([&](int w) {
         lpd_host_widen_rows(src, lds, dst, ldd, rows * w / T, rows * (w + 1) / T, cols);
     });
+}
+
+// Delivery ring geometry: LPD_RING_MB (default 8) per buffer, LPD_RING_SLOTS (6).
+// Measured on the B200 box (scripts/host_pipe_probe.cu): 8 MB x 6 reaches the PCIe
+// D2H rate (~110 GB/s of fp64 output) where 128 MB chunks reach ~75 GB/s, because
+// each buffer is widened while it is still in the CPU's last-level cache.
+void ensure_delivery_ring(DeviceState& ds) {
+    static const size_t mb = [] {
+        const char* e = std::getenv("LPD_RING_MB");
+        return static_cast<size_t>(e ? std::max(1, std::atoi(e)) : 8);
+    }();
+    static const int slots = [] {
+        const char* e = std::getenv("LPD_RING_SLOTS");
+        return e ? std::max(2, std::atoi(e)) : 6;
+    }();
+    if (!ds.dstream) CUDA_TRY(cudaStreamCreateWithFlags(&ds.dstream, cudaStreamNonBlocking));
+    if (ds.dring_bytes == (mb << 20) && static_cast<int>(ds.dring.size()) == slots) return;
+    for (float* b : ds.dring) cudaFreeHost(b);
+    ds.dring.clear();
+    ds.dring_bytes = mb << 20;
+    for (int i = 0; i < slots; ++i) {
+        float* b = nullptr;
+        CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&b), ds.dring_bytes, cudaHostAllocPortable));
+        ds.dring.push_back(b);
+    }
+    while (static_cast<int>(ds.dring_ev.size()) < slots) {
+        cudaEvent_t e;
+        CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ds.dring_ev.push_back(e);
+    }
 }
 
 lpd_context* check_ctx(lpd_context* ctx, bool need_basis) {
@@ -739,14 +784,16 @@ void run_parallel(lpd_context* ctx, const std::function<void(DeviceState&, int)>
 
 // Host-row pipeline shared by the dense and CSR entry points. Each device owns a
 // contiguous row shard (reference compute_G chunks rows, factor.cpp:97-108; rows
-// are independent, so no collective) and runs, per row chunk on alternating slots:
-//   stage_x (H2D of X rows) -> prep -> fused factor kernel (fp32 G) -> D2H into a
-//   pinned fp32 staging buffer
-// while its host workers widen the previous chunk to fp64 straight into the
-// caller's G rows (measured on the B200 box: 0.37 s for C2's 19 GB fp64 G, vs 0.46 s
-// for an fp64 DMA straight into a pinned G and ~1.1 s into a pageable one). `stage_x`
-// fills slot.x (dense fp64 [rows × d]) on the slot's
-// stream for global rows [r0, r0 + rows) and records ev[0].
+// are independent, so no collective). Per row chunk (~128 MB of fp32 G), on
+// alternating slots/streams: stage_x (H2D of X rows) -> prep -> fused factor kernel
+// (fp32 G into the slot's device buffer, or the resident G). Delivery runs on its own
+// stream over the whole shard as a sequence of small sub-chunks: D2H into a ring of
+// pinned buffers (ensure_delivery_ring), each widened to fp64 straight into the
+// caller's G rows by the spinning host team as soon as it lands, while later
+// sub-chunks are in flight and the next row chunk computes. A slot's device G buffer
+// is rewritten (chunk k + 2) only after its D2H of chunk k has drained (event).
+// `stage_x` fills slot.x (dense fp64 [rows × d]) on the slot's stream for global
+// rows [r0, r0 + rows) and records ev[0].
 template <typename StageX>
 void compute_rows_host(lpd_context* ctx, int64_t n, double* G, int64_t ldg, lpd_timings* tm,
                        StageX&& stage_x) {
@@ -755,7 +802,7 @@ void compute_rows_host(lpd_context* ctx, int64_t n, double* G, int64_t ldg, lpd_
     std::vector<double> h2d(nd, 0.0), ker(nd, 0.0), d2h(nd, 0.0), host(nd, 0.0);
     std::vector<int64_t> launches(nd, 0);
     const int64_t b_eff = ctx->dev[0].b_eff;
-    // Rows per pipeline chunk: ~128 MB of fp32 G, multiple of the 256-row pair tile.
+    // Rows per compute chunk: ~128 MB of fp32 G, multiple of the 256-row pair tile.
     const int64_t chunk = std::max<int64_t>(
         256, std::min<int64_t>(round_up(n, 256), (128ll << 20) / (4 * b_eff) / 256 * 256));
     const int hw = std::max(1u, std::thread::hardware_concurrency());
@@ -764,7 +811,6 @@ void compute_rows_host(lpd_context* ctx, int64_t n, double* G, int64_t ldg, lpd_
     std::vector<int> resident_ok(nd, 0);
     run_parallel(ctx, [&](DeviceState& ds, int di) {
         CUDA_TRY(cudaSetDevice(ds.device));
-        HostPool pool(workers);
         const int64_t per = round_up((n + nd - 1) / nd, 256);
         const int64_t r_begin = std::min<int64_t>(n, per * di);
         const int64_t r_end = std::min<int64_t>(n, per * (di + 1));
@@ -792,44 +838,88 @@ void compute_rows_host(lpd_context* ctx, int64_t n, double* G, int64_t ldg, lpd_
             }
         }
         if (!resident) ds.res_rows = 0;
-        int64_t pend_r0[2] = {-1, -1}, pend_rows[2] = {0, 0};
-        auto finish = [&](int k) {  // wait for slot k's chunk and widen it into G
-            Slot& s = ds.slot[k];
-            if (pend_r0[k] < 0) return;
-            CUDA_TRY(cudaStreamSynchronize(s.stream));
-            float a = 0, b = 0, c = 0;
-            cudaEventElapsedTime(&a, s.ev[0], s.ev[1]);
-            cudaEventElapsedTime(&b, s.ev[1], s.ev[2]);
-            cudaEventElapsedTime(&c, s.ev[2], s.ev[3]);
-            h2d[di] += a * 1e-3; ker[di] += b * 1e-3; d2h[di] += c * 1e-3;
-            const auto w0 = std::chrono::steady_clock::now();
-            widen_rows(pool, s.h, s.g_ld, G + pend_r0[k] * ldg, ldg, pend_rows[k], b_eff);
-            host[di] += std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
-            pend_r0[k] = -1;
+        resident_ok[di] = resident || r_end <= r_begin;
+        if (r_end <= r_begin) return;
+
+        ensure_delivery_ring(ds);
+        SpinTeam team(workers);
+        const int R = static_cast<int>(ds.dring.size());
+        const int64_t g_ld = round_up(b_eff, 4);
+        const int64_t sub_rows = std::max<int64_t>(1, static_cast<int64_t>(ds.dring_bytes / (4 * g_ld)));
+        const int64_t nchunks = (r_end - r_begin + chunk - 1) / chunk;
+        struct Sub { int64_t k, r0, rows; bool first, last; };  // r0: global row
+        std::vector<Sub> subs;
+        for (int64_t k = 0; k < nchunks; ++k) {
+            const int64_t c0 = r_begin + k * chunk, c1 = std::min(r_end, c0 + chunk);
+            for (int64_t r = c0; r < c1; r += sub_rows)
+                subs.push_back({k, r, std::min(sub_rows, c1 - r), r == c0, r + sub_rows >= c1});
+        }
+        auto gdst = [&](int64_t k) -> float* {
+            const int64_t c0 = r_begin + k * chunk;
+            return resident ? ds.res_g + (c0 - r_begin) * ds.res_ld : static_cast<float*>(ds.slot[k & 1].g);
         };
-        int64_t k = 0;
-        for (int64_t r0 = r_begin; r0 < r_end; r0 += chunk, ++k) {
-            const int64_t rows = std::min(chunk, r_end - r0);
-            const int sl = static_cast<int>(k & 1);
-            Slot& s = ds.slot[sl];
-            finish(sl);                // slot reuse: its chunk (k - 2) is widened by now
-            stage_x(ds, s, r0, rows);  // records ev[0] and fills s.x
+        auto elapsed = [](cudaEvent_t a, cudaEvent_t b) {
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) {
+                cudaGetLastError();  // not complete / not recorded: timing only
+                return 0.0;
+            }
+            return ms * 1e-3;
+        };
+        int64_t computed = 0;  // chunks enqueued for compute
+        auto compute = [&](int64_t k) {
+            Slot& s = ds.slot[k & 1];
+            const int64_t c0 = r_begin + k * chunk, rows = std::min(chunk, r_end - c0);
+            if (k >= 2) {  // fold in chunk k-2's times before its events are re-recorded
+                h2d[di] += elapsed(s.ev[0], s.ev[1]);
+                ker[di] += elapsed(s.ev[1], s.ev[2]);
+            }
+            stage_x(ds, s, c0, rows);  // records ev[0] and fills s.x
             CUDA_TRY(cudaEventRecord(s.ev[1], s.stream));
-            float* gdst = resident ? ds.res_g + (r0 - r_begin) * ds.res_ld : static_cast<float*>(s.g);
-            launch_factor(ds, s, s.x, rows, ds.d, gdst, s.g_ld, LPD_OUT_F32, s.stream, false);
+            // the slot's device G buffer: chunk k-2's D2H must have drained
+            if (k >= 2 && !resident) CUDA_TRY(cudaStreamWaitEvent(s.stream, s.ev[5], 0));
+            launch_factor(ds, s, s.x, rows, ds.d, gdst(k), g_ld, LPD_OUT_F32, s.stream, false);
             launches[di] += 2;
             CUDA_TRY(cudaEventRecord(s.ev[2], s.stream));
-            CUDA_TRY(cudaMemcpyAsync(s.h, gdst, sizeof(float) * static_cast<size_t>(rows * s.g_ld),
-                                     cudaMemcpyDeviceToHost, s.stream));
-            CUDA_TRY(cudaEventRecord(s.ev[3], s.stream));
-            pend_r0[sl] = r0;
-            pend_rows[sl] = rows;
-            if (k >= 1) finish(static_cast<int>((k - 1) & 1));  // overlaps chunk k on the GPU
+        };
+        auto enqueue = [&](size_t g) {
+            const Sub& u = subs[g];
+            Slot& s = ds.slot[u.k & 1];
+            if (u.first) {
+                // compute one chunk ahead of the delivery
+                while (computed <= u.k + 1 && computed < nchunks) compute(computed++);
+                CUDA_TRY(cudaStreamWaitEvent(ds.dstream, s.ev[2], 0));
+                CUDA_TRY(cudaEventRecord(s.ev[3], ds.dstream));
+            }
+            const float* src = gdst(u.k) + (u.r0 - (r_begin + u.k * chunk)) * g_ld;
+            CUDA_TRY(cudaMemcpyAsync(ds.dring[g % R], src, sizeof(float) * static_cast<size_t>(u.rows * g_ld),
+                                     cudaMemcpyDeviceToHost, ds.dstream));
+            CUDA_TRY(cudaEventRecord(ds.dring_ev[g % R], ds.dstream));
+            if (u.last) {
+                CUDA_TRY(cudaEventRecord(s.ev[4], ds.dstream));
+                CUDA_TRY(cudaEventRecord(s.ev[5], ds.dstream));
+            }
+        };
+        for (size_t g = 0; g < subs.size() && g < static_cast<size_t>(R); ++g) enqueue(g);
+        double widen_s = 0.0;
+        for (size_t g = 0; g < subs.size(); ++g) {
+            const Sub& u = subs[g];
+            cudaError_t q;
+            while ((q = cudaEventQuery(ds.dring_ev[g % R])) == cudaErrorNotReady) std::this_thread::yield();
+            if (q != cudaSuccess) CUDA_TRY(q);
+            const auto w0 = std::chrono::steady_clock::now();
+            widen_rows(team, ds.dring[g % R], g_ld, G + u.r0 * ldg, ldg, u.rows, b_eff);
+            widen_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
+            if (u.last) d2h[di] += elapsed(ds.slot[u.k & 1].ev[3], ds.slot[u.k & 1].ev[4]);
+            if (g + R < subs.size()) enqueue(g + R);
         }
-        finish(0);
-        finish(1);
+        CUDA_TRY(cudaStreamSynchronize(ds.dstream));
+        for (int64_t k = std::max<int64_t>(0, nchunks - 2); k < nchunks; ++k) {
+            h2d[di] += elapsed(ds.slot[k & 1].ev[0], ds.slot[k & 1].ev[1]);
+            ker[di] += elapsed(ds.slot[k & 1].ev[1], ds.slot[k & 1].ev[2]);
+        }
+        host[di] += widen_s;
         check_range_flag(ds);
-        resident_ok[di] = resident || r_end <= r_begin;
     });
     if (ctx->keep_resident && std::all_of(resident_ok.begin(), resident_ok.end(), [](int v) { return v; })) {
         ctx->res_n = n;
@@ -1063,6 +1153,9 @@ int lpd_context_destroy(lpd_context* ctx) {
         }
         for (auto& e : ds.kev)
             if (e) cudaEventDestroy(e);
+        for (float* b : ds.dring) cudaFreeHost(b);
+        for (auto& e : ds.dring_ev) cudaEventDestroy(e);
+        if (ds.dstream) cudaStreamDestroy(ds.dstream);
         for (auto& pr : ds.ring)
             for (auto& e : pr)
                 if (e) cudaEventDestroy(e);

@@ -21,9 +21,17 @@
 // TMA ring (each CTA loads its 128 rows of A and its 128 rows of B, hi and lo
 // planes, with cta_group::2 loads counted on the leader's barrier); the leader issues
 // three split products per chunk (A_hi·B_hi + A_lo·B_hi + A_hi·B_lo) as M=256, N=256
-// tcgen05 SS MMAs into one of TWO TMEM accumulators, so the epilogue of tile t
-// overlaps the main loop of tile t+1. Tiles are rastered in groups of row pairs so
-// the pairs in flight share A rows and B rows in L2.
+// tcgen05 SS MMAs. Tiles are rastered in groups of row pairs so the pairs in flight
+// share A rows and B rows in L2.
+//
+// Accumulation in segments: the tensor core adds each MMA's products into the fp32
+// TMEM accumulator with round-toward-zero, a bias that grows with the number of
+// K-steps (C4's projection has 3 x 1024 of them per tile; ~1e-3 relative error at
+// 8192 landmarks). So K is cut into segments of `seg_chunks` chunks;
+// the MMA alternates between TWO TMEM accumulators per segment, and the epilogue
+// adds each finished segment into an fp32 round-to-nearest running sum held in
+// registers (warpgroup register reallocation gives the epilogue warps 208 each)
+// while the MMA fills the other accumulator — no tensor-pipe stall.
 #pragma once
 
 #include "ptx.cuh"
@@ -46,6 +54,7 @@ struct PanelParams {
     void* G;                  // MODE_G output, row-major, leading dimension ldg
     long long ldg;
     int group_r;              // row pairs per raster group (L2 reuse of A and B rows)
+    int seg_chunks;           // K chunks per accumulator segment (>= 1)
 };
 
 namespace kp {
@@ -119,8 +128,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kp::THREADS, 1)
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // epilogue warpgroups hold 128 running-sum registers per thread
 
-    if (warp == 0) {
+    if (warp < 4) {
+      reg_dealloc<56>();
+      if (warp == 0) {
         // ============ TMA producer (both CTAs): this CTA's rows of A and B per K chunk ============
         if (lane == 0) {
             const uint64_t pol = policy_evict_normal();
@@ -143,71 +155,88 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kp::THREADS, 1)
                 }
             }
         }
-    } else if (warp == 1 && leader) {
+      } else if (warp == 1 && leader) {
         // ============ MMA issuer (pair leader) ============
         const uint64_t dbase = sdesc_kmajor_sw128(0);
         auto desc = [&](uint32_t addr) -> uint64_t { return dbase | static_cast<uint64_t>((addr >> 4) & 0x3FFF); };
-        uint32_t s = 0, ph = 0, it = 0;
-        for (int tile = pair; tile < num_tiles; tile += num_pairs, ++it) {
-            const uint32_t a = it & 1, aph = (it >> 1) & 1;
-            mbar_wait_cluster(acc_empty + a, aph ^ 1);
-            tc_fence_after();
-            const uint32_t d = tmem_base + a * BN;
-            for (int kc = 0; kc < p.n_kchunks; ++kc) {
-                mbar_wait_cluster(full + s, ph);
+        uint32_t s = 0, ph = 0, sc = 0;  // sc: segment sequence number (accumulator ping-pong)
+        for (int tile = pair; tile < num_tiles; tile += num_pairs) {
+            for (int kc0 = 0; kc0 < p.n_kchunks; kc0 += p.seg_chunks, ++sc) {
+                const uint32_t a = sc & 1, aph = (sc >> 1) & 1;
+                const int kc1 = min(p.n_kchunks, kc0 + p.seg_chunks);
+                mbar_wait_cluster(acc_empty + a, aph ^ 1);
                 tc_fence_after();
-                if (elect_one()) {
-                    const uint32_t st = base_addr + s * STAGE;
-                    const uint64_t ahi = desc(st), alo = desc(st + A_BYTES);
-                    const uint64_t bhi = desc(st + 2 * A_BYTES), blo = desc(st + 2 * A_BYTES + B_BYTES);
+                const uint32_t d = tmem_base + a * BN;
+                for (int kc = kc0; kc < kc1; ++kc) {
+                    mbar_wait_cluster(full + s, ph);
+                    tc_fence_after();
+                    if (elect_one()) {
+                        const uint32_t st = base_addr + s * STAGE;
+                        const uint64_t ahi = desc(st), alo = desc(st + A_BYTES);
+                        const uint64_t bhi = desc(st + 2 * A_BYTES), blo = desc(st + 2 * A_BYTES + B_BYTES);
 #pragma unroll
-                    for (int pass = 0; pass < 3; ++pass) {
-                        const uint64_t ad = (pass == 1) ? alo : ahi;
-                        const uint64_t bd = (pass == 2) ? blo : bhi;
+                        for (int pass = 0; pass < 3; ++pass) {
+                            const uint64_t ad = (pass == 1) ? alo : ahi;
+                            const uint64_t bd = (pass == 2) ? blo : bhi;
 #pragma unroll
-                        for (int k = 0; k < BK / 16; ++k)
-                            mma_f16_ss_2sm(d, ad + 2 * k, bd + 2 * k, IDESC, (kc | pass | k) != 0);
+                            for (int k = 0; k < BK / 16; ++k)
+                                mma_f16_ss_2sm(d, ad + 2 * k, bd + 2 * k, IDESC, kc != kc0 || pass != 0 || k != 0);
+                        }
+                        mma_commit_2sm_mc(empty + s, PAIR);
                     }
-                    mma_commit_2sm_mc(empty + s, PAIR);
+                    __syncwarp();
+                    if (++s == NS) { s = 0; ph ^= 1; }
                 }
+                if (elect_one()) mma_commit_2sm_mc(acc_full + a, PAIR);
                 __syncwarp();
-                if (++s == NS) { s = 0; ph ^= 1; }
             }
-            if (elect_one()) mma_commit_2sm_mc(acc_full + a, PAIR);
-            __syncwarp();
         }
-    } else if (warp >= 4) {
+      }
+    } else {
+        reg_alloc<208>();
         // ============ epilogue (both CTAs): 32 rows × 128 columns per warp ============
         const int ew = warp - 4;
         const int quad = warp & 3;
         const int half = ew >> 2;
         const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
         const uint32_t acc_empty_l = lead(acc_empty);
-        uint32_t it = 0;
-        for (int tile = pair; tile < num_tiles; tile += num_pairs, ++it) {
-            const uint32_t a = it & 1, aph = (it >> 1) & 1;
+        uint32_t sc = 0;
+        for (int tile = pair; tile < num_tiles; tile += num_pairs) {
             int rp, cb;
             tile_coords(tile, p.n_row_pairs, p.n_col_blocks, p.group_r, rp, cb);
             const long long row = static_cast<long long>(rp) * PM + rank * BM + quad * 32 + lane;
+            // running sum of this thread's row, columns [half·128, half·128 + 128) of the tile
+            float rs[128];
+            for (int kc0 = 0; kc0 < p.n_kchunks; kc0 += p.seg_chunks, ++sc) {
+                const uint32_t a = sc & 1, aph = (sc >> 1) & 1;
+                mbar_wait_cluster(acc_full + a, aph);
+                tc_fence_after();
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    uint32_t v[32];
+                    tmem_ld_32x32b_x32(tmem_base + lane_off + a * BN + half * 128 + m * 32, v);
+                    tmem_wait_ld();
+                    if (kc0 == 0) {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) rs[m * 32 + i] = __uint_as_float(v[i]);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) rs[m * 32 + i] += __uint_as_float(v[i]);
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(acc_empty_l + 8 * a);
+            }
             float R = 0.f, sx = 0.f;
             if constexpr (MODE == PANEL_Z) {
                 const float2 ra = p.row_aux[row];
                 R = ra.x;
                 sx = ra.y;
             }
-            mbar_wait_cluster(acc_full + a, aph);
-            tc_fence_after();
-#pragma unroll 1
+#pragma unroll
             for (int m = 0; m < 4; ++m) {
                 const int c0 = half * 128 + m * 32;
-                uint32_t v[32];
-                tmem_ld_32x32b_x32(tmem_base + lane_off + a * BN + c0, v);
-                tmem_wait_ld();
-                if (m == 3) {
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive_cluster(acc_empty_l + 8 * a);
-                }
                 const int gc0 = cb * BN + c0;
                 if constexpr (MODE == PANEL_Z) {
                     const uint64_t R2 = f2_pack(R, R), sx2 = f2_pack(sx, sx);
@@ -215,8 +244,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kp::THREADS, 1)
 #pragma unroll
                     for (int i = 0; i < 16; ++i) {
                         float t0, t1;
-                        f2_unpack(ffma2(f2_pack(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1])), sx2, R2),
-                                  t0, t1);
+                        f2_unpack(ffma2(f2_pack(rs[m * 32 + 2 * i], rs[m * 32 + 2 * i + 1]), sx2, R2), t0, t1);
                         const float z0 = ex2_approx(fminf(t0, 13.0f));
                         const float z1 = ex2_approx(fminf(t1, 13.0f));
                         const float h0 = __uint_as_float(__float_as_uint(z0) & 0xFFFFE000u);
@@ -239,11 +267,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kp::THREADS, 1)
                     float out[32];
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
-                        const float4 sc = __ldg(cs4 + i);
-                        out[4 * i + 0] = __uint_as_float(v[4 * i + 0]) * sc.x;
-                        out[4 * i + 1] = __uint_as_float(v[4 * i + 1]) * sc.y;
-                        out[4 * i + 2] = __uint_as_float(v[4 * i + 2]) * sc.z;
-                        out[4 * i + 3] = __uint_as_float(v[4 * i + 3]) * sc.w;
+                        const float4 sc4 = __ldg(cs4 + i);
+                        out[4 * i + 0] = rs[m * 32 + 4 * i + 0] * sc4.x;
+                        out[4 * i + 1] = rs[m * 32 + 4 * i + 1] * sc4.y;
+                        out[4 * i + 2] = rs[m * 32 + 4 * i + 2] * sc4.z;
+                        out[4 * i + 3] = rs[m * 32 + 4 * i + 3] * sc4.w;
                     }
                     OutT* dst = static_cast<OutT*>(p.G) + row * p.ldg + gc0;
                     const int ncols = min(32, p.n_cols - gc0);
