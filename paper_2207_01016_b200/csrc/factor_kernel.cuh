@@ -158,8 +158,10 @@ __device__ __forceinline__ uint32_t z_hi_col(uint32_t k) { return (k >> 1) * 32 
 __device__ __forceinline__ uint32_t z_lo_col(uint32_t k) { return z_hi_col(k) + 16; }
 
 // Segment boundaries of G half h (with split halves, staggered by half a segment).
+// S is a power of two (the host rounds it), so this is a mask, not a division: the
+// MMA warp evaluates it for every chunk and its issue slots are on the critical path.
 __device__ __forceinline__ bool seg_end(int h, int j, int n, int S, int split) {
-    return j == n - 1 || ((j + 1 + h * split * (S >> 1)) % S) == 0;
+    return j == n - 1 || ((j + 1 + h * split * (S >> 1)) & (S - 1)) == 0;
 }
 __device__ __forceinline__ bool seg_start(int h, int j, int n, int S, int split) {
     return j == 0 || seg_end(h, j - 1, n, S, split);
@@ -467,17 +469,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
             mbar_wait_cluster(acc_full + half, fseg & 1);
             pr.mark(5);
             tc_fence_after();
+            // two TMEM round trips of 64 columns (register budget: 128 sums + 64 loaded)
 #pragma unroll
-            for (int m = 0; m < 4; ++m) {
-                uint32_t v[32];
-                tmem_ld_32x32b_x32(tmem_base + lane_off + TM_G + half * 128 + m * 32, v);
+            for (int m = 0; m < 4; m += 2) {
+                uint32_t v[2][32];
+                tmem_ld_32x32b_x32(tmem_base + lane_off + TM_G + half * 128 + m * 32, v[0]);
+                tmem_ld_32x32b_x32(tmem_base + lane_off + TM_G + half * 128 + (m + 1) * 32, v[1]);
                 tmem_wait_ld();
-                if (first) {
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) rs[m * 32 + i] = __uint_as_float(v[i]);
-                } else {
+                for (int q = 0; q < 2; ++q) {
+                    if (first) {
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) rs[m * 32 + i] += __uint_as_float(v[i]);
+                        for (int i = 0; i < 32; ++i) rs[(m + q) * 32 + i] = __uint_as_float(v[q][i]);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) rs[(m + q) * 32 + i] += __uint_as_float(v[q][i]);
+                    }
                 }
             }
             tc_fence_before();

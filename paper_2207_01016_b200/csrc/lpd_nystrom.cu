@@ -431,20 +431,45 @@ void build_basis(DeviceState& ds, const double* lm_dev, int64_t B, int64_t d, in
 }
 
 // Host-L variant: stages L to the device, builds, frees the staging buffer.
+// LPD_TRACE=1: phase times of the host-call entry points on stderr (diagnostics).
+bool trace_on() {
+    static const bool on = [] {
+        const char* e = std::getenv("LPD_TRACE");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+struct PhaseTrace {
+    const char* what;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void lap(const char* phase) {
+        if (!trace_on()) return;
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[lpd] %s %s %.3f ms\n", what, phase,
+                     std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
+
 void build_basis_host_L(DeviceState& ds, const double* lm_dev, int64_t B, int64_t d,
                         const double* L_host, int64_t b_eff, double gamma) {
     CUDA_TRY(cudaSetDevice(ds.device));
     cudaStream_t st = ds.slot[0].stream;
+    PhaseTrace tr{"set_basis"};
     double* L_dev = nullptr;
     dev_alloc(&L_dev, static_cast<size_t>(B * b_eff));
+    tr.lap("alloc L");
     try {
         CUDA_TRY(cudaMemcpyAsync(L_dev, L_host, sizeof(double) * B * b_eff, cudaMemcpyHostToDevice, st));
+        tr.lap("H2D L (enqueue)");
         build_basis(ds, lm_dev, B, d, std::max<int64_t>(d, 1), L_dev, b_eff, gamma, st, true);
+        tr.lap("prep + sync");
     } catch (...) {
         dev_free(L_dev);
         throw;
     }
     dev_free(L_dev);
+    tr.lap("free L");
 }
 
 // K chunks (of 64) per fp32 accumulator segment: each segment's tensor-core sum
@@ -454,7 +479,10 @@ void build_basis_host_L(DeviceState& ds, const double* lm_dev, int64_t B, int64_
 int seg_chunks() {
     static const int v = [] {
         const char* e = std::getenv("LPD_SEG_CHUNKS");
-        return e ? std::max(1, std::atoi(e)) : 4;
+        int s = e ? std::max(1, std::atoi(e)) : 4;
+        int p2 = 1;
+        while (p2 * 2 <= s && p2 < (1 << 20)) p2 *= 2;
+        return p2;  // a power of two: the kernels test boundaries with a mask
     }();
     return v;
 }
@@ -668,15 +696,23 @@ public:
         for (int i = 1; i < n_; ++i) th_.emplace_back([this, i] { loop(i); });
     }
     ~SpinTeam() {
-        stop_.store(true, std::memory_order_relaxed);
+        {
+            std::lock_guard<std::mutex> l(mu_);
+            stop_.store(true);
+        }
+        cv_.notify_all();
         for (auto& t : th_) t.join();
     }
     int size() const { return n_; }
     // Runs fn(worker) on every worker (the caller is worker 0) and waits.
     void run(const std::function<void(int)>& fn) {
         fn_ = &fn;
-        done_.store(0, std::memory_order_relaxed);
-        gen_.fetch_add(1, std::memory_order_release);
+        done_.store(0);
+        gen_.fetch_add(1);
+        if (sleepers_.load() > 0) {
+            std::lock_guard<std::mutex> l(mu_);
+            cv_.notify_all();
+        }
         fn(0);
         while (done_.load(std::memory_order_acquire) != n_ - 1) cpu_relax();
     }
@@ -687,13 +723,24 @@ private:
         __builtin_ia32_pause();
 #endif
     }
+    // Spin for ~50 us between items, then sleep: a process with other busy threads
+    // (e.g. an OpenMP pool that spins after its parallel regions) must not lose its
+    // cores to idle spinners.
     void loop(int i) {
         uint64_t seen = 0;
         for (;;) {
-            uint64_t g;
-            while ((g = gen_.load(std::memory_order_acquire)) == seen) {
-                if (stop_.load(std::memory_order_relaxed)) return;
+            uint64_t g = gen_.load();
+            for (int k = 0; g == seen && k < 20000; ++k) {
                 cpu_relax();
+                g = gen_.load();
+            }
+            if (g == seen) {
+                std::unique_lock<std::mutex> l(mu_);
+                sleepers_.fetch_add(1);
+                cv_.wait(l, [&] { return stop_.load() || gen_.load() != seen; });
+                sleepers_.fetch_sub(1);
+                if (stop_.load() && gen_.load() == seen) return;
+                g = gen_.load();
             }
             seen = g;
             (*fn_)(i);
@@ -705,7 +752,10 @@ private:
     const std::function<void(int)>* fn_ = nullptr;
     std::atomic<uint64_t> gen_{0};
     std::atomic<int> done_{0};
+    std::atomic<int> sleepers_{0};
     std::atomic<bool> stop_{false};
+    std::mutex mu_;
+    std::condition_variable cv_;
 };
 
 // dst[r][c] = src[r][c] (fp32 -> fp64) for rows [0, rows), split over the team

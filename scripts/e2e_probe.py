@@ -1,4 +1,4 @@
-"""e2e host-path breakdown (lpd_compute_g_dense into pageable fp64 G), C2 by default."""
+"""e2e host-path breakdown (lpd_set_basis_dense + lpd_compute_g_dense into pageable fp64 G)."""
 import sys, time
 import numpy as np
 sys.path.insert(0, ".")
@@ -14,11 +14,13 @@ G = np.zeros((n, L.shape[1]))
 import torch
 Xp = torch.from_numpy(X).pin_memory().numpy()
 with P.Context(1) as ctx:
-    ctx.set_basis_dense(Y, L, cfg.gamma)
+    for i in range(3):
+        t0 = time.perf_counter(); ctx.set_basis_dense(Y, L, cfg.gamma); print(f"set_basis (before compute) {time.perf_counter()-t0:.4f} s", flush=True)
     ctx.compute_g_dense(Xp, out=G)
     for _ in range(3):
+        t0 = time.perf_counter(); ctx.set_basis_dense(Y, L, cfg.gamma); tb = time.perf_counter() - t0
         t = P.Timings()
         t0 = time.perf_counter()
         ctx.compute_g_dense(Xp, out=G, timings=t)
         dt = time.perf_counter() - t0
-        print(f"wall {dt:.3f} s  {n/dt/1e6:.2f} M rows/s  {G.nbytes/dt/1e9:.1f} GB/s fp64 out  timings {t.as_dict()}", flush=True)
+        print(f"set_basis {tb:.4f} s  compute wall {dt:.3f} s  {n/dt/1e6:.2f} M rows/s  {G.nbytes/dt/1e9:.1f} GB/s fp64 out  timings {t.as_dict()}", flush=True)
