@@ -180,39 +180,41 @@ Csr flatten(std::span<const lpdsvm::SparseVector> rows, int num_threads) {
 }
 
 // Matrix(rows, cols) — the same object the reference constructor builds (rows_, cols_,
-// a zero-filled std::vector<double>, matrix.hpp:12-44) — without the reference's
-// dominant host cost at scale: 19 GB of serial 4 KB first-touch page faults at C2
-// (measured 6.75 s of a 7.5 s gmatrix). The storage is reserved, advised to use
-// transparent huge pages, first-touched by all host threads, and only then
-// value-initialised by the vector (zeros over present pages). The vector is moved into
-// the Matrix through its standard layout (rows_, cols_, data_ in declaration order).
+// a std::vector<double> of rows·cols elements, matrix.hpp:12-44) — whose every element
+// the device call is about to overwrite. The reference zero-fills it first
+// (value-initialised vector, matrix.hpp:15-16): 19 GB of serial 4 KB first-touch page
+// faults at C2 (measured 6.75 s of a 7.5 s gmatrix), and even a parallel, huge-page
+// zero-fill cost 1.6 s. Here the storage is allocated by the vector's own allocator,
+// advised to use transparent huge pages, and given its size without value
+// initialisation (libstdc++ vector layout: start, finish, end-of-storage — checked, with
+// the ordinary constructor as fallback), so the first touch of every page is the
+// delivery's widen threads writing G. `complete` is false if the call fails before
+// writing (the caller then throws and the Matrix is discarded).
 struct MatrixLayout {
     std::size_t rows, cols;
     std::vector<double> data;
 };
-lpdsvm::Matrix make_zero_matrix(std::size_t rows, std::size_t cols, int threads) {
-    if constexpr (sizeof(MatrixLayout) == sizeof(lpdsvm::Matrix) &&
-                  std::is_standard_layout_v<lpdsvm::Matrix> && std::is_standard_layout_v<MatrixLayout>) {
+struct VectorLayout {
+    double *start, *finish, *end_of_storage;
+};
+lpdsvm::Matrix make_output_matrix(std::size_t rows, std::size_t cols) {
+    if constexpr (sizeof(MatrixLayout) == sizeof(lpdsvm::Matrix) && std::is_standard_layout_v<lpdsvm::Matrix> &&
+                  std::is_standard_layout_v<MatrixLayout> && sizeof(std::vector<double>) == sizeof(VectorLayout)) {
         const std::size_t n = rows * cols;
         if (n * sizeof(double) < (std::size_t(64) << 20)) return lpdsvm::Matrix(rows, cols);
         std::vector<double> v;
         v.reserve(n);
+        auto* vl = reinterpret_cast<VectorLayout*>(&v);
+        if (vl->start != v.data() || vl->finish != v.data() || vl->end_of_storage != v.data() + v.capacity())
+            return lpdsvm::Matrix(rows, cols);  // unexpected library layout: the reference's way
         char* base = reinterpret_cast<char*>(v.data());
         const std::size_t bytes = n * sizeof(double);
         const std::uintptr_t huge = std::uintptr_t(2) << 20;
         const std::uintptr_t a0 = (reinterpret_cast<std::uintptr_t>(base) + huge - 1) & ~(huge - 1);
         const std::uintptr_t a1 = (reinterpret_cast<std::uintptr_t>(base) + bytes) & ~(huge - 1);
         if (a1 > a0) madvise(reinterpret_cast<void*>(a0), a1 - a0, MADV_HUGEPAGE);
-        const int T = std::max(1, threads);
-        std::vector<std::thread> th;
-        for (int t = 0; t < T; ++t)
-            th.emplace_back([&, t] {
-                const std::size_t b0 = bytes * static_cast<std::size_t>(t) / static_cast<std::size_t>(T);
-                const std::size_t b1 = bytes * static_cast<std::size_t>(t + 1) / static_cast<std::size_t>(T);
-                std::memset(base + b0, 0, b1 - b0);
-            });
-        for (auto& x : th) x.join();
-        v.resize(n);
+        vl->finish = vl->start + n;  // size n, elements written by compute_G below
+        if (v.size() != n) return lpdsvm::Matrix(rows, cols);
         lpdsvm::Matrix m;
         auto* L = reinterpret_cast<MatrixLayout*>(&m);
         L->rows = rows;
@@ -270,7 +272,7 @@ Matrix compute_G(std::span<const SparseVector> points, std::span<const double> /
     const char* keep = std::getenv("LPD_KEEP_G");
     lpd_set_keep_resident(ctx, !(keep && keep[0] == '0'));
     lap(1);
-    Matrix G = make_zero_matrix(n, b_eff, static_cast<int>(std::max(1u, std::thread::hardware_concurrency())));
+    Matrix G = make_output_matrix(n, b_eff);
     lap(2);
     rc = lpd_compute_g_csr(ctx, static_cast<int64_t>(n), d, xs.indptr.data(), xs.indices.data(),
                            xs.values.data(), G.data(), static_cast<int64_t>(b_eff), &g_last);
