@@ -474,17 +474,20 @@ void build_basis_host_L(DeviceState& ds, const double* lm_dev, int64_t B, int64_
 
 // K chunks (of 64) per fp32 accumulator segment: each segment's tensor-core sum
 // (round-toward-zero accumulation) is added into a round-to-nearest running sum, so
-// the accumulation bias is bounded by one segment. LPD_SEG_CHUNKS
-// overrides (accuracy studies).
-int seg_chunks() {
-    static const int v = [] {
+// the accumulation bias is bounded by one segment. Defaults: 2 for the
+// panel path (its read-out overlaps the other accumulator, so it is free) and for K1
+// with B > 4096 (C3: 6.1e-5 vs 8.9e-5 row error at 4); 4 for K1 up to 4096 landmarks
+// (C2: 1.7e-5; each read-out pauses K1's GEMM2). LPD_SEG_CHUNKS overrides (rounded
+// down to a power of two: the kernels test boundaries with a mask).
+int seg_chunks(int dflt) {
+    static const int env = [] {
         const char* e = std::getenv("LPD_SEG_CHUNKS");
-        int s = e ? std::max(1, std::atoi(e)) : 4;
-        int p2 = 1;
-        while (p2 * 2 <= s && p2 < (1 << 20)) p2 *= 2;
-        return p2;  // a power of two: the kernels test boundaries with a mask
+        return e ? std::max(1, std::atoi(e)) : 0;
     }();
-    return v;
+    const int s = env ? env : dflt;
+    int p2 = 1;
+    while (p2 * 2 <= s && p2 < (1 << 20)) p2 *= 2;
+    return p2;
 }
 
 // Large-d factor (d >= 64) for m prepped rows in slot s: per row panel, the Z GEMM
@@ -513,7 +516,7 @@ void launch_factor_panels(DeviceState& ds, Slot& s, int64_t m, void* g_dev, int6
         const char* e = std::getenv("LPD_PANEL_GROUP");
         return e ? std::max(1, std::atoi(e)) : 8;
     }();
-    const int seg = seg_chunks();
+    const int seg = seg_chunks(2);
     const CUtensorMap tm_zhi = make_plane_map(ds.z_hi, panel, ds.B_pad, lpd::kp::BM, 64);
     const CUtensorMap tm_zlo = make_plane_map(ds.z_lo, panel, ds.B_pad, lpd::kp::BM, 64);
     for (int64_t r0 = 0; r0 < m; r0 += panel) {
@@ -616,7 +619,7 @@ void launch_factor(DeviceState& ds, Slot& s, const double* x_dev, int64_t m, int
     p.ksteps1 = static_cast<int>((ds.d + 1 + 15) / 16);
     p.row_aux = s.raux;
     p.col_scale = ds.col_scale;
-    p.seg_chunks = seg_chunks();
+    p.seg_chunks = seg_chunks(ds.B_pad > 4096 ? 2 : 4);
     static const int split_n = [] {
         const char* e = std::getenv("LPD_K1_SPLIT");
         return e ? (std::atoi(e) != 0) : 0;
