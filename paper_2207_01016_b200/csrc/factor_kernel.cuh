@@ -118,7 +118,13 @@ constexpr int KD = 64;         // padded feature dim (one 128-byte swizzle atom 
 constexpr int N2 = 256;        // G columns per tile (UMMA N of GEMM2)
 constexpr int N2H = 128;       // Lᵀ rows per tile held by one CTA
 constexpr int NS_LM = 4;       // landmark-chunk stages
-constexpr int NS_LT = 6;       // Lᵀ half-chunk stages (hi and lo travel separately)
+#ifndef LPD_K1_NS_LT
+#define LPD_K1_NS_LT 6
+#endif
+#ifndef LPD_K1_NSTG
+#define LPD_K1_NSTG 2
+#endif
+constexpr int NS_LT = LPD_K1_NS_LT;  // Lᵀ half-chunk stages (hi and lo travel separately)
 constexpr int NSZ = 3;         // S/Z TMEM buffers
 constexpr int EPI_WARPS = 8;
 constexpr int THREADS = 128 + 32 * EPI_WARPS;
@@ -127,7 +133,7 @@ constexpr int Z13 = 13;        // Z is carried as Z·2^13 in fp16
 constexpr uint32_t LM_BYTES = NCH * KD * 2;          // 4 KB per hi/lo plane (this CTA's half)
 constexpr uint32_t LT_BYTES = N2H * NC * 2;          // 16 KB per stage (this CTA's half)
 constexpr uint32_t STG_BYTES = 32 * 128;             // 4 KB G staging buffer
-constexpr int NSTG = 2;                              // staging buffers per epilogue warp
+constexpr int NSTG = LPD_K1_NSTG;                    // staging buffers per epilogue warp
 
 constexpr uint32_t OFF_LM = 0;                                      // stage s: hi, lo
 constexpr uint32_t OFF_LT = OFF_LM + NS_LM * 2 * LM_BYTES;          // stage s
@@ -563,61 +569,75 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
         };
 
         // G accumulator of a finished tile: TMEM -> scale -> global (128 columns per warp).
-        // G of a finished tile: last segment -> running sums -> ×col_scale -> global
-        // (128 columns per warp: two runs of 64 contiguous tile columns, half_col).
-        auto drain_g = [&](int tile, bool first) {
+        // 32 columns (run m of 4) of a finished tile's running sums -> ×col_scale ->
+        // fp64/fp32 -> swizzled SMEM staging -> TMA store. The four runs of a tile are
+        // interleaved with the next tile's first Z chunks, so the MMA is not left waiting
+        // for Z while the epilogue drains (the running sums are next overwritten by the
+        // next tile's first segment read-out, which first completes any runs left).
+        auto store_part = [&](int tile, int m) {
+            if (p.dbg & 64) return;  // bypass the stores
             const int cb = tile / p.n_row_tiles;
             const int rt = tile - cb * p.n_row_tiles;
-            flush(first);
-            if (p.dbg & 64) return;  // bypass the stores
             constexpr int SLAB = 128 / sizeof(OutT);  // columns per 128-byte staging row
+            const int c0 = half_col(half, m * 32, SP);
+            const int gc0 = cb * N2 + c0;
+            if (gc0 >= p.b_eff || (p.dbg & 2)) return;
+            const float4* cs4 = reinterpret_cast<const float4*>(p.col_scale + gc0);
+            float v[32];
 #pragma unroll
-            for (int m = 0; m < 4; ++m) {
-                const int c0 = half_col(half, m * 32, SP);
-                const int gc0 = cb * N2 + c0;
-                if (gc0 >= p.b_eff || (p.dbg & 2)) continue;
-                const float4* cs4 = reinterpret_cast<const float4*>(p.col_scale + gc0);
-                float v[32];
+            for (int i = 0; i < 8; ++i) {
+                const float4 sc = ldg_f4_inorder(cs4 + i);
+                v[4 * i + 0] = rs[m * 32 + 4 * i + 0] * sc.x;
+                v[4 * i + 1] = rs[m * 32 + 4 * i + 1] * sc.y;
+                v[4 * i + 2] = rs[m * 32 + 4 * i + 2] * sc.z;
+                v[4 * i + 3] = rs[m * 32 + 4 * i + 3] * sc.w;
+            }
+            // 32 rows x SLAB columns per store; 128-byte swizzled staging rows
+            // (16-byte chunk c of row r at chunk c ^ (r & 7)): conflict-free STS.
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const float4 sc = ldg_f4_inorder(cs4 + i);
-                    v[4 * i + 0] = rs[m * 32 + 4 * i + 0] * sc.x;
-                    v[4 * i + 1] = rs[m * 32 + 4 * i + 1] * sc.y;
-                    v[4 * i + 2] = rs[m * 32 + 4 * i + 2] * sc.z;
-                    v[4 * i + 3] = rs[m * 32 + 4 * i + 3] * sc.w;
+            for (int sl = 0; sl < 32 / SLAB; ++sl) {
+                // double-buffered staging: the store issued two slabs ago has
+                // finished reading this buffer once at most one group is pending
+                if (lane == 0) bulk_wait_group_read<NSTG - 1>();
+                __syncwarp();
+                const uint32_t sbuf = OFF_STG + (ew * NSTG + stg_k) * STG_BYTES;
+                stg_k = (stg_k + 1) % NSTG;
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    uint32_t w[4];
+                    if constexpr (sizeof(OutT) == 8) {
+                        const double d0 = v[sl * SLAB + 2 * c], d1 = v[sl * SLAB + 2 * c + 1];
+                        w[0] = __double2loint(d0); w[1] = __double2hiint(d0);
+                        w[2] = __double2loint(d1); w[3] = __double2hiint(d1);
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) w[e] = __float_as_uint(v[4 * c + e]);
+                    }
+                    st_shared_v4(base_addr + sbuf + lane * 128 + ((c ^ (lane & 7)) << 4), w[0], w[1], w[2], w[3]);
                 }
-                // 32 rows x SLAB columns per store; 128-byte swizzled staging rows
-                // (16-byte chunk c of row r at chunk c ^ (r & 7)): conflict-free STS.
-#pragma unroll
-                for (int sl = 0; sl < 32 / SLAB; ++sl) {
-                    // double-buffered staging: the store issued two slabs ago has
-                    // finished reading this buffer once at most one group is pending
-                    if (lane == 0) bulk_wait_group_read<NSTG - 1>();
-                    __syncwarp();
-                    const uint32_t sbuf = OFF_STG + (ew * NSTG + stg_k) * STG_BYTES;
-                    stg_k = (stg_k + 1) % NSTG;
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        uint32_t w[4];
-                        if constexpr (sizeof(OutT) == 8) {
-                            const double d0 = v[sl * SLAB + 2 * c], d1 = v[sl * SLAB + 2 * c + 1];
-                            w[0] = __double2loint(d0); w[1] = __double2hiint(d0);
-                            w[2] = __double2loint(d1); w[3] = __double2hiint(d1);
-                        } else {
-#pragma unroll
-                            for (int e = 0; e < 4; ++e) w[e] = __float_as_uint(v[4 * c + e]);
-                        }
-                        st_shared_v4(base_addr + sbuf + lane * 128 + ((c ^ (lane & 7)) << 4), w[0], w[1], w[2], w[3]);
-                    }
-                    fence_proxy_async_smem();
-                    __syncwarp();
-                    if (lane == 0) {
-                        tma_store_2d(&tm_g, smem + sbuf, gc0 + sl * SLAB, rt * PM + static_cast<int>(rank) * BM + quad * 32);
-                        bulk_commit_group();
-                    }
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store_2d(&tm_g, smem + sbuf, gc0 + sl * SLAB, rt * PM + static_cast<int>(rank) * BM + quad * 32);
+                    bulk_commit_group();
                 }
             }
-            pr.mark(6);
+        };
+        int pend_tile = -1, pend_m = 4;  // runs of the previous tile still to store
+        // (constant run indices, so the running sums stay in registers)
+        auto store_run = [&](int m) {
+            switch (m) {
+                case 0: store_part(pend_tile, 0); break;
+                case 1: store_part(pend_tile, 1); break;
+                case 2: store_part(pend_tile, 2); break;
+                default: store_part(pend_tile, 3); break;
+            }
+        };
+        auto store_some = [&]() {
+            if (pend_m < 4) store_run(pend_m++);
+        };
+        auto store_all = [&]() {
+            while (pend_m < 4) store_run(pend_m++);
         };
 
         // Per tile: Z for every chunk; the next tile's X goes into TMEM as soon as
@@ -636,7 +656,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
             for (int j = 0; j < n; ++j) {
                 // the segment that ended with GEMM2(j - 2) is complete by the time
                 // GEMM1(j) (issued after it) has produced S(j)
-                if (!LPD_K1_NOSEG && j >= 2 && seg_end(half, j - 2, n, S, SP)) { flush(first); first = false; }
+                if (!LPD_K1_NOSEG && j >= 2 && seg_end(half, j - 2, n, S, SP)) {
+                    if (first) store_all();
+                    flush(first);
+                    first = false;
+                }
                 if (p.dbg & 32) {  // bypass: keep the barrier protocol, skip Z math and stores
                     const uint32_t b = cnt % NSZ, ph = (cnt / NSZ) & 1;
                     mbar_wait_cluster(s_full + b, ph);
@@ -646,12 +670,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
                 } else {
                     produce_z(R2, sx2);
                 }
+                store_some();
             }
-            if (!LPD_K1_NOSEG && n >= 2 && seg_end(half, n - 2, n, S, SP)) { flush(first); first = false; }
+            if (!LPD_K1_NOSEG && n >= 2 && seg_end(half, n - 2, n, S, SP)) {
+                if (first) store_all();
+                flush(first);
+                first = false;
+            }
             if (next < num_tiles) write_x(it + 1);
             pr.mark(3);
-            drain_g(tile, first);
+            // last segment of the tile; its stores go out during the next tile
+            if (first) store_all();
+            flush(first);
+            pend_tile = tile;
+            pend_m = 0;
+            pr.mark(6);
         }
+        store_all();
         if (lane == 0) bulk_wait_group<0>();
         __syncwarp();
         pr.mark(7);
