@@ -64,12 +64,16 @@ def parse():
 
 
 def load_peaks():
+    """Dense bf16 peaks from MEASURED_PEAKS.json (driver-written on this pool's B200s):
+    the burst figure and the sustained one (back-to-back matmuls under the 1 kW cap)."""
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return {"tflops": float(p["bf16_tflops"]), "hbm": float(p["hbm_gbs"]), "src": "measured"}
+        burst = float(p["bf16_tflops"])
+        return {"burst": burst, "sustained": float(p.get("bf16_tflops_sustained", burst)),
+                "hbm": float(p["hbm_gbs"]), "src": "measured"}
     except Exception:
-        return {"tflops": 1590.0, "hbm": 6650.0, "src": "fallback"}
+        return {"burst": 1590.0, "sustained": 1590.0, "hbm": 6650.0, "src": "fallback (B200_PROFILING.md)"}
 
 
 def load_traffic(workload):
@@ -309,6 +313,13 @@ def main():
     F = 2.0 * n * B * cfg.d + 2.0 * n * B * b_eff
     peaks = load_peaks()
     achieved = F / (k_ms / 1e3) / 1e12
+    # The factor kernel runs back to back for the whole timed region (tens of ms per
+    # launch, sw_power_cap engaged): the sustained peak is its roof; a short region
+    # would be judged against the burst figure.
+    sustained = elapsed_ms >= 100.0 and k_ms >= 10.0
+    peak = peaks["sustained"] if sustained else peaks["burst"]
+    peak_src = (f"MEASURED_PEAKS.json bf16_tflops{'_sustained' if sustained else ''} ({peaks['src']}; "
+                f"kind::f16 runs at the bf16 rate; {'kernel timed inside a long step' if sustained else 'short timed region'})")
     traffic = load_traffic(cfg.name)
     # issued tensor work (3-term split, padded shapes, GEMM1 recomputed per 256-column block)
     npad, epad = -(-n // 256) * 256, -(-b_eff // 256) * 256
@@ -394,11 +405,12 @@ def main():
                        "path": "fused K1 (d <= 63)" if cfg.d <= 63 else "panel path: Z GEMM + projection GEMM (d >= 64)",
                        "l2": f"inputs larger than L2 (G {n * b_eff * 8 / 1e9:.1f} GB/step per GPU written, "
                              f"X {X.nbytes / 1e9:.2f} GB read)"},
-            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peaks["tflops"], "unit": "TFLOP/s",
-                         "frac": achieved / peaks["tflops"], "traffic": traffic,
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": traffic,
                          "kernel_ms": k_ms, "flops_per_launch": F, "issued_tensor_flops_per_launch": issued,
-                         "issued_frac": issued / (k_ms / 1e3) / 1e12 / peaks["tflops"],
-                         "peak_source": f"MEASURED_PEAKS.json bf16_tflops ({peaks['src']}; kind::f16 runs at the bf16 rate)"},
+                         "issued_frac": issued / (k_ms / 1e3) / 1e12 / peak,
+                         "peak_source": peak_src, "peak_burst": peaks["burst"],
+                         "frac_of_burst": achieved / peaks["burst"]},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches_per_step(n, cfg.d, B) * args.steps,

@@ -82,6 +82,12 @@ struct FactorParams {
 #ifndef LPD_K1_NOREG
 #define LPD_K1_NOREG 0
 #endif
+// Profiling ablations (LPD_K1_DEBUG bits 1/2/4/8/32/64) exist only in builds with
+// -DLPD_K1_ABLATIONS=1, so production MMA / epilogue loops carry no per-item tests.
+#ifndef LPD_K1_ABLATIONS
+#define LPD_K1_ABLATIONS 0
+#endif
+#define K1_ABL(bit) (LPD_K1_ABLATIONS && (p.dbg & (bit)))
 #if LPD_K1_PROBE
 struct PhaseProbe {
     bool on;
@@ -328,7 +334,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
                     const uint32_t a = tmem_base + ((pass == 2) ? TM_XLO : TM_XHI);
                     const uint64_t bb = (pass == 1) ? d_lmlo : d_lmhi;
                     for (int k = 0; k < p.ksteps1; ++k)
-                        if (!(p.dbg & 8)) mma_f16_ts_2sm(d, a + 8 * k, bb + 2 * k, IDESC_G1, (pass | k) != 0);
+                        if (!K1_ABL(8)) mma_f16_ts_2sm(d, a + 8 * k, bb + 2 * k, IDESC_G1, (pass | k) != 0);
                 }
                 mma_commit_2sm_mc(lm_empty + lm_s, PAIR);
                 mma_commit_2sm_mc(s_full + b, PAIR);
@@ -370,10 +376,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
                     const uint32_t d = tmem_base + TM_G;
 #pragma unroll
                     for (int k = 0; k < NC / 16; ++k)
-                        if (!(p.dbg & 4)) mma_f16_ts_2sm(d, zb + z_hi_col(k), d_lt + 2 * k, IDESC_G2, !(st0 && k == 0));
+                        if (!K1_ABL(4)) mma_f16_ts_2sm(d, zb + z_hi_col(k), d_lt + 2 * k, IDESC_G2, !(st0 && k == 0));
 #pragma unroll
                     for (int k = 0; k < NC / 16; ++k)
-                        if (!(p.dbg & 4)) mma_f16_ts_2sm(d, zb + z_lo_col(k), d_lt + 2 * k, IDESC_G2, 1);
+                        if (!K1_ABL(4)) mma_f16_ts_2sm(d, zb + z_lo_col(k), d_lt + 2 * k, IDESC_G2, 1);
                 }
                 __syncwarp();
             }
@@ -393,10 +399,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
                     const uint64_t bh = d_lt + ((h * LT_HALF) >> 4);
 #pragma unroll
                     for (int k = 0; k < NC / 16; ++k)
-                        if (!(p.dbg & 4)) mma_f16_ts_2sm(d, zb + z_hi_col(k), bh + 2 * k, IDESC_G2H, !(fresh && k == 0));
+                        if (!K1_ABL(4)) mma_f16_ts_2sm(d, zb + z_hi_col(k), bh + 2 * k, IDESC_G2H, !(fresh && k == 0));
 #pragma unroll
                     for (int k = 0; k < NC / 16; ++k)
-                        if (!(p.dbg & 4)) mma_f16_ts_2sm(d, zb + z_lo_col(k), bh + 2 * k, IDESC_G2H, 1);
+                        if (!K1_ABL(4)) mma_f16_ts_2sm(d, zb + z_lo_col(k), bh + 2 * k, IDESC_G2H, 1);
                 }
                 __syncwarp();
             }
@@ -417,12 +423,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
                         const uint64_t bh = d_lt2 + ((h * LT_HALF) >> 4);
 #pragma unroll
                         for (int k = 0; k < NC / 16; ++k)
-                            if (!(p.dbg & 4)) mma_f16_ts_2sm(d, zb + z_hi_col(k), bh + 2 * k, IDESC_G2H, 1);
+                            if (!K1_ABL(4)) mma_f16_ts_2sm(d, zb + z_hi_col(k), bh + 2 * k, IDESC_G2H, 1);
                     }
                 } else {
 #pragma unroll
                     for (int k = 0; k < NC / 16; ++k)
-                        if (!(p.dbg & 4)) mma_f16_ts_2sm(tmem_base + TM_G, zb + z_hi_col(k), d_lt2 + 2 * k, IDESC_G2, 1);
+                        if (!K1_ABL(4)) mma_f16_ts_2sm(tmem_base + TM_G, zb + z_hi_col(k), d_lt2 + 2 * k, IDESC_G2, 1);
                 }
                 mma_commit_2sm_mc(lt_empty + lt_s, PAIR);
                 mma_commit_2sm(sz_empty + b);
@@ -538,7 +544,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
             tmem_wait_ld();
             pr.mark(1);
             uint32_t hi[16], lo[16];
-            if (p.dbg & 1) {
+            if K1_ABL(1) {
 #pragma unroll
                 for (int i = 0; i < 16; ++i) { hi[i] = s[2 * i]; lo[i] = s[2 * i + 1]; }
             } else {
@@ -575,13 +581,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
         // for Z while the epilogue drains (the running sums are next overwritten by the
         // next tile's first segment read-out, which first completes any runs left).
         auto store_part = [&](int tile, int m) {
-            if (p.dbg & 64) return;  // bypass the stores
+            if K1_ABL(64) return;  // bypass the stores
             const int cb = tile / p.n_row_tiles;
             const int rt = tile - cb * p.n_row_tiles;
             constexpr int SLAB = 128 / sizeof(OutT);  // columns per 128-byte staging row
             const int c0 = half_col(half, m * 32, SP);
             const int gc0 = cb * N2 + c0;
-            if (gc0 >= p.b_eff || (p.dbg & 2)) return;
+            if (gc0 >= p.b_eff || K1_ABL(2)) return;
             const float4* cs4 = reinterpret_cast<const float4*>(p.col_scale + gc0);
             float v[32];
 #pragma unroll
@@ -661,7 +667,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
                     flush(first);
                     first = false;
                 }
-                if (p.dbg & 32) {  // bypass: keep the barrier protocol, skip Z math and stores
+                if K1_ABL(32) {  // bypass: keep the barrier protocol, skip Z math and stores
                     const uint32_t b = cnt % NSZ, ph = (cnt / NSZ) & 1;
                     mbar_wait_cluster(s_full + b, ph);
                     __syncwarp();

@@ -855,9 +855,13 @@ void compute_rows_host(lpd_context* ctx, int64_t n, double* G, int64_t ldg, lpd_
     std::vector<double> h2d(nd, 0.0), ker(nd, 0.0), d2h(nd, 0.0), host(nd, 0.0);
     std::vector<int64_t> launches(nd, 0);
     const int64_t b_eff = ctx->dev[0].b_eff;
-    // Rows per compute chunk: ~128 MB of fp32 G, multiple of the 256-row pair tile.
+    // Rows per compute chunk (multiple of the 256-row pair tile): ~512 MB of fp32 G for
+    // the fused kernel (≥ 32k rows at C2: ~7 waves of tiles per launch, few launches);
+    // a whole 2 GB Z panel on the large-d path, whose projection re-reads all of Lᵀ per
+    // launch (smaller chunks multiply that traffic). Delivery granularity is separate.
+    const int64_t chunk_bytes = ctx->dev[0].large ? (2ll << 30) : (512ll << 20);
     const int64_t chunk = std::max<int64_t>(
-        256, std::min<int64_t>(round_up(n, 256), (128ll << 20) / (4 * b_eff) / 256 * 256));
+        256, std::min<int64_t>(round_up(n, 256), chunk_bytes / (4 * b_eff) / 256 * 256));
     const int hw = std::max(1u, std::thread::hardware_concurrency());
     const int workers = std::max(1, std::min(16, hw / nd));
     ctx->res_n = 0;
