@@ -726,6 +726,14 @@ private:
         __builtin_ia32_pause();
 #endif
     }
+    // pause iterations before a helper sleeps (LPD_SPIN_LIMIT overrides)
+    static int spin_limit() {
+        static const int v = [] {
+            const char* e = std::getenv("LPD_SPIN_LIMIT");
+            return e ? std::max(0, std::atoi(e)) : 20000;
+        }();
+        return v;
+    }
     // Spin for ~50 us between items, then sleep: a process with other busy threads
     // (e.g. an OpenMP pool that spins after its parallel regions) must not lose its
     // cores to idle spinners.
@@ -733,7 +741,7 @@ private:
         uint64_t seen = 0;
         for (;;) {
             uint64_t g = gen_.load();
-            for (int k = 0; g == seen && k < 20000; ++k) {
+            for (int k = 0; g == seen && k < spin_limit(); ++k) {
                 cpu_relax();
                 g = gen_.load();
             }
@@ -863,7 +871,11 @@ void compute_rows_host(lpd_context* ctx, int64_t n, double* G, int64_t ldg, lpd_
     const int64_t chunk = std::max<int64_t>(
         256, std::min<int64_t>(round_up(n, 256), chunk_bytes / (4 * b_eff) / 256 * 256));
     const int hw = std::max(1u, std::thread::hardware_concurrency());
-    const int workers = std::max(1, std::min(16, hw / nd));
+    static const int env_workers = [] {
+        const char* e = std::getenv("LPD_WIDEN_THREADS");
+        return e ? std::max(1, std::atoi(e)) : 0;
+    }();
+    const int workers = env_workers ? env_workers : std::max(1, std::min(16, hw / nd));
     ctx->res_n = 0;
     std::vector<int> resident_ok(nd, 0);
     run_parallel(ctx, [&](DeviceState& ds, int di) {
