@@ -187,6 +187,9 @@ struct DeviceState {
     __half* z_hi = nullptr;    // large path: Z panel scratch [z_rows × B_pad]
     __half* z_lo = nullptr;
     int64_t z_rows = 0;
+    unsigned int* sync_ctr = nullptr;  // panel GEMM K-progress rendezvous counters [kSyncCtrs]
+    static constexpr int kSyncCtrs = 64;
+    int sync_seq = 0;
     double gamma = 1.0;
     double* mu = nullptr;
     __half* lm_hi = nullptr;
@@ -451,6 +454,8 @@ struct PhaseTrace {
     }
 };
 
+void h2d_staged(DeviceState& ds, void* dst, const void* src, size_t bytes, cudaStream_t st);
+
 void build_basis_host_L(DeviceState& ds, const double* lm_dev, int64_t B, int64_t d,
                         const double* L_host, int64_t b_eff, double gamma) {
     CUDA_TRY(cudaSetDevice(ds.device));
@@ -460,8 +465,8 @@ void build_basis_host_L(DeviceState& ds, const double* lm_dev, int64_t B, int64_
     dev_alloc(&L_dev, static_cast<size_t>(B * b_eff));
     tr.lap("alloc L");
     try {
-        CUDA_TRY(cudaMemcpyAsync(L_dev, L_host, sizeof(double) * B * b_eff, cudaMemcpyHostToDevice, st));
-        tr.lap("H2D L (enqueue)");
+        h2d_staged(ds, L_dev, L_host, sizeof(double) * B * b_eff, st);
+        tr.lap("H2D L");
         build_basis(ds, lm_dev, B, d, std::max<int64_t>(d, 1), L_dev, b_eff, gamma, st, true);
         tr.lap("prep + sync");
     } catch (...) {
@@ -488,6 +493,38 @@ int seg_chunks(int dflt) {
     int p2 = 1;
     while (p2 * 2 <= s && p2 < (1 << 20)) p2 *= 2;
     return p2;
+}
+
+// Launch of a panel GEMM. With a rendezvous counter the kernel's CTAs wait for each
+// other, so they must all be resident at once: the launch is cooperative (the driver
+// guarantees co-residency or refuses), and a refused launch runs without the
+// rendezvous instead of risking a hang.
+template <typename Kernel>
+void launch_panel(Kernel kernel, int grid, cudaStream_t st, const CUtensorMap& a0, const CUtensorMap& a1,
+                  const CUtensorMap& b0, const CUtensorMap& b1, lpd::PanelParams p) {
+    if (p.sync) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(lpd::kp::THREADS);
+        cfg.dynamicSmemBytes = lpd::kp::SMEM_BYTES;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, a0, a1, b0, b1, p);
+        if (e == cudaSuccess) return;
+        cudaGetLastError();
+        static bool warned = false;
+        if (!warned) {
+            warned = true;
+            std::fprintf(stderr, "[lpd] cooperative launch refused (%s): panel GEMMs run without the "
+                                 "K-progress rendezvous\n", cudaGetErrorString(e));
+        }
+        p.sync = nullptr;
+    }
+    kernel<<<grid, lpd::kp::THREADS, lpd::kp::SMEM_BYTES, st>>>(a0, a1, b0, b1, p);
 }
 
 // Large-d factor (d >= 64) for m prepped rows in slot s: per row panel, the Z GEMM
@@ -517,6 +554,24 @@ void launch_factor_panels(DeviceState& ds, Slot& s, int64_t m, void* g_dev, int6
         return e ? std::max(1, std::atoi(e)) : 8;
     }();
     const int seg = seg_chunks(2);
+    // K-progress rendezvous of the panel GEMMs' producers every 32 chunks (C4
+    // projection: DRAM reads 114 -> 35 GB per panel, 271 -> 230 ms per shard, clock
+    // 1.08 -> 1.24 GHz under the power cap). LPD_PANEL_SYNC=0 disables.
+    static const int sync_every = [] {
+        const char* e = std::getenv("LPD_PANEL_SYNC");
+        return e ? std::max(0, std::atoi(e)) : 32;
+    }();
+    if (sync_every > 0 && !ds.sync_ctr) {
+        dev_alloc(&ds.sync_ctr, DeviceState::kSyncCtrs);
+        CUDA_TRY(cudaMemset(ds.sync_ctr, 0, sizeof(unsigned int) * DeviceState::kSyncCtrs));
+    }
+    // a fresh counter per launch (launches on different streams never share one)
+    auto next_ctr = [&]() -> unsigned int* {
+        if (sync_every <= 0) return nullptr;
+        unsigned int* c = ds.sync_ctr + (ds.sync_seq++ % DeviceState::kSyncCtrs);
+        CUDA_TRY(cudaMemsetAsync(c, 0, sizeof(unsigned int), st));
+        return c;
+    };
     const CUtensorMap tm_zhi = make_plane_map(ds.z_hi, panel, ds.B_pad, lpd::kp::BM, 64);
     const CUtensorMap tm_zlo = make_plane_map(ds.z_lo, panel, ds.B_pad, lpd::kp::BM, 64);
     for (int64_t r0 = 0; r0 < m; r0 += panel) {
@@ -536,10 +591,13 @@ void launch_factor_panels(DeviceState& ds, Slot& s, int64_t m, void* g_dev, int6
         pz.ldz = ds.B_pad;
         pz.group_r = group_r;
         pz.seg_chunks = seg;
+        // no rendezvous for the Z GEMM: its tiles are short (K = d + 1, 33 chunks at C4)
+        // and its operands small; a tile-start wait costs it more (72.7 vs 85.8 % tensor)
+        pz.sync = nullptr;
+        pz.sync_every = 1;
         const int64_t tz = static_cast<int64_t>(pz.n_row_pairs) * pz.n_col_blocks;
         const int gz = 2 * static_cast<int>(std::min<int64_t>(tz, ds.num_sms / 2));
-        lpd::panel_gemm_kernel<lpd::PANEL_Z, float><<<gz, lpd::kp::THREADS, lpd::kp::SMEM_BYTES, st>>>(
-            tm_xhi, tm_xlo, ds.tm_lmhi, ds.tm_lmlo, pz);
+        launch_panel(lpd::panel_gemm_kernel<lpd::PANEL_Z, float>, gz, st, tm_xhi, tm_xlo, ds.tm_lmhi, ds.tm_lmlo, pz);
         lpd::PanelParams pg{};
         pg.n_row_pairs = pz.n_row_pairs;
         pg.n_col_blocks = static_cast<int>(ds.Beff_pad / lpd::kp::BN);
@@ -552,14 +610,16 @@ void launch_factor_panels(DeviceState& ds, Slot& s, int64_t m, void* g_dev, int6
         pg.ldg = ldg;
         pg.group_r = group_r;
         pg.seg_chunks = seg;
+        pg.sync = next_ctr();
+        pg.sync_every = std::max(1, sync_every);
         const int64_t tg = static_cast<int64_t>(pg.n_row_pairs) * pg.n_col_blocks;
         const int gg = 2 * static_cast<int>(std::min<int64_t>(tg, ds.num_sms / 2));
         if (out_dtype == LPD_OUT_F64)
-            lpd::panel_gemm_kernel<lpd::PANEL_G, double><<<gg, lpd::kp::THREADS, lpd::kp::SMEM_BYTES, st>>>(
-                tm_zhi, tm_zlo, ds.tm_lthi, ds.tm_ltlo, pg);
+            launch_panel(lpd::panel_gemm_kernel<lpd::PANEL_G, double>, gg, st, tm_zhi, tm_zlo, ds.tm_lthi,
+                         ds.tm_ltlo, pg);
         else
-            lpd::panel_gemm_kernel<lpd::PANEL_G, float><<<gg, lpd::kp::THREADS, lpd::kp::SMEM_BYTES, st>>>(
-                tm_zhi, tm_zlo, ds.tm_lthi, ds.tm_ltlo, pg);
+            launch_panel(lpd::panel_gemm_kernel<lpd::PANEL_G, float>, gg, st, tm_zhi, tm_zlo, ds.tm_lthi,
+                         ds.tm_ltlo, pg);
         CUDA_TRY(cudaGetLastError());
     }
     if (time_it) {
@@ -843,6 +903,39 @@ void run_parallel(lpd_context* ctx, const std::function<void(DeviceState&, int)>
         if (codes[i] != LPD_OK) fail(codes[i], "device " + std::to_string(i) + ": " + errs[i]);
 }
 
+// Host -> device copy of a caller's (pageable) buffer through the pinned delivery ring:
+// the host team copies 8 MB pieces into ring buffers while earlier pieces are in
+// flight. A plain pageable cudaMemcpy runs at ~10 GB/s; this at the DMA rate (C4's
+// 2.1 GB L: ~0.2 s -> ~0.05 s per set_basis).
+void h2d_staged(DeviceState& ds, void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    if (bytes < (size_t(32) << 20)) {  // small: the driver's own staging is fine
+        CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+        return;
+    }
+    ensure_delivery_ring(ds);
+    const int R = static_cast<int>(ds.dring.size());
+    const size_t piece = ds.dring_bytes;
+    const int hw = std::max(1u, std::thread::hardware_concurrency());
+    SpinTeam team(std::max(1, std::min(16, hw)));
+    const char* s8 = static_cast<const char*>(src);
+    char* d8 = static_cast<char*>(dst);
+    for (size_t g = 0, off = 0; off < bytes; ++g, off += piece) {
+        const int slot = static_cast<int>(g % R);
+        if (g >= static_cast<size_t>(R)) CUDA_TRY(cudaEventSynchronize(ds.dring_ev[slot]));
+        const size_t n = std::min(piece, bytes - off);
+        char* buf = reinterpret_cast<char*>(ds.dring[slot]);
+        const int T = team.size();
+        team.run([&](int w) {
+            const size_t a = (n * w / T) & ~size_t(63), b = (w + 1 == T) ? n : ((n * (w + 1) / T) & ~size_t(63));
+            if (b > a) std::memcpy(buf + a, s8 + off + a, b - a);
+        });
+        CUDA_TRY(cudaMemcpyAsync(d8 + off, buf, n, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaEventRecord(ds.dring_ev[slot], st));
+    }
+    // the ring buffers are reused by the next call: the copies must have read them
+    CUDA_TRY(cudaStreamSynchronize(st));
+}
+
 // Host-row pipeline shared by the dense and CSR entry points. Each device owns a
 // contiguous row shard (reference compute_G chunks rows, factor.cpp:97-108; rows
 // are independent, so no collective). Per row chunk (~128 MB of fp32 G), on
@@ -863,11 +956,12 @@ void compute_rows_host(lpd_context* ctx, int64_t n, double* G, int64_t ldg, lpd_
     std::vector<double> h2d(nd, 0.0), ker(nd, 0.0), d2h(nd, 0.0), host(nd, 0.0);
     std::vector<int64_t> launches(nd, 0);
     const int64_t b_eff = ctx->dev[0].b_eff;
-    // Rows per compute chunk (multiple of the 256-row pair tile): ~512 MB of fp32 G for
-    // the fused kernel (≥ 32k rows at C2: ~7 waves of tiles per launch, few launches);
-    // a whole 2 GB Z panel on the large-d path, whose projection re-reads all of Lᵀ per
-    // launch (smaller chunks multiply that traffic). Delivery granularity is separate.
-    const int64_t chunk_bytes = ctx->dev[0].large ? (2ll << 30) : (512ll << 20);
+    // Rows per compute chunk (multiple of the 256-row pair tile): ~512 MB of fp32 G
+    // (C2: 32k rows, ~7 waves of tiles per launch; C4: 8k-row panels). Larger chunks
+    // cut launches and (large d) Lᵀ re-reads but lengthen the pipeline fill and drain
+    // (C4 e2e: 0.29 s of compute+delivery with 2 GB chunks). Delivery granularity is
+    // separate (the 8 MB ring).
+    const int64_t chunk_bytes = 512ll << 20;
     const int64_t chunk = std::max<int64_t>(
         256, std::min<int64_t>(round_up(n, 256), chunk_bytes / (4 * b_eff) / 256 * 256));
     const int hw = std::max(1u, std::thread::hardware_concurrency());
@@ -947,6 +1041,9 @@ void compute_rows_host(lpd_context* ctx, int64_t n, double* G, int64_t ldg, lpd_
             CUDA_TRY(cudaEventRecord(s.ev[1], s.stream));
             // the slot's device G buffer: chunk k-2's D2H must have drained
             if (k >= 2 && !resident) CUDA_TRY(cudaStreamWaitEvent(s.stream, s.ev[5], 0));
+            // factor launches of consecutive chunks never run concurrently (each fills
+            // the GPU, and the panel GEMMs' CTAs rendezvous): after chunk k-1's kernels
+            if (k >= 1) CUDA_TRY(cudaStreamWaitEvent(s.stream, ds.slot[(k - 1) & 1].ev[2], 0));
             launch_factor(ds, s, s.x, rows, ds.d, gdst(k), g_ld, LPD_OUT_F32, s.stream, false);
             launches[di] += 2;
             CUDA_TRY(cudaEventRecord(s.ev[2], s.stream));
@@ -1212,6 +1309,7 @@ int lpd_context_destroy(lpd_context* ctx) {
         dev_free(ds.pairs);
         dev_free(ds.votes);
         dev_free(ds.res_g);
+        dev_free(ds.sync_ctr);
         if (ds.scratch) cudaFree(ds.scratch);
         if (ds.gtmp) cudaFree(ds.gtmp);
         for (auto& s : ds.slot) {
@@ -1248,7 +1346,9 @@ int lpd_set_basis_dense(lpd_context* ctx, const double* landmarks, int64_t B, in
             CUDA_TRY(cudaSetDevice(ds.device));
             double* lm = nullptr;
             dev_alloc(&lm, static_cast<size_t>(B * std::max<int64_t>(d, 1)));
-            if (d > 0)
+            if (d > 0 && ld == d)
+                h2d_staged(ds, lm, landmarks, sizeof(double) * static_cast<size_t>(B * d), ds.slot[0].stream);
+            else if (d > 0)
                 CUDA_TRY(cudaMemcpy2D(lm, sizeof(double) * d, landmarks, sizeof(double) * ld,
                                       sizeof(double) * d, static_cast<size_t>(B),
                                       cudaMemcpyHostToDevice));

@@ -22,7 +22,11 @@
 // planes, with cta_group::2 loads counted on the leader's barrier); the leader issues
 // three split products per chunk (A_hi·B_hi + A_lo·B_hi + A_hi·B_lo) as M=256, N=256
 // tcgen05 SS MMAs. Tiles are rastered in groups of row pairs so the pairs in flight
-// share A rows and B rows in L2.
+// share A rows and B rows in L2, and the producers of all pairs meet every 32 K-chunks
+// (a global counter), so those tiles also read the same K slice at nearly the same
+// time: without it the pairs drift apart within a tile, the in-flight working set
+// outgrows L2, and the C4 projection read 114 GB per panel from DRAM (79.5 % vs 55 %
+// L2 hits with it, 35 GB; the saved DRAM power buys clock under the 1 kW cap).
 //
 // Accumulation in segments: the tensor core adds each MMA's products into the fp32
 // TMEM accumulator with round-toward-zero, a bias that grows with the number of
@@ -55,6 +59,8 @@ struct PanelParams {
     long long ldg;
     int group_r;              // row pairs per raster group (L2 reuse of A and B rows)
     int seg_chunks;           // K chunks per accumulator segment (>= 1)
+    unsigned int* sync;       // K-progress rendezvous counter (zeroed per launch), or null
+    int sync_every;           // chunks between rendezvous points
 };
 
 namespace kp {
@@ -137,12 +143,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kp::THREADS, 1)
         if (lane == 0) {
             const uint64_t pol = policy_evict_normal();
             uint32_t s = 0, ph = 0;
-            for (int tile = pair; tile < num_tiles; tile += num_pairs) {
+            // Optional K-progress rendezvous of all producers (both CTAs of every pair
+            // with a tile in this wave) every sync_every chunks, so the tiles in flight
+            // read the same A rows / B rows at nearly the same time and L2 serves them.
+            const int cps = p.sync ? (p.n_kchunks + p.sync_every - 1) / p.sync_every : 0;
+            unsigned long long base = 0;
+            for (int tile = pair, w = 0; tile < num_tiles; tile += num_pairs, ++w) {
                 int rp, cb;
                 tile_coords(tile, p.n_row_pairs, p.n_col_blocks, p.group_r, rp, cb);
                 const int arow = rp * PM + static_cast<int>(rank) * BM;
                 const int brow = cb * BN + static_cast<int>(rank) * BNH;
+                const unsigned long long cnt_w = 2ull * min(num_pairs, num_tiles - w * num_pairs);
                 for (int kc = 0; kc < p.n_kchunks; ++kc) {
+                    if (p.sync && kc % p.sync_every == 0) {
+                        atomicAdd(p.sync, 1u);
+                        const unsigned long long target = base + cnt_w * (kc / p.sync_every + 1);
+                        while (ld_acquire_gpu_u32(p.sync) < target) __nanosleep(100);
+                    }
                     mbar_wait(empty + s, ph ^ 1);
                     if (leader) mbar_arrive_expect_tx(full + s, 2 * STAGE);
                     const uint32_t bar = lead(full + s);
@@ -153,6 +170,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kp::THREADS, 1)
                     tma_load_2d_2sm(&tm_blo, bar, dst + 2 * A_BYTES + B_BYTES, kc * BK, brow, pol);
                     if (++s == NS) { s = 0; ph ^= 1; }
                 }
+                base += cnt_w * cps;
             }
         }
       } else if (warp == 1 && leader) {
