@@ -916,7 +916,8 @@ void h2d_staged(DeviceState& ds, void* dst, const void* src, size_t bytes, cudaS
     const int R = static_cast<int>(ds.dring.size());
     const size_t piece = ds.dring_bytes;
     const int hw = std::max(1u, std::thread::hardware_concurrency());
-    SpinTeam team(std::max(1, std::min(16, hw)));
+    const char* lws = std::getenv("LOCAL_WORLD_SIZE");
+    SpinTeam team(std::max(1, std::min(16, hw / (lws ? std::max(1, std::atoi(lws)) : 1))));
     const char* s8 = static_cast<const char*>(src);
     char* d8 = static_cast<char*>(dst);
     for (size_t g = 0, off = 0; off < bytes; ++g, off += piece) {
@@ -969,7 +970,13 @@ void compute_rows_host(lpd_context* ctx, int64_t n, double* G, int64_t ldg, lpd_
         const char* e = std::getenv("LPD_WIDEN_THREADS");
         return e ? std::max(1, std::atoi(e)) : 0;
     }();
-    const int workers = env_workers ? env_workers : std::max(1, std::min(16, hw / nd));
+    // host threads per device: the box's cores shared by this context's devices and, under
+    // torchrun (one process per GPU), by the other local ranks
+    static const int local_ranks = [] {
+        const char* e = std::getenv("LOCAL_WORLD_SIZE");
+        return e ? std::max(1, std::atoi(e)) : 1;
+    }();
+    const int workers = env_workers ? env_workers : std::max(1, std::min(16, hw / (nd * local_ranks)));
     ctx->res_n = 0;
     std::vector<int> resident_ok(nd, 0);
     run_parallel(ctx, [&](DeviceState& ds, int di) {
