@@ -590,7 +590,14 @@ void launch_factor_panels(DeviceState& ds, Slot& s, int64_t m, void* g_dev, int6
         pz.z_lo = ds.z_lo;
         pz.ldz = ds.B_pad;
         pz.group_r = group_r;
-        pz.seg_chunks = seg;
+        // the Z GEMM's K is only d + 1 (33 chunks at C4): segments of 8 chunks keep its
+        // share of the error (C4 full shard 3.0e-5 at 2 or 8, 3.9e-5 unsegmented) with
+        // fewer read-outs (LPD_SEG_Z overrides)
+        static const int seg_z = [] {
+            const char* e = std::getenv("LPD_SEG_Z");
+            return e ? std::max(1, std::atoi(e)) : 8;
+        }();
+        pz.seg_chunks = seg_z;
         // no rendezvous for the Z GEMM: its tiles are short (K = d + 1, 33 chunks at C4)
         // and its operands small; a tile-start wait costs it more (72.7 vs 85.8 % tensor)
         pz.sync = nullptr;
