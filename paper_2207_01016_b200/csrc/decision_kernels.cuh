@@ -138,25 +138,78 @@ namespace lpd {
 //
 // gather_gw: D[i][p] = Σ_j G[rows[i]][j]·W[p][j] (fp64 accumulation), one warp per listed
 //   row, PB weight vectors per pass. Held-out scoring (modelsel.cpp:123-140) and the
-//   reactivation gradients 1 − y_i·G_i·w (dcd.cpp:150-172).
+//   reactivation gradients 1 − y_i·G_i·w (dcd.cpp:150-172). HBM-bound on the G rows:
+//   16-byte streaming loads of G (4 columns per lane, four in flight per lane), W read
+//   as double2 through L1 (it is shared by every row). Per-lane partial sums in column
+//   order, then a fixed warp-shuffle tree: deterministic.
+__device__ __forceinline__ float4 ld_stream_f4(const float4* p) {
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p));
+    return v;
+}
 template <int PB>
-__global__ void gather_gw_kernel(const float* __restrict__ G, long long ldg, int b_eff,
-                                 const int32_t* __restrict__ rows, int count,
-                                 const double* __restrict__ W, int P, int p0,
-                                 double* __restrict__ D) {
+__global__ void __launch_bounds__(256) gather_gw_kernel(const float* __restrict__ G, long long ldg, int b_eff,
+                                                        const int32_t* __restrict__ rows, int count,
+                                                        const double* __restrict__ W, int P, int p0,
+                                                        double* __restrict__ D) {
     const int lane = threadIdx.x & 31;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
     const int np = min(PB, P - p0);
+    // 16-byte path: rows and W rows 16-byte aligned (res_ld and b_eff multiples of 4)
+    const bool vec = ((ldg & 3) == 0) && ((b_eff & 3) == 0) && ((reinterpret_cast<uintptr_t>(G) & 15) == 0) &&
+                     ((reinterpret_cast<uintptr_t>(W) & 15) == 0);
     for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < count; i += nwarps) {
         const float* g = G + static_cast<long long>(rows[i]) * ldg;
         double acc[PB];
 #pragma unroll
         for (int q = 0; q < PB; ++q) acc[q] = 0.0;
-        for (int k = lane; k < b_eff; k += 32) {
-            const double a = static_cast<double>(g[k]);
+        if (vec) {
+            const float4* g4 = reinterpret_cast<const float4*>(g);
+            const int n4 = b_eff >> 2;
+            int k4 = lane;
+            for (; k4 + 96 < n4; k4 += 128) {  // four 16-byte loads in flight per lane
+                float4 v[4];
 #pragma unroll
-            for (int q = 0; q < PB; ++q)
-                if (q < np) acc[q] = fma(a, __ldg(W + static_cast<long long>(p0 + q) * b_eff + k), acc[q]);
+                for (int u = 0; u < 4; ++u) v[u] = ld_stream_f4(g4 + k4 + 32 * u);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+#pragma unroll
+                    for (int q = 0; q < PB; ++q) {
+                        if (q < np) {
+                            const double2* w2 = reinterpret_cast<const double2*>(
+                                W + static_cast<long long>(p0 + q) * b_eff + 4 * (k4 + 32 * u));
+                            const double2 wa = __ldg(w2), wb = __ldg(w2 + 1);
+                            acc[q] = fma(static_cast<double>(v[u].x), wa.x, acc[q]);
+                            acc[q] = fma(static_cast<double>(v[u].y), wa.y, acc[q]);
+                            acc[q] = fma(static_cast<double>(v[u].z), wb.x, acc[q]);
+                            acc[q] = fma(static_cast<double>(v[u].w), wb.y, acc[q]);
+                        }
+                    }
+                }
+            }
+            for (; k4 < n4; k4 += 32) {
+                const float4 v = ld_stream_f4(g4 + k4);
+#pragma unroll
+                for (int q = 0; q < PB; ++q) {
+                    if (q < np) {
+                        const double2* w2 = reinterpret_cast<const double2*>(W + static_cast<long long>(p0 + q) * b_eff + 4 * k4);
+                        const double2 wa = __ldg(w2), wb = __ldg(w2 + 1);
+                        acc[q] = fma(static_cast<double>(v.x), wa.x, acc[q]);
+                        acc[q] = fma(static_cast<double>(v.y), wa.y, acc[q]);
+                        acc[q] = fma(static_cast<double>(v.z), wb.x, acc[q]);
+                        acc[q] = fma(static_cast<double>(v.w), wb.y, acc[q]);
+                    }
+                }
+            }
+        } else {
+            for (int k = lane; k < b_eff; k += 32) {
+                const double a = static_cast<double>(g[k]);
+#pragma unroll
+                for (int q = 0; q < PB; ++q)
+                    if (q < np) acc[q] = fma(a, __ldg(W + static_cast<long long>(p0 + q) * b_eff + k), acc[q]);
+            }
         }
 #pragma unroll
         for (int q = 0; q < PB; ++q) {
@@ -169,21 +222,60 @@ __global__ void gather_gw_kernel(const float* __restrict__ G, long long ldg, int
 }
 
 // gather_gtv, pass 1: partial[g][j] = Σ_{i in row group g} coef[i]·G[rows[i]][j] (fp64),
-//   block = (column slab of 128 × row group); pass 2 sums the partials of each column
-//   in group order, so w = Σ_i coef_i·G_i (rebuild_w, dcd.cpp:91-102) is deterministic.
+//   block = (column slab × row group), each thread 4 consecutive columns (16-byte loads,
+//   eight rows in flight); pass 2 sums the partials of each column in group order, so
+//   w = Σ_i coef_i·G_i (rebuild_w, dcd.cpp:91-102) is deterministic.
 constexpr int GTV_ROWS = 256;   // rows per group
-__global__ void gather_gtv_partial_kernel(const float* __restrict__ G, long long ldg, int b_eff,
-                                          const int32_t* __restrict__ rows,
-                                          const double* __restrict__ coef, int count,
-                                          double* __restrict__ partial) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+constexpr int GTV_THREADS = 128;
+__global__ void __launch_bounds__(GTV_THREADS) gather_gtv_partial_kernel(
+    const float* __restrict__ G, long long ldg, int b_eff, const int32_t* __restrict__ rows,
+    const double* __restrict__ coef, int count, double* __restrict__ partial) {
     const int g = blockIdx.y;
-    if (j >= b_eff) return;
     const int i0 = g * GTV_ROWS, i1 = min(count, i0 + GTV_ROWS);
-    double acc = 0.0;
-    for (int i = i0; i < i1; ++i)
-        acc = fma(coef[i], static_cast<double>(G[static_cast<long long>(rows[i]) * ldg + j]), acc);
-    partial[static_cast<long long>(g) * b_eff + j] = acc;
+    const bool vec = ((ldg & 3) == 0) && ((b_eff & 3) == 0) && ((reinterpret_cast<uintptr_t>(G) & 15) == 0);
+    if (vec) {
+        const int j4 = blockIdx.x * blockDim.x + threadIdx.x;  // column quad
+        if (4 * j4 >= b_eff) return;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        int i = i0;
+        for (; i + 8 <= i1; i += 8) {
+            float4 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                v[u] = ld_stream_f4(reinterpret_cast<const float4*>(G + static_cast<long long>(rows[i + u]) * ldg) + j4);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const double c = coef[i + u];
+                acc[0] = fma(c, static_cast<double>(v[u].x), acc[0]);
+                acc[1] = fma(c, static_cast<double>(v[u].y), acc[1]);
+                acc[2] = fma(c, static_cast<double>(v[u].z), acc[2]);
+                acc[3] = fma(c, static_cast<double>(v[u].w), acc[3]);
+            }
+        }
+        for (; i < i1; ++i) {
+            const float4 v = ld_stream_f4(reinterpret_cast<const float4*>(G + static_cast<long long>(rows[i]) * ldg) + j4);
+            const double c = coef[i];
+            acc[0] = fma(c, static_cast<double>(v.x), acc[0]);
+            acc[1] = fma(c, static_cast<double>(v.y), acc[1]);
+            acc[2] = fma(c, static_cast<double>(v.z), acc[2]);
+            acc[3] = fma(c, static_cast<double>(v.w), acc[3]);
+        }
+        double* out = partial + static_cast<long long>(g) * b_eff + 4 * j4;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) out[e] = acc[e];
+    } else {
+        // scalar path: thread = one column, the grid's x extent covers b_eff / 4 quads,
+        // so each thread handles the 4 columns of its quad in turn
+        const int j4 = blockIdx.x * blockDim.x + threadIdx.x;
+        for (int e = 0; e < 4; ++e) {
+            const int j = 4 * j4 + e;
+            if (j >= b_eff) return;
+            double acc = 0.0;
+            for (int i = i0; i < i1; ++i)
+                acc = fma(coef[i], static_cast<double>(G[static_cast<long long>(rows[i]) * ldg + j]), acc);
+            partial[static_cast<long long>(g) * b_eff + j] = acc;
+        }
+    }
 }
 __global__ void gather_gtv_sum_kernel(const double* __restrict__ partial, int groups, int b_eff,
                                       double* __restrict__ w) {

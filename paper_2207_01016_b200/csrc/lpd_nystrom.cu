@@ -1760,6 +1760,11 @@ int lpd_resident_gw(lpd_context* ctx, const int32_t* rows, int64_t count, const 
                                                                  static_cast<int>(m), dw, static_cast<int>(P),
                                                                  static_cast<int>(p0), dd);
             CUDA_TRY(cudaGetLastError());
+            if (m == count) {  // every listed row on this device, in order: straight into D
+                CUDA_TRY(cudaMemcpyAsync(D, dd, sizeof(double) * m * P, cudaMemcpyDeviceToHost, st));
+                CUDA_TRY(cudaStreamSynchronize(st));
+                return;
+            }
             std::vector<double> hd(static_cast<size_t>(m * P));
             CUDA_TRY(cudaMemcpyAsync(hd.data(), dd, sizeof(double) * m * P, cudaMemcpyDeviceToHost, st));
             CUDA_TRY(cudaStreamSynchronize(st));
@@ -1803,8 +1808,10 @@ int lpd_resident_gtv(lpd_context* ctx, const int32_t* rows, const double* coef, 
             double* dw = reinterpret_cast<double*>(base + off_w);
             CUDA_TRY(cudaMemcpyAsync(drows, local.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, st));
             CUDA_TRY(cudaMemcpyAsync(dc, lc.data(), sizeof(double) * m, cudaMemcpyHostToDevice, st));
-            dim3 grid(static_cast<unsigned>((b_eff + 127) / 128), static_cast<unsigned>(groups));
-            lpd::gather_gtv_partial_kernel<<<grid, 128, 0, st>>>(ds.res_g, ds.res_ld, static_cast<int>(b_eff),
+            // each thread owns 4 consecutive columns
+            dim3 grid(static_cast<unsigned>(((b_eff + 3) / 4 + lpd::GTV_THREADS - 1) / lpd::GTV_THREADS),
+                      static_cast<unsigned>(groups));
+            lpd::gather_gtv_partial_kernel<<<grid, lpd::GTV_THREADS, 0, st>>>(ds.res_g, ds.res_ld, static_cast<int>(b_eff),
                                                                  drows, dc, static_cast<int>(m), dp);
             lpd::gather_gtv_sum_kernel<<<static_cast<int>((b_eff + 255) / 256), 256, 0, st>>>(
                 dp, static_cast<int>(groups), static_cast<int>(b_eff), dw);

@@ -343,12 +343,13 @@ def test_kernel_block_fp64_matches_reference(gpu_ctx, m, n, d, gamma):
         assert np.all(np.diag(K) == 1.0)
 
 
-def test_resident_g_products(gpu_ctx):
+@pytest.mark.parametrize("nb", [300, 301])  # b_eff % 4 == 0: 16-byte path; else scalar path
+def test_resident_g_products(gpu_ctx, nb):
     """K6: G kept resident (fp32, bit-identical to the returned fp64 G) serves the
     held-out scoring G[rows]·Wᵀ and rebuild_w's Σ coef_i·G_i in fp64 on the device."""
     rng = np.random.default_rng(12)
     X = rng.standard_normal((3000, 20)).astype(np.float32).astype(np.float64)
-    Y = X[:300]
+    Y = X[:nb]
     L = np_gaussian_L(Y, 0.05, 1e-10)
     gpu_ctx.set_basis_dense(Y, L, 0.05)
     gpu_ctx.set_keep_resident(True)
@@ -356,7 +357,7 @@ def test_resident_g_products(gpu_ctx):
         G = gpu_ctx.compute_g_dense(X)
         assert gpu_ctx.resident_shape() == (3000, L.shape[1])
         rows = rng.choice(3000, 777, replace=False).astype(np.int32)
-        W = rng.standard_normal((3, L.shape[1]))
+        W = rng.standard_normal((6, L.shape[1]))  # two passes of <= 4 vectors
         D = gpu_ctx.resident_gw(rows, W)
         Dref = G[rows] @ W.T
         assert np.max(np.abs(D - Dref)) <= 1e-12 * np.max(np.abs(Dref))
