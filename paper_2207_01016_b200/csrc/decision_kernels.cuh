@@ -154,69 +154,64 @@ __global__ void __launch_bounds__(256) gather_gw_kernel(const float* __restrict_
                                                         const int32_t* __restrict__ rows, int count,
                                                         const double* __restrict__ W, int P, int p0,
                                                         double* __restrict__ D) {
+    constexpr int RW = 4;  // rows per warp: each W load (L1) serves four rows
     const int lane = threadIdx.x & 31;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
     const int np = min(PB, P - p0);
     // 16-byte path: rows and W rows 16-byte aligned (res_ld and b_eff multiples of 4)
     const bool vec = ((ldg & 3) == 0) && ((b_eff & 3) == 0) && ((reinterpret_cast<uintptr_t>(G) & 15) == 0) &&
                      ((reinterpret_cast<uintptr_t>(W) & 15) == 0);
-    for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < count; i += nwarps) {
-        const float* g = G + static_cast<long long>(rows[i]) * ldg;
-        double acc[PB];
+    for (int i0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * RW; i0 < count; i0 += nwarps * RW) {
+        double acc[RW][PB];
 #pragma unroll
-        for (int q = 0; q < PB; ++q) acc[q] = 0.0;
+        for (int r = 0; r < RW; ++r)
+#pragma unroll
+            for (int q = 0; q < PB; ++q) acc[r][q] = 0.0;
+        const float* g[RW];
+#pragma unroll
+        for (int r = 0; r < RW; ++r) g[r] = G + static_cast<long long>(rows[min(i0 + r, count - 1)]) * ldg;
         if (vec) {
-            const float4* g4 = reinterpret_cast<const float4*>(g);
             const int n4 = b_eff >> 2;
-            int k4 = lane;
-            for (; k4 + 96 < n4; k4 += 128) {  // four 16-byte loads in flight per lane
-                float4 v[4];
+            for (int k4 = lane; k4 < n4; k4 += 32) {
+                float4 v[RW];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) v[u] = ld_stream_f4(g4 + k4 + 32 * u);
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-#pragma unroll
-                    for (int q = 0; q < PB; ++q) {
-                        if (q < np) {
-                            const double2* w2 = reinterpret_cast<const double2*>(
-                                W + static_cast<long long>(p0 + q) * b_eff + 4 * (k4 + 32 * u));
-                            const double2 wa = __ldg(w2), wb = __ldg(w2 + 1);
-                            acc[q] = fma(static_cast<double>(v[u].x), wa.x, acc[q]);
-                            acc[q] = fma(static_cast<double>(v[u].y), wa.y, acc[q]);
-                            acc[q] = fma(static_cast<double>(v[u].z), wb.x, acc[q]);
-                            acc[q] = fma(static_cast<double>(v[u].w), wb.y, acc[q]);
-                        }
-                    }
-                }
-            }
-            for (; k4 < n4; k4 += 32) {
-                const float4 v = ld_stream_f4(g4 + k4);
+                for (int r = 0; r < RW; ++r) v[r] = ld_stream_f4(reinterpret_cast<const float4*>(g[r]) + k4);
 #pragma unroll
                 for (int q = 0; q < PB; ++q) {
                     if (q < np) {
                         const double2* w2 = reinterpret_cast<const double2*>(W + static_cast<long long>(p0 + q) * b_eff + 4 * k4);
                         const double2 wa = __ldg(w2), wb = __ldg(w2 + 1);
-                        acc[q] = fma(static_cast<double>(v.x), wa.x, acc[q]);
-                        acc[q] = fma(static_cast<double>(v.y), wa.y, acc[q]);
-                        acc[q] = fma(static_cast<double>(v.z), wb.x, acc[q]);
-                        acc[q] = fma(static_cast<double>(v.w), wb.y, acc[q]);
+#pragma unroll
+                        for (int r = 0; r < RW; ++r) {
+                            acc[r][q] = fma(static_cast<double>(v[r].x), wa.x, acc[r][q]);
+                            acc[r][q] = fma(static_cast<double>(v[r].y), wa.y, acc[r][q]);
+                            acc[r][q] = fma(static_cast<double>(v[r].z), wb.x, acc[r][q]);
+                            acc[r][q] = fma(static_cast<double>(v[r].w), wb.y, acc[r][q]);
+                        }
                     }
                 }
             }
         } else {
             for (int k = lane; k < b_eff; k += 32) {
-                const double a = static_cast<double>(g[k]);
 #pragma unroll
-                for (int q = 0; q < PB; ++q)
-                    if (q < np) acc[q] = fma(a, __ldg(W + static_cast<long long>(p0 + q) * b_eff + k), acc[q]);
+                for (int q = 0; q < PB; ++q) {
+                    if (q < np) {
+                        const double w = __ldg(W + static_cast<long long>(p0 + q) * b_eff + k);
+#pragma unroll
+                        for (int r = 0; r < RW; ++r) acc[r][q] = fma(static_cast<double>(g[r][k]), w, acc[r][q]);
+                    }
+                }
             }
         }
 #pragma unroll
-        for (int q = 0; q < PB; ++q) {
-            double v = acc[q];
+        for (int r = 0; r < RW; ++r) {
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            if (lane == 0 && q < np) D[static_cast<long long>(i) * P + p0 + q] = v;
+            for (int q = 0; q < PB; ++q) {
+                double v = acc[r][q];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (lane == 0 && q < np && i0 + r < count) D[static_cast<long long>(i0 + r) * P + p0 + q] = v;
+            }
         }
     }
 }

@@ -1737,30 +1737,32 @@ int lpd_resident_gw(lpd_context* ctx, const int32_t* rows, int64_t count, const 
         if (P < 0 || (P > 0 && !W) || (count > 0 && P > 0 && !D)) fail(LPD_ERR_INVALID_ARGUMENT, "bad W / D");
         if (count == 0 || P == 0) return;
         const int64_t b_eff = ctx->res_b_eff;
-        auto parts = split_rows(ctx, rows, count);
+        // one device holding every row: the caller's list is the device's list
+        const bool single = ctx->dev.size() == 1 && ctx->dev[0].res_r0 == 0;
+        auto parts = single ? std::vector<std::vector<std::pair<int32_t, int64_t>>>(1) : split_rows(ctx, rows, count);
         run_parallel(ctx, [&](DeviceState& ds, int di) {
             const auto& part = parts[static_cast<size_t>(di)];
-            if (part.empty()) return;
+            if (!single && part.empty()) return;
             CUDA_TRY(cudaSetDevice(ds.device));
             cudaStream_t st = ds.slot[0].stream;
-            const int64_t m = static_cast<int64_t>(part.size());
+            const int64_t m = single ? count : static_cast<int64_t>(part.size());
             const size_t off_w = round_up(sizeof(int32_t) * m, 256);
             const size_t off_d = off_w + round_up(sizeof(double) * P * b_eff, 256);
             char* base = static_cast<char*>(scratch(ds, off_d + sizeof(double) * m * P));
-            std::vector<int32_t> local(static_cast<size_t>(m));
-            for (int64_t i = 0; i < m; ++i) local[i] = part[i].first;
+            std::vector<int32_t> local(single ? 0 : static_cast<size_t>(m));
+            for (int64_t i = 0; i < static_cast<int64_t>(local.size()); ++i) local[i] = part[i].first;
             int32_t* drows = reinterpret_cast<int32_t*>(base);
             double* dw = reinterpret_cast<double*>(base + off_w);
             double* dd = reinterpret_cast<double*>(base + off_d);
-            CUDA_TRY(cudaMemcpyAsync(drows, local.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, st));
+            CUDA_TRY(cudaMemcpyAsync(drows, single ? rows : local.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, st));
             CUDA_TRY(cudaMemcpyAsync(dw, W, sizeof(double) * P * b_eff, cudaMemcpyHostToDevice, st));
-            const int blocks = static_cast<int>(std::min<int64_t>((m + 7) / 8, static_cast<int64_t>(ds.num_sms) * 16));
+            const int blocks = static_cast<int>(std::min<int64_t>((m + 31) / 32, static_cast<int64_t>(ds.num_sms) * 16));
             for (int64_t p0 = 0; p0 < P; p0 += 4)
                 lpd::gather_gw_kernel<4><<<blocks, 256, 0, st>>>(ds.res_g, ds.res_ld, static_cast<int>(b_eff), drows,
                                                                  static_cast<int>(m), dw, static_cast<int>(P),
                                                                  static_cast<int>(p0), dd);
             CUDA_TRY(cudaGetLastError());
-            if (m == count) {  // every listed row on this device, in order: straight into D
+            if (single || m == count) {  // every listed row on this device, in order: straight into D
                 CUDA_TRY(cudaMemcpyAsync(D, dd, sizeof(double) * m * P, cudaMemcpyDeviceToHost, st));
                 CUDA_TRY(cudaStreamSynchronize(st));
                 return;
@@ -1782,23 +1784,24 @@ int lpd_resident_gtv(lpd_context* ctx, const int32_t* rows, const double* coef, 
         if (count > 0 && !coef) fail(LPD_ERR_INVALID_ARGUMENT, "null coef");
         std::fill(w, w + b_eff, 0.0);
         if (count == 0) return;
-        auto parts = split_rows(ctx, rows, count);
+        const bool single = ctx->dev.size() == 1 && ctx->dev[0].res_r0 == 0;
+        auto parts = single ? std::vector<std::vector<std::pair<int32_t, int64_t>>>(1) : split_rows(ctx, rows, count);
         const int nd = static_cast<int>(ctx->dev.size());
         std::vector<std::vector<double>> partial(nd);
         run_parallel(ctx, [&](DeviceState& ds, int di) {
             const auto& part = parts[static_cast<size_t>(di)];
-            if (part.empty()) return;
+            if (!single && part.empty()) return;
             CUDA_TRY(cudaSetDevice(ds.device));
             cudaStream_t st = ds.slot[0].stream;
-            const int64_t m = static_cast<int64_t>(part.size());
+            const int64_t m = single ? count : static_cast<int64_t>(part.size());
             const int64_t groups = (m + lpd::GTV_ROWS - 1) / lpd::GTV_ROWS;
             const size_t off_c = round_up(sizeof(int32_t) * m, 256);
             const size_t off_p = off_c + round_up(sizeof(double) * m, 256);
             const size_t off_w = off_p + round_up(sizeof(double) * groups * b_eff, 256);
             char* base = static_cast<char*>(scratch(ds, off_w + sizeof(double) * b_eff));
-            std::vector<int32_t> local(static_cast<size_t>(m));
-            std::vector<double> lc(static_cast<size_t>(m));
-            for (int64_t i = 0; i < m; ++i) {
+            std::vector<int32_t> local(single ? 0 : static_cast<size_t>(m));
+            std::vector<double> lc(single ? 0 : static_cast<size_t>(m));
+            for (int64_t i = 0; i < static_cast<int64_t>(local.size()); ++i) {
                 local[i] = part[i].first;
                 lc[i] = coef[part[i].second];
             }
@@ -1806,8 +1809,8 @@ int lpd_resident_gtv(lpd_context* ctx, const int32_t* rows, const double* coef, 
             double* dc = reinterpret_cast<double*>(base + off_c);
             double* dp = reinterpret_cast<double*>(base + off_p);
             double* dw = reinterpret_cast<double*>(base + off_w);
-            CUDA_TRY(cudaMemcpyAsync(drows, local.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, st));
-            CUDA_TRY(cudaMemcpyAsync(dc, lc.data(), sizeof(double) * m, cudaMemcpyHostToDevice, st));
+            CUDA_TRY(cudaMemcpyAsync(drows, single ? rows : local.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, st));
+            CUDA_TRY(cudaMemcpyAsync(dc, single ? coef : lc.data(), sizeof(double) * m, cudaMemcpyHostToDevice, st));
             // each thread owns 4 consecutive columns
             dim3 grid(static_cast<unsigned>(((b_eff + 3) / 4 + lpd::GTV_THREADS - 1) / lpd::GTV_THREADS),
                       static_cast<unsigned>(groups));
