@@ -24,6 +24,13 @@
  * reference's std::vector<Feature> (proj/include/lpdsvm/dataio.hpp:14-24).
  * Functions never throw; they return an LPD_* status and leave a message
  * retrievable with lpd_last_error() (thread-local).
+ *
+ * Threading: a context is used by one host thread at a time (the reference calls
+ * compute_G from a single thread, factor.cpp:131-132; the library runs its own
+ * host threads per device and per delivery inside each call). Calls on different
+ * contexts may run concurrently; the *_device entry points enqueue on the
+ * caller's stream, and two such calls must not run concurrently on different
+ * streams of the same device (the large-d GEMMs rendezvous across their CTAs).
  */
 #ifndef LPD_NYSTROM_H
 #define LPD_NYSTROM_H
