@@ -360,7 +360,11 @@ void build_basis(DeviceState& ds, const double* lm_dev, int64_t B, int64_t d, in
     CUDA_TRY(cudaSetDevice(ds.device));
     // d <= 63: the fused kernel (features + norm column in one 64-wide atom);
     // otherwise the panel path, whose Z GEMM tiles the landmarks 256 at a time.
-    const bool large = d > lpd::KD_MAX - 1;
+    static const int force_panel = [] {  // LPD_FORCE_PANEL=1: the two-GEMM path for any d (studies)
+        const char* e = std::getenv("LPD_FORCE_PANEL");
+        return e ? std::atoi(e) : 0;
+    }();
+    const bool large = d > lpd::KD_MAX - 1 || force_panel;
     const int64_t kd = large ? round_up(d + 1, lpd::kp::BK) : lpd::KD_MAX;
     const int64_t B_pad = round_up(B, large ? lpd::kp::BN : lpd::k1::NC);
     const int64_t Beff_pad = round_up(b_eff, lpd::k1::N2);
