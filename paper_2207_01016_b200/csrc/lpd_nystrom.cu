@@ -797,11 +797,12 @@ private:
         __builtin_ia32_pause();
 #endif
     }
-    // pause iterations before a helper sleeps (LPD_SPIN_LIMIT overrides)
-    static int spin_limit() {
-        static const int v = [] {
-            const char* e = std::getenv("LPD_SPIN_LIMIT");
-            return e ? std::max(0, std::atoi(e)) : 20000;
+    // microseconds a helper spins between items before it sleeps (LPD_SPIN_US overrides;
+    // time-based, since a PAUSE costs ~10-140 cycles depending on the CPU)
+    static int64_t spin_ns() {
+        static const int64_t v = [] {
+            const char* e = std::getenv("LPD_SPIN_US");
+            return static_cast<int64_t>(e ? std::max(0, std::atoi(e)) : 200) * 1000;
         }();
         return v;
     }
@@ -812,9 +813,16 @@ private:
         uint64_t seen = 0;
         for (;;) {
             uint64_t g = gen_.load();
-            for (int k = 0; g == seen && k < spin_limit(); ++k) {
-                cpu_relax();
-                g = gen_.load();
+            if (g == seen) {
+                const auto t0 = std::chrono::steady_clock::now();
+                for (int k = 1; g == seen && !stop_.load(std::memory_order_relaxed); ++k) {
+                    cpu_relax();
+                    g = gen_.load();
+                    if ((k & 63) == 0 &&
+                        std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0)
+                                .count() > spin_ns())
+                        break;
+                }
             }
             if (g == seen) {
                 std::unique_lock<std::mutex> l(mu_);
