@@ -84,6 +84,9 @@ struct FactorParams {
 #endif
 // Profiling ablations (LPD_K1_DEBUG bits 1/2/4/8/32/64) exist only in builds with
 // -DLPD_K1_ABLATIONS=1, so production MMA / epilogue loops carry no per-item tests.
+#ifndef LPD_K1_STORE_HINT
+#define LPD_K1_STORE_HINT 1
+#endif
 #ifndef LPD_K1_ABLATIONS
 #define LPD_K1_ABLATIONS 0
 #endif
@@ -580,6 +583,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
         // interleaved with the next tile's first Z chunks, so the MMA is not left waiting
         // for Z while the epilogue drains (the running sums are next overwritten by the
         // next tile's first segment read-out, which first completes any runs left).
+#if LPD_K1_STORE_HINT
+        const uint64_t g_policy = policy_evict_first();
+#endif
         auto store_part = [&](int tile, int m) {
             if K1_ABL(64) return;  // bypass the stores
             const int cb = tile / p.n_row_tiles;
@@ -624,7 +630,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) {
+#if LPD_K1_STORE_HINT
+                    tma_store_2d_hint(&tm_g, smem + sbuf, gc0 + sl * SLAB, rt * PM + static_cast<int>(rank) * BM + quad * 32,
+                                      g_policy);
+#else
                     tma_store_2d(&tm_g, smem + sbuf, gc0 + sl * SLAB, rt * PM + static_cast<int>(rank) * BM + quad * 32);
+#endif
                     bulk_commit_group();
                 }
             }

@@ -170,6 +170,39 @@ def test_host_pipeline_multi_chunk_bitwise(gpu_ctx, n, d, B):
     torch.cuda.empty_cache()
 
 
+def test_two_shard_context_on_one_gpu(gpu_ctx):
+    """Multi-device host logic on one B200: a context over two device states that
+    share GPU 0 shards the rows (one host thread, stream set and delivery ring per
+    shard, disjoint G row ranges), keeps each shard's G resident, and splits the
+    resident-G products by shard. Rows are independent, so G, the scores and the
+    predictions equal the one-shard context's bitwise; rebuild_w sums per shard first
+    (order differs at the 1e-16 level)."""
+    rng = np.random.default_rng(21)
+    n, d, B = 40_000, 54, 1024
+    X = rng.standard_normal((n, d)).astype(np.float32).astype(np.float64)
+    Y = np.ascontiguousarray(X[rng.choice(n, B, replace=False)])
+    L = np_gaussian_L(Y, 1.0 / d, 1e-10)
+    gpu_ctx.set_basis_dense(Y, L, 1.0 / d)
+    gpu_ctx.set_keep_resident(True)
+    ctx2 = P.Context(device_ids=[0, 0])
+    try:
+        assert ctx2.num_devices == 2
+        ctx2.set_basis_dense(Y, L, 1.0 / d)
+        ctx2.set_keep_resident(True)
+        G1 = gpu_ctx.compute_g_dense(X)
+        G2 = ctx2.compute_g_dense(X)
+        assert np.array_equal(G1, G2)
+        rows = rng.permutation(n)[:9_000].astype(np.int32)  # both shards, shuffled
+        W = rng.standard_normal((5, L.shape[1]))
+        assert np.array_equal(gpu_ctx.resident_gw(rows, W), ctx2.resident_gw(rows, W))
+        coef = rng.standard_normal(rows.size)
+        w1, w2 = gpu_ctx.resident_gtv(rows, coef), ctx2.resident_gtv(rows, coef)
+        assert np.max(np.abs(w1 - w2)) <= 1e-12 * np.max(np.abs(w1))
+    finally:
+        gpu_ctx.set_keep_resident(False)
+        ctx2.close()
+
+
 def test_empty_and_duplicate_points(gpu_ctx):
     rng = np.random.default_rng(4)
     X = rng.standard_normal((260, 12))
