@@ -337,9 +337,18 @@ def main():
     if not args.no_e2e:
         import psutil
 
-        g_bytes = n * b_eff * 8
-        if psutil.virtual_memory().available > 2.5 * g_bytes * max(1, torch.cuda.device_count() if world > 1 else 1):
-            Xh = torch.from_numpy(X).pin_memory()
+        # every local rank holds its own fp64 G in host RAM: at N > 1 on one host the
+        # e2e rows per GPU shrink to what fits (stated in the line), never skipped
+        local_ranks = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
+        budget = psutil.virtual_memory().available / (2.5 * max(1, local_ranks))
+        n_fit = int(budget // (8 * b_eff))
+        n_e2e = n if n_fit >= n else n_fit // 256 * 256
+        if dist:
+            t_n = torch.tensor([n_e2e], dtype=torch.int64, device=dev)
+            dist.all_reduce(t_n, op=dist.ReduceOp.MIN)
+            n_e2e = int(t_n.item())
+        if n_e2e >= 256:
+            Xh = torch.from_numpy(np.ascontiguousarray(X[:n_e2e])).pin_memory()
             Yh = lm_dev.cpu().numpy()
             Lh = L_dev.cpu().numpy()
             Xn = Xh.numpy()
@@ -361,17 +370,19 @@ def main():
                     ts.append(float(dt.item()))
                     tb.append(t1 - t0)
                 # spot-check the host result against the device-path result
-                assert np.array_equal(Gout[:1000], G_dev[:1000].cpu().numpy())
+                k = min(1000, Gout.shape[0])
+                assert np.array_equal(Gout[:k], G_dev[:k].cpu().numpy())
                 return statistics.median(ts), statistics.median(tb)
 
             # the caller's G is ordinary pageable, pre-touched memory, like the
             # reference's zero-filled Matrix (matrix.hpp:15-16)
-            Gn = np.zeros((n, b_eff), dtype=np.float64)
+            Gn = np.zeros((n_e2e, b_eff), dtype=np.float64)
             t_e2e, t_basis = run_e2e(Gn)
-            e2e = {"value": N * n / t_e2e, "unit": UNIT,
-                   "h2d_bytes_per_step": int(X.nbytes + Yh.nbytes + Lh.nbytes),
-                   "d2h_bytes_per_step": int(n * (-(-b_eff // 4) * 4) * 4),
+            e2e = {"value": N * n_e2e / t_e2e, "unit": UNIT,
+                   "h2d_bytes_per_step": int(Xn.nbytes + Yh.nbytes + Lh.nbytes),
+                   "d2h_bytes_per_step": int(n_e2e * (-(-b_eff // 4) * 4) * 4),
                    "seconds_per_step": t_e2e, "basis_seconds_per_step": t_basis,
+                   "rows_per_gpu": n_e2e,
                    "path": "lpd_set_basis_dense + lpd_compute_g_dense: pinned host X -> device; fp32 G -> "
                            "8 MB pinned ring -> host threads widen each buffer (AVX-512 streaming stores) "
                            "into the caller's pageable fp64 G; median of the steps"}
