@@ -30,14 +30,12 @@
 //
 // Segmented G accumulation. The tensor core adds every MMA into the fp32 TMEM
 // accumulator with round-toward-zero; over C2's 768 K-steps per tile that bias alone
-// costs ~2e-4 relative error in G (C3: ~3e-3). GEMM2 is therefore
-// issued as two N=128 halves (TMEM columns [0,128) and [128,256)), and each half's
-// K range is cut into segments of `seg_chunks` chunks: at a segment end the epilogue
-// warps owning that half (they own exactly those 128 TMEM columns) add it into an
-// fp32 round-to-nearest running sum held in registers and release it; the next
-// segment restarts the accumulator from zero. The two halves' segment boundaries are
-// staggered by half a segment, and the MMA issues the other half first at a boundary,
-// so the tensor pipe keeps working while one half is read out.
+// costs ~2e-4 relative error in G (C3: ~3e-3). The K range is therefore
+// cut into segments of `seg_chunks` chunks: at a segment end the epilogue warps (each
+// owns one row × 128 of the 256 accumulator columns) add the accumulator into an fp32
+// round-to-nearest running sum held in registers and release it, and the next segment
+// restarts it from zero; GEMM2 waits for that read-out (~3 % of the kernel at C2; a
+// staggered two-half variant that hides it measured slower).
 //
 // Precision: operands are unevaluated sums hi + lo of two fp16 values after exact
 // power-of-two scaling, and each product is three kind::f16 MMAs (hi·hi + hi·lo +
@@ -63,7 +61,6 @@ struct FactorParams {
     // output G: the tm_g tensor map (TMA store, 16-byte aligned rows; the host stages
     // through an aligned buffer otherwise)
     int seg_chunks;         // chunks per G accumulator segment (>= 1)
-    int split_n;            // 1: GEMM2 as two N=128 halves with staggered segments; 0: one N=256 MMA
     int dbg;                // profiling ablations (LPD_K1_DEBUG), 0 in production
     unsigned long long* dbg_out;  // [2 roles x 8 phases] cycle sums when dbg & 16
 };
@@ -160,9 +157,7 @@ constexpr uint32_t TM_XHI = 448;
 constexpr uint32_t TM_XLO = 480;
 
 constexpr uint32_t IDESC_G1 = idesc_f16_f32(PM, NC);
-constexpr uint32_t IDESC_G2H = idesc_f16_f32(PM, N2 / 2);  // one half of the G tile
-constexpr uint32_t IDESC_G2 = idesc_f16_f32(PM, N2);        // the whole G tile
-constexpr uint32_t LT_HALF = (N2H / 2) * 128;               // bytes of 64 Lᵀ rows (8 swizzle atoms)
+constexpr uint32_t IDESC_G2 = idesc_f16_f32(PM, N2);
 constexpr uint16_t PAIR = 0x3;     // multicast mask: both CTAs of the pair
 
 // Column of K-step k (16 landmarks) of the Z hi / lo planes inside an S/Z buffer.
@@ -172,21 +167,11 @@ constexpr uint16_t PAIR = 0x3;     // multicast mask: both CTAs of the pair
 __device__ __forceinline__ uint32_t z_hi_col(uint32_t k) { return (k >> 1) * 32 + (k & 1) * 8; }
 __device__ __forceinline__ uint32_t z_lo_col(uint32_t k) { return z_hi_col(k) + 16; }
 
-// Segment boundaries of G half h (with split halves, staggered by half a segment).
-// S is a power of two (the host rounds it), so this is a mask, not a division: the
-// MMA warp evaluates it for every chunk and its issue slots are on the critical path.
-__device__ __forceinline__ bool seg_end(int h, int j, int n, int S, int split) {
-    return j == n - 1 || ((j + 1 + h * split * (S >> 1)) & (S - 1)) == 0;
-}
-__device__ __forceinline__ bool seg_start(int h, int j, int n, int S, int split) {
-    return j == 0 || seg_end(h, j - 1, n, S, split);
-}
-// Tile column of running-sum entry e (0..127) of G half h. One N=256 MMA: TMEM
-// columns are tile columns. Split halves: TMEM half h holds 64 Lᵀ rows of each CTA of
-// the pair (CTA r holds tile columns [128r, 128r + 128)).
-__device__ __forceinline__ int half_col(int h, int e, int split) {
-    return split ? (e < 64 ? 0 : 64) + 64 * h + e : 128 * h + e;
-}
+// Segment boundaries (chunk j of n, segments of S chunks). S is a power of two (the
+// host rounds it), so this is a mask, not a division: the MMA warp evaluates it for
+// every chunk and its issue slots are on the critical path.
+__device__ __forceinline__ bool seg_end(int j, int n, int S) { return j == n - 1 || ((j + 1) & (S - 1)) == 0; }
+__device__ __forceinline__ bool seg_start(int j, int n, int S) { return j == 0 || seg_end(j - 1, n, S); }
 }  // namespace k1
 
 template <typename OutT>
@@ -347,69 +332,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
             if (++lm_s == NS_LM) { lm_s = 0; lm_ph ^= 1; }
             ++c1;
         };
-        // GEMM2 of chunk j: G += Z_hi·Lᵀ_hi + Z_lo·Lᵀ_hi + Z_hi·Lᵀ_lo, Z from TMEM, as two
-        // N=128 halves. A half starting a new segment first waits until the epilogue
-        // has read its previous segment, and restarts from zero; the other half is
-        // issued first so the tensor pipe stays busy meanwhile.
-        const int S = p.seg_chunks, n = p.n_chunks, SP = p.split_n;
-        uint32_t hseg[2] = {0, 0};  // segments started per half (acc_empty parity)
+        // GEMM2 of chunk j: G += Z_hi·Lᵀ_hi + Z_lo·Lᵀ_hi + Z_hi·Lᵀ_lo, Z from TMEM, one
+        // N=256 MMA per K-step. At the start of a segment it first waits until the
+        // epilogue has read the previous segment out of both accumulator halves, and
+        // restarts from zero.
+        const int S = p.seg_chunks, n = p.n_chunks;
+        uint32_t nseg = 0;  // segments started (acc_empty parity)
         auto gemm2 = [&](int j) {
             const uint32_t b = c2 % NSZ, ph = (c2 / NSZ) & 1;
             const uint32_t zb = tmem_base + TM_SZ + b * NC;
-            const bool st0 = seg_start(0, j, n, S, SP), st1 = seg_start(1, j, n, S, SP);
-            const int h0 = (st0 && !st1) ? 1 : 0;  // issue order of the halves
+            const bool fresh = seg_start(j, n, S);
             pr.mark(5);
             mbar_wait_cluster(z_full + b, ph);
             pr.mark(2);
             mbar_wait_cluster(lt_full + lt_s, lt_ph);
             pr.mark(3);
+            if (fresh) {
+                pr.mark(5);
+                mbar_wait_cluster(acc_empty + 0, (nseg & 1) ^ 1);
+                mbar_wait_cluster(acc_empty + 1, (nseg & 1) ^ 1);
+                pr.mark(4);
+                ++nseg;
+            }
             tc_fence_after();
-            const uint64_t d_lt = d_lt0 + ((lt_s * LT_BYTES) >> 4);
-            if (!SP) {  // one N=256 MMA per K-step: both halves restart together
-                if (st0) {
-                    pr.mark(5);
-                    mbar_wait_cluster(acc_empty + 0, (hseg[0] & 1) ^ 1);
-                    mbar_wait_cluster(acc_empty + 1, (hseg[1] & 1) ^ 1);
-                    pr.mark(4);
-                    ++hseg[0];
-                    ++hseg[1];
-                    tc_fence_after();
-                }
-                if (elect_one()) {
-                    const uint32_t d = tmem_base + TM_G;
+            if (elect_one()) {
+                const uint64_t d_lt = d_lt0 + ((lt_s * LT_BYTES) >> 4);
+                const uint32_t d = tmem_base + TM_G;
 #pragma unroll
-                    for (int k = 0; k < NC / 16; ++k)
-                        if (!K1_ABL(4)) mma_f16_ts_2sm(d, zb + z_hi_col(k), d_lt + 2 * k, IDESC_G2, !(st0 && k == 0));
+                for (int k = 0; k < NC / 16; ++k)
+                    if (!K1_ABL(4)) mma_f16_ts_2sm(d, zb + z_hi_col(k), d_lt + 2 * k, IDESC_G2, !(fresh && k == 0));
 #pragma unroll
-                    for (int k = 0; k < NC / 16; ++k)
-                        if (!K1_ABL(4)) mma_f16_ts_2sm(d, zb + z_lo_col(k), d_lt + 2 * k, IDESC_G2, 1);
-                }
-                __syncwarp();
+                for (int k = 0; k < NC / 16; ++k)
+                    if (!K1_ABL(4)) mma_f16_ts_2sm(d, zb + z_lo_col(k), d_lt + 2 * k, IDESC_G2, 1);
+                mma_commit_2sm_mc(lt_empty + lt_s, PAIR);
             }
-#pragma unroll
-            for (int q = 0; q < 2 * SP; ++q) {
-                const int h = h0 ^ q;
-                const bool fresh = h ? st1 : st0;
-                if (fresh) {
-                    pr.mark(5);
-                    mbar_wait_cluster(acc_empty + h, (hseg[h] & 1) ^ 1);
-                    pr.mark(4);
-                    ++hseg[h];
-                    tc_fence_after();
-                }
-                if (elect_one()) {
-                    const uint32_t d = tmem_base + TM_G + h * (N2 / 2);
-                    const uint64_t bh = d_lt + ((h * LT_HALF) >> 4);
-#pragma unroll
-                    for (int k = 0; k < NC / 16; ++k)
-                        if (!K1_ABL(4)) mma_f16_ts_2sm(d, zb + z_hi_col(k), bh + 2 * k, IDESC_G2H, !(fresh && k == 0));
-#pragma unroll
-                    for (int k = 0; k < NC / 16; ++k)
-                        if (!K1_ABL(4)) mma_f16_ts_2sm(d, zb + z_lo_col(k), bh + 2 * k, IDESC_G2H, 1);
-                }
-                __syncwarp();
-            }
-            if (elect_one()) mma_commit_2sm_mc(lt_empty + lt_s, PAIR);
             __syncwarp();
             if (++lt_s == NS_LT) { lt_s = 0; lt_ph ^= 1; }
             pr.mark(5);
@@ -417,26 +373,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
             pr.mark(3);
             tc_fence_after();
             if (elect_one()) {
-                const uint64_t d_lt2 = d_lt0 + ((lt_s * LT_BYTES) >> 4);
-                if (SP) {
+                const uint64_t d_lt = d_lt0 + ((lt_s * LT_BYTES) >> 4);
 #pragma unroll
-                    for (int q = 0; q < 2; ++q) {
-                        const int h = h0 ^ q;
-                        const uint32_t d = tmem_base + TM_G + h * (N2 / 2);
-                        const uint64_t bh = d_lt2 + ((h * LT_HALF) >> 4);
-#pragma unroll
-                        for (int k = 0; k < NC / 16; ++k)
-                            if (!K1_ABL(4)) mma_f16_ts_2sm(d, zb + z_hi_col(k), bh + 2 * k, IDESC_G2H, 1);
-                    }
-                } else {
-#pragma unroll
-                    for (int k = 0; k < NC / 16; ++k)
-                        if (!K1_ABL(4)) mma_f16_ts_2sm(tmem_base + TM_G, zb + z_hi_col(k), d_lt2 + 2 * k, IDESC_G2, 1);
-                }
+                for (int k = 0; k < NC / 16; ++k)
+                    if (!K1_ABL(4)) mma_f16_ts_2sm(tmem_base + TM_G, zb + z_hi_col(k), d_lt + 2 * k, IDESC_G2, 1);
                 mma_commit_2sm_mc(lt_empty + lt_s, PAIR);
                 mma_commit_2sm(sz_empty + b);
-                if (seg_end(0, j, n, S, SP)) mma_commit_2sm_mc(acc_full + 0, PAIR);
-                if (seg_end(1, j, n, S, SP)) mma_commit_2sm_mc(acc_full + 1, PAIR);
+                if (seg_end(j, n, S)) {
+                    mma_commit_2sm_mc(acc_full + 0, PAIR);
+                    mma_commit_2sm_mc(acc_full + 1, PAIR);
+                }
             }
             __syncwarp();
             if (++lt_s == NS_LT) { lt_s = 0; lt_ph ^= 1; }
@@ -473,7 +419,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
         uint32_t cnt = 0, stg_k = 0;
         PhaseProbe pr((p.dbg & 16) != 0);
         const uint32_t x_full_l = lead(x_full), acc_empty_l = lead(acc_empty + half), z_full_l = lead(z_full);
-        const int S = p.seg_chunks, n = p.n_chunks, SP = p.split_n;
+        const int S = p.seg_chunks, n = p.n_chunks;
         float rs[128];      // fp32 round-to-nearest running sum of this thread's G row, TMEM half `half`
         uint32_t fseg = 0;  // segments of this half read so far (acc_full parity)
 
@@ -591,7 +537,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
             const int cb = tile / p.n_row_tiles;
             const int rt = tile - cb * p.n_row_tiles;
             constexpr int SLAB = 128 / sizeof(OutT);  // columns per 128-byte staging row
-            const int c0 = half_col(half, m * 32, SP);
+            const int c0 = half * 128 + m * 32;
             const int gc0 = cb * N2 + c0;
             if (gc0 >= p.b_eff || K1_ABL(2)) return;
             const float4* cs4 = reinterpret_cast<const float4*>(p.col_scale + gc0);
@@ -673,7 +619,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
             for (int j = 0; j < n; ++j) {
                 // the segment that ended with GEMM2(j - 2) is complete by the time
                 // GEMM1(j) (issued after it) has produced S(j)
-                if (!LPD_K1_NOSEG && j >= 2 && seg_end(half, j - 2, n, S, SP)) {
+                if (!LPD_K1_NOSEG && j >= 2 && seg_end(j - 2, n, S)) {
                     if (first) store_all();
                     flush(first);
                     first = false;
@@ -689,7 +635,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
                 }
                 store_some();
             }
-            if (!LPD_K1_NOSEG && n >= 2 && seg_end(half, n - 2, n, S, SP)) {
+            if (!LPD_K1_NOSEG && n >= 2 && seg_end(n - 2, n, S)) {
                 if (first) store_all();
                 flush(first);
                 first = false;

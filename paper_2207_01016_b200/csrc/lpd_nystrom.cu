@@ -691,11 +691,6 @@ void launch_factor(DeviceState& ds, Slot& s, const double* x_dev, int64_t m, int
     p.row_aux = s.raux;
     p.col_scale = ds.col_scale;
     p.seg_chunks = seg_chunks(ds.B_pad > 4096 ? 2 : 4);
-    static const int split_n = [] {
-        const char* e = std::getenv("LPD_K1_SPLIT");
-        return e ? (std::atoi(e) != 0) : 0;
-    }();
-    p.split_n = split_n;
     static const int dbg = [] {
         const char* e = std::getenv("LPD_K1_DEBUG");
         return e ? std::atoi(e) : 0;
