@@ -147,7 +147,7 @@ constexpr uint32_t OFF_STG = OFF_LT + NS_LT * LT_BYTES;             // warp w, b
 constexpr uint32_t X_BYTES = BM * KD * 2;           // 16 KB: one X plane of this CTA's rows
 constexpr uint32_t OFF_X = OFF_STG + EPI_WARPS * NSTG * STG_BYTES;  // hi, lo
 constexpr uint32_t OFF_BAR = OFF_X + 2 * X_BYTES;
-constexpr uint32_t NUM_BARS = 6 + 2 * NS_LM + 2 * NS_LT + 3 * NSZ + 2;
+constexpr uint32_t NUM_BARS = 4 + 2 * NS_LM + 2 * NS_LT + 3 * NSZ + 2;
 constexpr uint32_t SMEM_BYTES = OFF_BAR + NUM_BARS * 8 + 16 + 1024;  // + alignment slack
 
 constexpr uint32_t TMEM_COLS = 512;
@@ -200,9 +200,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
     uint64_t* s_full = lt_empty + NS_LT;
     uint64_t* z_full = s_full + NSZ;
     uint64_t* sz_empty = z_full + NSZ;
-    uint64_t* acc_full = sz_empty + NSZ;  // [2] G half h: segment complete (MMA commit)
-    uint64_t* acc_empty = acc_full + 2;   // [2] G half h: segment read into the running sums
-    uint64_t* xs_full = acc_empty + 2;    // X tile landed in SMEM (TMA)
+    uint64_t* acc_full = sz_empty + NSZ;  // G segment complete (MMA commit)
+    uint64_t* acc_empty = acc_full + 1;   // G segment read into the running sums (all epilogue warps)
+    uint64_t* xs_full = acc_empty + 1;    // X tile landed in SMEM (TMA)
     uint64_t* xs_empty = xs_full + 1;  // X tile copied from SMEM into TMEM
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NUM_BARS);
 
@@ -225,7 +225,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
             mbar_init(z_full + b, 2 * EPI_WARPS);
             mbar_init(sz_empty + b, 1);
         }
-        for (int h = 0; h < 2; ++h) { mbar_init(acc_full + h, 1); mbar_init(acc_empty + h, EPI_WARPS); }
+        mbar_init(acc_full, 1);
+        mbar_init(acc_empty, 2 * EPI_WARPS);
         mbar_init(xs_full, 1);
         mbar_init(xs_empty, EPI_WARPS);
         fence_mbar_init();
@@ -349,8 +350,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
             pr.mark(3);
             if (fresh) {
                 pr.mark(5);
-                mbar_wait_cluster(acc_empty + 0, (nseg & 1) ^ 1);
-                mbar_wait_cluster(acc_empty + 1, (nseg & 1) ^ 1);
+                mbar_wait_cluster(acc_empty, (nseg & 1) ^ 1);
                 pr.mark(4);
                 ++nseg;
             }
@@ -379,10 +379,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
                     if (!K1_ABL(4)) mma_f16_ts_2sm(tmem_base + TM_G, zb + z_hi_col(k), d_lt + 2 * k, IDESC_G2, 1);
                 mma_commit_2sm_mc(lt_empty + lt_s, PAIR);
                 mma_commit_2sm(sz_empty + b);
-                if (seg_end(j, n, S)) {
-                    mma_commit_2sm_mc(acc_full + 0, PAIR);
-                    mma_commit_2sm_mc(acc_full + 1, PAIR);
-                }
+                if (seg_end(j, n, S)) mma_commit_2sm_mc(acc_full, PAIR);
             }
             __syncwarp();
             if (++lt_s == NS_LT) { lt_s = 0; lt_ph ^= 1; }
@@ -418,16 +415,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
         const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
         uint32_t cnt = 0, stg_k = 0;
         PhaseProbe pr((p.dbg & 16) != 0);
-        const uint32_t x_full_l = lead(x_full), acc_empty_l = lead(acc_empty + half), z_full_l = lead(z_full);
+        const uint32_t x_full_l = lead(x_full), acc_empty_l = lead(acc_empty), z_full_l = lead(z_full);
         const int S = p.seg_chunks, n = p.n_chunks;
         float rs[128];      // fp32 round-to-nearest running sum of this thread's G row, TMEM half `half`
-        uint32_t fseg = 0;  // segments of this half read so far (acc_full parity)
+        uint32_t fseg = 0;  // segments read so far (acc_full parity)
 
         // One finished segment of this warp's G half: TMEM -> registers, added into the
         // running sums (the first segment of a tile initialises them), then released.
         auto flush = [&](bool first) {
             pr.mark(7);
-            mbar_wait_cluster(acc_full + half, fseg & 1);
+            mbar_wait_cluster(acc_full, fseg & 1);
             pr.mark(5);
             tc_fence_after();
             // two TMEM round trips of 64 columns (register budget: 128 sums + 64 loaded)
