@@ -174,7 +174,9 @@ __device__ __forceinline__ bool seg_end(int j, int n, int S) { return j == n - 1
 __device__ __forceinline__ bool seg_start(int j, int n, int S) { return j == 0 || seg_end(j - 1, n, S); }
 }  // namespace k1
 
-template <typename OutT>
+// KS1 = ceil((d + 1) / 16), the K-steps of GEMM1 (1..4): a compile-time count, so the
+// MMA warp's GEMM1 issue is fully unrolled (its issue slots are on the critical path).
+template <typename OutT, int KS1>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
     nystrom_factor_kernel(const __grid_constant__ CUtensorMap tm_xhi,
                           const __grid_constant__ CUtensorMap tm_xlo,
@@ -322,7 +324,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
                 for (int pass = 0; pass < 3; ++pass) {
                     const uint32_t a = tmem_base + ((pass == 2) ? TM_XLO : TM_XHI);
                     const uint64_t bb = (pass == 1) ? d_lmlo : d_lmhi;
-                    for (int k = 0; k < p.ksteps1; ++k)
+#pragma unroll
+                    for (int k = 0; k < KS1; ++k)
                         if (!K1_ABL(8)) mma_f16_ts_2sm(d, a + 8 * k, bb + 2 * k, IDESC_G1, (pass | k) != 0);
                 }
                 mma_commit_2sm_mc(lm_empty + lm_s, PAIR);

@@ -285,6 +285,18 @@ void ensure_slot(DeviceState& ds, Slot& s, int64_t rows, bool need_g, int64_t nn
     }
 }
 
+using FactorKernel = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap,
+                              CUtensorMap, lpd::FactorParams);
+// K1 instance for the output type and GEMM1's K-step count (ceil((d + 1) / 16), 1..4)
+FactorKernel factor_kernel_for(bool f64, int ks1) {
+    switch (ks1) {
+        case 1: return f64 ? lpd::nystrom_factor_kernel<double, 1> : lpd::nystrom_factor_kernel<float, 1>;
+        case 2: return f64 ? lpd::nystrom_factor_kernel<double, 2> : lpd::nystrom_factor_kernel<float, 2>;
+        case 3: return f64 ? lpd::nystrom_factor_kernel<double, 3> : lpd::nystrom_factor_kernel<float, 3>;
+        default: return f64 ? lpd::nystrom_factor_kernel<double, 4> : lpd::nystrom_factor_kernel<float, 4>;
+    }
+}
+
 void init_device(DeviceState& ds, int device) {
     ds.device = device;
     CUDA_TRY(cudaSetDevice(device));
@@ -305,10 +317,12 @@ void init_device(DeviceState& ds, int device) {
     CUDA_TRY(cudaMemset(ds.err, 0, sizeof(int)));
     for (auto& pr : ds.ring)
         for (auto& e : pr) CUDA_TRY(cudaEventCreate(&e));
-    CUDA_TRY(cudaFuncSetAttribute(lpd::nystrom_factor_kernel<double>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, lpd::k1::SMEM_BYTES));
-    CUDA_TRY(cudaFuncSetAttribute(lpd::nystrom_factor_kernel<float>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, lpd::k1::SMEM_BYTES));
+    for (int ks = 1; ks <= 4; ++ks) {
+        CUDA_TRY(cudaFuncSetAttribute(factor_kernel_for(true, ks), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      lpd::k1::SMEM_BYTES));
+        CUDA_TRY(cudaFuncSetAttribute(factor_kernel_for(false, ks), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      lpd::k1::SMEM_BYTES));
+    }
     // Load every kernel now (CUDA lazy loading would otherwise charge the first call of
     // each one): context creation runs in the background when the adapter loads.
     {
@@ -714,12 +728,8 @@ void launch_factor(DeviceState& ds, Slot& s, const double* x_dev, int64_t m, int
     }
     const CUtensorMap tm_xhi = make_plane_map(s.xhi, m_pad, lpd::KD_MAX, lpd::k1::BM, 64);
     const CUtensorMap tm_xlo = make_plane_map(s.xlo, m_pad, lpd::KD_MAX, lpd::k1::BM, 64);
-    if (out_dtype == LPD_OUT_F64)
-        lpd::nystrom_factor_kernel<double><<<grid, lpd::k1::THREADS, lpd::k1::SMEM_BYTES, st>>>(
-            tm_xhi, tm_xlo, ds.tm_lmhi, ds.tm_lmlo, ds.tm_lthi, ds.tm_ltlo, tm_g, p);
-    else
-        lpd::nystrom_factor_kernel<float><<<grid, lpd::k1::THREADS, lpd::k1::SMEM_BYTES, st>>>(
-            tm_xhi, tm_xlo, ds.tm_lmhi, ds.tm_lmlo, ds.tm_lthi, ds.tm_ltlo, tm_g, p);
+    factor_kernel_for(out_dtype == LPD_OUT_F64, p.ksteps1)<<<grid, lpd::k1::THREADS, lpd::k1::SMEM_BYTES, st>>>(
+        tm_xhi, tm_xlo, ds.tm_lmhi, ds.tm_lmlo, ds.tm_lthi, ds.tm_ltlo, tm_g, p);
     if (dbg & 16) {
         unsigned long long h[16];
         CUDA_TRY(cudaMemcpyAsync(h, dbg_out, sizeof(h), cudaMemcpyDeviceToHost, st));
