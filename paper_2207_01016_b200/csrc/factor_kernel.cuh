@@ -430,13 +430,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
             mbar_wait_cluster(acc_full, fseg & 1);
             pr.mark(5);
             tc_fence_after();
-            // two TMEM round trips of 64 columns (register budget: 128 sums + 64 loaded)
-#pragma unroll
-            for (int m = 0; m < 4; m += 2) {
-                uint32_t v[2][32];
-                tmem_ld_32x32b_x32(tmem_base + lane_off + TM_G + half * 128 + m * 32, v[0]);
-                tmem_ld_32x32b_x32(tmem_base + lane_off + TM_G + half * 128 + (m + 1) * 32, v[1]);
-                tmem_wait_ld();
+            // two TMEM round trips of 64 columns (register budget: 128 sums + 64 loaded);
+            // the accumulator is released as soon as the second load has landed, before
+            // its additions, so GEMM2's wait does not include them
+            auto accumulate = [&](int m, const uint32_t (&v)[2][32]) {
 #pragma unroll
                 for (int q = 0; q < 2; ++q) {
                     if (first) {
@@ -447,10 +444,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
                         for (int i = 0; i < 32; ++i) rs[(m + q) * 32 + i] += __uint_as_float(v[q][i]);
                     }
                 }
-            }
+            };
+            uint32_t v[2][32];
+            tmem_ld_32x32b_x32(tmem_base + lane_off + TM_G + half * 128, v[0]);
+            tmem_ld_32x32b_x32(tmem_base + lane_off + TM_G + half * 128 + 32, v[1]);
+            tmem_wait_ld();
+            accumulate(0, v);
+            tmem_ld_32x32b_x32(tmem_base + lane_off + TM_G + half * 128 + 64, v[0]);
+            tmem_ld_32x32b_x32(tmem_base + lane_off + TM_G + half * 128 + 96, v[1]);
+            tmem_wait_ld();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(acc_empty_l);
+            accumulate(2, v);
             ++fseg;
         };
 
