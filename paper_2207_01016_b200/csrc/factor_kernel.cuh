@@ -125,25 +125,25 @@ constexpr int N2 = 256;        // G columns per tile (UMMA N of GEMM2)
 constexpr int N2H = 128;       // Lᵀ rows per tile held by one CTA
 constexpr int NS_LM = 4;       // landmark-chunk stages
 #ifndef LPD_K1_NS_LT
-#define LPD_K1_NS_LT 6
+#define LPD_K1_NS_LT 3
 #endif
 #ifndef LPD_K1_NSTG
 #define LPD_K1_NSTG 2
 #endif
-constexpr int NS_LT = LPD_K1_NS_LT;  // Lᵀ half-chunk stages (hi and lo travel separately)
+constexpr int NS_LT = LPD_K1_NS_LT;  // Lᵀ chunk stages (hi and lo planes of one chunk share a stage)
 constexpr int NSZ = 3;         // S/Z TMEM buffers
 constexpr int EPI_WARPS = 8;
 constexpr int THREADS = 128 + 32 * EPI_WARPS;
 constexpr int Z13 = 13;        // Z is carried as Z·2^13 in fp16
 
 constexpr uint32_t LM_BYTES = NCH * KD * 2;          // 4 KB per hi/lo plane (this CTA's half)
-constexpr uint32_t LT_BYTES = N2H * NC * 2;          // 16 KB per stage (this CTA's half)
+constexpr uint32_t LT_BYTES = N2H * NC * 2;          // 16 KB per plane (this CTA's half)
 constexpr uint32_t STG_BYTES = 32 * 128;             // 4 KB G staging buffer
 constexpr int NSTG = LPD_K1_NSTG;                    // staging buffers per epilogue warp
 
 constexpr uint32_t OFF_LM = 0;                                      // stage s: hi, lo
 constexpr uint32_t OFF_LT = OFF_LM + NS_LM * 2 * LM_BYTES;          // stage s
-constexpr uint32_t OFF_STG = OFF_LT + NS_LT * LT_BYTES;             // warp w, buffer k
+constexpr uint32_t OFF_STG = OFF_LT + NS_LT * 2 * LT_BYTES;         // warp w, buffer k
 constexpr uint32_t X_BYTES = BM * KD * 2;           // 16 KB: one X plane of this CTA's rows
 constexpr uint32_t OFF_X = OFF_STG + EPI_WARPS * NSTG * STG_BYTES;  // hi, lo
 constexpr uint32_t OFF_BAR = OFF_X + 2 * X_BYTES;
@@ -276,7 +276,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
             }
         }
       } else if (warp == 3) {
-        // ============ TMA producer: this CTA's half of the tile's Lᵀ rows, per half-chunk ============
+        // ============ TMA producer: this CTA's half of the tile's Lᵀ rows, hi and lo per chunk ============
         if (lane == 0) {
             const uint64_t keep = policy_evict_last();
             uint32_t lt_s = 0, lt_ph = 0;
@@ -284,14 +284,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
                 const int cb = tile / p.n_row_tiles;
                 const int row = cb * N2 + static_cast<int>(rank) * N2H;
                 for (int j = 0; j < p.n_chunks; ++j) {
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        mbar_wait_cluster(lt_empty + lt_s, lt_ph ^ 1);
-                        if (leader) mbar_arrive_expect_tx(lt_full + lt_s, 2 * LT_BYTES);
-                        tma_load_2d_2sm(h ? &tm_ltlo : &tm_lthi, lead(lt_full + lt_s),
-                                        smem + OFF_LT + lt_s * LT_BYTES, j * NC, row, keep);
-                        if (++lt_s == NS_LT) { lt_s = 0; lt_ph ^= 1; }
-                    }
+                    mbar_wait_cluster(lt_empty + lt_s, lt_ph ^ 1);
+                    if (leader) mbar_arrive_expect_tx(lt_full + lt_s, 2 * 2 * LT_BYTES);
+                    const uint32_t bar = lead(lt_full + lt_s);
+                    uint8_t* dst = smem + OFF_LT + lt_s * 2 * LT_BYTES;
+                    tma_load_2d_2sm(&tm_lthi, bar, dst, j * NC, row, keep);
+                    tma_load_2d_2sm(&tm_ltlo, bar, dst + LT_BYTES, j * NC, row, keep);
+                    if (++lt_s == NS_LT) { lt_s = 0; lt_ph ^= 1; }
                 }
             }
         }
@@ -359,27 +358,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
             }
             tc_fence_after();
             if (elect_one()) {
-                const uint64_t d_lt = d_lt0 + ((lt_s * LT_BYTES) >> 4);
+                const uint64_t d_lthi = d_lt0 + ((lt_s * 2 * LT_BYTES) >> 4);
+                const uint64_t d_ltlo = d_lthi + (LT_BYTES >> 4);
                 const uint32_t d = tmem_base + TM_G;
 #pragma unroll
                 for (int k = 0; k < NC / 16; ++k)
-                    if (!K1_ABL(4)) mma_f16_ts_2sm(d, zb + z_hi_col(k), d_lt + 2 * k, IDESC_G2, !(fresh && k == 0));
+                    if (!K1_ABL(4)) mma_f16_ts_2sm(d, zb + z_hi_col(k), d_lthi + 2 * k, IDESC_G2, !(fresh && k == 0));
 #pragma unroll
                 for (int k = 0; k < NC / 16; ++k)
-                    if (!K1_ABL(4)) mma_f16_ts_2sm(d, zb + z_lo_col(k), d_lt + 2 * k, IDESC_G2, 1);
-                mma_commit_2sm_mc(lt_empty + lt_s, PAIR);
-            }
-            __syncwarp();
-            if (++lt_s == NS_LT) { lt_s = 0; lt_ph ^= 1; }
-            pr.mark(5);
-            mbar_wait_cluster(lt_full + lt_s, lt_ph);
-            pr.mark(3);
-            tc_fence_after();
-            if (elect_one()) {
-                const uint64_t d_lt = d_lt0 + ((lt_s * LT_BYTES) >> 4);
+                    if (!K1_ABL(4)) mma_f16_ts_2sm(d, zb + z_lo_col(k), d_lthi + 2 * k, IDESC_G2, 1);
 #pragma unroll
                 for (int k = 0; k < NC / 16; ++k)
-                    if (!K1_ABL(4)) mma_f16_ts_2sm(tmem_base + TM_G, zb + z_hi_col(k), d_lt + 2 * k, IDESC_G2, 1);
+                    if (!K1_ABL(4)) mma_f16_ts_2sm(d, zb + z_hi_col(k), d_ltlo + 2 * k, IDESC_G2, 1);
                 mma_commit_2sm_mc(lt_empty + lt_s, PAIR);
                 mma_commit_2sm(sz_empty + b);
                 if (seg_end(j, n, S)) mma_commit_2sm_mc(acc_full, PAIR);
