@@ -14,7 +14,7 @@
 //   warp 0     TMA producer: landmark half-chunks (hi/lo planes)       [both CTAs]
 //   warp 1     MMA issuer (one elected lane)                            [leader CTA]
 //   warp 2     TMEM allocator (cta_group::2)                            [both CTAs]
-//   warp 3     TMA producer: Lᵀ half-chunks of the tile's column block [both CTAs]
+//   warp 3     TMA producer: Lᵀ chunks (hi + lo) of the tile's column block [both CTAs]
 //   warps 4-11 epilogue: X → TMEM; S → Z (in place, TMEM); G segments → fp32
 //              running sums in registers; G → SMEM → TMA store
 // Barriers the MMA waits on live in the leader CTA (TMA bytes and epilogue arrivals
