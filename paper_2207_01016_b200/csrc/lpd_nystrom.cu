@@ -187,6 +187,7 @@ struct DeviceState {
     __half* z_hi = nullptr;    // large path: Z panel scratch [z_rows × B_pad]
     __half* z_lo = nullptr;
     int64_t z_rows = 0;
+    int host_share = 1;                // device states of this context sharing the host's cores
     unsigned int* sync_ctr = nullptr;  // panel GEMM K-progress rendezvous counters [kSyncCtrs]
     static constexpr int kSyncCtrs = 64;
     int sync_seq = 0;
@@ -941,7 +942,7 @@ void h2d_staged(DeviceState& ds, void* dst, const void* src, size_t bytes, cudaS
     const size_t piece = ds.dring_bytes;
     const int hw = std::max(1u, std::thread::hardware_concurrency());
     const char* lws = std::getenv("LOCAL_WORLD_SIZE");
-    SpinTeam team(std::max(1, std::min(16, hw / (lws ? std::max(1, std::atoi(lws)) : 1))));
+    SpinTeam team(std::max(1, std::min(16, hw / (ds.host_share * (lws ? std::max(1, std::atoi(lws)) : 1)))));
     const char* s8 = static_cast<const char*>(src);
     char* d8 = static_cast<char*>(dst);
     for (size_t g = 0, off = 0; off < bytes; ++g, off += piece) {
@@ -1298,7 +1299,10 @@ int lpd_context_create(lpd_context** out, int num_devices) {
         auto* ctx = new lpd_context();
         try {
             ctx->dev.resize(want);
-            for (int i = 0; i < want; ++i) init_device(ctx->dev[i], i);
+            for (int i = 0; i < want; ++i) {
+                init_device(ctx->dev[i], i);
+                ctx->dev[i].host_share = want;
+            }
         } catch (...) {
             lpd_context_destroy(ctx);
             throw;
@@ -1320,7 +1324,10 @@ int lpd_context_create_devices(lpd_context** out, const int* device_ids, int cou
         auto* ctx = new lpd_context();
         try {
             ctx->dev.resize(count);
-            for (int i = 0; i < count; ++i) init_device(ctx->dev[i], device_ids[i]);
+            for (int i = 0; i < count; ++i) {
+                init_device(ctx->dev[i], device_ids[i]);
+                ctx->dev[i].host_share = count;
+            }
         } catch (...) {
             lpd_context_destroy(ctx);
             throw;
