@@ -356,15 +356,17 @@ def main():
             def run_e2e(Gout):
                 ctx.set_basis_dense(Yh, Lh, cfg.gamma)
                 ctx.compute_g_dense(Xn, out=Gout)  # warm-up (also first-touches Gout)
-                ts, tb = [], []
+                ts, tb, tm = [], [], []
                 for _ in range(args.e2e_steps):
                     if dist:
                         dist.barrier()
                     t0 = time.perf_counter()
                     ctx.set_basis_dense(Yh, Lh, cfg.gamma)
                     t1 = time.perf_counter()
-                    ctx.compute_g_dense(Xn, out=Gout)
+                    tmg = P.Timings()
+                    ctx.compute_g_dense(Xn, out=Gout, timings=tmg)
                     dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+                    tm.append(tmg.as_dict())
                     if dist:
                         dist.all_reduce(dt, op=dist.ReduceOp.MAX)
                     ts.append(float(dt.item()))
@@ -372,17 +374,23 @@ def main():
                 # spot-check the host result against the device-path result
                 k = min(1000, Gout.shape[0])
                 assert np.array_equal(Gout[:k], G_dev[:k].cpu().numpy())
-                return statistics.median(ts), statistics.median(tb)
+                mid = sorted(range(len(ts)), key=lambda i: ts[i])[len(ts) // 2]
+                return statistics.median(ts), statistics.median(tb), tm[mid]
 
             # the caller's G is ordinary pageable, pre-touched memory, like the
             # reference's zero-filled Matrix (matrix.hpp:15-16)
             Gn = np.zeros((n_e2e, b_eff), dtype=np.float64)
-            t_e2e, t_basis = run_e2e(Gn)
+            t_e2e, t_basis, phases = run_e2e(Gn)
             e2e = {"value": N * n_e2e / t_e2e, "unit": UNIT,
                    "h2d_bytes_per_step": int(Xn.nbytes + Yh.nbytes + Lh.nbytes),
                    "d2h_bytes_per_step": int(n_e2e * (-(-b_eff // 4) * 4) * 4),
                    "seconds_per_step": t_e2e, "basis_seconds_per_step": t_basis,
                    "rows_per_gpu": n_e2e,
+                   # the median step's library timings: D2H stream busy time, the host team's
+                   # widening time, the factor launches (CUDA events) — they overlap
+                   "phases": {"d2h_seconds": phases["d2h_seconds"], "d2h_gbs": n_e2e * (-(-b_eff // 4) * 4) * 4 / max(phases["d2h_seconds"], 1e-9) / 1e9,
+                              "host_widen_seconds": phases["host_copy_seconds"], "kernel_seconds": phases["kernel_seconds"],
+                              "library_seconds": phases["total_seconds"]},
                    "path": "lpd_set_basis_dense + lpd_compute_g_dense: pinned host X -> device; fp32 G -> "
                            "8 MB pinned ring -> host threads widen each buffer (AVX-512 streaming stores) "
                            "into the caller's pageable fp64 G; median of the steps"}
