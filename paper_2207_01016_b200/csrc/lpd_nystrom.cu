@@ -1,15 +1,18 @@
 // liblpd_nystrom.so — host runtime behind include/lpd_nystrom.h.
 //
 // Owns one DeviceState per GPU of a context: the replicated basis (landmark
-// split planes, Lᵀ split planes, TMA descriptors), two pipeline slots with
-// their own streams, and the launch logic for K2/K3 (prep_kernels.cuh), K1
-// (factor_kernel.cuh) and K4 (decision_kernels.cuh).
+// split planes, Lᵀ split planes, TMA descriptors), two compute slots with their
+// own streams, the delivery ring (pinned buffers + stream), the resident G, and
+// the launch logic for K2/K3 (prep_kernels.cuh), K1 (factor_kernel.cuh), the
+// large-d panel GEMMs (panel_kernels.cuh), K5-K7 (decision_kernels.cuh,
+// gram_kernels.cuh).
 //
 // Host-row calls (lpd_compute_g_*) shard rows contiguously across devices
 // (reference compute_G splits rows into chunks, proj/src/factor.cpp:97-108;
-// here each device owns a contiguous shard, no collective) and pipeline
-// H2D → prep → factor → D2H in row chunks on two streams per device, one host
-// thread per device. Errors never escape as exceptions: every entry point
+// here each device owns a contiguous shard, no collective), compute ~512 MB row
+// chunks on alternating slots, and deliver G through 8 MB pinned sub-chunks that
+// a host team widens to fp64 in the caller's buffer (compute_rows_host), one
+// host thread per device. Errors never escape as exceptions: every entry point
 // returns a status and records a message (lpd_last_error).
 #include <cuda.h>
 #include <cuda_runtime.h>
