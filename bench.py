@@ -233,12 +233,20 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test-only: every rank on GPU 0 with gloo collectives, to exercise the N > 1 code
+    # path on a one-GPU machine (numbers meaningless; never used for measurements)
+    one_gpu_test = os.environ.get("LPD_BENCH_ONE_GPU_TEST") == "1"
+    if one_gpu_test:
+        local = 0
     dist = None
     if world > 1:
         import torch.distributed as dist
 
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu_test:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     from paper_2207_01016_b200 import synthetic
 
