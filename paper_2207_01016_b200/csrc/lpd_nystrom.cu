@@ -212,6 +212,7 @@ struct DeviceState {
     // in, each widened into the caller's fp64 G right after it lands (still in the
     // CPU's last-level cache), on their own stream
     cudaStream_t dstream = nullptr;
+    cudaStream_t dstream2 = nullptr;  // second D2H stream (LPD_D2H_STREAMS=2)
     std::vector<float*> dring;
     std::vector<cudaEvent_t> dring_ev;
     size_t dring_bytes = 0;
@@ -871,6 +872,15 @@ void widen_rows(SpinTeam& team, const float* src, int64_t lds, double* dst, int6
 // Measured on the B200 box (scripts/host_pipe_probe.cu): 8 MB x 6 reaches the PCIe
 // D2H rate (~110 GB/s of fp64 output) where 128 MB chunks reach ~75 GB/s, because
 // each buffer is widened while it is still in the CPU's last-level cache.
+// D2H streams of the delivery (LPD_D2H_STREAMS: 1 or 2; sub-chunks alternate)
+int d2h_streams() {
+    static const int v = [] {
+        const char* e = std::getenv("LPD_D2H_STREAMS");
+        return (e && std::atoi(e) == 2) ? 2 : 1;
+    }();
+    return v;
+}
+
 void ensure_delivery_ring(DeviceState& ds) {
     static const size_t mb = [] {
         const char* e = std::getenv("LPD_RING_MB");
@@ -881,6 +891,7 @@ void ensure_delivery_ring(DeviceState& ds) {
         return e ? std::max(2, std::atoi(e)) : 6;
     }();
     if (!ds.dstream) CUDA_TRY(cudaStreamCreateWithFlags(&ds.dstream, cudaStreamNonBlocking));
+    if (d2h_streams() == 2 && !ds.dstream2) CUDA_TRY(cudaStreamCreateWithFlags(&ds.dstream2, cudaStreamNonBlocking));
     if (ds.dring_bytes == (mb << 20) && static_cast<int>(ds.dring.size()) == slots) return;
     for (float* b : ds.dring) cudaFreeHost(b);
     ds.dring.clear();
@@ -1086,18 +1097,27 @@ void compute_rows_host(lpd_context* ctx, int64_t n, double* G, int64_t ldg, lpd_
         auto enqueue = [&](size_t g) {
             const Sub& u = subs[g];
             Slot& s = ds.slot[u.k & 1];
+            const bool two = ds.dstream2 != nullptr;
+            cudaStream_t ds_g = (two && (g & 1)) ? ds.dstream2 : ds.dstream;
             if (u.first) {
                 // compute one chunk ahead of the delivery
                 while (computed <= u.k + 1 && computed < nchunks) compute(computed++);
                 CUDA_TRY(cudaStreamWaitEvent(ds.dstream, s.ev[2], 0));
+                if (two) CUDA_TRY(cudaStreamWaitEvent(ds.dstream2, s.ev[2], 0));
                 CUDA_TRY(cudaEventRecord(s.ev[3], ds.dstream));
             }
             const float* src = gdst(u.k) + (u.r0 - (r_begin + u.k * chunk)) * g_ld;
             CUDA_TRY(cudaMemcpyAsync(ds.dring[g % R], src, sizeof(float) * static_cast<size_t>(u.rows * g_ld),
-                                     cudaMemcpyDeviceToHost, ds.dstream));
-            CUDA_TRY(cudaEventRecord(ds.dring_ev[g % R], ds.dstream));
+                                     cudaMemcpyDeviceToHost, ds_g));
+            CUDA_TRY(cudaEventRecord(ds.dring_ev[g % R], ds_g));
             if (u.last) {
-                CUDA_TRY(cudaEventRecord(s.ev[4], ds.dstream));
+                // ev[5] ("chunk drained") must cover the copies on both streams
+                if (two) {
+                    CUDA_TRY(cudaEventRecord(s.ev[4], ds.dstream2));
+                    CUDA_TRY(cudaStreamWaitEvent(ds.dstream, s.ev[4], 0));
+                } else {
+                    CUDA_TRY(cudaEventRecord(s.ev[4], ds.dstream));
+                }
                 CUDA_TRY(cudaEventRecord(s.ev[5], ds.dstream));
             }
         };
@@ -1115,6 +1135,7 @@ void compute_rows_host(lpd_context* ctx, int64_t n, double* G, int64_t ldg, lpd_
             if (g + R < subs.size()) enqueue(g + R);
         }
         CUDA_TRY(cudaStreamSynchronize(ds.dstream));
+        if (ds.dstream2) CUDA_TRY(cudaStreamSynchronize(ds.dstream2));
         for (int64_t k = std::max<int64_t>(0, nchunks - 2); k < nchunks; ++k) {
             h2d[di] += elapsed(ds.slot[k & 1].ev[0], ds.slot[k & 1].ev[1]);
             ker[di] += elapsed(ds.slot[k & 1].ev[1], ds.slot[k & 1].ev[2]);
@@ -1364,6 +1385,7 @@ int lpd_context_destroy(lpd_context* ctx) {
         for (float* b : ds.dring) cudaFreeHost(b);
         for (auto& e : ds.dring_ev) cudaEventDestroy(e);
         if (ds.dstream) cudaStreamDestroy(ds.dstream);
+        if (ds.dstream2) cudaStreamDestroy(ds.dstream2);
         for (auto& pr : ds.ring)
             for (auto& e : pr)
                 if (e) cudaEventDestroy(e);
