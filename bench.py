@@ -398,7 +398,9 @@ def main():
                    # widening time, the factor launches (CUDA events) — they overlap
                    "phases": {"d2h_seconds": phases["d2h_seconds"], "d2h_gbs": n_e2e * (-(-b_eff // 4) * 4) * 4 / max(phases["d2h_seconds"], 1e-9) / 1e9,
                               "host_widen_seconds": phases["host_copy_seconds"], "kernel_seconds": phases["kernel_seconds"],
-                              "library_seconds": phases["total_seconds"]},
+                              "library_seconds": phases["total_seconds"],
+                              # share of the serial sum (D2H + widen + kernels) hidden by overlap
+                              "overlap": 1.0 - phases["total_seconds"] / max(1e-9, phases["d2h_seconds"] + phases["host_copy_seconds"] + phases["kernel_seconds"])},
                    "path": "lpd_set_basis_dense + lpd_compute_g_dense: pinned host X -> device; fp32 G -> "
                            "8 MB pinned ring -> host threads widen each buffer (AVX-512 streaming stores) "
                            "into the caller's pageable fp64 G; median of the steps"}
