@@ -97,6 +97,9 @@ def ref_lib() -> ctypes.CDLL:
         lib.ref_factor_free.argtypes = [ctypes.c_void_p]
         lib.ref_vote.argtypes = [_dp, ctypes.c_int64, ctypes.c_int64]
         lib.ref_vote.restype = ctypes.c_int
+        lib.ref_solve_binary.argtypes = [ctypes.c_int64, ctypes.c_int64, _dp, _dp, ctypes.c_double,
+                                         ctypes.c_double, ctypes.c_int64, ctypes.c_int, ctypes.c_uint64,
+                                         ctypes.c_uint64, _dp, _dp, _dp, _dp]
         _ref = lib
     return _ref
 
@@ -291,3 +294,26 @@ def ref_build_L(landmarks, gamma: float, tau: float = 1e-12, threads: int = 1) -
 def ref_vote(decisions: np.ndarray, num_classes: int) -> int:
     d = np.ascontiguousarray(decisions, np.float64)
     return int(ref_lib().ref_vote(_p(d), d.shape[0], int(num_classes)))
+
+
+def ref_solve_binary(G: np.ndarray, y: np.ndarray, C: float = 1.0, eps: float = 1e-3,
+                     max_epochs: int = 1000, shrinking: bool = True, seed: int = 1,
+                     problem_tag: int = 0, warm_alpha: Optional[np.ndarray] = None) -> dict:
+    """The reference's make_binary_problem + solve_binary (dcd.cpp:60-89, 212-259) over all
+    rows of G: alpha, w and the SolveReport (dual objective D(alpha) = sum(alpha) - |w|^2/2,
+    dcd.cpp:104-108)."""
+    G = np.ascontiguousarray(G, np.float64)
+    y = np.ascontiguousarray(y, np.float64)
+    n, b = G.shape
+    alpha = np.empty(n)
+    w = np.empty(b)
+    rep = np.empty(6)
+    wa = None if warm_alpha is None else np.ascontiguousarray(warm_alpha, np.float64)
+    rc = ref_lib().ref_solve_binary(n, b, _p(G), _p(y), float(C), float(eps), int(max_epochs),
+                                    int(bool(shrinking)), int(seed), int(problem_tag),
+                                    None if wa is None else _p(wa), _p(alpha), _p(w), _p(rep))
+    if rc != 0:
+        raise (ValueError if rc == 1 else RuntimeError)(_ref_err())
+    return {"alpha": alpha, "w": w, "dual_objective": float(rep[0]), "epochs": int(rep[1]),
+            "visits": int(rep[2]), "final_violation": float(rep[3]), "converged": bool(rep[4]),
+            "shrunk_peak": int(rep[5])}

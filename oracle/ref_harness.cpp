@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "lpdsvm/dataio.hpp"
+#include "lpdsvm/dcd.hpp"
 #include "lpdsvm/factor.hpp"
 #include "lpdsvm/kernel.hpp"
 #include "lpdsvm/multiclass.hpp"
@@ -210,6 +211,42 @@ __attribute__((visibility("default"))) int ref_vote(const double* decisions, int
                                                     int64_t num_classes) {
     return vote(std::span<const double>(decisions, static_cast<size_t>(num_pairs)),
                 static_cast<size_t>(num_classes));
+}
+
+// dcd.cpp:60-89 (make_binary_problem) + dcd.cpp:212-259 (solve_binary) over every row of
+// a caller-given G (n x b_eff, row-major): the reference's stage-2 solver, unchanged, so
+// the downstream effect of a G from another implementation can be measured with the
+// solver held fixed. report6 = {dual_objective, epochs, coordinate_visits,
+// final_violation, converged, shrunk_peak}.
+__attribute__((visibility("default"))) int ref_solve_binary(
+    int64_t n, int64_t b_eff, const double* G, const double* y, double C, double eps,
+    int64_t max_epochs, int shrinking, uint64_t seed, uint64_t problem_tag,
+    const double* warm_alpha, double* alpha_out, double* w_out, double* report6) {
+    return guard([&] {
+        Matrix Gm(static_cast<size_t>(n), static_cast<size_t>(b_eff));
+        std::memcpy(Gm.data(), G, sizeof(double) * static_cast<size_t>(n * b_eff));
+        std::vector<int> rows(static_cast<size_t>(n));
+        for (int64_t i = 0; i < n; ++i) rows[static_cast<size_t>(i)] = static_cast<int>(i);
+        BinaryProblem problem =
+            make_binary_problem(Gm, std::move(rows), std::vector<double>(y, y + n), C);
+        SolveOptions opt;
+        opt.eps = eps;
+        opt.max_epochs = max_epochs;
+        opt.shrinking = shrinking != 0;
+        opt.seed = seed;
+        opt.problem_tag = problem_tag;
+        std::span<const double> warm;
+        if (warm_alpha) warm = std::span<const double>(warm_alpha, static_cast<size_t>(n));
+        SolveResult r = solve_binary(problem, Gm, opt, warm);
+        std::memcpy(alpha_out, r.alpha.data(), sizeof(double) * r.alpha.size());
+        std::memcpy(w_out, r.w.data(), sizeof(double) * r.w.size());
+        report6[0] = r.report.dual_objective;
+        report6[1] = static_cast<double>(r.report.epochs);
+        report6[2] = static_cast<double>(r.report.coordinate_visits);
+        report6[3] = r.report.final_violation;
+        report6[4] = r.report.converged ? 1.0 : 0.0;
+        report6[5] = static_cast<double>(r.report.shrunk_peak);
+    });
 }
 
 }  // extern "C"

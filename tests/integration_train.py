@@ -42,7 +42,7 @@ def main():
     ap.add_argument("--gamma", type=float, default=0.05)
     ap.add_argument("--C", type=float, default=1.0)
     ap.add_argument("--classes", type=int, default=2)
-    ap.add_argument("--threads", type=int, default=4)
+    ap.add_argument("--threads", type=int, default=4, help="0 = all host threads")
     ap.add_argument("--tau", type=float, default=1e-6)
     ap.add_argument("--seed", type=int, default=11)
     ap.add_argument("--train-only", action="store_true", help="train + predict only (timing runs)")
@@ -109,6 +109,7 @@ def main():
                "test_error": float(np.mean(pred2 != y[args.n:])), **{k: stats2[k] for k in stats2}}
         with open(args.out, "w") as f:
             json.dump(out, f)
+        np.save(args.out + ".pred.npy", pred2)
         print(json.dumps(out))
         return
     dv = model.decision_values(test)

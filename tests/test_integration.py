@@ -104,3 +104,26 @@ def test_reference_api_on_gpu_matches_reference(tmp_path, classes):
     dv_g, dv_r = g["dv"], r["dv"]
     err = np.max(np.abs(dv_g - dv_r)) / max(1e-12, np.max(np.abs(dv_r)))
     assert err <= 2e-2, err
+
+
+@pytest.mark.gpu
+def test_c1_train_through_reference_api(tmp_path):
+    """BASELINE.json config 1 end to end through the reference's own `lpdsvm.train`
+    (n=20,000 d=50 B=1,000 γ=0.02 C=1, τ=1e-12 default, landmarks seed 1): the GPU build
+    (factor, landmark Gram, solver sweeps and prediction on the B200) against the
+    unmodified reference build. Test error within ±0.1 pp on 10,000
+    held-out rows, ≥ 99.5 % identical predictions, same effective rank."""
+    import json
+
+    args = ["--n", "20000", "--n-test", "10000", "--d", "50", "--budget", "1000", "--gamma", "0.02",
+            "--C", "1", "--tau", "1e-12", "--seed", "1", "--threads", "0", "--train-only"]
+    _run(INTEG, str(tmp_path / "gpu.json"), *args)
+    _run(REF, str(tmp_path / "ref.json"), *args)
+    g = json.load(open(tmp_path / "gpu.json"))
+    r = json.load(open(tmp_path / "ref.json"))
+    assert g["effective_rank"] == r["effective_rank"] == 1000
+    assert abs(g["test_error"] - r["test_error"]) * 100 <= 0.1, (g["test_error"], r["test_error"])
+    pg = np.load(str(tmp_path / "gpu.json") + ".pred.npy")
+    pr = np.load(str(tmp_path / "ref.json") + ".pred.npy")
+    assert float(np.mean(pg == pr)) >= 0.995
+    assert g["unconverged_pairs"] == r["unconverged_pairs"] == 0
