@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the drop-in e2e, the train-seconds runs and the C4 shard record")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU-baseline sample time")
     return ap.parse_args()
 
@@ -201,7 +203,7 @@ def run_reference(args, cfg, rank):
     Y, L = make_basis(X, cfg, device="cuda" if torch.cuda.is_available() else None)
     threads = O.ref_lib().ref_hardware_threads()
     # size each step so warmup + steps stay within a few minutes
-    per_step = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    per_step = max(2.0, min(20.0, 100.0 / max(1, args.steps + args.warmup)))
     rate, rows, secs = cpu_reference_rate(X, Y, L, cfg.gamma, per_step, threads, n)
     ycsr = O.dense_to_csr(Y)
     xs = O.dense_to_csr(X[:rows])
@@ -222,6 +224,12 @@ def run_reference(args, cfg, rank):
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
                          "sample": f"{rows} contiguous rows of the {n}-row workload per step, chunk_size={chunk}"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        # the reference's compute_G above IS its drop-in API (squared_norms + compute_G into a
+        # fresh Matrix, oracle/ref_harness.cpp ref_compute_g): same number
+        "e2e_dropin": {"value": value, "unit": UNIT, "seconds_per_step": sum(ts) / len(ts), "rows": rows,
+                       "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        # lpdsvm.train's train_impl (module.cpp:35-78) on the unmodified reference build
+        "train_seconds": None if args.no_extras else {c: e2e_train("ref", c) for c in ("c1", "c2")},
     }
     print(json.dumps(line), flush=True)
 
@@ -264,8 +272,110 @@ def main():
     torch.cuda.set_device(dev)
     n = args.rows or synthetic.rows_per_gpu(cfg)
     N = world
-    # weak scaling: this rank's rows of an N·n-row dataset
-    X, _ = synthetic.make(cfg, rows=slice(rank * n, (rank + 1) * n), n=N * n)
+    res = measure(args, cfg, n, N, rank, local, dist, dev, P, args.steps, args.warmup, not args.no_e2e)
+
+    cpu = dropin = trains = c4 = None
+    if rank == 0 and N == 1:
+        if not args.no_cpu_baseline:
+            from oracle import oracle as O
+
+            if O.ref_available():
+                threads = O.ref_lib().ref_hardware_threads()
+                rate, rows, secs = cpu_reference_rate(res["X"], res["Y"], res["L"], cfg.gamma, args.cpu_seconds,
+                                                      threads, n)
+                cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
+                       "sample": f"{rows} contiguous rows of the {n}-row workload, same landmarks/L, "
+                                 f"{secs:.1f}s, chunk_size={max(64, -(-rows // threads))}"}
+        if not args.no_extras:
+            dropin = e2e_dropin("b200", cfg, res, n)
+            trains = {c: e2e_train("b200", c) for c in ("c1", "c2")}
+            if args.workload != "c4":
+                c4cfg = synthetic.CONFIGS["c4"]
+                r4 = measure(args, c4cfg, synthetic.rows_per_gpu(c4cfg), 1, 0, local, None, dev, P,
+                             max(2, min(args.steps, 5)), 3, not args.no_e2e)
+                c4 = {"workload": c4cfg.name, "value": r4["value"], "unit": UNIT, "n_per_gpu": r4["n"],
+                      "d": c4cfg.d, "B": r4["B"], "b_eff": r4["b_eff"], "gamma": c4cfg.gamma,
+                      "ms_per_step": r4["ms_per_step"], "steps": r4["steps"],
+                      "path": "panel path: Z GEMM + projection GEMM (d >= 64)",
+                      "roofline": r4["roofline"], "e2e": r4["e2e"], "clocks": r4["clocks"]}
+                del r4
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": N, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "f16x3 split operands, f32 accumulate, f64 G",
+            "data": (f"synthetic ({'1000-class non-negative ImageNet-feature-shaped' if cfg.classes > 2 else 'two-class Gaussian blobs'}"
+                     f", seed {cfg.seed}; landmarks drawn like the reference select_landmarks, L from eigh(K))"),
+            "config": {"workload": cfg.name, "n_per_gpu": n, "d": cfg.d, "B": res["B"], "b_eff": res["b_eff"],
+                       "gamma": cfg.gamma, "parallelism": f"rows sharded over {N} GPU(s), basis broadcast",
+                       "path": "fused K1 (d <= 63)" if cfg.d <= 63 else "panel path: Z GEMM + projection GEMM (d >= 64)",
+                       "l2": f"inputs larger than L2 (G {n * res['b_eff'] * 8 / 1e9:.1f} GB/step per GPU written, "
+                             f"X {res['X'].nbytes / 1e9:.2f} GB read)"},
+            "roofline": res["roofline"],
+            "cpu_baseline": cpu,
+            "e2e": res["e2e"],
+            # the reference's own C++ API (compute_G with SparseVector rows into a fresh
+            # Matrix, the gmatrix stage of factor.cpp:129-133) on the drop-in build
+            "e2e_dropin": dropin,
+            # lpdsvm.train's train_impl (module.cpp:35-78) end to end on the drop-in build
+            "train_seconds": trains,
+            "c4_shard": c4,
+            "gpu_launches": launches_per_step(n, cfg.d, res["B"]) * args.steps,
+            "clocks": res["clocks"],
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def _run_e2e_subprocess(argv, timeout):
+    """integration/e2e_run.py in its own process (the two builds define the same C++
+    symbols); returns its JSON or an error record."""
+    cmd = [sys.executable, os.path.join(ROOT, "integration", "e2e_run.py"), *argv]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout)
+    except subprocess.TimeoutExpired:
+        return {"error": f"timeout after {timeout}s"}
+    if r.returncode != 0:
+        return {"error": (r.stderr or r.stdout).strip().splitlines()[-1:] or ["rc != 0"]}
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+def e2e_dropin(build, cfg, res, rows):
+    """The gmatrix stage through the reference's compute_G signature (SparseVector rows,
+    a fresh Matrix per call) on `build`, with the bench's landmarks and L."""
+    import tempfile
+
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "basis.npz")
+        np.savez(path, Y=res["Y"], L=res["L"], gamma=cfg.gamma, workload=cfg.name,
+                 **({"G_sample": res["G_sample"]} if res.get("G_sample") is not None else {}))
+        out = _run_e2e_subprocess([build, "compute_g", path, "--rows", str(rows)], 900)
+    if "error" in out:
+        return out
+    b_eff = out["b_eff"]
+    return {"value": out["rows_per_s"], "unit": UNIT, "seconds_per_step": out["gmatrix_seconds"],
+            "compute_G_seconds": out["compute_G_seconds"], "rows": out["rows"], "steps": out["steps"],
+            "h2d_bytes_per_step": int(rows * cfg.d * 12 + res["B"] * cfg.d * 12 + res["B"] * b_eff * 8),
+            "d2h_bytes_per_step": int(rows * (-(-b_eff // 4) * 4) * 4),
+            "sample_max_row_rel_diff_vs_device_path": out.get("sample_max_row_rel_diff"),
+            "path": "lpdsvm::squared_norms + lpdsvm::compute_G (factor.hpp:52-55) with std::vector<Feature> rows "
+                    "into a fresh lpdsvm::Matrix (adapter -> C ABI -> B200), median of the steps"}
+
+
+def e2e_train(build, config):
+    return _run_e2e_subprocess([build, "train", config, "--n-test", "10000" if config == "c1" else "20000"], 1500)
+
+
+def measure(args, cfg, n, N, rank, local, dist, dev, P, steps, warmup, want_e2e):
+    """Device value (inputs resident in HBM), the factor kernel's roofline and the C-ABI
+    e2e for one workload; rank r owns rows [r·n, (r+1)·n) of an N·n-row dataset."""
+    import torch
+
+    X, _ = synthetic_rows(cfg, rank, n, N)
     if rank == 0:
         Y, L = make_basis(X, cfg, device=dev)
         meta = torch.tensor([Y.shape[0], L.shape[1]], dtype=torch.int64, device=dev)
@@ -292,7 +402,7 @@ def main():
         ctx.set_basis_device(lm_dev, L_dev, cfg.gamma, stream=stream)
         ctx.compute_g_device(X_dev, G_dev, stream=stream)
 
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step()
     torch.cuda.synchronize(dev)
     ctx.factor_kernel_stats(reset=True)
@@ -303,7 +413,7 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
         e0.record(stream)
-        for _ in range(args.steps):
+        for _ in range(steps):
             step()
         e1.record(stream)
         torch.cuda.synchronize(dev)
@@ -317,7 +427,7 @@ def main():
     k_total_ms, k_launches = ctx.factor_kernel_stats(reset=True)
     k_ms = k_total_ms / max(1, k_launches)
 
-    value = N * n * args.steps / (elapsed_ms / 1e3)
+    value = N * n * steps / (elapsed_ms / 1e3)
     F = 2.0 * n * B * cfg.d + 2.0 * n * B * b_eff
     peaks = load_peaks()
     achieved = F / (k_ms / 1e3) / 1e12
@@ -339,10 +449,17 @@ def main():
         bpad = -(-B // 256) * 256
         kd = -(-(cfg.d + 1) // 64) * 64
         issued = 3 * (2.0 * npad * bpad * kd + 2.0 * npad * bpad * epad)
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "kernel_ms": k_ms, "flops_per_launch": F, "issued_tensor_flops_per_launch": issued,
+                "issued_frac": issued / (k_ms / 1e3) / 1e12 / peak,
+                "peak_source": peak_src, "peak_burst": peaks["burst"],
+                "frac_of_burst": achieved / peaks["burst"]}
 
     # ---------------- end to end through the C ABI with host buffers ----------------
     e2e = None
-    if not args.no_e2e:
+    G_sample = G_dev[: min(256, n)].cpu().numpy()
+    if want_e2e:
         import psutil
 
         # every local rank holds its own fp64 G in host RAM: at N > 1 on one host the
@@ -408,48 +525,19 @@ def main():
         else:
             e2e = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                    "skipped": "host RAM too small for a pinned fp64 G of this workload"}
-
-    cpu = None
-    if rank == 0 and N == 1 and not args.no_cpu_baseline:
-        from oracle import oracle as O
-
-        if O.ref_available():
-            threads = O.ref_lib().ref_hardware_threads()
-            rate, rows, secs = cpu_reference_rate(X, lm_dev.cpu().numpy(), L_dev.cpu().numpy(), cfg.gamma,
-                                                  args.cpu_seconds, threads, n)
-            cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
-                   "sample": f"{rows} contiguous rows of the {n}-row workload, same landmarks/L, "
-                             f"{secs:.1f}s, chunk_size={max(64, -(-rows // threads))}"}
-
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None,
-            "dtype": "f16x3 split operands, f32 accumulate, f64 G",
-            "data": (f"synthetic ({'1000-class non-negative ImageNet-feature-shaped' if cfg.classes > 2 else 'two-class Gaussian blobs'}"
-                     f", seed {cfg.seed}; landmarks drawn like the reference select_landmarks, L from eigh(K))"),
-            "config": {"workload": cfg.name, "n_per_gpu": n, "d": cfg.d, "B": B, "b_eff": b_eff,
-                       "gamma": cfg.gamma, "parallelism": f"rows sharded over {N} GPU(s), basis broadcast",
-                       "path": "fused K1 (d <= 63)" if cfg.d <= 63 else "panel path: Z GEMM + projection GEMM (d >= 64)",
-                       "l2": f"inputs larger than L2 (G {n * b_eff * 8 / 1e9:.1f} GB/step per GPU written, "
-                             f"X {X.nbytes / 1e9:.2f} GB read)"},
-            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "kernel_ms": k_ms, "flops_per_launch": F, "issued_tensor_flops_per_launch": issued,
-                         "issued_frac": issued / (k_ms / 1e3) / 1e12 / peak,
-                         "peak_source": peak_src, "peak_burst": peaks["burst"],
-                         "frac_of_burst": achieved / peaks["burst"]},
-            "cpu_baseline": cpu,
-            "e2e": e2e,
-            "gpu_launches": launches_per_step(n, cfg.d, B) * args.steps,
-            "clocks": clocks.summary(),
-        }
-        print(json.dumps(line), flush=True)
+    out = {"value": value, "ms_per_step": elapsed_ms / steps, "steps": steps, "n": n, "B": B, "b_eff": b_eff,
+           "roofline": roofline, "e2e": e2e, "clocks": clocks.summary(), "X": X,
+           "Y": lm_dev.cpu().numpy(), "L": L_dev.cpu().numpy(), "G_sample": G_sample}
     ctx.close()
-    if dist:
-        dist.barrier()
-        dist.destroy_process_group()
+    del X_dev, G_dev, lm_dev, L_dev
+    torch.cuda.empty_cache()
+    return out
+
+
+def synthetic_rows(cfg, rank, n, N):
+    from paper_2207_01016_b200 import synthetic
+
+    return synthetic.make(cfg, rows=slice(rank * n, (rank + 1) * n), n=N * n)
 
 
 if __name__ == "__main__":

@@ -17,7 +17,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 @pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref is built where /root/reference exists")
 def test_reference_arm_json_line():
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--workload", "c1",
-                          "--rows", "2048", "--steps", "1", "--warmup", "1"],
+                          "--rows", "2048", "--steps", "1", "--warmup", "1", "--no-extras"],
                          capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-2000:]
     lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
@@ -42,3 +42,24 @@ def test_issued_work_and_launch_counts():
     assert bench.launches_per_step(581_012, 54, 4096) == 8          # K2 (6) + K3 + K1
     # C4 panel path: 7 prep launches + Z and projection GEMMs per <= 2 GB Z panel
     assert bench.launches_per_step(160_146, 2048, 16_384) == 7 + 2 * 5
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref is built where /root/reference exists")
+def test_e2e_harness_reference_train_c1():
+    """integration/e2e_run.py (bench.py's train_seconds) over the reference build at C1."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "integration", "e2e_run.py"), "ref", "train", "c1"],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    j = json.loads(out.stdout.strip().splitlines()[-1])
+    assert j["b_eff"] == 1000 and j["unconverged_pairs"] == 0
+    assert 0.14 < j["test_error"] < 0.18  # Bayes error of the C1 blobs is Φ(−1) ≈ 15.9 %
+    assert j["train_seconds"] >= j["gmatrix_seconds"] + j["training_seconds"]
+
+
+def test_e2e_harness_b200_build_links_the_adapter():
+    so = os.path.join(ROOT, "integration", "_build", "libe2e_b200.so")
+    if not os.path.exists(so):
+        pytest.skip("integration build needs /root/reference at build time")
+    syms = subprocess.run(["nm", "-D", so], capture_output=True, text=True).stdout
+    assert "T e2e_train" in syms and "T e2e_compute_g" in syms
+    assert "U lpd_compute_g_csr" in syms  # compute_G is the adapter's, over the C ABI
