@@ -136,6 +136,38 @@ int lpd_predict_ovo_csr(lpd_context* ctx, int64_t n, int64_t d, const int64_t* i
                         const int32_t* indices, const double* values, int64_t num_classes,
                         int32_t* classes);
 
+/* Per-point decision values of a trained one-vs-one model (K8): replaces
+ * lpdsvm::decision_values (proj/include/lpdsvm/multiclass.hpp:84-86,
+ * proj/src/multiclass.cpp:137-151), which Python Model.decision_values calls once per
+ * point (proj/bindings/module.cpp:157-171). The model is set once: B landmarks with d
+ * features (dense ld, or CSR), betas (P x B row-major, the OvoModel::betas of
+ * multiclass.hpp:63), gamma. Then D[i][p] = sum_j exp(-gamma*||x_i - b_j||^2)*betas[p][j]
+ * for n points (D row-major, ld = ldd >= P), in fp64 with the reference's operation
+ * order (direct squared distance in ascending feature order, products rounded then
+ * added, exp, then the dot with betas in ascending j): equal to the reference up to the
+ * last ulp of exp. Points may have a different feature width d than the landmarks
+ * (missing features are zeros, as in the sparse merge of squared_distance,
+ * dataio.cpp:38-58); CSR indices outside [0, d) are LPD_ERR_INVALID_ARGUMENT. Runs on
+ * the context's first device. */
+int lpd_set_model_dense(lpd_context* ctx, const double* landmarks, int64_t B, int64_t d, int64_t ld,
+                        const double* betas, int64_t P, double gamma);
+int lpd_set_model_csr(lpd_context* ctx, int64_t B, int64_t d, const int64_t* indptr,
+                      const int32_t* indices, const double* values, const double* betas, int64_t P,
+                      double gamma);
+int lpd_model_decision_values_dense(lpd_context* ctx, const double* X, int64_t n, int64_t d,
+                                    int64_t ldx, double* D, int64_t ldd);
+int lpd_model_decision_values_csr(lpd_context* ctx, int64_t n, int64_t d, const int64_t* indptr,
+                                  const int32_t* indices, const double* values, double* D,
+                                  int64_t ldd);
+
+/* The one-vs-one vote on given decision values (D: n x P host, row-major, ld = ldd,
+ * P = num_classes*(num_classes-1)/2): classes[i] = the winning class INDEX, with the
+ * reference's rule (proj/src/multiclass.cpp:153-168: a strictly positive decision votes
+ * for the pair's first class, anything else for the second; most votes wins, ties to
+ * the smaller index). The same device kernel ovo_predict's K5 path ends with. */
+int lpd_ovo_vote(lpd_context* ctx, const double* D, int64_t n, int64_t ldd, int64_t num_classes,
+                 int32_t* classes);
+
 /* Kernel block K[i][j] = exp(-gamma * max(0, norms_a[i] + norms_b[j] - 2<a_i, b_j>)) in fp64
  * with the reference's operation order (K7; replaces lpdsvm::kernel_block,
  * proj/include/lpdsvm/kernel.hpp:26-32, proj/src/kernel.cpp:31-57, whose main caller is

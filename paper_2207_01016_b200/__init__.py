@@ -74,6 +74,11 @@ EXPORTED_SYMBOLS = (
     "lpd_resident_shape",
     "lpd_resident_gw",
     "lpd_resident_gtv",
+    "lpd_set_model_dense",
+    "lpd_set_model_csr",
+    "lpd_model_decision_values_dense",
+    "lpd_model_decision_values_csr",
+    "lpd_ovo_vote",
 )
 
 
@@ -160,6 +165,12 @@ def load_library(path: Optional[str] = None) -> ctypes.CDLL:
     lib.lpd_resident_gtv.argtypes = [vp, _c_i32_p, _c_dbl_p, i64, _c_dbl_p]
     lib.lpd_predict_ovo_dense.argtypes = [vp, _c_dbl_p, i64, i64, i64, i64, _c_i32_p]
     lib.lpd_predict_ovo_csr.argtypes = [vp, i64, i64, _c_i64_p, _c_i32_p, _c_dbl_p, i64, _c_i32_p]
+    lib.lpd_set_model_dense.argtypes = [vp, _c_dbl_p, i64, i64, i64, _c_dbl_p, i64, ctypes.c_double]
+    lib.lpd_set_model_csr.argtypes = [vp, i64, i64, _c_i64_p, _c_i32_p, _c_dbl_p, _c_dbl_p, i64,
+                                      ctypes.c_double]
+    lib.lpd_model_decision_values_dense.argtypes = [vp, _c_dbl_p, i64, i64, i64, _c_dbl_p, i64]
+    lib.lpd_model_decision_values_csr.argtypes = [vp, i64, i64, _c_i64_p, _c_i32_p, _c_dbl_p, _c_dbl_p, i64]
+    lib.lpd_ovo_vote.argtypes = [vp, _c_dbl_p, i64, i64, i64, _c_i32_p]
     if path is None:
         _lib = lib
     return lib
@@ -232,6 +243,7 @@ class Context:
         self._h = h
         self.b_eff = 0
         self.dim = 0
+        self.model_pairs = 0
 
     @property
     def handle(self) -> ctypes.c_void_p:
@@ -375,6 +387,60 @@ class Context:
         _check(self._lib.lpd_predict_ovo_csr(self._h, n, self.dim, _ptr(ip, ctypes.c_int64),
                                              _ptr(ix, ctypes.c_int32), _ptr(vv), num_classes,
                                              _ptr(out, ctypes.c_int32)))
+        return out
+
+    # ------------------------------------------------- per-point decision values (K8)
+    def set_model_dense(self, landmarks: np.ndarray, betas: np.ndarray, gamma: float) -> None:
+        """A trained OVO model (landmarks B × d, betas P × B — OvoModel::betas,
+        multiclass.hpp:63) for model_decision_values_*."""
+        lm = _f64(landmarks)
+        bt = _f64(np.atleast_2d(betas))
+        if lm.ndim != 2 or bt.shape[1] != lm.shape[0]:
+            raise ValueError("betas must be P x B with B = landmark count")
+        self.model_dim = lm.shape[1]
+        _check(self._lib.lpd_set_model_dense(self._h, _ptr(lm), lm.shape[0], lm.shape[1], lm.shape[1],
+                                             _ptr(bt), bt.shape[0], float(gamma)))
+        self.model_pairs = bt.shape[0]
+
+    def set_model_csr(self, indptr, indices, values, dim: int, betas: np.ndarray, gamma: float) -> None:
+        ip = np.ascontiguousarray(indptr, dtype=np.int64)
+        ix = np.ascontiguousarray(indices, dtype=np.int32)
+        vv = _f64(values)
+        bt = _f64(np.atleast_2d(betas))
+        if bt.shape[1] != ip.shape[0] - 1:
+            raise ValueError("betas must be P x B with B = landmark count")
+        self.model_dim = int(dim)
+        _check(self._lib.lpd_set_model_csr(self._h, ip.shape[0] - 1, int(dim), _ptr(ip, ctypes.c_int64),
+                                           _ptr(ix, ctypes.c_int32), _ptr(vv), _ptr(bt), bt.shape[0],
+                                           float(gamma)))
+        self.model_pairs = bt.shape[0]
+
+    def model_decision_values_dense(self, X: np.ndarray) -> np.ndarray:
+        """Per-point decision values D (n × P) in fp64, the reference's
+        decision_values (multiclass.cpp:137-151) for every row of X."""
+        x = _f64(np.atleast_2d(X))
+        D = np.empty((x.shape[0], self.model_pairs))
+        _check(self._lib.lpd_model_decision_values_dense(self._h, _ptr(x), x.shape[0], x.shape[1], x.shape[1],
+                                                         _ptr(D), self.model_pairs))
+        return D
+
+    def model_decision_values_csr(self, indptr, indices, values, dim: int) -> np.ndarray:
+        ip = np.ascontiguousarray(indptr, dtype=np.int64)
+        ix = np.ascontiguousarray(indices, dtype=np.int32)
+        vv = _f64(values)
+        D = np.empty((ip.shape[0] - 1, self.model_pairs))
+        _check(self._lib.lpd_model_decision_values_csr(self._h, ip.shape[0] - 1, int(dim),
+                                                       _ptr(ip, ctypes.c_int64), _ptr(ix, ctypes.c_int32),
+                                                       _ptr(vv), _ptr(D), self.model_pairs))
+        return D
+
+    def ovo_vote(self, D: np.ndarray, num_classes: int) -> np.ndarray:
+        """Class indices of the one-vs-one vote on given decision values
+        (multiclass.cpp:153-168), on the device."""
+        d = _f64(np.atleast_2d(D))
+        out = np.empty(d.shape[0], dtype=np.int32)
+        _check(self._lib.lpd_ovo_vote(self._h, _ptr(d), d.shape[0], d.shape[1], int(num_classes),
+                                      _ptr(out, ctypes.c_int32)))
         return out
 
     # ------------------------------------------------------- resident G (K6)

@@ -62,6 +62,7 @@ lpd_context* g_ctx = nullptr;
 std::atomic<long long> g_calls{0};
 std::atomic<long long> g_predict_calls{0};
 std::atomic<long long> g_block_calls{0};
+std::atomic<long long> g_dv_calls{0};      // per-point decision values served on device (K8)
 std::atomic<long long> g_sweep_calls{0};   // rebuild_w / reactivation_pass served on device
 std::atomic<long long> g_score_calls{0};   // CV held-out scorings served on device
 
@@ -595,6 +596,70 @@ std::vector<double> ovo_predict(const OvoModel& model, std::span<const SparseVec
     return predictions;
 }
 
+// Strong definition of
+//   std::vector<double> lpdsvm::decision_values(const OvoModel&, const SparseVector&)
+// (reference proj/include/lpdsvm/multiclass.hpp:74, proj/src/multiclass.cpp:137-151),
+// weakened in multiclass.o. Python Model.decision_values calls it once per point
+// (module.cpp:157-171), so the model (landmarks, betas, γ) stays on the device between
+// calls — matched by address, shape and a probe of its betas, like the resident G — and
+// each call ships one dense point and reads back its P decisions: K8, fp64 in the
+// reference's operation order (direct squared distance, exp, sequential dot).
+struct DeviceModel {
+    const lpdsvm::OvoModel* model = nullptr;
+    const double* betas = nullptr;
+    std::size_t B = 0, P = 0;
+    double gamma = 0.0;
+    double probe[4] = {};
+    int64_t d = 0;
+    std::vector<double> x;  // the point, dense
+} g_model;
+
+bool model_matches(const lpdsvm::OvoModel& m) {
+    if (g_model.model != &m || g_model.betas != m.betas.data() || g_model.B != m.landmarks.size() ||
+        g_model.P != m.num_pairs() || g_model.gamma != m.kernel.gamma)
+        return false;
+    const std::size_t n = g_model.B * g_model.P;
+    for (int k = 0; k < 4; ++k)
+        if (m.betas.data()[(n - 1) * static_cast<std::size_t>(k) / 3] != g_model.probe[k]) return false;
+    return true;
+}
+
+std::vector<double> decision_values(const OvoModel& model, const SparseVector& point) {
+    const std::size_t b = model.landmarks.size();
+    const std::size_t P = model.num_pairs();
+    std::vector<double> decisions(P, 0.0);
+    if (P == 0) return decisions;
+    if (b == 0) return decisions;  // the reference's empty sum
+    std::lock_guard<std::mutex> lock(g_mu);
+    ++g_dv_calls;
+    lpd_context* ctx = context();
+    if (!model_matches(model)) {
+        g_model = DeviceModel{};
+        Csr ls = flatten(model.landmarks, 1);
+        const int64_t dl = 1 + ls.max_index;
+        const int rc = lpd_set_model_csr(ctx, static_cast<int64_t>(b), dl, ls.indptr.data(), ls.indices.data(),
+                                         ls.values.data(), model.betas.data(), static_cast<int64_t>(P),
+                                         model.kernel.gamma);
+        if (rc != LPD_OK) rethrow_status(rc, "lpd_set_model_csr");
+        g_model.model = &model;
+        g_model.betas = model.betas.data();
+        g_model.B = b;
+        g_model.P = P;
+        g_model.gamma = model.kernel.gamma;
+        g_model.d = dl;
+        for (int k = 0; k < 4; ++k) g_model.probe[k] = model.betas.data()[(b * P - 1) * static_cast<std::size_t>(k) / 3];
+    }
+    int32_t mx = -1;
+    for (const Feature& f : point) mx = std::max(mx, f.index);
+    const int64_t dx = 1 + mx;
+    g_model.x.assign(static_cast<std::size_t>(std::max<int64_t>(dx, 1)), 0.0);
+    for (const Feature& f : point) g_model.x[static_cast<std::size_t>(f.index)] = f.value;
+    const int rc = lpd_model_decision_values_dense(ctx, g_model.x.data(), 1, dx, std::max<int64_t>(dx, 1),
+                                                   decisions.data(), static_cast<int64_t>(P));
+    if (rc != LPD_OK) rethrow_status(rc, "lpd_model_decision_values_dense");
+    return decisions;
+}
+
 }  // namespace lpdsvm
 
 // Introspection for the integration tests: proves the reference's call went here.
@@ -609,6 +674,9 @@ extern "C" __attribute__((visibility("default"))) long long lpd_adapter_score_ca
 }
 extern "C" __attribute__((visibility("default"))) long long lpd_adapter_block_calls(void) {
     return g_block_calls.load();
+}
+extern "C" __attribute__((visibility("default"))) long long lpd_adapter_dv_calls(void) {
+    return g_dv_calls.load();
 }
 extern "C" __attribute__((visibility("default"))) long long lpd_adapter_predict_calls(void) {
     return g_predict_calls.load();

@@ -37,6 +37,7 @@
 #include "factor_kernel.cuh"
 #include "gram_kernels.cuh"
 #include "panel_kernels.cuh"
+#include "pointdv_kernels.cuh"
 #include "prep_kernels.cuh"
 
 extern "C" void lpd_host_widen_rows(const float* src, int64_t lds, double* dst, int64_t ldd,
@@ -224,6 +225,31 @@ struct DeviceState {
     cudaEvent_t ring[kRing][2] = {};
     int64_t ring_count = 0;  // launches recorded since the last reset
 
+    // K8 (lpd_set_model_* / lpd_model_decision_values_*): a trained OVO model's fp64
+    // landmarks [B × d] and betas [P × B], plus the per-call point chunk buffers
+    struct ModelState {
+        bool set = false;
+        int64_t B = 0, d = 0, P = 0;
+        double gamma = 1.0;
+        double* lm = nullptr;
+        double* beta = nullptr;
+        double* x = nullptr;   // [rows_cap × x_cols] points, dense fp64
+        double* zt = nullptr;  // [B × rows_cap] landmark-major z
+        double* dv = nullptr;  // [rows_cap × P]
+        int64_t rows_cap = 0, x_cols = 0;
+        double* hx = nullptr;  // pinned host staging of the points and the results
+        double* hd = nullptr;
+        size_t hx_cap = 0, hd_cap = 0;
+        void free_all() {
+            dev_free(lm); dev_free(beta); dev_free(x); dev_free(zt); dev_free(dv);
+            if (hx) cudaFreeHost(hx);
+            if (hd) cudaFreeHost(hd);
+            hx = hd = nullptr;
+            hx_cap = hd_cap = 0;
+            rows_cap = x_cols = 0;
+            set = false;
+        }
+    } model;
     struct {
         size_t mu = 0, lm_hi = 0, lm_lo = 0, consts = 0, lm_nb = 0, lm_mx = 0, lt_hi = 0, lt_lo = 0,
                col_scale = 0, colmax = 0;
@@ -1286,6 +1312,134 @@ std::vector<std::vector<std::pair<int32_t, int64_t>>> split_rows(lpd_context* ct
     return parts;
 }
 
+// ------------------------------------------------------------------ K8 (per-point decision values)
+// Host rows, dense (X, ldx) or CSR, read as dense fp64 of width d with implicit zeros
+// (dataio.hpp:14-24). A CSR index outside [0, d) is an error, not a silent drop.
+struct HostRows {
+    const double* X = nullptr;
+    int64_t ldx = 0;
+    const int64_t* indptr = nullptr;
+    const int32_t* indices = nullptr;
+    const double* values = nullptr;
+    int64_t d = 0;
+    void fill(double* dst, int64_t r0, int64_t rows) const {
+        if (d == 0) return;
+        if (X) {
+            for (int64_t i = 0; i < rows; ++i)
+                std::memcpy(dst + i * d, X + (r0 + i) * ldx, sizeof(double) * static_cast<size_t>(d));
+            return;
+        }
+        std::memset(dst, 0, sizeof(double) * static_cast<size_t>(rows * d));
+        for (int64_t i = 0; i < rows; ++i)
+            for (int64_t e = indptr[r0 + i]; e < indptr[r0 + i + 1]; ++e) {
+                const int32_t c = indices[e];
+                if (c < 0 || c >= d)
+                    fail(LPD_ERR_INVALID_ARGUMENT, "feature index " + std::to_string(c) + " outside [0, " +
+                                                       std::to_string(d) + ")");
+                dst[i * d + c] = values[e];
+            }
+    }
+};
+
+void set_model(lpd_context* ctx, int64_t B, const HostRows& lm, const double* betas, int64_t P, double gamma) {
+    check_ctx(ctx, false);
+    if (B <= 0) fail(LPD_ERR_INVALID_ARGUMENT, "landmark count must be positive");
+    if (P <= 0) fail(LPD_ERR_INVALID_ARGUMENT, "pair count must be positive");
+    if (lm.d < 0) fail(LPD_ERR_INVALID_ARGUMENT, "feature dimension must be non-negative");
+    if (!betas) fail(LPD_ERR_INVALID_ARGUMENT, "betas is null");
+    if (!(gamma > 0.0) || !std::isfinite(gamma))
+        fail(LPD_ERR_INVALID_ARGUMENT, "kernel gamma must be positive and finite");
+    if (B > (1 << 30) || lm.d > (1 << 30) || P > (1 << 30) || B * P > (int64_t(1) << 34))
+        fail(LPD_ERR_UNSUPPORTED, "model too large");
+    DeviceState& ds = ctx->dev[0];
+    auto& m = ds.model;
+    CUDA_TRY(cudaSetDevice(ds.device));
+    m.set = false;
+    dev_free(m.lm);
+    dev_free(m.beta);
+    std::vector<double> dense(static_cast<size_t>(B * std::max<int64_t>(lm.d, 1)));
+    lm.fill(dense.data(), 0, B);
+    dev_alloc(&m.lm, dense.size());
+    dev_alloc(&m.beta, static_cast<size_t>(B * P));
+    CUDA_TRY(cudaMemcpy(m.lm, dense.data(), sizeof(double) * dense.size(), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(m.beta, betas, sizeof(double) * static_cast<size_t>(B * P), cudaMemcpyHostToDevice));
+    m.B = B;
+    m.d = lm.d;
+    m.P = P;
+    m.gamma = gamma;
+    m.set = true;
+}
+
+// D (n × P, ld) for host rows: per chunk, dense fp64 points into pinned staging -> H2D ->
+// pointdv_z_kernel -> pointdv_beta_kernel -> D2H. fp64 SIMT work (3·B·d flops per point
+// for z, 2·B·P for D), compute-bound; chunks hold ≤ 256 MB of z.
+void model_decision_values(lpd_context* ctx, int64_t n, const HostRows& xs, double* D, int64_t ldd) {
+    check_ctx(ctx, false);
+    DeviceState& ds = ctx->dev[0];
+    auto& m = ds.model;
+    if (!m.set) fail(LPD_ERR_INVALID_ARGUMENT, "no model (lpd_set_model_* first)");
+    if (n < 0) fail(LPD_ERR_INVALID_ARGUMENT, "negative row count");
+    if (xs.d < 0) fail(LPD_ERR_INVALID_ARGUMENT, "feature dimension must be non-negative");
+    if (ldd < m.P) fail(LPD_ERR_INVALID_ARGUMENT, "ldd < number of pairs");
+    if (n == 0) return;
+    if (!D) fail(LPD_ERR_INVALID_ARGUMENT, "null output");
+    if (xs.d > (1 << 30) || n > (int64_t(1) << 40)) fail(LPD_ERR_UNSUPPORTED, "too many points");
+    CUDA_TRY(cudaSetDevice(ds.device));
+    cudaStream_t st = ds.slot[0].stream;
+    const int64_t by_z = std::max<int64_t>(lpd::DV_T, (int64_t(256) << 20) / (8 * m.B) / lpd::DV_T * lpd::DV_T);
+    const int64_t chunk = std::min(round_up(n, lpd::DV_T), std::min<int64_t>(by_z, 1 << 20));
+    const int64_t xc = std::max<int64_t>(xs.d, 1);
+    if (m.rows_cap < chunk || m.x_cols < xc) {
+        dev_free(m.x); dev_free(m.zt); dev_free(m.dv);
+        m.rows_cap = m.x_cols = 0;
+        dev_alloc(&m.x, static_cast<size_t>(chunk * xc));
+        dev_alloc(&m.zt, static_cast<size_t>(chunk * m.B));
+        m.rows_cap = chunk;
+        m.x_cols = xc;
+    }
+    dev_free(m.dv);
+    dev_alloc(&m.dv, static_cast<size_t>(m.rows_cap * m.P));
+    const size_t hx_need = sizeof(double) * static_cast<size_t>(chunk * xc);
+    const size_t hd_need = sizeof(double) * static_cast<size_t>(chunk * m.P);
+    if (m.hx_cap < hx_need) {
+        if (m.hx) cudaFreeHost(m.hx);
+        m.hx = nullptr;
+        m.hx_cap = 0;
+        CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&m.hx), hx_need, cudaHostAllocDefault));
+        m.hx_cap = hx_need;
+    }
+    if (m.hd_cap < hd_need) {
+        if (m.hd) cudaFreeHost(m.hd);
+        m.hd = nullptr;
+        m.hd_cap = 0;
+        CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&m.hd), hd_need, cudaHostAllocDefault));
+        m.hd_cap = hd_need;
+    }
+    for (int64_t r0 = 0; r0 < n; r0 += chunk) {
+        const int64_t rows = std::min(chunk, n - r0);
+        xs.fill(m.hx, r0, rows);
+        if (xs.d > 0)
+            CUDA_TRY(cudaMemcpyAsync(m.x, m.hx, sizeof(double) * static_cast<size_t>(rows * xs.d),
+                                     cudaMemcpyHostToDevice, st));
+        const dim3 gz(static_cast<unsigned>((m.B + lpd::DV_T - 1) / lpd::DV_T),
+                      static_cast<unsigned>((rows + lpd::DV_T - 1) / lpd::DV_T));
+        lpd::pointdv_z_kernel<<<gz, 256, 0, st>>>(m.x, std::max<int64_t>(xs.d, 1), static_cast<int>(rows),
+                                                  static_cast<int>(xs.d), m.lm, std::max<int64_t>(m.d, 1),
+                                                  static_cast<int>(m.B), static_cast<int>(m.d), m.gamma, m.zt,
+                                                  rows);
+        CUDA_TRY(cudaGetLastError());
+        const dim3 gb(static_cast<unsigned>((rows + 127) / 128), static_cast<unsigned>(std::min<int64_t>(m.P, 65535)));
+        lpd::pointdv_beta_kernel<<<gb, 128, 0, st>>>(m.zt, rows, static_cast<int>(rows), static_cast<int>(m.B),
+                                                     m.beta, static_cast<int>(m.P), m.dv, m.P);
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaMemcpyAsync(m.hd, m.dv, sizeof(double) * static_cast<size_t>(rows * m.P),
+                                 cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        for (int64_t i = 0; i < rows; ++i)
+            std::memcpy(D + (r0 + i) * ldd, m.hd + i * m.P, sizeof(double) * static_cast<size_t>(m.P));
+    }
+}
+
 }  // namespace
 
 // =================================================================== C ABI
@@ -1372,6 +1526,7 @@ int lpd_context_destroy(lpd_context* ctx) {
         dev_free(ds.votes);
         dev_free(ds.res_g);
         dev_free(ds.sync_ctr);
+        ds.model.free_all();
         if (ds.scratch) cudaFree(ds.scratch);
         if (ds.gtmp) cudaFree(ds.gtmp);
         for (auto& s : ds.slot) {
@@ -1875,6 +2030,102 @@ int lpd_resident_gtv(lpd_context* ctx, const int32_t* rows, const double* coef, 
         for (int di = 0; di < nd; ++di)  // fixed device order: deterministic
             if (!partial[di].empty())
                 for (int64_t j = 0; j < b_eff; ++j) w[j] += partial[di][j];
+    });
+}
+
+int lpd_set_model_dense(lpd_context* ctx, const double* landmarks, int64_t B, int64_t d, int64_t ld,
+                        const double* betas, int64_t P, double gamma) {
+    return guarded([&] {
+        HostRows r;
+        r.X = landmarks;
+        r.ldx = ld;
+        r.d = d;
+        if (d > 0 && (!landmarks || ld < d)) fail(LPD_ERR_INVALID_ARGUMENT, "bad landmark array");
+        set_model(ctx, B, r, betas, P, gamma);
+    });
+}
+
+int lpd_set_model_csr(lpd_context* ctx, int64_t B, int64_t d, const int64_t* indptr, const int32_t* indices,
+                      const double* values, const double* betas, int64_t P, double gamma) {
+    return guarded([&] {
+        if (!indptr) fail(LPD_ERR_INVALID_ARGUMENT, "null indptr");
+        HostRows r;
+        r.indptr = indptr;
+        r.indices = indices;
+        r.values = values;
+        r.d = d;
+        set_model(ctx, B, r, betas, P, gamma);
+    });
+}
+
+int lpd_model_decision_values_dense(lpd_context* ctx, const double* X, int64_t n, int64_t d, int64_t ldx,
+                                    double* D, int64_t ldd) {
+    return guarded([&] {
+        if (n > 0 && d > 0 && (!X || ldx < d)) fail(LPD_ERR_INVALID_ARGUMENT, "bad point array");
+        HostRows r;
+        r.X = X;
+        r.ldx = ldx;
+        r.d = d;
+        model_decision_values(ctx, n, r, D, ldd);
+    });
+}
+
+int lpd_model_decision_values_csr(lpd_context* ctx, int64_t n, int64_t d, const int64_t* indptr,
+                                  const int32_t* indices, const double* values, double* D, int64_t ldd) {
+    return guarded([&] {
+        if (n > 0 && !indptr) fail(LPD_ERR_INVALID_ARGUMENT, "null indptr");
+        HostRows r;
+        r.indptr = indptr;
+        r.indices = indices;
+        r.values = values;
+        r.d = d;
+        model_decision_values(ctx, n, r, D, ldd);
+    });
+}
+
+int lpd_ovo_vote(lpd_context* ctx, const double* D, int64_t n, int64_t ldd, int64_t num_classes,
+                 int32_t* classes) {
+    return guarded([&] {
+        check_ctx(ctx, false);
+        if (n < 0) fail(LPD_ERR_INVALID_ARGUMENT, "negative row count");
+        if (num_classes < 2 || num_classes > lpd::VOTE_MAX_CLASSES)
+            fail(num_classes < 2 ? LPD_ERR_INVALID_ARGUMENT : LPD_ERR_UNSUPPORTED,
+                 "num_classes must be in [2, " + std::to_string(lpd::VOTE_MAX_CLASSES) + "]");
+        const int64_t P = num_classes * (num_classes - 1) / 2;
+        if (ldd < P) fail(LPD_ERR_INVALID_ARGUMENT, "ldd < num_classes*(num_classes-1)/2");
+        if (n == 0) return;
+        if (!D || !classes) fail(LPD_ERR_INVALID_ARGUMENT, "null buffer");
+        DeviceState& ds = ctx->dev[0];
+        CUDA_TRY(cudaSetDevice(ds.device));
+        cudaStream_t st = ds.slot[0].stream;
+        if (ds.pairs_classes != num_classes) {
+            dev_free(ds.pairs);
+            ds.pairs_classes = 0;
+            dev_alloc(&ds.pairs, static_cast<size_t>(P));
+            lpd::ovo_pair_table_kernel<<<static_cast<int>(num_classes), 128, 0, st>>>(static_cast<int>(num_classes),
+                                                                                     ds.pairs);
+            CUDA_TRY(cudaGetLastError());
+            ds.pairs_classes = static_cast<int>(num_classes);
+        }
+        double* dd = nullptr;
+        int32_t* dc = nullptr;
+        CUDA_TRY(cudaMalloc(&dd, sizeof(double) * static_cast<size_t>(n * ldd)));
+        if (cudaMalloc(&dc, sizeof(int32_t) * static_cast<size_t>(n)) != cudaSuccess) {
+            cudaFree(dd);
+            fail(LPD_ERR_OUT_OF_MEMORY, "vote buffer");
+        }
+        struct Free {
+            void* a; void* b;
+            ~Free() { cudaFree(a); cudaFree(b); }
+        } guard{dd, dc};
+        CUDA_TRY(cudaMemcpyAsync(dd, D, sizeof(double) * static_cast<size_t>(n * ldd), cudaMemcpyHostToDevice, st));
+        const int blocks = static_cast<int>(std::min<int64_t>((n + lpd::VOTE_WARPS - 1) / lpd::VOTE_WARPS,
+                                                              static_cast<int64_t>(ds.num_sms) * 8));
+        lpd::ovo_vote_kernel<double><<<blocks, 32 * lpd::VOTE_WARPS, sizeof(int) * lpd::VOTE_WARPS * num_classes, st>>>(
+            dd, ldd, static_cast<int>(n), static_cast<int>(num_classes), ds.pairs, static_cast<int>(P), dc);
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaMemcpyAsync(classes, dc, sizeof(int32_t) * static_cast<size_t>(n), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
     });
 }
 

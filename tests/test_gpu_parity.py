@@ -404,3 +404,69 @@ def test_resident_g_products(gpu_ctx, nb):
     finally:
         gpu_ctx.set_keep_resident(False)
     assert gpu_ctx.resident_shape()[0] == 0
+
+
+def _ref_point_dv(X, Y, betas, gamma):
+    """The reference's decision_values (multiclass.cpp:137-151) on dense rows: its own
+    gaussian (kernel.cpp:17-19, sparse merge over the nonzeros) per landmark, then the
+    sequential dot with each betas row."""
+    out = np.zeros((X.shape[0], betas.shape[0]))
+    lm = [(np.flatnonzero(y).astype(np.int32), y[y != 0]) for y in Y]
+    for i, x in enumerate(X):
+        xi = np.flatnonzero(x).astype(np.int32)
+        z = [O.ref_gaussian(xi, x[xi], li, lv, gamma) for li, lv in lm]
+        for p in range(betas.shape[0]):
+            s = 0.0
+            for j in range(len(z)):
+                s += z[j] * betas[p, j]
+            out[i, p] = s
+    return out
+
+
+@pytest.mark.parametrize("n,d,dx,B,P", [(1, 7, 7, 1, 1), (37, 20, 20, 130, 3), (70, 9, 13, 65, 10),
+                                        (3, 40, 33, 200, 1)])
+def test_model_decision_values_match_reference(gpu_ctx, n, d, dx, B, P):
+    """K8 (lpd_model_decision_values_*) against the reference's own gaussian + dot, on
+    sparse rows whose feature widths differ (dx ≠ d: features only one side has).
+    fp64 with the reference's operation order: ≤ a few ulps of exp apart."""
+    rng = np.random.default_rng(n + d + B)
+    Y = rng.standard_normal((B, d))
+    Y[rng.random(Y.shape) < 0.3] = 0.0
+    X = rng.standard_normal((n, dx))
+    X[rng.random(X.shape) < 0.3] = 0.0
+    betas = rng.standard_normal((P, B))
+    gamma = 0.07
+    gpu_ctx.set_model_dense(Y, betas, gamma)
+    D = gpu_ctx.model_decision_values_dense(X)
+    R = _ref_point_dv(X, Y, betas, gamma)
+    bound = 4 * np.finfo(float).eps * np.abs(betas).sum(1)[None, :]
+    assert np.all(np.abs(D - R) <= bound), float(np.max(np.abs(D - R) / bound))
+    # CSR entry points agree bitwise with the dense ones
+    lp, li, lv = O.dense_to_csr(Y)
+    gpu_ctx.set_model_csr(lp, li, lv, d, betas, gamma)
+    ip, ix, vv = O.dense_to_csr(X)
+    assert np.array_equal(gpu_ctx.model_decision_values_csr(ip, ix, vv, dx), D)
+
+
+def test_model_decision_values_errors(gpu_ctx):
+    gpu_ctx.set_model_dense(np.ones((4, 3)), np.ones((1, 4)), 0.5)
+    with pytest.raises(ValueError):  # CSR index outside [0, d)
+        gpu_ctx.model_decision_values_csr(np.array([0, 1]), np.array([3]), np.array([1.0]), 3)
+    with pytest.raises(ValueError):
+        gpu_ctx.set_model_dense(np.ones((4, 3)), np.ones((1, 4)), float("nan"))
+    assert gpu_ctx.model_decision_values_dense(np.zeros((0, 3))).shape == (0, 1)
+
+
+@pytest.mark.parametrize("classes", [2, 3, 7, 40])
+def test_ovo_vote_bit_exact(gpu_ctx, classes):
+    """The device vote (the kernel K5 ends with) on identical decision values, against the
+    reference's own vote (multiclass.cpp:153-168): index-exact on every row, with exact
+    zeros (a zero votes for the second class), -0.0, and dense ties."""
+    P = classes * (classes - 1) // 2
+    rng = np.random.default_rng(classes)
+    D = rng.choice([-1.0, -0.0, 0.0, 1e-300, 2.0, -3.0], size=(3000, P))
+    D[:500] = rng.standard_normal((500, P))
+    D[500:600] = 0.0
+    got = gpu_ctx.ovo_vote(D, classes)
+    want = np.array([O.ref_vote(row, classes) for row in D], dtype=np.int32)
+    assert np.array_equal(got, want)
