@@ -362,6 +362,7 @@ def e2e_dropin(build, cfg, res, rows):
             "h2d_bytes_per_step": int(rows * cfg.d * 12 + res["B"] * cfg.d * 12 + res["B"] * b_eff * 8),
             "d2h_bytes_per_step": int(rows * (-(-b_eff // 4) * 4) * 4),
             "sample_max_row_rel_diff_vs_device_path": out.get("sample_max_row_rel_diff"),
+            "phases": out.get("adapter_phases"),
             "path": "lpdsvm::squared_norms + lpdsvm::compute_G (factor.hpp:52-55) with std::vector<Feature> rows "
                     "into a fresh lpdsvm::Matrix (adapter -> C ABI -> B200), median of the steps"}
 

@@ -52,7 +52,19 @@ extern "C" {
 #define LPD_OUT_F64 0
 #define LPD_OUT_F32 1
 
+#define LPD_PRECISION_AUTO 0 /* per basis: high when 2^-22*sqrt(lambda_max/lambda_min) > 2.5e-4 */
+#define LPD_PRECISION_FAST 1 /* tensor-core split-fp16 path (K1 / panel path) */
+#define LPD_PRECISION_HIGH 2 /* fp64 Z (direct distance) + fp64 DMMA projection */
+
 typedef struct lpd_context lpd_context;
+
+/* One stored feature of a sparse point: the layout of the reference's lpdsvm::Feature
+ * {int32 index (0-based); double value} (proj/include/lpdsvm/dataio.hpp:14-19), so a
+ * std::vector<Feature>'s storage is an array of these. */
+typedef struct lpd_feature {
+    int32_t index;
+    double value;
+} lpd_feature;
 
 /* Per-call phase timings (seconds, host wall clock unless noted). */
 typedef struct lpd_timings {
@@ -96,6 +108,17 @@ int lpd_set_basis_device(lpd_context* ctx, int device_index, const double* landm
                          int64_t B, int64_t d, int64_t ld, const double* L_dev, int64_t b_eff,
                          double gamma, void* stream);
 
+/* Precision of the factor path (default LPD_PRECISION_AUTO, or the LPD_PRECISION environment
+ * variable: auto | fast | high). The fast path holds G within ~2^-22*sqrt(lambda_max/lambda_min)
+ * of the fp64 reference (row-normwise); the high path computes Z in fp64 by direct distance and
+ * G = Z*L on the fp64 tensor cores, for the ill-conditioned bases of small gamma with the
+ * reference default tau = 1e-12 (proj/include/lpdsvm/factor.hpp:59). Applies from the next
+ * lpd_set_basis_* call. */
+int lpd_set_precision(lpd_context* ctx, int mode);
+/* The current basis' choice: *high = 1 on the high-precision path; *estimate = the fast
+ * path's row-error estimate 2^-22*sqrt(lambda_max/lambda_min) from L's column norms. */
+int lpd_basis_precision(const lpd_context* ctx, int* high, double* estimate);
+
 /* G (n x b_eff, leading dimension ldg >= b_eff) for host rows; rows are sharded
  * across the context's devices, results streamed back into G. */
 int lpd_compute_g_dense(lpd_context* ctx, const double* X, int64_t n, int64_t d, int64_t ldx,
@@ -103,6 +126,13 @@ int lpd_compute_g_dense(lpd_context* ctx, const double* X, int64_t n, int64_t d,
 int lpd_compute_g_csr(lpd_context* ctx, int64_t n, int64_t d, const int64_t* indptr,
                       const int32_t* indices, const double* values, double* G, int64_t ldg,
                       lpd_timings* timings);
+
+/* The same for rows in the reference's own storage (no intermediate CSR): rows[i] points at
+ * nnz[i] features of point i (a std::vector<Feature>'s data(), strictly ascending indices,
+ * dataio.hpp:20-24), indices in [0, d). Chunks are densified by the library's host threads
+ * into pinned memory and copied up while earlier chunks compute and deliver. */
+int lpd_compute_g_rows(lpd_context* ctx, int64_t n, int64_t d, const lpd_feature* const* rows,
+                       const int64_t* nnz, double* G, int64_t ldg, lpd_timings* timings);
 
 /* Device-resident variant: X_dev (n x d fp64, ld ldx) and G_dev on device
  * `device_index` of the context; out_dtype LPD_OUT_F64 or LPD_OUT_F32; stream is a
@@ -195,6 +225,16 @@ int lpd_resident_gw(lpd_context* ctx, const int32_t* rows, int64_t count, const 
  * warm starts (proj/src/dcd.cpp:91-102). */
 int lpd_resident_gtv(lpd_context* ctx, const int32_t* rows, const double* coef, int64_t count,
                      double* w);
+/* W[s][j] = sum_i coef[i][s] * G[rows[i]][j] for `sets` coefficient vectors at once (coef is
+ * count x sets row-major, W is sets x b_eff): one read of the listed rows serves every set.
+ * The warm starts of every (fold, pair) problem of cross_validate at a new C
+ * (proj/src/modelsel.cpp:104-112 -> dcd.cpp:91-102, 115-121) in one pass. */
+int lpd_resident_gtv_sets(lpd_context* ctx, const int32_t* rows, const double* coef, int64_t count,
+                          int64_t sets, double* W);
+/* q[i] = sum_j G[i][j]^2 for every row of the resident G (n values), fp64 in ascending j with
+ * each product rounded then added: make_binary_problem's q_diag (proj/src/dcd.cpp:60-89,
+ * row.squaredNorm()), bit-identical to a sequential host pass over the returned fp64 G. */
+int lpd_resident_row_sqnorms(lpd_context* ctx, double* q);
 
 /* Last kernel timing of the fused factor kernel on device_index (milliseconds,
  * CUDA events around the launch on its stream), for benchmarks. */

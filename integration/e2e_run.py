@@ -95,6 +95,14 @@ def run_compute_g(lib, args):
            "gmatrix_seconds": stage, "compute_G_seconds": statistics.median(r[1] for r in runs),
            "matrix_free_seconds": statistics.median(r[2] for r in runs), "rows_per_s": n / stage,
            "steps": args.steps, "warmup": args.warmup}
+    if hasattr(lib, "lpd_adapter_phases"):  # the B200 build: where the last call's time went
+        ph = (ctypes.c_double * 4)()
+        lib.lpd_adapter_phases(ph)
+        tm = (ctypes.c_double * 8)()  # lpd_timings: total, h2d, kernel, d2h, host_copy (s), ...
+        lib.lpd_adapter_last_timings(ctypes.cast(tm, ctypes.c_void_p))
+        out["adapter_phases"] = {"flatten": ph[0], "basis": ph[1], "matrix_alloc": ph[2], "device_call": ph[3],
+                                 "h2d_event_s": tm[1], "kernel_event_s": tm[2], "d2h_event_s": tm[3],
+                                 "host_widen_s": tm[4]}
     if "G_sample" in z.files:  # spot check against the device-path rows bench.py produced
         ref = z["G_sample"][:k]
         out["sample_max_row_rel_diff"] = float(np.max(np.linalg.norm(sample - ref, axis=1)

@@ -47,6 +47,9 @@ LPD_ERR_OUT_OF_MEMORY = 4
 LPD_ERR_NO_DEVICE = 5
 LPD_OUT_F64 = 0
 LPD_OUT_F32 = 1
+LPD_PRECISION_AUTO = 0
+LPD_PRECISION_FAST = 1
+LPD_PRECISION_HIGH = 2
 
 # Every symbol include/lpd_nystrom.h declares (checked by the CPU test suite).
 EXPORTED_SYMBOLS = (
@@ -79,6 +82,11 @@ EXPORTED_SYMBOLS = (
     "lpd_model_decision_values_dense",
     "lpd_model_decision_values_csr",
     "lpd_ovo_vote",
+    "lpd_resident_gtv_sets",
+    "lpd_resident_row_sqnorms",
+    "lpd_set_precision",
+    "lpd_basis_precision",
+    "lpd_compute_g_rows",
 )
 
 
@@ -171,6 +179,10 @@ def load_library(path: Optional[str] = None) -> ctypes.CDLL:
     lib.lpd_model_decision_values_dense.argtypes = [vp, _c_dbl_p, i64, i64, i64, _c_dbl_p, i64]
     lib.lpd_model_decision_values_csr.argtypes = [vp, i64, i64, _c_i64_p, _c_i32_p, _c_dbl_p, _c_dbl_p, i64]
     lib.lpd_ovo_vote.argtypes = [vp, _c_dbl_p, i64, i64, i64, _c_i32_p]
+    lib.lpd_resident_gtv_sets.argtypes = [vp, _c_i32_p, _c_dbl_p, i64, i64, _c_dbl_p]
+    lib.lpd_resident_row_sqnorms.argtypes = [vp, _c_dbl_p]
+    lib.lpd_set_precision.argtypes = [vp, ctypes.c_int]
+    lib.lpd_basis_precision.argtypes = [vp, ctypes.POINTER(ctypes.c_int), _c_dbl_p]
     if path is None:
         _lib = lib
     return lib
@@ -389,6 +401,21 @@ class Context:
                                              _ptr(out, ctypes.c_int32)))
         return out
 
+    # ---------------------------------------------------------------- precision
+    def set_precision(self, mode: str) -> None:
+        """'auto' (default), 'fast' (tensor-core split-fp16) or 'high' (fp64 Z + fp64 DMMA
+        projection); applies from the next set_basis_*."""
+        modes = {"auto": LPD_PRECISION_AUTO, "fast": LPD_PRECISION_FAST, "high": LPD_PRECISION_HIGH}
+        if mode not in modes:
+            raise ValueError(f"precision mode must be one of {sorted(modes)}")
+        _check(self._lib.lpd_set_precision(self._h, modes[mode]))
+
+    def basis_precision(self) -> tuple:
+        """(high: bool, estimate: float) for the current basis."""
+        hi, est = ctypes.c_int(), ctypes.c_double()
+        _check(self._lib.lpd_basis_precision(self._h, ctypes.byref(hi), ctypes.byref(est)))
+        return bool(hi.value), est.value
+
     # ------------------------------------------------- per-point decision values (K8)
     def set_model_dense(self, landmarks: np.ndarray, betas: np.ndarray, gamma: float) -> None:
         """A trained OVO model (landmarks B × d, betas P × B — OvoModel::betas,
@@ -469,6 +496,22 @@ class Context:
         w = np.empty(self.resident_shape()[1])
         _check(self._lib.lpd_resident_gtv(self._h, _ptr(r, ctypes.c_int32), _ptr(c), r.shape[0], _ptr(w)))
         return w
+
+    def resident_gtv_sets(self, rows, coef) -> np.ndarray:
+        """W[s] = Σ_i coef[i, s] · G[rows_i] for every column s of coef at once (the warm
+        starts of all (fold, pair) problems, dcd.cpp:91-102)."""
+        r = np.ascontiguousarray(rows, dtype=np.int32)
+        c = _f64(np.atleast_2d(np.asarray(coef).T).T if np.ndim(coef) == 1 else coef)
+        W = np.empty((c.shape[1], self.resident_shape()[1]))
+        _check(self._lib.lpd_resident_gtv_sets(self._h, _ptr(r, ctypes.c_int32), _ptr(c), r.shape[0], c.shape[1],
+                                               _ptr(W)))
+        return W
+
+    def resident_row_sqnorms(self) -> np.ndarray:
+        """q_i = Σ_j G_ij² for every resident row (make_binary_problem's q_diag, dcd.cpp:60-89)."""
+        q = np.empty(self.resident_shape()[0])
+        _check(self._lib.lpd_resident_row_sqnorms(self._h, _ptr(q)))
+        return q
 
     def kernel_block(self, A: np.ndarray, B: np.ndarray, gamma: float, norms_a=None,
                      norms_b=None) -> np.ndarray:

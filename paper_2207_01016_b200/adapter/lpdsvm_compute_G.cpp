@@ -32,6 +32,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstring>
+#include <cstddef>
 #include <type_traits>
 #include <chrono>
 #include <cmath>
@@ -77,6 +78,30 @@ struct ResidentG {
     double probe_val[8] = {};
 } g_res;
 
+// Per-factor products of the resident G: the row squared norms (make_binary_problem's
+// q_diag, computed once per G on the device instead of once per binary problem on the
+// host) and the warm-start w of every (fold, pair) problem of the current C, computed in
+// one device pass by cross_validate and handed to rebuild_w by content (FNV-1a of the
+// clamped α the solver passes, dcd.cpp:115-121).
+std::vector<double> g_rowsq;
+struct WarmW {
+    std::size_t size;
+    std::uint64_t hash;  // of the clamped α
+    std::uint64_t rows;  // of the problem's row ids
+    std::vector<double> w;
+};
+std::vector<WarmW> g_warm_w;
+std::atomic<long long> g_qdiag_calls{0};   // make_binary_problem q_diag served from the device norms
+std::atomic<long long> g_warm_batches{0};  // batched warm-start passes (one per cross_validate with warm α)
+
+template <typename T>
+std::uint64_t fnv1a(const T* v, std::size_t n) {
+    std::uint64_t h = 1469598103934665603ull;
+    const unsigned char* b = reinterpret_cast<const unsigned char*>(v);
+    for (std::size_t i = 0; i < n * sizeof(T); ++i) h = (h ^ b[i]) * 1099511628211ull;
+    return h;
+}
+
 // Device products are used above this many G elements per call (below it the host
 // loop is faster than a launch + transfers); LPD_DEVICE_MIN_ELEMS overrides (tests).
 std::size_t device_min_elems() {
@@ -97,10 +122,23 @@ double g_phase[4] = {};
     throw std::runtime_error(msg);
 }
 
-// One process-wide context over LPD_NUM_GPUS (or all visible) devices; the
-// reference's FactorOptions has no device field (factor.hpp:57-63). CUDA context
-// creation (~0.7 s) starts in the background when the module is loaded, so the first
-// train/predict call does not pay it; context() waits for it (or re-raises its error).
+// One process-wide context, created on the first call that needs the device (importing
+// the module touches no GPU, so a process that forks after import or never trains holds
+// no CUDA state). Devices: LPD_NUM_GPUS (or all visible) — the reference's FactorOptions
+// has no device field (factor.hpp:57-63) — except under a launcher that sets LOCAL_RANK
+// without LPD_NUM_GPUS, where each process takes its own device (one process per GPU).
+// LPD_EAGER_INIT=1 starts the context creation (~0.7 s) in the background at load time.
+int create_context(lpd_context** out) {
+    const char* lr = std::getenv("LOCAL_RANK");
+    if (lr && !std::getenv("LPD_NUM_GPUS")) {
+        const int nd = lpd_device_count();
+        if (nd <= 0) return lpd_context_create(out, 0);  // reports "no CUDA device"
+        const int dev = std::atoi(lr) % nd;
+        return lpd_context_create_devices(out, &dev, 1);
+    }
+    return lpd_context_create(out, 0);
+}
+
 struct EagerContext {
     std::thread th;
     int rc = LPD_OK;
@@ -108,9 +146,9 @@ struct EagerContext {
     lpd_context* ctx = nullptr;
     EagerContext() {
         const char* e = std::getenv("LPD_EAGER_INIT");
-        if (e && e[0] == '0') return;
+        if (!(e && e[0] == '1')) return;
         th = std::thread([this] {
-            rc = lpd_context_create(&ctx, 0);
+            rc = create_context(&ctx);
             if (rc != LPD_OK) err = lpd_last_error();
         });
     }
@@ -128,7 +166,7 @@ lpd_context* context() {
                 return g_ctx;
             }
         }
-        int rc = lpd_context_create(&g_ctx, 0);
+        int rc = create_context(&g_ctx);
         if (rc != LPD_OK) rethrow_status(rc, "lpd_context_create");
     }
     return g_ctx;
@@ -257,11 +295,38 @@ Matrix compute_G(std::span<const SparseVector> points, std::span<const double> /
         t0 = t1;
     };
     const int threads = std::max(1, num_threads);
-    Csr xs = flatten(points, threads);
+    // The points go to the library in their own storage (lpd_compute_g_rows: a pointer
+    // and a length per std::vector<Feature>); indices ascend within a point
+    // (dataio.hpp:20-24), so its largest index is its last. The landmarks are few: CSR.
+    static_assert(sizeof(lpd_feature) == sizeof(Feature) && offsetof(lpd_feature, index) == offsetof(Feature, index) &&
+                      offsetof(lpd_feature, value) == offsetof(Feature, value),
+                  "lpd_feature must mirror lpdsvm::Feature");
+    std::vector<const lpd_feature*> xrows(n);
+    std::vector<int64_t> xnnz(n);
+    int32_t xmax = -1;
+    {
+        const int T = std::max(1, std::min<int>(threads, static_cast<int>((n + 65535) / 65536)));
+        std::vector<int32_t> mx(static_cast<std::size_t>(T), -1);
+        auto work = [&](int t) {
+            int32_t m = -1;
+            for (std::size_t i = n * t / T; i < n * (t + 1) / T; ++i) {
+                const SparseVector& p = points[i];
+                xrows[i] = reinterpret_cast<const lpd_feature*>(p.data());
+                xnnz[i] = static_cast<int64_t>(p.size());
+                if (!p.empty()) m = std::max(m, p.back().index);
+            }
+            mx[static_cast<std::size_t>(t)] = m;
+        };
+        std::vector<std::thread> th;
+        for (int t = 1; t < T; ++t) th.emplace_back(work, t);
+        work(0);
+        for (auto& x : th) x.join();
+        for (int32_t m : mx) xmax = std::max(xmax, m);
+    }
     Csr ls = flatten(landmarks, threads);
     lap(0);
     // compute_G is not passed the dimension: d = 1 + max index over both sets.
-    const int64_t d = std::max<int64_t>(1, 1 + std::max(xs.max_index, ls.max_index));
+    const int64_t d = std::max<int64_t>(1, 1 + std::max(xmax, ls.max_index));
 
     lpd_context* ctx = context();
     int rc = lpd_set_basis_csr(ctx, static_cast<int64_t>(b), d, ls.indptr.data(), ls.indices.data(),
@@ -275,13 +340,15 @@ Matrix compute_G(std::span<const SparseVector> points, std::span<const double> /
     lap(1);
     Matrix G = make_output_matrix(n, b_eff);
     lap(2);
-    rc = lpd_compute_g_csr(ctx, static_cast<int64_t>(n), d, xs.indptr.data(), xs.indices.data(),
-                           xs.values.data(), G.data(), static_cast<int64_t>(b_eff), &g_last);
-    if (rc != LPD_OK) rethrow_status(rc, "lpd_compute_g_csr");
+    rc = lpd_compute_g_rows(ctx, static_cast<int64_t>(n), d, xrows.data(), xnnz.data(), G.data(),
+                            static_cast<int64_t>(b_eff), &g_last);
+    if (rc != LPD_OK) rethrow_status(rc, "lpd_compute_g_rows");
     lap(3);
     int64_t rn = 0, rb = 0;
     lpd_resident_shape(ctx, &rn, &rb);
     g_res = ResidentG{};
+    g_rowsq.clear();
+    g_warm_w.clear();
     if (rn == static_cast<int64_t>(n) && rb == static_cast<int64_t>(b_eff)) {
         g_res.ptr = G.data();
         g_res.rows = n;
@@ -319,6 +386,21 @@ namespace lpdsvm {
 // G; host: the reference's sequential loop.
 std::vector<double> rebuild_w(const BinaryProblem& problem, const Matrix& G,
                               std::span<const double> alpha) {
+    {
+        std::lock_guard<std::mutex> lock(g_mu);
+        if (!g_warm_w.empty() && resident_matches(G)) {
+            const std::uint64_t h = fnv1a(alpha.data(), alpha.size());
+            const std::uint64_t hr = fnv1a(problem.row_ids.data(), problem.row_ids.size());
+            for (std::size_t k = 0; k < g_warm_w.size(); ++k)
+                if (g_warm_w[k].size == alpha.size() && g_warm_w[k].hash == h && g_warm_w[k].rows == hr &&
+                    g_warm_w[k].w.size() == G.cols()) {
+                    std::vector<double> w = std::move(g_warm_w[k].w);
+                    g_warm_w.erase(g_warm_w.begin() + static_cast<std::ptrdiff_t>(k));
+                    ++g_sweep_calls;
+                    return w;
+                }
+        }
+    }
     std::vector<double> w(G.cols(), 0.0);
     std::vector<int32_t> rows;
     std::vector<double> coef;
@@ -391,6 +473,135 @@ std::size_t reactivation_pass(DualState& state, const BinaryProblem& problem, co
     return reactivated;
 }
 
+// make_binary_problem (dcd.hpp:23-26, dcd.cpp:60-89), weakened in dcd.o: the reference's
+// checks, then q_diag[i] = ‖G_{row_i}‖² from the row norms of the resident G (one device
+// pass per factor, bit-identical to the reference's sequential squaredNorm) instead of a
+// host pass over every problem row for every (fold, pair, C).
+BinaryProblem make_binary_problem(const Matrix& G, std::vector<int> row_ids, std::vector<double> y, double C) {
+    if (row_ids.size() != y.size()) throw std::invalid_argument("row_ids and y must have equal length");
+    if (row_ids.empty()) throw std::invalid_argument("empty binary problem");
+    if (!(C > 0.0) || !std::isfinite(C)) throw std::invalid_argument("C must be positive");
+    bool pos = false, neg = false;
+    for (double v : y) {
+        if (v == 1.0)
+            pos = true;
+        else if (v == -1.0)
+            neg = true;
+        else
+            throw std::invalid_argument("labels must be +1 or -1");
+    }
+    if (!pos || !neg) throw std::invalid_argument("binary problem needs both classes");
+    BinaryProblem problem;
+    problem.row_ids = std::move(row_ids);
+    problem.y = std::move(y);
+    problem.C = C;
+    problem.q_diag.resize(problem.row_ids.size());
+    {
+        std::lock_guard<std::mutex> lock(g_mu);
+        if (resident_matches(G)) {
+            if (g_rowsq.size() != G.rows()) {
+                g_rowsq.resize(G.rows());
+                const int rc = lpd_resident_row_sqnorms(context(), g_rowsq.data());
+                if (rc != LPD_OK) {
+                    g_rowsq.clear();
+                    rethrow_status(rc, "lpd_resident_row_sqnorms");
+                }
+            }
+            for (std::size_t i = 0; i < problem.row_ids.size(); ++i)
+                problem.q_diag[i] = g_rowsq[static_cast<std::size_t>(problem.row_ids[i])];
+            ++g_qdiag_calls;
+            return problem;
+        }
+    }
+    for (std::size_t i = 0; i < problem.row_ids.size(); ++i) {
+        const double* row = G.row(static_cast<std::size_t>(problem.row_ids[i]));
+        double s = 0.0;
+        for (std::size_t j = 0; j < G.cols(); ++j) s += row[j] * row[j];
+        problem.q_diag[i] = s;
+    }
+    return problem;
+}
+
+}  // namespace lpdsvm
+
+namespace {
+
+// The warm starts of every (fold, pair) problem cross_validate is about to solve at this C
+// (make_state: α = clamp(warm, 0, C), w = Σ α_i y_i G_i, dcd.cpp:115-121), as one device
+// pass over the union of their rows (lpd_resident_gtv_sets); rebuild_w picks them up by
+// content. The problems are the ones ovo_train builds (make_pair_specs over the fold's
+// training rows, multiclass.cpp:75-80).
+void batch_warm_starts(const lpdsvm::LowRankFactor& factor, std::span<const double> labels,
+                       const lpdsvm::LabelMap& label_map, const lpdsvm::FoldAssignment& folds, double C,
+                       const lpdsvm::WarmStore& warm) {
+    const std::size_t n = labels.size();
+    const std::size_t be = factor.G.cols();
+    std::vector<std::vector<double>> alphas;  // clamped α per set
+    std::vector<std::uint64_t> row_hash;
+    std::vector<std::int32_t> set_rows_flat;
+    std::vector<double> set_coef_flat;
+    std::vector<std::size_t> set_begin{0};
+    for (int f = 0; f < folds.k; ++f) {
+        const auto& store = warm[static_cast<std::size_t>(f)];
+        bool any = false;
+        for (const auto& a : store) any = any || !a.empty();
+        if (!any) continue;
+        std::vector<std::uint8_t> include(n, 0);
+        for (std::size_t r = 0; r < n; ++r) include[r] = folds.fold_of[r] != f;
+        std::vector<lpdsvm::PairSpec> specs;
+        try {
+            specs = lpdsvm::make_pair_specs(labels, label_map, include);
+        } catch (const std::exception&) {
+            continue;  // the fold's own checks in ovo_train report it
+        }
+        for (std::size_t p = 0; p < specs.size() && p < store.size(); ++p) {
+            const auto& a = store[p];
+            if (a.empty() || a.size() != specs[p].row_ids.size()) continue;
+            std::vector<double> al(a.size());
+            for (std::size_t i = 0; i < a.size(); ++i) al[i] = std::clamp(a[i], 0.0, C);
+            for (std::size_t i = 0; i < al.size(); ++i)
+                if (al[i] != 0.0) {
+                    set_rows_flat.push_back(specs[p].row_ids[i]);
+                    set_coef_flat.push_back(al[i] * specs[p].y[i]);
+                }
+            set_begin.push_back(set_rows_flat.size());
+            alphas.push_back(std::move(al));
+            row_hash.push_back(fnv1a(specs[p].row_ids.data(), specs[p].row_ids.size()));
+        }
+    }
+    const std::size_t S = alphas.size();
+    if (S == 0) return;
+    // union of the rows, ascending; coef as |union| × S
+    std::vector<std::int32_t> slot(n, -1);
+    std::vector<std::int32_t> rows;
+    for (std::int32_t r : set_rows_flat)
+        if (slot[static_cast<std::size_t>(r)] < 0) slot[static_cast<std::size_t>(r)] = 0;
+    for (std::size_t r = 0; r < n; ++r)
+        if (slot[r] == 0) {
+            slot[r] = static_cast<std::int32_t>(rows.size());
+            rows.push_back(static_cast<std::int32_t>(r));
+        }
+    if (rows.size() * be * S < device_min_elems()) return;
+    std::vector<double> coef(rows.size() * S, 0.0);
+    for (std::size_t s = 0; s < S; ++s)
+        for (std::size_t k = set_begin[s]; k < set_begin[s + 1]; ++k)
+            coef[static_cast<std::size_t>(slot[static_cast<std::size_t>(set_rows_flat[k])]) * S + s] = set_coef_flat[k];
+    std::vector<double> W(S * be);
+    const int rc = lpd_resident_gtv_sets(context(), rows.data(), coef.data(), static_cast<int64_t>(rows.size()),
+                                         static_cast<int64_t>(S), W.data());
+    if (rc != LPD_OK) rethrow_status(rc, "lpd_resident_gtv_sets");
+    g_warm_w.clear();
+    for (std::size_t s = 0; s < S; ++s)
+        g_warm_w.push_back({alphas[s].size(), fnv1a(alphas[s].data(), alphas[s].size()), row_hash[s],
+                            std::vector<double>(W.begin() + static_cast<std::ptrdiff_t>(s * be),
+                                                W.begin() + static_cast<std::ptrdiff_t>((s + 1) * be))});
+    ++g_warm_batches;
+}
+
+}  // namespace
+
+namespace lpdsvm {
+
 // cross_validate (modelsel.hpp:49-51, modelsel.cpp:65-161): per fold, train every pair on
 // the other folds (ovo_train, warm-started from the store when given) and score the
 // held-out rows on their G rows — the scoring D = G_heldout·pair_wᵀ runs on the device
@@ -415,6 +626,10 @@ CvResult cross_validate(const LowRankFactor& factor, std::span<const double> lab
 
     std::vector<int> cls(n);
     for (std::size_t r = 0; r < n; ++r) cls[r] = label_map.index_of(labels[r]);
+    if (warm) {
+        std::lock_guard<std::mutex> lock(g_mu);
+        if (resident_matches(factor.G)) batch_warm_starts(factor, labels, label_map, folds, C, *warm);
+    }
 
     for (int f = 0; f < k; ++f) {
         const auto start = std::chrono::steady_clock::now();
@@ -674,6 +889,12 @@ extern "C" __attribute__((visibility("default"))) long long lpd_adapter_score_ca
 }
 extern "C" __attribute__((visibility("default"))) long long lpd_adapter_block_calls(void) {
     return g_block_calls.load();
+}
+extern "C" __attribute__((visibility("default"))) long long lpd_adapter_qdiag_calls(void) {
+    return g_qdiag_calls.load();
+}
+extern "C" __attribute__((visibility("default"))) long long lpd_adapter_warm_batches(void) {
+    return g_warm_batches.load();
 }
 extern "C" __attribute__((visibility("default"))) long long lpd_adapter_dv_calls(void) {
     return g_dv_calls.load();

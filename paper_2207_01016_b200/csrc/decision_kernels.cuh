@@ -216,22 +216,29 @@ __global__ void __launch_bounds__(256) gather_gw_kernel(const float* __restrict_
     }
 }
 
-// gather_gtv, pass 1: partial[g][j] = Σ_{i in row group g} coef[i]·G[rows[i]][j] (fp64),
-//   block = (column slab × row group), each thread 4 consecutive columns (16-byte loads,
-//   eight rows in flight); pass 2 sums the partials of each column in group order, so
-//   w = Σ_i coef_i·G_i (rebuild_w, dcd.cpp:91-102) is deterministic.
+// gather_gtv, pass 1: partial[g][s][j] = Σ_{i in row group g} coef[i][s0+s]·G[rows[i]][j]
+//   (fp64) for SB coefficient sets at once (one read of each listed G row serves every
+//   set), block = (column slab × row group), each thread 4 consecutive columns (16-byte
+//   loads, eight rows in flight); pass 2 sums the partials of each column in group order,
+//   so w_s = Σ_i coef_i,s·G_i (rebuild_w, dcd.cpp:91-102) is deterministic. SB = 1 is the
+//   single warm start; SB = 8 batches the warm starts of every (fold, pair) problem at a
+//   new C (cross_validate with a WarmStore, modelsel.cpp:104-112).
 constexpr int GTV_ROWS = 256;   // rows per group
 constexpr int GTV_THREADS = 128;
+template <int SB>
 __global__ void __launch_bounds__(GTV_THREADS) gather_gtv_partial_kernel(
     const float* __restrict__ G, long long ldg, int b_eff, const int32_t* __restrict__ rows,
-    const double* __restrict__ coef, int count, double* __restrict__ partial) {
+    const double* __restrict__ coef, long long ldc, int s0, int ns, int count,
+    double* __restrict__ partial) {
     const int g = blockIdx.y;
     const int i0 = g * GTV_ROWS, i1 = min(count, i0 + GTV_ROWS);
     const bool vec = ((ldg & 3) == 0) && ((b_eff & 3) == 0) && ((reinterpret_cast<uintptr_t>(G) & 15) == 0);
     if (vec) {
         const int j4 = blockIdx.x * blockDim.x + threadIdx.x;  // column quad
         if (4 * j4 >= b_eff) return;
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        double acc[SB][4];
+#pragma unroll
+        for (int s = 0; s < SB; ++s) acc[s][0] = acc[s][1] = acc[s][2] = acc[s][3] = 0.0;
         int i = i0;
         for (; i + 8 <= i1; i += 8) {
             float4 v[8];
@@ -240,45 +247,92 @@ __global__ void __launch_bounds__(GTV_THREADS) gather_gtv_partial_kernel(
                 v[u] = ld_stream_f4(reinterpret_cast<const float4*>(G + static_cast<long long>(rows[i + u]) * ldg) + j4);
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
-                const double c = coef[i + u];
-                acc[0] = fma(c, static_cast<double>(v[u].x), acc[0]);
-                acc[1] = fma(c, static_cast<double>(v[u].y), acc[1]);
-                acc[2] = fma(c, static_cast<double>(v[u].z), acc[2]);
-                acc[3] = fma(c, static_cast<double>(v[u].w), acc[3]);
+#pragma unroll
+                for (int s = 0; s < SB; ++s) {
+                    if (s < ns) {
+                        const double c = coef[static_cast<long long>(i + u) * ldc + s0 + s];
+                        acc[s][0] = fma(c, static_cast<double>(v[u].x), acc[s][0]);
+                        acc[s][1] = fma(c, static_cast<double>(v[u].y), acc[s][1]);
+                        acc[s][2] = fma(c, static_cast<double>(v[u].z), acc[s][2]);
+                        acc[s][3] = fma(c, static_cast<double>(v[u].w), acc[s][3]);
+                    }
+                }
             }
         }
         for (; i < i1; ++i) {
             const float4 v = ld_stream_f4(reinterpret_cast<const float4*>(G + static_cast<long long>(rows[i]) * ldg) + j4);
-            const double c = coef[i];
-            acc[0] = fma(c, static_cast<double>(v.x), acc[0]);
-            acc[1] = fma(c, static_cast<double>(v.y), acc[1]);
-            acc[2] = fma(c, static_cast<double>(v.z), acc[2]);
-            acc[3] = fma(c, static_cast<double>(v.w), acc[3]);
-        }
-        double* out = partial + static_cast<long long>(g) * b_eff + 4 * j4;
 #pragma unroll
-        for (int e = 0; e < 4; ++e) out[e] = acc[e];
+            for (int s = 0; s < SB; ++s) {
+                if (s < ns) {
+                    const double c = coef[static_cast<long long>(i) * ldc + s0 + s];
+                    acc[s][0] = fma(c, static_cast<double>(v.x), acc[s][0]);
+                    acc[s][1] = fma(c, static_cast<double>(v.y), acc[s][1]);
+                    acc[s][2] = fma(c, static_cast<double>(v.z), acc[s][2]);
+                    acc[s][3] = fma(c, static_cast<double>(v.w), acc[s][3]);
+                }
+            }
+        }
+#pragma unroll
+        for (int s = 0; s < SB; ++s) {
+            if (s < ns) {
+                double* out = partial + (static_cast<long long>(g) * SB + s) * b_eff + 4 * j4;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) out[e] = acc[s][e];
+            }
+        }
     } else {
-        // scalar path: thread = one column, the grid's x extent covers b_eff / 4 quads,
-        // so each thread handles the 4 columns of its quad in turn
+        // scalar path: thread = one column quad, its 4 columns in turn
         const int j4 = blockIdx.x * blockDim.x + threadIdx.x;
         for (int e = 0; e < 4; ++e) {
             const int j = 4 * j4 + e;
             if (j >= b_eff) return;
-            double acc = 0.0;
-            for (int i = i0; i < i1; ++i)
-                acc = fma(coef[i], static_cast<double>(G[static_cast<long long>(rows[i]) * ldg + j]), acc);
-            partial[static_cast<long long>(g) * b_eff + j] = acc;
+            for (int s = 0; s < ns; ++s) {
+                double acc = 0.0;
+                for (int i = i0; i < i1; ++i)
+                    acc = fma(coef[static_cast<long long>(i) * ldc + s0 + s],
+                              static_cast<double>(G[static_cast<long long>(rows[i]) * ldg + j]), acc);
+                partial[(static_cast<long long>(g) * SB + s) * b_eff + j] = acc;
+            }
         }
     }
 }
-__global__ void gather_gtv_sum_kernel(const double* __restrict__ partial, int groups, int b_eff,
-                                      double* __restrict__ w) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= b_eff) return;
+// pass 2: w[s0 + s][j] = Σ_g partial[g][s][j], groups in order
+__global__ void gather_gtv_sum_kernel(const double* __restrict__ partial, int groups, int sb, int ns,
+                                      int b_eff, int s0, double* __restrict__ w) {
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= static_cast<long long>(ns) * b_eff) return;
+    const int s = static_cast<int>(t / b_eff), j = static_cast<int>(t % b_eff);
     double acc = 0.0;
-    for (int g = 0; g < groups; ++g) acc += partial[static_cast<long long>(g) * b_eff + j];
-    w[j] = acc;
+    for (int g = 0; g < groups; ++g) acc += partial[(static_cast<long long>(g) * sb + s) * b_eff + j];
+    w[static_cast<long long>(s0 + s) * b_eff + j] = acc;
+}
+
+// Row squared norms of the resident G, q_i = Σ_j G_ij² in ascending j with every product
+// rounded then added — the order of make_binary_problem's row.squaredNorm()
+// (dcd.cpp:60-89; the reference build is compiled without FP contraction), so q matches
+// a host pass over the same fp64 G bit for bit. One thread per row, 16-byte loads.
+__global__ void __launch_bounds__(128) row_sqnorm_seq_kernel(const float* __restrict__ G, long long ldg,
+                                                             int rows, int cols, double* __restrict__ q) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= rows) return;
+    const float* g = G + static_cast<long long>(i) * ldg;
+    double s = 0.0;
+    int j = 0;
+    if ((ldg & 3) == 0 && (reinterpret_cast<uintptr_t>(G) & 15) == 0) {
+        for (; j + 4 <= cols; j += 4) {
+            const float4 v = *reinterpret_cast<const float4*>(g + j);
+            const double a = v.x, b = v.y, c = v.z, d = v.w;
+            s = __dadd_rn(s, __dmul_rn(a, a));
+            s = __dadd_rn(s, __dmul_rn(b, b));
+            s = __dadd_rn(s, __dmul_rn(c, c));
+            s = __dadd_rn(s, __dmul_rn(d, d));
+        }
+    }
+    for (; j < cols; ++j) {
+        const double a = g[j];
+        s = __dadd_rn(s, __dmul_rn(a, a));
+    }
+    q[i] = s;
 }
 
 }  // namespace lpd

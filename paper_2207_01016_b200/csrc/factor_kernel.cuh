@@ -241,6 +241,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
     }
     if (warp == 2) tmem_alloc_2sm(tmem_slot, TMEM_COLS);
     tc_fence_before();
+    // the allocator's write of the TMEM address into this CTA's shared memory is ordered
+    // before the reads below by the CTA barrier (compute-sanitizer racecheck models
+    // bar.sync, not the cluster barrier that follows)
+    __syncthreads();
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;

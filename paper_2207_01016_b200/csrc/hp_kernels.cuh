@@ -1,0 +1,170 @@
+// High-precision factor path (LPD_PRECISION=high, or auto for ill-conditioned bases):
+//
+//   Z = exp(−γ·‖x_i − b_j‖²) in fp64 (direct distance, pointdv_z_kernel<false>), then
+//   G = Z · L on the fp64 tensor cores (DMMA, mma.sync m8n8k4 f64), fp64 accumulation.
+//
+// Why: the fast path (K1/K1L) forms Z from split-fp16 operands with fp32 accumulation, so Z
+// carries ~2^-22 relative error, and G = Z·L amplifies it by ‖L‖₂ = 1/√λ_min (L = U·D^-1/2,
+// factor.cpp:68-81). For the paper's own SUSY/Adult setting γ = 2^-7 with the reference
+// default τ = 1e-12 (factor.hpp:59) λ_min/λ_max ≈ 5e-11 and no
+// fp32-level Z can hold a 1e-4 row error. Here Z and the
+// projection are fp64 end to end: the row error is then set by fp64 rounding (≈1e-12·κ).
+//
+// hp_dgemm_nt_kernel: C[i][c] = Σ_k A[i][k]·Bt[c][k], A = Z (M × K, row-major, K a multiple
+// of 16, zero-padded), Bt = Lᵀ (N_pad × K, zero-padded rows and columns). CTA tile 128 × 128,
+// K staged 16 at a time through a 3-stage cp.async ring; 8 warps as 4 (M) × 2 (N), warp tile
+// 32 × 64 = 4 × 8 DMMA tiles (64 fp64 accumulators per thread). Shared-memory rows are
+// padded to 20 doubles so each half-warp's 8×4 fragment read hits 16 distinct bank pairs.
+// Fragments (PTX m8n8k4 .f64, row.col): A[m = lane>>2][k = lane&3], B[k = lane&3][n = lane>>2],
+// C[m = lane>>2][n = 2·(lane&3) + v].
+#pragma once
+
+namespace lpd {
+namespace hp {
+constexpr int BM = 128, BN = 128, BK = 16, STAGES = 3, THREADS = 256;
+constexpr int LDS = BK + 4;  // padded shared row (doubles)
+constexpr int SMEM_BYTES = STAGES * (BM + BN) * LDS * 8;  // 122,880
+}  // namespace hp
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    const int n = valid ? 16 : 0;  // src-size 0: zero fill
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+template <typename OutT>
+__global__ void __launch_bounds__(hp::THREADS, 1)
+    hp_dgemm_nt_kernel(const double* __restrict__ A, long long lda, const double* __restrict__ Bt,
+                       long long ldb, int M, int N, int K, OutT* __restrict__ C, long long ldc) {
+    extern __shared__ __align__(16) double hp_smem[];
+    double* As = hp_smem;                                  // [STAGES][BM][LDS]
+    double* Bs = hp_smem + hp::STAGES * hp::BM * hp::LDS;  // [STAGES][BN][LDS]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp & 3, wn = warp >> 2;  // warp tile origin: rows 32·wm, cols 64·wn
+    const int m0 = blockIdx.y * hp::BM, n0 = blockIdx.x * hp::BN;
+    const int kblocks = K / hp::BK;
+
+    // each thread moves 4 + 4 16-byte pieces per stage: row r = (tid + 256q) >> 3, piece tid & 7
+    auto load = [&](int stage, int kb) {
+        const int k0 = kb * hp::BK;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int e = tid + hp::THREADS * q;
+            const int r = e >> 3, c = (e & 7) * 2;
+            const int gm = m0 + r;
+            const double* srcA = A + static_cast<long long>(gm < M ? gm : 0) * lda + k0 + c;
+            cp_async16(As + (stage * hp::BM + r) * hp::LDS + c, srcA, gm < M);
+            const double* srcB = Bt + static_cast<long long>(n0 + r) * ldb + k0 + c;
+            cp_async16(Bs + (stage * hp::BN + r) * hp::LDS + c, srcB, true);
+        }
+    };
+
+    double acc[4][8][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+    for (int s = 0; s < hp::STAGES - 1; ++s) {
+        if (s < kblocks) load(s, s);
+        cp_async_commit();
+    }
+    const int fr = lane >> 2, fk = lane & 3;
+    for (int kb = 0; kb < kblocks; ++kb) {
+        cp_async_wait<hp::STAGES - 2>();
+        __syncthreads();
+        {  // refill the stage consumed two iterations ago
+            const int nk = kb + hp::STAGES - 1;
+            if (nk < kblocks) load(nk % hp::STAGES, nk);
+            cp_async_commit();
+        }
+        const double* as = As + (kb % hp::STAGES) * hp::BM * hp::LDS;
+        const double* bs = Bs + (kb % hp::STAGES) * hp::BN * hp::LDS;
+#pragma unroll
+        for (int kk = 0; kk < hp::BK; kk += 4) {
+            double a[4], b[8];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = as[(32 * wm + 8 * i + fr) * hp::LDS + kk + fk];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) b[j] = bs[(64 * wn + 8 * j + fr) * hp::LDS + kk + fk];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+        }
+    }
+    cp_async_wait<0>();
+    // epilogue: thread holds C[m][n], C[m][n+1] of each 8×8 tile
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int gm = m0 + 32 * wm + 8 * i + fr;
+        if (gm >= M) continue;
+        OutT* crow = C + static_cast<long long>(gm) * ldc;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int gn = n0 + 64 * wn + 8 * j + 2 * fk;
+            if (gn < N) crow[gn] = static_cast<OutT>(acc[i][j][0]);
+            if (gn + 1 < N) crow[gn + 1] = static_cast<OutT>(acc[i][j][1]);
+        }
+    }
+}
+
+// Lᵀ (fp64, [Beff_pad × K_pad], zero-padded) from L (B × b_eff row-major): 32×32 tiles
+// through shared memory.
+__global__ void hp_transpose_kernel(const double* __restrict__ L, int B, int b_eff, double* __restrict__ LT,
+                                    long long ldt, int Beff_pad, int K_pad) {
+    __shared__ double t[32][33];
+    const int k0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int k = k0 + r, c = c0 + threadIdx.x;
+        t[r][threadIdx.x] = (k < B && c < b_eff) ? L[static_cast<long long>(k) * b_eff + c] : 0.0;
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int c = c0 + r, k = k0 + threadIdx.x;
+        if (c < Beff_pad && k < K_pad) LT[static_cast<long long>(c) * ldt + k] = t[threadIdx.x][r];
+    }
+}
+
+// Column norms of L for the precision choice: the columns of L = U·D^-1/2 are orthogonal
+// with norms 1/√λ_j, so max_j ‖L[:, j]‖² = 1/λ_min and min_j = 1/λ_max (out[0], out[1]; the
+// caller zeroes out[0] and fills out[1] with 0xff bytes). One thread per column (coalesced
+// across a warp); non-negative doubles order like their bit patterns.
+__global__ void col_norm_range_kernel(const double* __restrict__ L, int B, int b_eff, double* __restrict__ out) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    double s = 0.0;
+    if (c < b_eff)
+        for (int k = 0; k < B; ++k) {
+            const double v = L[static_cast<long long>(k) * b_eff + c];
+            s += v * v;
+        }
+    __shared__ double mx[256], mn[256];
+    mx[threadIdx.x] = s;
+    mn[threadIdx.x] = c < b_eff ? s : INFINITY;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) {
+            mx[threadIdx.x] = fmax(mx[threadIdx.x], mx[threadIdx.x + o]);
+            mn[threadIdx.x] = fmin(mn[threadIdx.x], mn[threadIdx.x + o]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        atomicMax(reinterpret_cast<unsigned long long*>(out), static_cast<unsigned long long>(__double_as_longlong(mx[0])));
+        atomicMin(reinterpret_cast<unsigned long long*>(out + 1),
+                  static_cast<unsigned long long>(__double_as_longlong(mn[0])));
+    }
+}
+
+}  // namespace lpd

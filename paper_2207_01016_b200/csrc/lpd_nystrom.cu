@@ -26,6 +26,7 @@
 #include <cmath>
 #include <cstring>
 #include <functional>
+#include <limits>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -38,6 +39,7 @@
 #include "gram_kernels.cuh"
 #include "panel_kernels.cuh"
 #include "pointdv_kernels.cuh"
+#include "hp_kernels.cuh"
 #include "prep_kernels.cuh"
 
 extern "C" void lpd_host_widen_rows(const float* src, int64_t lds, double* dst, int64_t ldd,
@@ -166,6 +168,8 @@ struct Slot {
     int64_t kd = 0;          // plane width the x planes were sized for
     int64_t d_cap = 0;       // columns the fp64 x buffer was sized for
     int64_t nnz_cap = 0;
+    double* hx = nullptr;    // pinned staging of dense X rows (lpd_compute_g_rows)
+    size_t hx_cap = 0;       // bytes
     int64_t* indptr = nullptr;
     int32_t* indices = nullptr;
     double* values = nullptr;
@@ -225,6 +229,22 @@ struct DeviceState {
     cudaEvent_t ring[kRing][2] = {};
     int64_t ring_count = 0;  // launches recorded since the last reset
 
+    // high-precision path (hp_kernels.cuh): chosen per basis by precision_mode and the
+    // conditioning estimate; fp64 landmarks [B × d], Lᵀ [hp_npad × hp_kpad], Z panel scratch
+    int precision_mode = LPD_PRECISION_AUTO;
+    bool hp = false;
+    double cond_est = 0.0;
+    double* hp_norms = nullptr;  // [2] column-norm range of L
+    double* hp_lm = nullptr;
+    double* hp_lt = nullptr;
+    double* hp_z = nullptr;
+    int64_t hp_kpad = 0, hp_npad = 0, hp_z_rows = 0, hp_z_ld = 0;
+    size_t hp_lm_cap = 0, hp_lt_cap = 0;
+    void free_hp() {
+        dev_free(hp_lm); dev_free(hp_lt); dev_free(hp_z);
+        hp_lm_cap = hp_lt_cap = 0;
+        hp_z_rows = hp_z_ld = 0;
+    }
     // K8 (lpd_set_model_* / lpd_model_decision_values_*): a trained OVO model's fp64
     // landmarks [B × d] and betas [P × B], plus the per-call point chunk buffers
     struct ModelState {
@@ -258,11 +278,15 @@ struct DeviceState {
         dev_free(mu); dev_free(lm_hi); dev_free(lm_lo); dev_free(consts); dev_free(lm_nb); dev_free(lm_mx);
         dev_free(lt_hi); dev_free(lt_lo); dev_free(col_scale);
         dev_free(z_hi); dev_free(z_lo);
+        free_hp();
         cap = {};
         z_rows = 0;
         has_basis = false;
     }
     void free_slot(Slot& s) {
+        if (s.hx) cudaFreeHost(s.hx);
+        s.hx = nullptr;
+        s.hx_cap = 0;
         dev_free(s.x); dev_free(s.xhi); dev_free(s.xlo); dev_free(s.raux); dev_free(s.g);
         dev_free(s.indptr); dev_free(s.indices); dev_free(s.values);
         s.rows_cap = 0; s.g_cols = 0; s.g_elems = 0; s.nnz_cap = 0;
@@ -346,6 +370,15 @@ void init_device(DeviceState& ds, int device) {
     for (auto& e : ds.kev) CUDA_TRY(cudaEventCreate(&e));
     dev_alloc(&ds.err, 1);
     CUDA_TRY(cudaMemset(ds.err, 0, sizeof(int)));
+    {
+        const char* e = std::getenv("LPD_PRECISION");  // auto (default) | fast | high
+        if (e && std::strcmp(e, "fast") == 0) ds.precision_mode = LPD_PRECISION_FAST;
+        if (e && std::strcmp(e, "high") == 0) ds.precision_mode = LPD_PRECISION_HIGH;
+    }
+    CUDA_TRY(cudaFuncSetAttribute(lpd::hp_dgemm_nt_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  lpd::hp::SMEM_BYTES));
+    CUDA_TRY(cudaFuncSetAttribute(lpd::hp_dgemm_nt_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  lpd::hp::SMEM_BYTES));
     for (auto& pr : ds.ring)
         for (auto& e : pr) CUDA_TRY(cudaEventCreate(&e));
     for (int ks = 1; ks <= 4; ++ks) {
@@ -371,7 +404,12 @@ void init_device(DeviceState& ds, int device) {
             reinterpret_cast<const void*>(lpd::ovo_vote_kernel<float>),
             reinterpret_cast<const void*>(lpd::ovo_pair_table_kernel),
             reinterpret_cast<const void*>(lpd::gather_gw_kernel<4>),
-            reinterpret_cast<const void*>(lpd::gather_gtv_partial_kernel),
+            reinterpret_cast<const void*>(lpd::gather_gtv_partial_kernel<1>),
+            reinterpret_cast<const void*>(lpd::gather_gtv_partial_kernel<8>),
+            reinterpret_cast<const void*>(lpd::row_sqnorm_seq_kernel),
+            reinterpret_cast<const void*>(lpd::pointdv_z_kernel<true>),
+            reinterpret_cast<const void*>(lpd::pointdv_z_kernel<false>),
+            reinterpret_cast<const void*>(lpd::pointdv_beta_kernel),
             reinterpret_cast<const void*>(lpd::gather_gtv_sum_kernel),
         };
         for (const void* f : fns) CUDA_TRY(cudaFuncGetAttributes(&fa, f));
@@ -400,6 +438,119 @@ void validate_basis_args(int64_t B, int64_t d, int64_t b_eff, double gamma, cons
 // L (B × b_eff, row-major), both already on that device. Buffers are reused when
 // the padded shapes are unchanged (new γ / new L on the same budget is the
 // common case: grid search, reference modelsel.cpp:180-190).
+// Precision choice per basis. The fast path's Z carries ~2^-22 relative error
+// and G = Z·L amplifies it by ‖L‖₂·‖Z_i‖/‖G_i‖ ≤ √(λ_max/λ_min); estimate = 2^-22·√(λ_max/λ_min)
+// from the column norms of L (1/√λ_j). Measured max row error / estimate: C1 1.2, C2 1.1,
+// C3 0.41. LPD_PRECISION_AUTO takes the high-precision path when the estimate exceeds
+// LPD_HP_THRESHOLD (default 2.5e-4): the paper's γ = 2^-7, τ = 1e-12 SUSY basis (estimate
+// 3.4e-2) goes there, C1–C4 stay on the tensor-core fast path.
+double hp_threshold() {
+    static const double t = [] {
+        const char* e = std::getenv("LPD_HP_THRESHOLD");
+        return e ? std::atof(e) : 2.5e-4;
+    }();
+    return t;
+}
+
+void choose_precision(DeviceState& ds, const double* lm_dev, int64_t B, int64_t d, int64_t ld_lm,
+                      const double* L_dev, int64_t b_eff, cudaStream_t st) {
+    if (!ds.hp_norms) dev_alloc(&ds.hp_norms, 2);
+    CUDA_TRY(cudaMemsetAsync(ds.hp_norms, 0, sizeof(double), st));
+    CUDA_TRY(cudaMemsetAsync(ds.hp_norms + 1, 0xff, sizeof(double), st));
+    lpd::col_norm_range_kernel<<<static_cast<int>((b_eff + 255) / 256), 256, 0, st>>>(
+        L_dev, static_cast<int>(B), static_cast<int>(b_eff), ds.hp_norms);
+    CUDA_TRY(cudaGetLastError());
+    double h[2] = {0.0, 0.0};
+    CUDA_TRY(cudaMemcpyAsync(h, ds.hp_norms, sizeof(h), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    ds.cond_est = (h[1] > 0.0 && std::isfinite(h[0])) ? std::ldexp(std::sqrt(h[0] / h[1]), -22)
+                                                      : std::numeric_limits<double>::infinity();
+    ds.hp = ds.precision_mode == LPD_PRECISION_HIGH ||
+            (ds.precision_mode == LPD_PRECISION_AUTO && ds.cond_est > hp_threshold());
+    if (!ds.hp) return;
+    // fp64 landmarks (packed B × max(d, 1)) and Lᵀ (zero-padded to 128-row N tiles and a
+    // K that is a multiple of 16) for the DMMA projection
+    const int64_t dp = std::max<int64_t>(d, 1);
+    const int64_t kpad = round_up(B, lpd::hp::BK), npad = round_up(b_eff, lpd::hp::BN);
+    if (ds.hp_lm_cap < static_cast<size_t>(B * dp)) {
+        CUDA_TRY(cudaStreamSynchronize(st));
+        dev_free(ds.hp_lm);
+        dev_alloc(&ds.hp_lm, static_cast<size_t>(B * dp));
+        ds.hp_lm_cap = static_cast<size_t>(B * dp);
+    }
+    if (ds.hp_lt_cap < static_cast<size_t>(npad * kpad)) {
+        CUDA_TRY(cudaStreamSynchronize(st));
+        dev_free(ds.hp_lt);
+        dev_alloc(&ds.hp_lt, static_cast<size_t>(npad * kpad));
+        ds.hp_lt_cap = static_cast<size_t>(npad * kpad);
+    }
+    if (d > 0)
+        CUDA_TRY(cudaMemcpy2DAsync(ds.hp_lm, sizeof(double) * dp, lm_dev, sizeof(double) * ld_lm, sizeof(double) * d,
+                                   static_cast<size_t>(B), cudaMemcpyDeviceToDevice, st));
+    const dim3 tg(static_cast<unsigned>(kpad / 16 * 16 / 32 + (kpad % 32 ? 1 : 0)), static_cast<unsigned>(npad / 32));
+    lpd::hp_transpose_kernel<<<tg, dim3(32, 8), 0, st>>>(L_dev, static_cast<int>(B), static_cast<int>(b_eff), ds.hp_lt,
+                                                         kpad, static_cast<int>(npad), static_cast<int>(kpad));
+    CUDA_TRY(cudaGetLastError());
+    if (ds.hp_z_ld != kpad) {  // the Z panel's padding columns must read as 0 (Lᵀ's are 0 too)
+        CUDA_TRY(cudaStreamSynchronize(st));
+        dev_free(ds.hp_z);
+        ds.hp_z_rows = 0;
+        ds.hp_z_ld = kpad;
+    }
+    ds.hp_kpad = kpad;
+    ds.hp_npad = npad;
+}
+
+// High-precision factor launch (hp_kernels.cuh) for m rows of fp64 X on the device: per row
+// panel (≤ 1 GB of fp64 Z), Z by direct distance, then G = Z·L on DMMA.
+void launch_factor_hp(DeviceState& ds, const double* x_dev, int64_t m, int64_t ldx, void* g_dev, int64_t ldg,
+                      int out_dtype, cudaStream_t st, bool time_it) {
+    const int64_t kpad = ds.hp_kpad;
+    const int64_t panel = std::min<int64_t>(round_up(m, lpd::hp::BM),
+                                            std::max<int64_t>(lpd::hp::BM, ((int64_t(1) << 30) / (8 * kpad)) /
+                                                                               lpd::hp::BM * lpd::hp::BM));
+    if (ds.hp_z_rows < panel) {
+        CUDA_TRY(cudaStreamSynchronize(st));
+        dev_free(ds.hp_z);
+        dev_alloc(&ds.hp_z, static_cast<size_t>(panel * kpad));
+        CUDA_TRY(cudaMemsetAsync(ds.hp_z, 0, sizeof(double) * static_cast<size_t>(panel * kpad), st));
+        ds.hp_z_rows = panel;
+    }
+    cudaEvent_t* pr = nullptr;
+    if (time_it) {
+        pr = ds.ring[ds.ring_count % DeviceState::kRing];
+        CUDA_TRY(cudaEventRecord(ds.kev[0], st));
+        if (ds.ring_count < DeviceState::kRing) CUDA_TRY(cudaEventRecord(pr[0], st));
+    }
+    const size_t es = out_dtype == LPD_OUT_F64 ? 8 : 4;
+    for (int64_t r0 = 0; r0 < m; r0 += panel) {
+        const int64_t rows = std::min(panel, m - r0);
+        const dim3 gz(static_cast<unsigned>((ds.B + lpd::DV_T - 1) / lpd::DV_T),
+                      static_cast<unsigned>((rows + lpd::DV_T - 1) / lpd::DV_T));
+        lpd::pointdv_z_kernel<false><<<gz, 256, 0, st>>>(x_dev + r0 * ldx, ldx, static_cast<int>(rows),
+                                                        static_cast<int>(ds.d), ds.hp_lm, std::max<int64_t>(ds.d, 1),
+                                                        static_cast<int>(ds.B), static_cast<int>(ds.d), ds.gamma,
+                                                        ds.hp_z, kpad);
+        const dim3 gg(static_cast<unsigned>(ds.hp_npad / lpd::hp::BN),
+                      static_cast<unsigned>((rows + lpd::hp::BM - 1) / lpd::hp::BM));
+        void* gout = static_cast<char*>(g_dev) + static_cast<size_t>(r0) * ldg * es;
+        if (out_dtype == LPD_OUT_F64)
+            lpd::hp_dgemm_nt_kernel<double><<<gg, lpd::hp::THREADS, lpd::hp::SMEM_BYTES, st>>>(
+                ds.hp_z, kpad, ds.hp_lt, kpad, static_cast<int>(rows), static_cast<int>(ds.b_eff),
+                static_cast<int>(kpad), static_cast<double*>(gout), ldg);
+        else
+            lpd::hp_dgemm_nt_kernel<float><<<gg, lpd::hp::THREADS, lpd::hp::SMEM_BYTES, st>>>(
+                ds.hp_z, kpad, ds.hp_lt, kpad, static_cast<int>(rows), static_cast<int>(ds.b_eff),
+                static_cast<int>(kpad), static_cast<float*>(gout), ldg);
+        CUDA_TRY(cudaGetLastError());
+    }
+    if (time_it) {
+        CUDA_TRY(cudaEventRecord(ds.kev[1], st));
+        if (ds.ring_count < DeviceState::kRing) CUDA_TRY(cudaEventRecord(pr[1], st));
+        ++ds.ring_count;
+    }
+}
+
 void build_basis(DeviceState& ds, const double* lm_dev, int64_t B, int64_t d, int64_t ld_lm,
                  const double* L_dev, int64_t b_eff, double gamma, cudaStream_t st, bool sync) {
     CUDA_TRY(cudaSetDevice(ds.device));
@@ -478,6 +629,7 @@ void build_basis(DeviceState& ds, const double* lm_dev, int64_t B, int64_t d, in
                                                         ds.lt_lo, static_cast<int>(B_pad),
                                                         static_cast<int>(Beff_pad), ds.col_scale);
     CUDA_TRY(cudaGetLastError());
+    choose_precision(ds, lm_dev, B, d, ld_lm, L_dev, b_eff, st);
     if (sync) CUDA_TRY(cudaStreamSynchronize(st));
     ds.has_basis = true;
 }
@@ -505,25 +657,64 @@ struct PhaseTrace {
 
 void h2d_staged(DeviceState& ds, void* dst, const void* src, size_t bytes, cudaStream_t st);
 
-void build_basis_host_L(DeviceState& ds, const double* lm_dev, int64_t B, int64_t d,
-                        const double* L_host, int64_t b_eff, double gamma) {
-    CUDA_TRY(cudaSetDevice(ds.device));
-    cudaStream_t st = ds.slot[0].stream;
-    PhaseTrace tr{"set_basis"};
-    double* L_dev = nullptr;
-    dev_alloc(&L_dev, static_cast<size_t>(B * b_eff));
-    tr.lap("alloc L");
-    try {
-        h2d_staged(ds, L_dev, L_host, sizeof(double) * B * b_eff, st);
-        tr.lap("H2D L");
-        build_basis(ds, lm_dev, B, d, std::max<int64_t>(d, 1), L_dev, b_eff, gamma, st, true);
-        tr.lap("prep + sync");
-    } catch (...) {
-        dev_free(L_dev);
-        throw;
+// A device buffer freed on scope exit (basis staging).
+struct DevBuf {
+    void* p = nullptr;
+    int device = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    void alloc(int dev, size_t bytes) {
+        device = dev;
+        CUDA_TRY(cudaSetDevice(dev));
+        CUDA_TRY(cudaMalloc(&p, std::max<size_t>(bytes, 8)));
     }
-    dev_free(L_dev);
-    tr.lap("free L");
+    ~DevBuf() {
+        if (p) {
+            cudaSetDevice(device);
+            cudaFree(p);
+        }
+    }
+    double* d() { return static_cast<double*>(p); }
+};
+
+// The basis of one γ on every device of the context ("one broadcast of
+// the basis per γ"): the landmarks (dense fp64 [B × max(d, 1)], produced on the first
+// device by fill_lm0) and L go up from the host ONCE, to the first device; the other
+// devices copy both from it device-to-device (cudaMemcpyPeerAsync: NVLink / NVSwitch on a
+// B200 node, peer access enabled at context creation), then every device builds its
+// split planes (K2) in parallel. The reference shares one L across all row chunks
+// (factor.cpp:94-107).
+template <typename FillLm0>
+void set_basis_all(lpd_context* ctx, int64_t B, int64_t d, const double* L_host, int64_t b_eff, double gamma,
+                   FillLm0&& fill_lm0) {
+    DeviceState& d0 = ctx->dev[0];
+    const size_t lm_bytes = sizeof(double) * static_cast<size_t>(B * std::max<int64_t>(d, 1));
+    const size_t L_bytes = sizeof(double) * static_cast<size_t>(B * b_eff);
+    PhaseTrace tr{"set_basis"};
+    DevBuf lm0, L0;
+    lm0.alloc(d0.device, lm_bytes);
+    L0.alloc(d0.device, L_bytes);
+    cudaStream_t st0 = d0.slot[0].stream;
+    fill_lm0(d0, lm0.d());
+    h2d_staged(d0, L0.d(), L_host, L_bytes, st0);
+    CUDA_TRY(cudaStreamSynchronize(st0));
+    tr.lap("H2D to device 0");
+    run_parallel(ctx, [&](DeviceState& ds, int di) {
+        CUDA_TRY(cudaSetDevice(ds.device));
+        cudaStream_t st = ds.slot[0].stream;
+        if (di == 0) {
+            build_basis(ds, lm0.d(), B, d, std::max<int64_t>(d, 1), L0.d(), b_eff, gamma, st, true);
+            return;
+        }
+        DevBuf lm, L;
+        lm.alloc(ds.device, lm_bytes);
+        L.alloc(ds.device, L_bytes);
+        CUDA_TRY(cudaMemcpyPeerAsync(lm.p, ds.device, lm0.p, d0.device, lm_bytes, st));
+        CUDA_TRY(cudaMemcpyPeerAsync(L.p, ds.device, L0.p, d0.device, L_bytes, st));
+        build_basis(ds, lm.d(), B, d, std::max<int64_t>(d, 1), L.d(), b_eff, gamma, st, true);
+    });
+    tr.lap("peer copies + K2");
 }
 
 // K chunks (of 64) per fp32 accumulator segment: each segment's tensor-core sum
@@ -689,6 +880,10 @@ void launch_factor_panels(DeviceState& ds, Slot& s, int64_t m, void* g_dev, int6
 void launch_factor(DeviceState& ds, Slot& s, const double* x_dev, int64_t m, int64_t ldx,
                    void* g_dev, int64_t ldg, int out_dtype, cudaStream_t st, bool time_it) {
     if (m <= 0) return;
+    if (ds.hp) {
+        launch_factor_hp(ds, x_dev, m, ldx, g_dev, ldg, out_dtype, st, time_it);
+        return;
+    }
     const int64_t m_pad = round_up(m, lpd::k1::PM);
     {
         const int threads = 256, rows_per_block = threads / 32;
@@ -790,6 +985,8 @@ void check_range_flag(DeviceState& ds) {
     CUDA_TRY(cudaMemcpy(&flag, ds.err, sizeof(int), cudaMemcpyDeviceToHost));
     if (flag) {
         CUDA_TRY(cudaMemset(ds.err, 0, sizeof(int)));
+        if (flag & LPD_FLAG_BAD_INDEX)
+            fail(LPD_ERR_INVALID_ARGUMENT, "CSR feature index outside [0, d)");
         fail(LPD_ERR_UNSUPPORTED,
              "point features too large for the split-fp16 operands (|x - mean| >= 2^28)");
     }
@@ -886,11 +1083,40 @@ private:
 
 // dst[r][c] = src[r][c] (fp32 -> fp64) for rows [0, rows), split over the team
 // (host_widen.cpp: AVX-512 streaming stores).
+// First touch of a contiguous stretch [a, e) of the caller's G, ahead of its widening, by
+// worker w of T: the 4 KB pages are dealt out by 2 MB (huge) page, so each huge page is
+// faulted — and zeroed by the kernel — by exactly one thread. Widening a fresh Matrix
+// (the reference's compute_G returns a new one every call, factor.cpp:93) otherwise has
+// every 2 MB fault contended by the threads whose row slices share it. Only addresses
+// inside [a, e) are written (a 0.0 the widening overwrites later), so the stretches of
+// neighbouring sub-chunks are never touched.
+void prefault_stretch(int w, int T, double* a, double* e) {
+    const uintptr_t ua = reinterpret_cast<uintptr_t>(a), ue = reinterpret_cast<uintptr_t>(e);
+    if (ue <= ua) return;
+    for (uintptr_t pg = ua >> 12; pg <= (ue - 1) >> 12; ++pg) {
+        if (static_cast<int>((pg >> 9) % static_cast<uintptr_t>(T)) != w) continue;
+        const uintptr_t at = std::max(pg << 12, (ua + 7) & ~uintptr_t(7));
+        if (at < ue) *reinterpret_cast<volatile double*>(at) = 0.0;
+    }
+}
+
+// LPD_PREFAULT: sub-chunks of look-ahead for the first touch (default 4; 0 = off)
+int prefault_ahead() {
+    static const int v = [] {
+        const char* e = std::getenv("LPD_PREFAULT");
+        return e ? std::max(0, std::atoi(e)) : 4;
+    }();
+    return v;
+}
+
+// Widen fp32 rows into the caller's fp64 G; optionally first-touch a later stretch
+// [pf_a, pf_e) of G in the same team pass (prefault_stretch).
 void widen_rows(SpinTeam& team, const float* src, int64_t lds, double* dst, int64_t ldd,
-                int64_t rows, int64_t cols) {
+                int64_t rows, int64_t cols, double* pf_a = nullptr, double* pf_e = nullptr) {
     const int T = team.size();
     team.run([&](int w) {
         lpd_host_widen_rows(src, lds, dst, ldd, rows * w / T, rows * (w + 1) / T, cols);
+        if (pf_a) prefault_stretch(w, T, pf_a, pf_e);
     });
 }
 
@@ -932,6 +1158,22 @@ void ensure_delivery_ring(DeviceState& ds) {
         CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         ds.dring_ev.push_back(e);
     }
+}
+
+// Peer access from every device of the context to the first (the basis broadcast reads
+// it over NVLink); best effort — cudaMemcpyPeerAsync also works without it.
+void enable_peers(lpd_context* ctx) {
+    const int d0 = ctx->dev[0].device;
+    for (size_t i = 1; i < ctx->dev.size(); ++i) {
+        const int di = ctx->dev[i].device;
+        if (di == d0) continue;
+        int can = 0;
+        if (cudaDeviceCanAccessPeer(&can, di, d0) == cudaSuccess && can) {
+            cudaSetDevice(di);
+            if (cudaDeviceEnablePeerAccess(d0, 0) != cudaSuccess) cudaGetLastError();
+        }
+    }
+    cudaSetDevice(d0);
 }
 
 lpd_context* check_ctx(lpd_context* ctx, bool need_basis) {
@@ -1109,7 +1351,7 @@ void compute_rows_host(lpd_context* ctx, int64_t n, double* G, int64_t ldg, lpd_
                 h2d[di] += elapsed(s.ev[0], s.ev[1]);
                 ker[di] += elapsed(s.ev[1], s.ev[2]);
             }
-            stage_x(ds, s, c0, rows);  // records ev[0] and fills s.x
+            stage_x(ds, s, c0, rows, team);  // records ev[0] and fills s.x
             CUDA_TRY(cudaEventRecord(s.ev[1], s.stream));
             // the slot's device G buffer: chunk k-2's D2H must have drained
             if (k >= 2 && !resident) CUDA_TRY(cudaStreamWaitEvent(s.stream, s.ev[5], 0));
@@ -1148,6 +1390,27 @@ void compute_rows_host(lpd_context* ctx, int64_t n, double* G, int64_t ldg, lpd_
             }
         };
         for (size_t g = 0; g < subs.size() && g < static_cast<size_t>(R); ++g) enqueue(g);
+        // first touch of the caller's G runs `ahead` sub-chunks in front of the widening
+        // (contiguous G only: with ldg > b_eff the gaps are the caller's)
+        const size_t ahead = ldg == b_eff ? static_cast<size_t>(prefault_ahead()) : 0;
+        // every `every`-th round touches `every` sub-chunks: about one 2 MB page per worker,
+        // so the faults of a round are spread over the whole team
+        const size_t sub_bytes = static_cast<size_t>(sub_rows * ldg) * sizeof(double);
+        const size_t every = std::max<size_t>(1, (static_cast<size_t>(team.size()) << 21) / std::max<size_t>(1, sub_bytes));
+        // G rows of sub-chunks [g0, g1) (consecutive sub-chunks are consecutive rows)
+        auto stretch = [&](size_t g0, size_t g1, double*& a, double*& e) {
+            a = e = nullptr;
+            g1 = std::min(g1, subs.size());
+            if (ahead == 0 || g0 >= g1) return;
+            a = G + subs[g0].r0 * ldg;
+            e = G + (subs[g1 - 1].r0 + subs[g1 - 1].rows) * ldg;
+        };
+        if (ahead > 0) {
+            double *a, *e;
+            stretch(0, ahead, a, e);
+            const int T = team.size();
+            if (a) team.run([&](int w) { prefault_stretch(w, T, a, e); });
+        }
         double widen_s = 0.0;
         for (size_t g = 0; g < subs.size(); ++g) {
             const Sub& u = subs[g];
@@ -1155,7 +1418,9 @@ void compute_rows_host(lpd_context* ctx, int64_t n, double* G, int64_t ldg, lpd_
             while ((q = cudaEventQuery(ds.dring_ev[g % R])) == cudaErrorNotReady) std::this_thread::yield();
             if (q != cudaSuccess) CUDA_TRY(q);
             const auto w0 = std::chrono::steady_clock::now();
-            widen_rows(team, ds.dring[g % R], g_ld, G + u.r0 * ldg, ldg, u.rows, b_eff);
+            double *pa = nullptr, *pe = nullptr;
+            if (g % every == 0) stretch(g + ahead, g + ahead + every, pa, pe);
+            widen_rows(team, ds.dring[g % R], g_ld, G + u.r0 * ldg, ldg, u.rows, b_eff, pa, pe);
             widen_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
             if (u.last) d2h[di] += elapsed(ds.slot[u.k & 1].ev[3], ds.slot[u.k & 1].ev[4]);
             if (g + R < subs.size()) enqueue(g + R);
@@ -1210,7 +1475,7 @@ void stage_csr_rows(DeviceState& ds, Slot& s, int64_t r0, int64_t rows, int64_t 
     }
     if (d > 0)
         lpd::csr_to_dense_kernel<<<static_cast<int>((rows + 7) / 8), 256, 0, s.stream>>>(
-            s.indptr, s.indices, s.values, static_cast<int>(rows), static_cast<int>(d), s.x);
+            s.indptr, s.indices, s.values, static_cast<int>(rows), static_cast<int>(d), s.x, ds.err);
     CUDA_TRY(cudaGetLastError());
     // ip must outlive the async copy: synchronise the H2D before returning
     CUDA_TRY(cudaStreamSynchronize(s.stream));
@@ -1423,7 +1688,7 @@ void model_decision_values(lpd_context* ctx, int64_t n, const HostRows& xs, doub
                                      cudaMemcpyHostToDevice, st));
         const dim3 gz(static_cast<unsigned>((m.B + lpd::DV_T - 1) / lpd::DV_T),
                       static_cast<unsigned>((rows + lpd::DV_T - 1) / lpd::DV_T));
-        lpd::pointdv_z_kernel<<<gz, 256, 0, st>>>(m.x, std::max<int64_t>(xs.d, 1), static_cast<int>(rows),
+        lpd::pointdv_z_kernel<true><<<gz, 256, 0, st>>>(m.x, std::max<int64_t>(xs.d, 1), static_cast<int>(rows),
                                                   static_cast<int>(xs.d), m.lm, std::max<int64_t>(m.d, 1),
                                                   static_cast<int>(m.B), static_cast<int>(m.d), m.gamma, m.zt,
                                                   rows);
@@ -1438,6 +1703,73 @@ void model_decision_values(lpd_context* ctx, int64_t n, const HostRows& xs, doub
         for (int64_t i = 0; i < rows; ++i)
             std::memcpy(D + (r0 + i) * ldd, m.hd + i * m.P, sizeof(double) * static_cast<size_t>(m.P));
     }
+}
+
+// W[s] = Σ_i coef[i][s]·G[rows[i]] for `sets` coefficient vectors (coef row-major, count ×
+// sets) over the resident G: per device its listed rows, SB = 8 sets per read of the rows,
+// fixed group then device order (deterministic). rebuild_w (dcd.cpp:91-102), one set or
+// the warm starts of every (fold, pair) problem at once.
+void resident_gtv_sets(lpd_context* ctx, const int32_t* rows, const double* coef, int64_t count, int64_t sets,
+                       double* W) {
+    check_resident(ctx, rows, count);
+    const int64_t b_eff = ctx->res_b_eff;
+    if (sets <= 0) fail(LPD_ERR_INVALID_ARGUMENT, "sets must be positive");
+    if (!W) fail(LPD_ERR_INVALID_ARGUMENT, "null w");
+    if (count > 0 && !coef) fail(LPD_ERR_INVALID_ARGUMENT, "null coef");
+    std::fill(W, W + sets * b_eff, 0.0);
+    if (count == 0) return;
+    const bool single = ctx->dev.size() == 1 && ctx->dev[0].res_r0 == 0;
+    auto parts = single ? std::vector<std::vector<std::pair<int32_t, int64_t>>>(1) : split_rows(ctx, rows, count);
+    const int nd = static_cast<int>(ctx->dev.size());
+    const int SB = sets == 1 ? 1 : 8;
+    std::vector<std::vector<double>> partial(nd);
+    run_parallel(ctx, [&](DeviceState& ds, int di) {
+        const auto& part = parts[static_cast<size_t>(di)];
+        if (!single && part.empty()) return;
+        CUDA_TRY(cudaSetDevice(ds.device));
+        cudaStream_t st = ds.slot[0].stream;
+        const int64_t m = single ? count : static_cast<int64_t>(part.size());
+        const int64_t groups = (m + lpd::GTV_ROWS - 1) / lpd::GTV_ROWS;
+        const size_t off_c = round_up(sizeof(int32_t) * m, 256);
+        const size_t off_p = off_c + round_up(sizeof(double) * m * sets, 256);
+        const size_t off_w = off_p + round_up(sizeof(double) * groups * SB * b_eff, 256);
+        char* base = static_cast<char*>(scratch(ds, off_w + sizeof(double) * sets * b_eff));
+        std::vector<int32_t> local(single ? 0 : static_cast<size_t>(m));
+        std::vector<double> lc(single ? 0 : static_cast<size_t>(m * sets));
+        for (int64_t i = 0; i < static_cast<int64_t>(local.size()); ++i) {
+            local[i] = part[i].first;
+            std::memcpy(lc.data() + i * sets, coef + part[i].second * sets, sizeof(double) * sets);
+        }
+        int32_t* drows = reinterpret_cast<int32_t*>(base);
+        double* dc = reinterpret_cast<double*>(base + off_c);
+        double* dp = reinterpret_cast<double*>(base + off_p);
+        double* dw = reinterpret_cast<double*>(base + off_w);
+        CUDA_TRY(cudaMemcpyAsync(drows, single ? rows : local.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaMemcpyAsync(dc, single ? coef : lc.data(), sizeof(double) * m * sets, cudaMemcpyHostToDevice, st));
+        // each thread owns 4 consecutive columns
+        const dim3 grid(static_cast<unsigned>(((b_eff + 3) / 4 + lpd::GTV_THREADS - 1) / lpd::GTV_THREADS),
+                        static_cast<unsigned>(groups));
+        for (int64_t s0 = 0; s0 < sets; s0 += SB) {
+            const int ns = static_cast<int>(std::min<int64_t>(SB, sets - s0));
+            if (SB == 1)
+                lpd::gather_gtv_partial_kernel<1><<<grid, lpd::GTV_THREADS, 0, st>>>(
+                    ds.res_g, ds.res_ld, static_cast<int>(b_eff), drows, dc, sets, static_cast<int>(s0), ns,
+                    static_cast<int>(m), dp);
+            else
+                lpd::gather_gtv_partial_kernel<8><<<grid, lpd::GTV_THREADS, 0, st>>>(
+                    ds.res_g, ds.res_ld, static_cast<int>(b_eff), drows, dc, sets, static_cast<int>(s0), ns,
+                    static_cast<int>(m), dp);
+            lpd::gather_gtv_sum_kernel<<<static_cast<int>((ns * b_eff + 255) / 256), 256, 0, st>>>(
+                dp, static_cast<int>(groups), SB, ns, static_cast<int>(b_eff), static_cast<int>(s0), dw);
+            CUDA_TRY(cudaGetLastError());
+        }
+        partial[di].resize(static_cast<size_t>(sets * b_eff));
+        CUDA_TRY(cudaMemcpyAsync(partial[di].data(), dw, sizeof(double) * sets * b_eff, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+    });
+    for (int di = 0; di < nd; ++di)  // fixed device order: deterministic
+        if (!partial[di].empty())
+            for (int64_t j = 0; j < sets * b_eff; ++j) W[j] += partial[di][j];
 }
 
 }  // namespace
@@ -1481,6 +1813,7 @@ int lpd_context_create(lpd_context** out, int num_devices) {
                 init_device(ctx->dev[i], i);
                 ctx->dev[i].host_share = want;
             }
+            enable_peers(ctx);
         } catch (...) {
             lpd_context_destroy(ctx);
             throw;
@@ -1506,6 +1839,7 @@ int lpd_context_create_devices(lpd_context** out, const int* device_ids, int cou
                 init_device(ctx->dev[i], device_ids[i]);
                 ctx->dev[i].host_share = count;
             }
+            enable_peers(ctx);
         } catch (...) {
             lpd_context_destroy(ctx);
             throw;
@@ -1527,6 +1861,8 @@ int lpd_context_destroy(lpd_context* ctx) {
         dev_free(ds.res_g);
         dev_free(ds.sync_ctr);
         ds.model.free_all();
+        ds.free_hp();
+        dev_free(ds.hp_norms);
         if (ds.scratch) cudaFree(ds.scratch);
         if (ds.gtmp) cudaFree(ds.gtmp);
         for (auto& s : ds.slot) {
@@ -1560,25 +1896,14 @@ int lpd_set_basis_dense(lpd_context* ctx, const double* landmarks, int64_t B, in
         validate_basis_args(B, d, b_eff, gamma, L);
         if (!landmarks && d > 0) fail(LPD_ERR_INVALID_ARGUMENT, "landmarks is null");
         if (ld < d) fail(LPD_ERR_INVALID_ARGUMENT, "landmark leading dimension < d");
-        run_parallel(ctx, [&](DeviceState& ds, int) {
-            CUDA_TRY(cudaSetDevice(ds.device));
-            double* lm = nullptr;
-            dev_alloc(&lm, static_cast<size_t>(B * std::max<int64_t>(d, 1)));
+        set_basis_all(ctx, B, d, L, b_eff, gamma, [&](DeviceState& ds, double* lm) {
             if (d > 0 && ld == d)
                 h2d_staged(ds, lm, landmarks, sizeof(double) * static_cast<size_t>(B * d), ds.slot[0].stream);
             else if (d > 0)
-                CUDA_TRY(cudaMemcpy2D(lm, sizeof(double) * d, landmarks, sizeof(double) * ld,
-                                      sizeof(double) * d, static_cast<size_t>(B),
-                                      cudaMemcpyHostToDevice));
+                CUDA_TRY(cudaMemcpy2D(lm, sizeof(double) * d, landmarks, sizeof(double) * ld, sizeof(double) * d,
+                                      static_cast<size_t>(B), cudaMemcpyHostToDevice));
             else
-                CUDA_TRY(cudaMemset(lm, 0, sizeof(double)));
-            try {
-                build_basis_host_L(ds, lm, B, d, L, b_eff, gamma);
-            } catch (...) {
-                dev_free(lm);
-                throw;
-            }
-            dev_free(lm);
+                CUDA_TRY(cudaMemset(lm, 0, sizeof(double) * static_cast<size_t>(B)));
         });
     });
 }
@@ -1593,33 +1918,27 @@ int lpd_set_basis_csr(lpd_context* ctx, int64_t B, int64_t d, const int64_t* ind
         const int64_t nnz = indptr[B] - indptr[0];
         if (nnz < 0) fail(LPD_ERR_INVALID_ARGUMENT, "indptr is not monotone");
         if (nnz > 0 && (!indices || !values)) fail(LPD_ERR_INVALID_ARGUMENT, "CSR arrays are null");
-        run_parallel(ctx, [&](DeviceState& ds, int) {
-            CUDA_TRY(cudaSetDevice(ds.device));
+        set_basis_all(ctx, B, d, L, b_eff, gamma, [&](DeviceState& ds, double* lm) {
             std::vector<int64_t> ip(static_cast<size_t>(B + 1));
             for (int64_t i = 0; i <= B; ++i) ip[i] = indptr[i] - indptr[0];
-            int64_t *dip = nullptr;
-            int32_t* didx = nullptr;
-            double *dval = nullptr, *lm = nullptr;
-            dev_alloc(&dip, static_cast<size_t>(B + 1));
-            dev_alloc(&didx, static_cast<size_t>(nnz));
-            dev_alloc(&dval, static_cast<size_t>(nnz));
-            dev_alloc(&lm, static_cast<size_t>(B * std::max<int64_t>(d, 1)));
-            CUDA_TRY(cudaMemcpy(dip, ip.data(), sizeof(int64_t) * (B + 1), cudaMemcpyHostToDevice));
+            DevBuf dip, didx, dval;
+            dip.alloc(ds.device, sizeof(int64_t) * static_cast<size_t>(B + 1));
+            didx.alloc(ds.device, sizeof(int32_t) * static_cast<size_t>(nnz));
+            dval.alloc(ds.device, sizeof(double) * static_cast<size_t>(nnz));
+            CUDA_TRY(cudaMemcpy(dip.p, ip.data(), sizeof(int64_t) * (B + 1), cudaMemcpyHostToDevice));
             if (nnz > 0) {
-                CUDA_TRY(cudaMemcpy(didx, indices + indptr[0], sizeof(int32_t) * nnz, cudaMemcpyHostToDevice));
-                CUDA_TRY(cudaMemcpy(dval, values + indptr[0], sizeof(double) * nnz, cudaMemcpyHostToDevice));
+                CUDA_TRY(cudaMemcpy(didx.p, indices + indptr[0], sizeof(int32_t) * nnz, cudaMemcpyHostToDevice));
+                CUDA_TRY(cudaMemcpy(dval.p, values + indptr[0], sizeof(double) * nnz, cudaMemcpyHostToDevice));
             }
             if (d > 0)
                 lpd::csr_to_dense_kernel<<<static_cast<int>((B + 7) / 8), 256, 0, ds.slot[0].stream>>>(
-                    dip, didx, dval, static_cast<int>(B), static_cast<int>(d), lm);
+                    static_cast<const int64_t*>(dip.p), static_cast<const int32_t*>(didx.p), dval.d(),
+                    static_cast<int>(B), static_cast<int>(d), lm, ds.err);
+            else
+                CUDA_TRY(cudaMemsetAsync(lm, 0, sizeof(double) * static_cast<size_t>(B), ds.slot[0].stream));
             CUDA_TRY(cudaGetLastError());
-            try {
-                build_basis_host_L(ds, lm, B, d, L, b_eff, gamma);
-            } catch (...) {
-                dev_free(dip); dev_free(didx); dev_free(dval); dev_free(lm);
-                throw;
-            }
-            dev_free(dip); dev_free(didx); dev_free(dval); dev_free(lm);
+            CUDA_TRY(cudaStreamSynchronize(ds.slot[0].stream));
+            check_range_flag(ds);
         });
     });
 }
@@ -1634,7 +1953,7 @@ int lpd_compute_g_dense(lpd_context* ctx, const double* X, int64_t n, int64_t d,
         if (ldx < d) fail(LPD_ERR_INVALID_ARGUMENT, "ldx < d");
         if (ldg < b_eff) fail(LPD_ERR_INVALID_ARGUMENT, "ldg < b_eff");
         if (n > 0 && (!G || (!X && d > 0))) fail(LPD_ERR_INVALID_ARGUMENT, "null buffer");
-        compute_rows_host(ctx, n, G, ldg, timings, [&](DeviceState& ds, Slot& s, int64_t r0, int64_t rows) {
+        compute_rows_host(ctx, n, G, ldg, timings, [&](DeviceState& ds, Slot& s, int64_t r0, int64_t rows, SpinTeam&) {
             ensure_slot(ds, s, rows, true, 0);
             CUDA_TRY(cudaEventRecord(s.ev[0], s.stream));
             if (d > 0)
@@ -1656,8 +1975,64 @@ int lpd_compute_g_csr(lpd_context* ctx, int64_t n, int64_t d, const int64_t* ind
         if (d != ctx->dev[0].d) fail(LPD_ERR_INVALID_ARGUMENT, "point dimension does not match the basis");
         if (ldg < b_eff) fail(LPD_ERR_INVALID_ARGUMENT, "ldg < b_eff");
         if (n > 0 && (!G || !indptr)) fail(LPD_ERR_INVALID_ARGUMENT, "null buffer");
-        compute_rows_host(ctx, n, G, ldg, timings, [&](DeviceState& ds, Slot& s, int64_t r0, int64_t rows) {
+        compute_rows_host(ctx, n, G, ldg, timings, [&](DeviceState& ds, Slot& s, int64_t r0, int64_t rows, SpinTeam&) {
             stage_csr_rows(ds, s, r0, rows, d, indptr, indices, values);
+        });
+    });
+}
+
+int lpd_compute_g_rows(lpd_context* ctx, int64_t n, int64_t d, const lpd_feature* const* rows_ptr,
+                       const int64_t* nnz, double* G, int64_t ldg, lpd_timings* timings) {
+    return guarded([&] {
+        check_ctx(ctx, true);
+        const int64_t b_eff = ctx->dev[0].b_eff;
+        if (n < 0) fail(LPD_ERR_INVALID_ARGUMENT, "negative row count");
+        if (d != ctx->dev[0].d) fail(LPD_ERR_INVALID_ARGUMENT, "point dimension does not match the basis");
+        if (ldg < b_eff) fail(LPD_ERR_INVALID_ARGUMENT, "ldg < b_eff");
+        if (n > 0 && (!G || !rows_ptr || !nnz)) fail(LPD_ERR_INVALID_ARGUMENT, "null buffer");
+        // Each chunk is densified by the delivery's host team straight from the caller's
+        // rows into a pinned buffer (no intermediate CSR), then copied up; the pinned
+        // buffer of a slot is rewritten only after its previous copy (ev[1]) completed.
+        compute_rows_host(ctx, n, G, ldg, timings, [&](DeviceState& ds, Slot& s, int64_t r0, int64_t rows,
+                                                       SpinTeam& team) {
+            ensure_slot(ds, s, rows, true, 0);
+            const int64_t dc = std::max<int64_t>(d, 1);
+            const size_t need = sizeof(double) * static_cast<size_t>(rows * dc);
+            if (s.hx_cap < need) {
+                CUDA_TRY(cudaStreamSynchronize(s.stream));
+                if (s.hx) cudaFreeHost(s.hx);
+                s.hx = nullptr;
+                s.hx_cap = 0;
+                const size_t cap = sizeof(double) * static_cast<size_t>(s.rows_cap * dc);
+                CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&s.hx), std::max(cap, need), cudaHostAllocDefault));
+                s.hx_cap = std::max(cap, need);
+            } else {
+                CUDA_TRY(cudaEventSynchronize(s.ev[1]));  // the slot's previous H2D has read s.hx
+            }
+            std::atomic<int> bad{0};
+            const int T = team.size();
+            double* hx = s.hx;
+            team.run([&](int w) {
+                const int64_t a = rows * w / T, b = rows * (w + 1) / T;
+                std::memset(hx + a * dc, 0, sizeof(double) * static_cast<size_t>((b - a) * dc));
+                for (int64_t i = a; i < b; ++i) {
+                    const lpd_feature* f = rows_ptr[r0 + i];
+                    double* o = hx + i * dc;
+                    for (int64_t e = 0, m = nnz[r0 + i]; e < m; ++e) {
+                        const int32_t c = f[e].index;
+                        if (c < 0 || c >= d) {
+                            bad.store(1, std::memory_order_relaxed);
+                            continue;
+                        }
+                        o[c] = f[e].value;
+                    }
+                }
+            });
+            if (bad.load()) fail(LPD_ERR_INVALID_ARGUMENT, "feature index outside [0, d)");
+            CUDA_TRY(cudaEventRecord(s.ev[0], s.stream));
+            if (d > 0)
+                CUDA_TRY(cudaMemcpyAsync(s.x, hx, sizeof(double) * static_cast<size_t>(rows * d),
+                                         cudaMemcpyHostToDevice, s.stream));
         });
     });
 }
@@ -1884,9 +2259,10 @@ int lpd_kernel_block(lpd_context* ctx, int64_t m, const int64_t* a_indptr, const
                 }
                 if (d > 0)
                     lpd::csr_to_dense_kernel<<<static_cast<int>((rows + 7) / 8), 256, 0, st>>>(
-                        dip, dix, dvv, static_cast<int>(rows), static_cast<int>(d), dense);
+                        dip, dix, dvv, static_cast<int>(rows), static_cast<int>(d), dense, ds.err);
                 CUDA_TRY(cudaGetLastError());
                 CUDA_TRY(cudaStreamSynchronize(st));  // rb must outlive its copy
+                check_range_flag(ds);
                 return dense;
             };
             double* A = stage(m, a_indptr, a_indices, a_values);
@@ -1981,55 +2357,50 @@ int lpd_resident_gw(lpd_context* ctx, const int32_t* rows, int64_t count, const 
 }
 
 int lpd_resident_gtv(lpd_context* ctx, const int32_t* rows, const double* coef, int64_t count, double* w) {
+    return guarded([&] { resident_gtv_sets(ctx, rows, coef, count, 1, w); });
+}
+
+int lpd_resident_gtv_sets(lpd_context* ctx, const int32_t* rows, const double* coef, int64_t count, int64_t sets,
+                          double* W) {
+    return guarded([&] { resident_gtv_sets(ctx, rows, coef, count, sets, W); });
+}
+
+int lpd_resident_row_sqnorms(lpd_context* ctx, double* q) {
     return guarded([&] {
-        check_resident(ctx, rows, count);
+        check_ctx(ctx, false);
+        if (ctx->res_n <= 0) fail(LPD_ERR_INVALID_ARGUMENT, "no resident G (lpd_set_keep_resident before lpd_compute_g_*)");
+        if (!q) fail(LPD_ERR_INVALID_ARGUMENT, "null output");
         const int64_t b_eff = ctx->res_b_eff;
-        if (!w) fail(LPD_ERR_INVALID_ARGUMENT, "null w");
-        if (count > 0 && !coef) fail(LPD_ERR_INVALID_ARGUMENT, "null coef");
-        std::fill(w, w + b_eff, 0.0);
-        if (count == 0) return;
-        const bool single = ctx->dev.size() == 1 && ctx->dev[0].res_r0 == 0;
-        auto parts = single ? std::vector<std::vector<std::pair<int32_t, int64_t>>>(1) : split_rows(ctx, rows, count);
-        const int nd = static_cast<int>(ctx->dev.size());
-        std::vector<std::vector<double>> partial(nd);
-        run_parallel(ctx, [&](DeviceState& ds, int di) {
-            const auto& part = parts[static_cast<size_t>(di)];
-            if (!single && part.empty()) return;
+        run_parallel(ctx, [&](DeviceState& ds, int) {
+            if (ds.res_rows <= 0) return;
             CUDA_TRY(cudaSetDevice(ds.device));
             cudaStream_t st = ds.slot[0].stream;
-            const int64_t m = single ? count : static_cast<int64_t>(part.size());
-            const int64_t groups = (m + lpd::GTV_ROWS - 1) / lpd::GTV_ROWS;
-            const size_t off_c = round_up(sizeof(int32_t) * m, 256);
-            const size_t off_p = off_c + round_up(sizeof(double) * m, 256);
-            const size_t off_w = off_p + round_up(sizeof(double) * groups * b_eff, 256);
-            char* base = static_cast<char*>(scratch(ds, off_w + sizeof(double) * b_eff));
-            std::vector<int32_t> local(single ? 0 : static_cast<size_t>(m));
-            std::vector<double> lc(single ? 0 : static_cast<size_t>(m));
-            for (int64_t i = 0; i < static_cast<int64_t>(local.size()); ++i) {
-                local[i] = part[i].first;
-                lc[i] = coef[part[i].second];
-            }
-            int32_t* drows = reinterpret_cast<int32_t*>(base);
-            double* dc = reinterpret_cast<double*>(base + off_c);
-            double* dp = reinterpret_cast<double*>(base + off_p);
-            double* dw = reinterpret_cast<double*>(base + off_w);
-            CUDA_TRY(cudaMemcpyAsync(drows, single ? rows : local.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, st));
-            CUDA_TRY(cudaMemcpyAsync(dc, single ? coef : lc.data(), sizeof(double) * m, cudaMemcpyHostToDevice, st));
-            // each thread owns 4 consecutive columns
-            dim3 grid(static_cast<unsigned>(((b_eff + 3) / 4 + lpd::GTV_THREADS - 1) / lpd::GTV_THREADS),
-                      static_cast<unsigned>(groups));
-            lpd::gather_gtv_partial_kernel<<<grid, lpd::GTV_THREADS, 0, st>>>(ds.res_g, ds.res_ld, static_cast<int>(b_eff),
-                                                                 drows, dc, static_cast<int>(m), dp);
-            lpd::gather_gtv_sum_kernel<<<static_cast<int>((b_eff + 255) / 256), 256, 0, st>>>(
-                dp, static_cast<int>(groups), static_cast<int>(b_eff), dw);
+            double* dq = static_cast<double*>(scratch(ds, sizeof(double) * ds.res_rows));
+            lpd::row_sqnorm_seq_kernel<<<static_cast<int>((ds.res_rows + 127) / 128), 128, 0, st>>>(
+                ds.res_g, ds.res_ld, static_cast<int>(ds.res_rows), static_cast<int>(b_eff), dq);
             CUDA_TRY(cudaGetLastError());
-            partial[di].resize(static_cast<size_t>(b_eff));
-            CUDA_TRY(cudaMemcpyAsync(partial[di].data(), dw, sizeof(double) * b_eff, cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaMemcpyAsync(q + ds.res_r0, dq, sizeof(double) * ds.res_rows, cudaMemcpyDeviceToHost, st));
             CUDA_TRY(cudaStreamSynchronize(st));
         });
-        for (int di = 0; di < nd; ++di)  // fixed device order: deterministic
-            if (!partial[di].empty())
-                for (int64_t j = 0; j < b_eff; ++j) w[j] += partial[di][j];
+    });
+}
+
+int lpd_set_precision(lpd_context* ctx, int mode) {
+    return guarded([&] {
+        check_ctx(ctx, false);
+        if (mode != LPD_PRECISION_AUTO && mode != LPD_PRECISION_FAST && mode != LPD_PRECISION_HIGH)
+            fail(LPD_ERR_INVALID_ARGUMENT, "precision mode must be LPD_PRECISION_AUTO, _FAST or _HIGH");
+        for (auto& ds : ctx->dev) ds.precision_mode = mode;
+    });
+}
+
+int lpd_basis_precision(const lpd_context* ctx, int* high, double* estimate) {
+    return guarded([&] {
+        if (!ctx || ctx->dev.empty()) fail(LPD_ERR_INVALID_ARGUMENT, "null context");
+        const DeviceState& ds = ctx->dev[0];
+        if (!ds.has_basis) fail(LPD_ERR_INVALID_ARGUMENT, "no basis (lpd_set_basis_* first)");
+        if (high) *high = ds.hp ? 1 : 0;
+        if (estimate) *estimate = ds.cond_est;
     });
 }
 

@@ -16,7 +16,8 @@
 // which uses the norm expansion of kernel_block on the tensor cores) this is the direct
 // distance, as decision_values uses it (SPEC.md:130 notes the two differ at 1e-12).
 //
-// pointdv_z_kernel: Zt[j][i] (landmark-major, so the reduction below reads it coalesced)
+// pointdv_z_kernel<true>: Zt[j][i] (landmark-major, so the reduction below reads it coalesced;
+//   <false>: row-major Z[i][j], the A operand of the high-precision factor path, hp_kernels.cuh)
 //   for a chunk of points; register tile 4 points × 4 landmarks per thread, 64 × 64 per
 //   256-thread block, features staged through shared memory 16 at a time. Features beyond
 //   either row set's width read as 0 (the points may name features the landmarks do not).
@@ -29,6 +30,7 @@ namespace lpd {
 constexpr int DV_T = 64;  // points × landmarks per block
 constexpr int DV_K = 16;  // features per shared-memory stage
 
+template <bool TRANSPOSED>
 __global__ void __launch_bounds__(256)
     pointdv_z_kernel(const double* __restrict__ X, long long ldx, int n, int dx,
                      const double* __restrict__ Lm, long long ldl, int B, int dl, double gamma,
@@ -78,7 +80,13 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
             const int i = i0 + ty + 16 * a;
-            if (i < n) Zt[static_cast<long long>(j) * ldz + i] = exp(__dmul_rn(-gamma, acc[a][b]));
+            if (i < n) {
+                const double z = exp(__dmul_rn(-gamma, acc[a][b]));
+                if (TRANSPOSED)
+                    Zt[static_cast<long long>(j) * ldz + i] = z;
+                else
+                    Zt[static_cast<long long>(i) * ldz + j] = z;  // row-major Z (high-precision path)
+            }
         }
     }
 }

@@ -15,6 +15,10 @@
 //   that and the 2^13 carried by Z.
 #pragma once
 
+// bits of the per-device error flag (DeviceState::err), checked after each call
+#define LPD_FLAG_OVERFLOW 1   // |x - mean| >= 2^28: outside the split-fp16 operand range
+#define LPD_FLAG_BAD_INDEX 2  // a CSR feature index outside [0, d)
+
 #include <cuda_fp16.h>
 #include <stdint.h>
 
@@ -180,7 +184,7 @@ __global__ void prep_rows_kernel(const double* __restrict__ X, long long ldx, in
         if (lane == 0) {
             aux[row] = make_float2(static_cast<float>(13.0 + g * ss),
                                    static_cast<float>(-2.0 * g / (sigma * beta)));
-            if (row < m && mx >= 0x1p28) atomicExch(err, 1);
+            if (row < m && mx >= 0x1p28) atomicOr(err, LPD_FLAG_OVERFLOW);
         }
     }
 }
@@ -190,7 +194,7 @@ __global__ void prep_rows_kernel(const double* __restrict__ X, long long ldx, in
 __global__ void csr_to_dense_kernel(const int64_t* __restrict__ indptr,
                                     const int32_t* __restrict__ indices,
                                     const double* __restrict__ values, int m, int d,
-                                    double* __restrict__ out) {
+                                    double* __restrict__ out, int* __restrict__ err) {
     const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (row >= m) return;
@@ -199,7 +203,10 @@ __global__ void csr_to_dense_kernel(const int64_t* __restrict__ indptr,
     __syncwarp();
     for (int64_t e = indptr[row] + lane; e < indptr[row + 1]; e += 32) {
         const int c = indices[e];
-        if (c >= 0 && c < d) o[c] = values[e];
+        if (c >= 0 && c < d)
+            o[c] = values[e];
+        else
+            atomicOr(err, LPD_FLAG_BAD_INDEX);  // the caller fails the call: no silent drop
     }
 }
 

@@ -1,0 +1,47 @@
+"""Every device kernel of liblpd_nystrom.so once, at small sizes, for compute-sanitizer
+(memcheck / racecheck / synccheck): K1 fused factor (dense + CSR), K1L panel path
+(d >= 64), K2/K3 prep, K5 prediction + vote, K7 fp64 kernel block, K4/K6 decision values
+and resident-G sweeps, K8 per-point decision values.
+  compute-sanitizer --tool racecheck python scripts/sanitize_kernels.py"""
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+import paper_2207_01016_b200 as P  # noqa: E402
+from conftest import np_gaussian_L  # noqa: E402
+
+rng = np.random.default_rng(0)
+ctx = P.Context(1)
+for n, d, B in ((300, 50, 100), (600, 100, 300)):  # fused K1, then the d >= 64 panel path
+    X = rng.standard_normal((n, d)).astype(np.float32).astype(np.float64)
+    Y = X[rng.choice(n, B, replace=False)]
+    L = np_gaussian_L(Y, 1.0 / d)
+    ctx.set_basis_dense(Y, L, 1.0 / d)
+    ctx.set_keep_resident(True)
+    G = ctx.compute_g_dense(X)
+    ip = np.zeros(n + 1, np.int64)
+    ip[1:] = np.cumsum(np.full(n, d))
+    G2 = ctx.compute_g_csr(ip, np.tile(np.arange(d, dtype=np.int32), n), X.ravel())
+    assert np.array_equal(G, G2)
+    rows = np.arange(0, n, 3, dtype=np.int32)
+    ctx.resident_gw(rows, rng.standard_normal((1, G.shape[1])))
+    ctx.resident_gw(rows, rng.standard_normal((5, G.shape[1])))
+    ctx.resident_gtv(rows, rng.standard_normal(rows.shape[0]))
+    if hasattr(ctx, "resident_gtv_sets"):
+        ctx.resident_gtv_sets(rows, rng.standard_normal((rows.shape[0], 11)))
+        ctx.resident_row_sqnorms()
+    ctx.decision_values(G, rng.standard_normal((3, G.shape[1])))
+    ctx.set_keep_resident(False)
+    ctx.kernel_block(X[:70], Y, 1.0 / d)
+    betas = rng.standard_normal((3, B))
+    ctx.set_basis_dense(Y, np.ascontiguousarray(betas.T), 1.0 / d)
+    ctx.predict_ovo_dense(X, 3)
+    ctx.set_model_dense(Y, betas, 1.0 / d)
+    ctx.model_decision_values_dense(X[:50])
+    ctx.ovo_vote(rng.standard_normal((100, 3)), 3)
+ctx.close()
+print("sanitize_kernels: every kernel ran")

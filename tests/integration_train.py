@@ -122,7 +122,7 @@ def main():
     so = glob.glob(os.path.join(os.path.dirname(lpdsvm.__file__), "_core*.so"))[0]
     # (for the package layout, __file__ is lpdsvm/__init__.py next to _core*.so)
     lib = ctypes.CDLL(so)
-    adapter_calls = predict_calls = block_calls = sweep_calls = score_calls = -1
+    adapter_calls = predict_calls = block_calls = sweep_calls = score_calls = qdiag_calls = warm_batches = -1
     if hasattr(lib, "lpd_adapter_calls"):
         lib.lpd_adapter_calls.restype = ctypes.c_longlong
         lib.lpd_adapter_predict_calls.restype = ctypes.c_longlong
@@ -134,6 +134,10 @@ def main():
         lib.lpd_adapter_score_calls.restype = ctypes.c_longlong
         sweep_calls = int(lib.lpd_adapter_sweep_calls())
         score_calls = int(lib.lpd_adapter_score_calls())
+        lib.lpd_adapter_qdiag_calls.restype = ctypes.c_longlong
+        lib.lpd_adapter_warm_batches.restype = ctypes.c_longlong
+        qdiag_calls = int(lib.lpd_adapter_qdiag_calls())
+        warm_batches = int(lib.lpd_adapter_warm_batches())
     np.savez(
         args.out,
         pred=pred,
@@ -153,6 +157,8 @@ def main():
         block_calls=block_calls,
         sweep_calls=sweep_calls,
         score_calls=score_calls,
+        qdiag_calls=qdiag_calls,
+        warm_batches=warm_batches,
         grid_errors=np.array([e["mean_error"] for e in grid["entries"]]),
         grid_warm=grid["warm_started_solves"],
         model_text=np.array(model.to_string()),

@@ -62,4 +62,4 @@ def test_e2e_harness_b200_build_links_the_adapter():
         pytest.skip("integration build needs /root/reference at build time")
     syms = subprocess.run(["nm", "-D", so], capture_output=True, text=True).stdout
     assert "T e2e_train" in syms and "T e2e_compute_g" in syms
-    assert "U lpd_compute_g_csr" in syms  # compute_G is the adapter's, over the C ABI
+    assert "U lpd_compute_g_rows" in syms  # compute_G is the adapter's, over the C ABI

@@ -33,7 +33,14 @@ def _setup(workload):
     import bench
     from paper_2207_01016_b200 import synthetic
 
-    cfg = synthetic.CONFIGS[workload]
+    if workload == "c3_ill":
+        # the paper's own SUSY hyperparameter γ = 2^-7 with the reference
+        # default τ = 1e-12 (factor.hpp:59): λ_min/λ_max ≈ 5e-11, the high-precision path
+        import dataclasses
+
+        cfg = dataclasses.replace(synthetic.CONFIGS["c3"], name="c3_susy_shaped_gamma_2^-7", gamma=2.0 ** -7)
+    else:
+        cfg = synthetic.CONFIGS[workload]
     n = synthetic.rows_per_gpu(cfg)
     X, _ = synthetic.make(cfg, rows=slice(0, n))
     dev = torch.device("cuda", 0)
@@ -50,7 +57,7 @@ def _reference_rows(X, rows, Y, L, gamma):
     return O.ref_compute_g(xs, O.dense_to_csr(Y), L, gamma, chunk, threads)
 
 
-@pytest.mark.parametrize("workload,n_sample", [("c2", 384), ("c3", 384), ("c4", 48)])
+@pytest.mark.parametrize("workload,n_sample", [("c2", 384), ("c3", 384), ("c4", 48), ("c3_ill", 384)])
 def test_full_shard_properties(workload, n_sample):
     import torch
 
@@ -62,6 +69,9 @@ def test_full_shard_properties(workload, n_sample):
     G_dev = torch.empty((n, b_eff), dtype=torch.float32, device=dev)
     with P.Context(device_ids=[0]) as ctx:
         ctx.set_basis_device(lm_dev, L_dev, cfg.gamma)
+        high, est = ctx.basis_precision()
+        # the precision choice: fast tensor-core path for C2-C4, fp64 path for γ = 2^-7
+        assert high == (workload == "c3_ill"), (workload, est)
         ctx.compute_g_device(X_dev, G_dev)
         torch.cuda.synchronize(dev)
 
@@ -93,6 +103,8 @@ def test_full_shard_properties(workload, n_sample):
         R = _reference_rows(X, rows, Y, L, cfg.gamma)
         Gs = G_dev[torch.from_numpy(rows).to(dev)].double().cpu().numpy()
         err = row_rel_err(Gs, R)
+        print(f"{workload}: precision high={high} estimate={est:.3g} max row error on "
+              f"{len(rows)} sampled rows = {err:.3g}")
         assert err <= TOL_G, err
 
         # batching invariance: an unaligned sub-range recomputed alone is bitwise equal

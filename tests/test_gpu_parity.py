@@ -399,6 +399,20 @@ def test_resident_g_products(gpu_ctx, nb):
         wref = coef @ G[rows]
         assert np.max(np.abs(w - wref)) <= 1e-12 * np.max(np.abs(wref))
         assert np.array_equal(w, gpu_ctx.resident_gtv(rows, coef))  # deterministic
+        # all (fold, pair) warm starts at once: 11 coefficient sets (two passes of <= 8)
+        C = rng.standard_normal((777, 11))
+        C[rng.random(C.shape) < 0.4] = 0.0
+        Ws = gpu_ctx.resident_gtv_sets(rows, C)
+        Wref = C.T @ G[rows]
+        assert np.max(np.abs(Ws - Wref)) <= 1e-12 * np.max(np.abs(Wref))
+        assert np.array_equal(gpu_ctx.resident_gtv_sets(rows, coef[:, None])[0], w)
+        # make_binary_problem's q_diag: sequential fp64 Σ_j G_ij² (dcd.cpp:60-89), bitwise
+        q = gpu_ctx.resident_row_sqnorms()
+        for i in list(range(0, 3000, 97)) + [2999]:
+            acc = 0.0
+            for v in G[i]:
+                acc += v * v
+            assert q[i] == acc, (i, q[i], acc)
         with pytest.raises(ValueError):
             gpu_ctx.resident_gw(np.array([3000], np.int32), W)
     finally:
@@ -470,3 +484,55 @@ def test_ovo_vote_bit_exact(gpu_ctx, classes):
     got = gpu_ctx.ovo_vote(D, classes)
     want = np.array([O.ref_vote(row, classes) for row in D], dtype=np.int32)
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("name,tol", [("c1_mini.npz", 2e-7), ("sparse_mini.npz", 2e-7), ("susy_mini.npz", 2e-7)])
+def test_high_precision_path_golden(gpu_ctx, name, tol):
+    """LPD_PRECISION_HIGH: Z in fp64 by direct distance, G = Z·L on the fp64 tensor cores
+    (DMMA), delivered through the host path's fp32 staging: G agrees with the reference's
+    fp64 G to the fp32 rounding of the delivered values (≤ 2^-24 per element), far inside
+    the fast path's 1e-4 — the ill-conditioned fixture included. The device-resident fp64
+    output carries no such rounding (test_precision_auto_choice, full-shard test)."""
+    g = load_golden(name)
+    X = g["X"].astype(np.float64)
+    gpu_ctx.set_precision("high")
+    try:
+        gpu_ctx.set_basis_dense(X[g["ids"]], g["L"], float(g["gamma"]))
+        assert gpu_ctx.basis_precision()[0]
+        G = gpu_ctx.compute_g_dense(X)
+        ip, ix, vv = O.dense_to_csr(X)
+        G2 = gpu_ctx.compute_g_csr(ip, ix, vv)
+    finally:
+        gpu_ctx.set_precision("auto")
+    assert row_rel_err(G, g["G"]) <= tol, row_rel_err(G, g["G"])
+    assert np.array_equal(G, G2)
+
+
+def test_precision_auto_choice(gpu_ctx):
+    """Auto precision: a well-conditioned basis stays on the tensor-core path, the paper's
+    γ = 2^-7 SUSY-shaped basis at τ = 1e-12 (λ_min/λ_max ~ 1e-11) goes to the fp64 path and
+    then matches the reference within 1e-7 where the fast path cannot hold 1e-4."""
+    from paper_2207_01016_b200 import synthetic
+
+    X, _ = synthetic.blobs(6000, 18, seed=3)
+    Y = X[np.random.default_rng(1).choice(6000, 1024, replace=False)]
+    gpu_ctx.set_basis_dense(Y, np_gaussian_L(Y, 1.0 / 18, 1e-12), 1.0 / 18)
+    assert not gpu_ctx.basis_precision()[0]
+    gamma = 2.0 ** -7
+    L = O.ref_build_L(O.dense_to_csr(Y), gamma, 1e-12)
+    gpu_ctx.set_basis_dense(Y, L, gamma)
+    high, est = gpu_ctx.basis_precision()
+    assert high and est > 2.5e-4, est
+    G = gpu_ctx.compute_g_dense(X)
+    R = O.ref_compute_g(O.dense_to_csr(X), O.dense_to_csr(Y), L, gamma, 4096, 8)
+    err = row_rel_err(G, R)
+    assert err <= 1e-7, err
+    gpu_ctx.set_precision("fast")
+    try:
+        gpu_ctx.set_basis_dense(Y, L, gamma)
+        err_fast = row_rel_err(gpu_ctx.compute_g_dense(X), R)
+    finally:
+        gpu_ctx.set_precision("auto")
+    print(f"gamma=2^-7 tau=1e-12 B=1024: estimate {est:.3g}, high-precision row error {err:.3g}, "
+          f"fast path {err_fast:.3g}")
+    assert err_fast > err

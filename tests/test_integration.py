@@ -47,7 +47,7 @@ def test_override_is_linked():
     syms = subprocess.run(["nm", "-D", so], capture_output=True, text=True).stdout
     assert f"T {COMPUTE_G}" in syms
     assert f"T {OVO_PREDICT}" in syms
-    for s in ("lpd_set_basis_csr", "lpd_compute_g_csr", "lpd_context_create", "lpd_predict_ovo_csr"):
+    for s in ("lpd_set_basis_csr", "lpd_compute_g_rows", "lpd_context_create", "lpd_predict_ovo_csr"):
         assert f"U {s}" in syms
     weak = os.path.join(INTEG, "obj", "factor_weak.o")
     if os.path.exists(weak):
@@ -91,6 +91,9 @@ def test_reference_api_on_gpu_matches_reference(tmp_path, classes):
     # solver sweeps (reactivation passes, warm-start rebuild_w) and CV held-out scoring
     # ran on the resident device G
     assert int(g["sweep_calls"]) >= 1 and int(g["score_calls"]) >= 3
+    # every binary problem's q_diag came from the device row norms; the warm starts of the
+    # grid's second C were rebuilt for all (fold, pair) problems in one device pass
+    assert int(g["qdiag_calls"]) >= 3 and int(g["warm_batches"]) >= 1
     assert int(g["grid_warm"]) == int(r["grid_warm"]) > 0
     assert np.max(np.abs(g["grid_errors"] - r["grid_errors"])) <= 0.01
     assert int(g["effective_rank"]) == int(r["effective_rank"])
