@@ -52,7 +52,7 @@ extern "C" {
 #define LPD_OUT_F64 0
 #define LPD_OUT_F32 1
 
-#define LPD_PRECISION_AUTO 0 /* per basis: high when 2^-22*sqrt(lambda_max/lambda_min) > 2.5e-4 */
+#define LPD_PRECISION_AUTO 0 /* per basis: high when the fast path's error estimate > 5e-5 */
 #define LPD_PRECISION_FAST 1 /* tensor-core split-fp16 path (K1 / panel path) */
 #define LPD_PRECISION_HIGH 2 /* fp64 Z (direct distance) + fp64 DMMA projection */
 
@@ -109,14 +109,15 @@ int lpd_set_basis_device(lpd_context* ctx, int device_index, const double* landm
                          double gamma, void* stream);
 
 /* Precision of the factor path (default LPD_PRECISION_AUTO, or the LPD_PRECISION environment
- * variable: auto | fast | high). The fast path holds G within ~2^-22*sqrt(lambda_max/lambda_min)
- * of the fp64 reference (row-normwise); the high path computes Z in fp64 by direct distance and
+ * variable: auto | fast | high). The fast path holds G within ~2x its estimate
+ * 2^-22*sqrt(lambda_max)*||L||_F/sqrt(B) of the fp64 reference (row-normwise; the lambda_j are
+ * read off L's column norms 1/sqrt(lambda_j)); the high path computes Z in fp64 by direct distance and
  * G = Z*L on the fp64 tensor cores, for the ill-conditioned bases of small gamma with the
  * reference default tau = 1e-12 (proj/include/lpdsvm/factor.hpp:59). Applies from the next
  * lpd_set_basis_* call. */
 int lpd_set_precision(lpd_context* ctx, int mode);
 /* The current basis' choice: *high = 1 on the high-precision path; *estimate = the fast
- * path's row-error estimate 2^-22*sqrt(lambda_max/lambda_min) from L's column norms. */
+ * path's row-error estimate 2^-22*sqrt(lambda_max)*||L||_F/sqrt(B) from L's column norms. */
 int lpd_basis_precision(const lpd_context* ctx, int* high, double* estimate);
 
 /* G (n x b_eff, leading dimension ldg >= b_eff) for host rows; rows are sharded

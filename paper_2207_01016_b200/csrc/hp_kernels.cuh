@@ -138,9 +138,10 @@ __global__ void hp_transpose_kernel(const double* __restrict__ L, int B, int b_e
 }
 
 // Column norms of L for the precision choice: the columns of L = U·D^-1/2 are orthogonal
-// with norms 1/√λ_j, so max_j ‖L[:, j]‖² = 1/λ_min and min_j = 1/λ_max (out[0], out[1]; the
-// caller zeroes out[0] and fills out[1] with 0xff bytes). One thread per column (coalesced
-// across a warp); non-negative doubles order like their bit patterns.
+// with norms 1/√λ_j. out[0] = max_j ‖L[:, j]‖² (= 1/λ_min), out[1] = min_j (= 1/λ_max),
+// out[2] = Σ_j ‖L[:, j]‖² (= ‖L‖_F²). The caller zeroes out[0] and out[2] and fills out[1]
+// with 0xff bytes. One thread per column (coalesced across a warp); non-negative doubles
+// order like their bit patterns.
 __global__ void col_norm_range_kernel(const double* __restrict__ L, int B, int b_eff, double* __restrict__ out) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     double s = 0.0;
@@ -149,14 +150,16 @@ __global__ void col_norm_range_kernel(const double* __restrict__ L, int B, int b
             const double v = L[static_cast<long long>(k) * b_eff + c];
             s += v * v;
         }
-    __shared__ double mx[256], mn[256];
+    __shared__ double mx[256], mn[256], sm[256];
     mx[threadIdx.x] = s;
+    sm[threadIdx.x] = s;
     mn[threadIdx.x] = c < b_eff ? s : INFINITY;
     __syncthreads();
     for (int o = blockDim.x / 2; o > 0; o >>= 1) {
         if (threadIdx.x < o) {
             mx[threadIdx.x] = fmax(mx[threadIdx.x], mx[threadIdx.x + o]);
             mn[threadIdx.x] = fmin(mn[threadIdx.x], mn[threadIdx.x + o]);
+            sm[threadIdx.x] += sm[threadIdx.x + o];
         }
         __syncthreads();
     }
@@ -164,6 +167,7 @@ __global__ void col_norm_range_kernel(const double* __restrict__ L, int B, int b
         atomicMax(reinterpret_cast<unsigned long long*>(out), static_cast<unsigned long long>(__double_as_longlong(mx[0])));
         atomicMin(reinterpret_cast<unsigned long long*>(out + 1),
                   static_cast<unsigned long long>(__double_as_longlong(mn[0])));
+        atomicAdd(out + 2, sm[0]);
     }
 }
 

@@ -11,7 +11,7 @@ from typing import Tuple
 
 import numpy as np
 
-__all__ = ["row_shard", "broadcast_basis"]
+__all__ = ["row_shard", "broadcast_basis", "compute_g_sharded"]
 
 ROW_ALIGN = 256  # one CTA-pair tile (2 x 128-row UMMA M halves)
 
@@ -58,3 +58,19 @@ def broadcast_basis(landmarks: np.ndarray | None, L: np.ndarray | None, gamma: f
     dist.broadcast(lm, src=0, group=group)
     dist.broadcast(Lt, src=0, group=group)
     return lm.cpu().numpy(), Lt.cpu().numpy(), g
+
+
+def compute_g_sharded(ctx, X: np.ndarray, landmarks: np.ndarray | None, L: np.ndarray | None,
+                      gamma: float | None, group=None):
+    """One process per GPU under torch.distributed (torchrun): rank 0's basis (landmarks,
+    L, γ) is broadcast (the only exchange), then every rank computes the
+    G rows of its contiguous row_shard of X through its own context (`ctx`, e.g.
+    Context(device_ids=[local_rank])) — no collective on G. X holds all n rows (or at least
+    this rank's shard at the same offsets); other ranks may pass None for the basis.
+    Returns (begin, end, G_local)."""
+    import torch.distributed as dist
+
+    lm, Lb, g = broadcast_basis(landmarks, L, gamma, group=group)
+    b, e = row_shard(X.shape[0], dist.get_world_size(group), dist.get_rank(group))
+    ctx.set_basis_dense(lm, Lb, g)
+    return b, e, ctx.compute_g_dense(np.ascontiguousarray(X[b:e], dtype=np.float64))

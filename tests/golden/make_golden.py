@@ -7,7 +7,9 @@ compiled unmodified by oracle/Makefile):  python tests/golden/make_golden.py
   c1_mini.npz              C1 blobs, first 1024 rows, 128 landmarks chosen by the
                            reference select_landmarks(seed=1), L and G from the
                            reference build_factor_with_landmarks (factor.cpp:112-143)
-  susy_mini.npz            SUSY-shaped d=18, gamma=2^-7 (ill-conditioned), n=512, B=256
+  susy_mini.npz            SUSY-shaped d=18, gamma=2^-7 (ill-conditioned), n=512, B=256, tau=1e-6
+  susy_mini_t12.npz        the same points and landmarks at the reference default tau=1e-12
+                           (the high-precision path's fixture: lambda_min/lambda_max ~ 1e-12)
   sparse_mini.npz          random sparse CSR points incl. empty rows, n=300, d=40, B=64
 """
 import json
@@ -58,6 +60,9 @@ def main():
     ids, f = factor_fixture(Xs, 256, 2.0 ** -7, 1e-6)
     np.savez_compressed(os.path.join(HERE, "susy_mini.npz"), X=Xs.astype(np.float32), ids=ids,
                         L=f["L"], G=f["G"], gamma=2.0 ** -7, tau=1e-6)
+    ids, f = factor_fixture(Xs, 256, 2.0 ** -7, 1e-12)
+    np.savez_compressed(os.path.join(HERE, "susy_mini_t12.npz"), X=Xs.astype(np.float32), ids=ids,
+                        L=f["L"], G=f["G"], gamma=2.0 ** -7, tau=1e-12)
 
     rng = np.random.default_rng(11)
     Xp = rng.standard_normal((300, 40)).astype(np.float32).astype(np.float64)
