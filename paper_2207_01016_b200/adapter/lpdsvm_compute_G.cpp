@@ -22,6 +22,9 @@
 //                                   through kernel_block only when there are rows)
 //   * device/driver failure      -> std::runtime_error
 //   * output: Matrix(n, L.cols()) row-major fp64, returned by value.
+// Inputs above 65,536 features (or too sparse to densify, host_serves) go to the
+// reference's own compute_G / kernel_block / ovo_predict / decision_values, kept under
+// lpd_ref_* names. On the device path
 // `norms` / `landmark_norms` are not read: the device recomputes both from the same
 // values its tensor cores consume (so x == b gives d² = 0 exactly as in the
 // reference's clamp at kernel.cpp:49-51). `chunk_size` is validated and otherwise
@@ -55,6 +58,24 @@
 #include "lpdsvm/multiclass.hpp"
 #include "lpdsvm/rng.hpp"
 #include "lpd_nystrom.h"
+
+// The reference's own definitions, kept callable for the inputs the device path does not
+// take (host_serves below): integration/Makefile copies factor.o, kernel.o and
+// multiclass.o, renames these four definitions — and, inside the copies, their calls to
+// kernel_block — to the names below and localises every other symbol of the copies.
+// Same signatures and calling convention as the lpdsvm:: functions they were.
+extern "C" {
+lpdsvm::Matrix lpd_ref_compute_G(std::span<const lpdsvm::SparseVector> points, std::span<const double> norms,
+                                 std::span<const lpdsvm::SparseVector> landmarks,
+                                 std::span<const double> landmark_norms, const lpdsvm::Matrix& L,
+                                 const lpdsvm::KernelParams& params, std::size_t chunk_size, int num_threads);
+lpdsvm::Matrix lpd_ref_kernel_block(std::span<const lpdsvm::SparseVector> rows_a, std::span<const double> norms_a,
+                                    std::span<const lpdsvm::SparseVector> rows_b, std::span<const double> norms_b,
+                                    const lpdsvm::KernelParams& params, int num_threads);
+std::vector<double> lpd_ref_ovo_predict(const lpdsvm::OvoModel& model,
+                                        std::span<const lpdsvm::SparseVector> points, int num_threads);
+std::vector<double> lpd_ref_decision_values(const lpdsvm::OvoModel& model, const lpdsvm::SparseVector& point);
+}
 
 namespace {
 
@@ -111,6 +132,37 @@ std::size_t device_min_elems() {
     }();
     return v;
 }
+// Which side computes kernel values for a set of sparse rows of dimension d with
+// `nnz` stored features in total over `rows` rows. The device densifies: its kernel
+// work per (row, landmark) pair is ~6·d tensor flops (3 split passes of the
+// inner-product GEMM) at ~1.4 PFLOP/s, against the reference's sparse merge of ~2·nnz
+// scalar operations at ~2e10/s on 16 host cores — the device is faster while
+// d < ~2.3e4 · nnz/row. Above that, and above the C ABI's 65,536-feature limit
+// (LPD_ERR_UNSUPPORTED; the sparse text sets news20 d = 1.36 M, url 3.2 M, webspam
+// 16.6 M), the reference's own sparse host code runs (lpd_ref_*), so those inputs train
+// exactly as they do on the reference. LPD_HOST_FEATURES_ABOVE lowers the cut (tests).
+std::atomic<long long> g_host_calls{0};  // calls served by the reference's host code
+bool host_serves(int64_t d, std::size_t nnz, std::size_t rows) {
+    static const int64_t cut = [] {
+        const char* e = std::getenv("LPD_HOST_FEATURES_ABOVE");
+        return e ? static_cast<int64_t>(std::strtoll(e, nullptr, 10)) : int64_t(65536);
+    }();
+    if (d > cut) return true;
+    const double per_row = rows ? static_cast<double>(nnz) / static_cast<double>(rows) : 0.0;
+    return static_cast<double>(d) > 2.3e4 * std::max(per_row, 1.0);
+}
+std::size_t total_nnz(std::span<const lpdsvm::SparseVector> rows) {
+    std::size_t s = 0;
+    for (const auto& r : rows) s += r.size();
+    return s;
+}
+int32_t max_feature(std::span<const lpdsvm::SparseVector> rows) {
+    int32_t m = -1;  // indices ascend within a point (dataio.hpp:20-24)
+    for (const auto& r : rows)
+        if (!r.empty()) m = std::max(m, r.back().index);
+    return m;
+}
+
 lpd_timings g_last{};
 // host-side phases of the last compute_G (seconds): flatten, basis, Matrix allocation
 // (the reference Matrix zero-fills, matrix.hpp:15-16), device call
@@ -269,9 +321,9 @@ lpdsvm::Matrix make_output_matrix(std::size_t rows, std::size_t cols) {
 
 namespace lpdsvm {
 
-Matrix compute_G(std::span<const SparseVector> points, std::span<const double> /*norms*/,
+Matrix compute_G(std::span<const SparseVector> points, std::span<const double> norms,
                  std::span<const SparseVector> landmarks,
-                 std::span<const double> /*landmark_norms*/, const Matrix& L,
+                 std::span<const double> landmark_norms, const Matrix& L,
                  const KernelParams& params, std::size_t chunk_size, int num_threads) {
     if (chunk_size == 0) throw std::invalid_argument("chunk_size must be positive");
     const std::size_t n = points.size();
@@ -327,6 +379,15 @@ Matrix compute_G(std::span<const SparseVector> points, std::span<const double> /
     lap(0);
     // compute_G is not passed the dimension: d = 1 + max index over both sets.
     const int64_t d = std::max<int64_t>(1, 1 + std::max(xmax, ls.max_index));
+    std::size_t xnnz_total = 0;
+    for (int64_t v : xnnz) xnnz_total += static_cast<std::size_t>(v);
+    if (host_serves(d, xnnz_total + ls.indices.size(), n + b)) {
+        g_res = ResidentG{};  // this G lives on the host only
+        g_rowsq.clear();
+        g_warm_w.clear();
+        ++g_host_calls;
+        return lpd_ref_compute_G(points, norms, landmarks, landmark_norms, L, params, chunk_size, num_threads);
+    }
 
     lpd_context* ctx = context();
     int rc = lpd_set_basis_csr(ctx, static_cast<int64_t>(b), d, ls.indptr.data(), ls.indices.data(),
@@ -725,8 +786,15 @@ Matrix kernel_block(std::span<const SparseVector> rows_a, std::span<const double
                     const KernelParams& params, int num_threads) {
     validate(params);
     const std::size_t m = rows_a.size(), n = rows_b.size();
+    if (m == 0 || n == 0) return Matrix(m, n);
+    {
+        const int64_t d = std::max<int64_t>(1, 1 + std::max(max_feature(rows_a), max_feature(rows_b)));
+        if (host_serves(d, total_nnz(rows_a) + total_nnz(rows_b), m + n)) {
+            ++g_host_calls;
+            return lpd_ref_kernel_block(rows_a, norms_a, rows_b, norms_b, params, num_threads);
+        }
+    }
     Matrix block(m, n);
-    if (m == 0 || n == 0) return block;
     std::lock_guard<std::mutex> lock(g_mu);
     ++g_block_calls;
     const int threads = std::max(1, num_threads);
@@ -787,6 +855,13 @@ std::vector<double> ovo_predict(const OvoModel& model, std::span<const SparseVec
         return predictions;
     }
     validate(model.kernel);
+    {
+        const int64_t d = std::max<int64_t>(1, 1 + std::max(max_feature(points), max_feature(model.landmarks)));
+        if (host_serves(d, total_nnz(points) + total_nnz(model.landmarks), n + b)) {
+            ++g_host_calls;
+            return lpd_ref_ovo_predict(model, points, num_threads);
+        }
+    }
     std::lock_guard<std::mutex> lock(g_mu);
     ++g_predict_calls;
     const int threads = std::max(1, num_threads);
@@ -845,6 +920,14 @@ std::vector<double> decision_values(const OvoModel& model, const SparseVector& p
     std::vector<double> decisions(P, 0.0);
     if (P == 0) return decisions;
     if (b == 0) return decisions;  // the reference's empty sum
+    {
+        const int32_t mp = point.empty() ? -1 : point.back().index;
+        const int64_t d = std::max<int64_t>(1, 1 + std::max(mp, max_feature(model.landmarks)));
+        if (host_serves(d, point.size() + total_nnz(model.landmarks), 1 + b)) {
+            ++g_host_calls;
+            return lpd_ref_decision_values(model, point);
+        }
+    }
     std::lock_guard<std::mutex> lock(g_mu);
     ++g_dv_calls;
     lpd_context* ctx = context();
@@ -895,6 +978,9 @@ extern "C" __attribute__((visibility("default"))) long long lpd_adapter_qdiag_ca
 }
 extern "C" __attribute__((visibility("default"))) long long lpd_adapter_warm_batches(void) {
     return g_warm_batches.load();
+}
+extern "C" __attribute__((visibility("default"))) long long lpd_adapter_host_calls(void) {
+    return g_host_calls.load();
 }
 extern "C" __attribute__((visibility("default"))) long long lpd_adapter_dv_calls(void) {
     return g_dv_calls.load();

@@ -22,11 +22,12 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def libsvm_text(X, y):
-    # repr() of a float64 holding an fp32 value round-trips exactly through strtod
+def libsvm_text(X, y, stride=1):
+    # repr() of a float64 holding an fp32 value round-trips exactly through strtod;
+    # feature j is written at index j·stride + 1 (stride > 1: a high-dimensional sparse set)
     lines = []
     for xi, yi in zip(X, y):
-        feats = " ".join(f"{j + 1}:{float(v)!r}" for j, v in enumerate(xi) if v != 0.0)
+        feats = " ".join(f"{j * stride + 1}:{float(v)!r}" for j, v in enumerate(xi) if v != 0.0)
         lines.append(f"{int(yi)} {feats}")
     return "\n".join(lines) + "\n"
 
@@ -46,6 +47,8 @@ def main():
     ap.add_argument("--tau", type=float, default=1e-6)
     ap.add_argument("--seed", type=int, default=11)
     ap.add_argument("--train-only", action="store_true", help="train + predict only (timing runs)")
+    ap.add_argument("--index-stride", type=int, default=1,
+                    help="feature j at index j*stride+1 (a sparse set of dimension ~d*stride)")
     args = ap.parse_args()
 
     mdir = args.module_dir if os.path.isabs(args.module_dir) else os.path.join(ROOT, args.module_dir)
@@ -65,8 +68,8 @@ def main():
         X = X / 4.0  # keep γ·d² in a useful range for the small test
         X = X.astype(np.float32).astype(np.float64)
     t0 = time.perf_counter()
-    train = lpdsvm.parse_dataset(libsvm_text(X[: args.n], y[: args.n]))
-    test = lpdsvm.parse_dataset(libsvm_text(X[args.n :], y[args.n :]))
+    train = lpdsvm.parse_dataset(libsvm_text(X[: args.n], y[: args.n], args.index_stride))
+    test = lpdsvm.parse_dataset(libsvm_text(X[args.n :], y[args.n :], args.index_stride))
     parse_s = time.perf_counter() - t0
 
     t0 = time.perf_counter()
@@ -123,6 +126,7 @@ def main():
     # (for the package layout, __file__ is lpdsvm/__init__.py next to _core*.so)
     lib = ctypes.CDLL(so)
     adapter_calls = predict_calls = block_calls = sweep_calls = score_calls = qdiag_calls = warm_batches = -1
+    host_calls = -1
     if hasattr(lib, "lpd_adapter_calls"):
         lib.lpd_adapter_calls.restype = ctypes.c_longlong
         lib.lpd_adapter_predict_calls.restype = ctypes.c_longlong
@@ -138,6 +142,8 @@ def main():
         lib.lpd_adapter_warm_batches.restype = ctypes.c_longlong
         qdiag_calls = int(lib.lpd_adapter_qdiag_calls())
         warm_batches = int(lib.lpd_adapter_warm_batches())
+        lib.lpd_adapter_host_calls.restype = ctypes.c_longlong
+        host_calls = int(lib.lpd_adapter_host_calls())
     np.savez(
         args.out,
         pred=pred,
@@ -159,6 +165,8 @@ def main():
         score_calls=score_calls,
         qdiag_calls=qdiag_calls,
         warm_batches=warm_batches,
+        host_calls=host_calls,
+        cv_fold_epochs=np.array(cv["fold_epochs"]) if "fold_epochs" in cv else np.zeros(0),
         grid_errors=np.array([e["mean_error"] for e in grid["entries"]]),
         grid_warm=grid["warm_started_solves"],
         model_text=np.array(model.to_string()),

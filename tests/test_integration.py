@@ -71,6 +71,31 @@ def test_no_cpu_fallback_without_gpu(tmp_path):
     assert "no CUDA device" in (r.stderr + r.stdout)
 
 
+@pytest.mark.skipif(_core_so(INTEG) is None or _core_so(REF) is None,
+                    reason="integration build / oracle/_ref need /root/reference at build time")
+@pytest.mark.parametrize("classes", [2, 3])
+def test_high_dimensional_sparse_runs_reference_host_code(tmp_path, classes):
+    """Inputs above the device's 65,536-feature limit (the sparse text sets: news20,
+    url, webspam) train through the drop-in exactly as on the reference: the adapter
+    hands compute_G, the landmark Gram, ovo_predict and decision_values to the
+    reference's own definitions (renamed copies, integration/Makefile), and the solver
+    overrides take their host loops on the host-only G. Every result is bitwise equal
+    to the unmodified reference build — this also pins the host branches of the
+    rebuild_w / reactivation_pass / make_binary_problem / cross_validate overrides
+    against the reference's own code. No GPU is touched."""
+    args = ["--n", "600", "--n-test", "200", "--budget", "100", "--d", "20", "--index-stride", "4000",
+            "--classes", str(classes), "--threads", "4"]
+    _run(INTEG, str(tmp_path / "gpu.npz"), *args)
+    _run(REF, str(tmp_path / "ref.npz"), *args)
+    g = np.load(tmp_path / "gpu.npz")
+    r = np.load(tmp_path / "ref.npz")
+    assert int(g["host_calls"]) >= 3 + 200  # Gram x2, compute_G x2+, predict, dv per point
+    assert int(g["block_calls"]) == int(g["predict_calls"]) == int(g["sweep_calls"]) == 0
+    for k in ("pred", "dv", "error_rate", "cv_mean_error", "cv_fold_errors", "effective_rank", "epochs",
+              "grid_errors", "grid_warm", "model_text"):
+        assert np.array_equal(g[k], r[k]), k
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("classes", [2, 3])
 def test_reference_api_on_gpu_matches_reference(tmp_path, classes):
