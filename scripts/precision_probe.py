@@ -1,0 +1,78 @@
+"""Row-error study of the fast factor path against an fp64 G (numpy, direct distances)
+over γ multipliers and far-from-the-landmarks rows: where does the split-fp16 / fp32
+exponent path lose its 1e-4 row bound, and which per-row quantity predicts it?
+
+  python scripts/precision_probe.py [out.json]
+
+Per case: basis conditioning estimate (lpd_basis_precision), and per row
+  r   = ‖x − μ‖ (μ = landmark mean), dmin = min_j ‖x − b_j‖,
+  err = ‖G_dev − G_64‖ / ‖G_64‖.
+"""
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+import paper_2207_01016_b200 as P  # noqa: E402
+from conftest import np_gaussian_L  # noqa: E402
+
+
+def g64(X, Y, L, gamma):
+    out = np.empty((X.shape[0], L.shape[1]))
+    for i in range(0, X.shape[0], 512):
+        D = ((X[i:i + 512, None, :] - Y[None, :, :]) ** 2).sum(-1)
+        out[i:i + 512] = np.exp(-gamma * D) @ L
+    return out
+
+
+def main():
+    out_path = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/precision_probe.json"
+    rng = np.random.default_rng(5)
+    d, B, n = 32, 1024, 3072
+    res = []
+    ctx = P.Context(1)
+    for scale in (1.0, 10.0):  # unit-variance vs unscaled (×10) features
+        base = rng.standard_normal((B + n, d)).astype(np.float32).astype(np.float64) * scale
+        Y = base[:B]
+        for mult in (1.0, 4.0, 8.0, 16.0, 64.0):
+            gamma = mult / (d * scale * scale)
+            L = np_gaussian_L(Y, gamma, tau=1e-6)
+            for shift in (0.0, 1.0, 2.0, 4.0):
+                X = base[B:].copy()
+                # a third of the rows moved away from the landmark cloud along a random direction
+                u = rng.standard_normal(d)
+                u /= np.linalg.norm(u)
+                X[: n // 3] += shift * scale * np.sqrt(d) * u
+                X = X.astype(np.float32).astype(np.float64)
+                ctx.set_precision("fast")
+                ctx.set_basis_dense(Y, L, gamma)
+                hp, est = ctx.basis_precision()
+                G = ctx.compute_g_dense(X)
+                R = g64(X, Y, L, gamma)
+                nr = np.linalg.norm(R, axis=1)
+                ok = nr > 0
+                err = np.full(n, np.nan)
+                err[ok] = np.linalg.norm(G - R, axis=1)[ok] / nr[ok]
+                mu = Y.mean(0)
+                r = np.linalg.norm(X - mu, axis=1)
+                rb = np.linalg.norm(Y - mu, axis=1)
+                dmin = np.sqrt(np.min(((X[:, None, :] - Y[None, :, :]) ** 2).sum(-1), axis=1))
+                res.append({
+                    "scale": scale, "gamma_mult": mult, "gamma": gamma, "shift": shift, "b_eff": int(L.shape[1]),
+                    "est": est, "Rb_max": float(rb.max()), "Rb_min": float(rb.min()),
+                    "max_err": float(np.nanmax(err)), "zero_rows": int((~ok).sum()),
+                    "rows": {"r": r.round(4).tolist(), "dmin": dmin.round(4).tolist(),
+                             "err": [None if not np.isfinite(e) else float(f"{e:.4g}") for e in err]},
+                })
+                print(f"scale {scale:4} mult {mult:5} shift {shift:3} b_eff {L.shape[1]:5} est {est:.2e} "
+                      f"max err {np.nanmax(err):.2e} zero rows {(~ok).sum()}", flush=True)
+    os.makedirs(os.path.dirname(out_path) or ".", exist_ok=True)
+    json.dump(res, open(out_path, "w"))
+
+
+if __name__ == "__main__":
+    main()
