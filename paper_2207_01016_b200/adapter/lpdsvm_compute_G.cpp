@@ -288,7 +288,23 @@ struct MatrixLayout {
 struct VectorLayout {
     double *start, *finish, *end_of_storage;
 };
+// Off (the reference's own constructor) with LPD_FAST_MATRIX=0, in debug-container and
+// sanitizer builds (their vectors carry annotations this layout does not), and whenever
+// the runtime layout check fails.
+#if defined(_GLIBCXX_DEBUG) || defined(_GLIBCXX_SANITIZE_VECTOR) || defined(__SANITIZE_ADDRESS__)
+constexpr bool kFastMatrixBuild = false;
+#else
+constexpr bool kFastMatrixBuild = true;
+#endif
+bool fast_matrix_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("LPD_FAST_MATRIX");
+        return kFastMatrixBuild && !(e && e[0] == '0');
+    }();
+    return on;
+}
 lpdsvm::Matrix make_output_matrix(std::size_t rows, std::size_t cols) {
+    if (!fast_matrix_enabled()) return lpdsvm::Matrix(rows, cols);
     if constexpr (sizeof(MatrixLayout) == sizeof(lpdsvm::Matrix) && std::is_standard_layout_v<lpdsvm::Matrix> &&
                   std::is_standard_layout_v<MatrixLayout> && sizeof(std::vector<double>) == sizeof(VectorLayout)) {
         const std::size_t n = rows * cols;

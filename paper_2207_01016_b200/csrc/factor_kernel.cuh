@@ -45,6 +45,7 @@
 // Z·2^13 = 2^min(t, 13).
 #pragma once
 
+#include "prep_kernels.cuh"
 #include "ptx.cuh"
 
 namespace lpd {
@@ -56,7 +57,7 @@ struct FactorParams {
     int n_col_blocks;       // Beff_pad / 256
     int b_eff;              // valid G columns
     int ksteps1;            // ceil((d + 1) / 16): K-steps of GEMM1 (d features + norm column)
-    const float2* row_aux;  // [n_pad] (R_i, sx_i): t = R_i + acc*sx_i (prep_rows_kernel)
+    const RowAux* row_aux;  // [n_pad] t = R_i + acc*sx_i, clamp, rscale (prep_kernels.cuh)
     const float* col_scale; // [Beff_pad] 2^-13 / u_k (undoes Z and Lᵀ-row scaling)
     // output G: the tm_g tensor map (TMA store, 16-byte aligned rows; the host stages
     // through an aligned buffer otherwise)
@@ -481,7 +482,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
         // t = R + acc*sx (landmark norm already inside acc, prep_rows_kernel), so an
         // element costs half an FFMA2, one FMNMX, one MUFU.EX2, one LOP3 (hi =
         // top 11 significant bits), half an FSUB2 (lo = z - hi) and one F2FP.
-        auto produce_z = [&](uint64_t R2, uint64_t sx2) {
+        auto produce_z = [&](uint64_t R2, uint64_t sx2, float clampv) {
             const uint32_t b = cnt % NSZ, ph = (cnt / NSZ) & 1;
             const uint32_t col = tmem_base + lane_off + TM_SZ + b * NC + half * 32;
             uint32_t s[32];
@@ -502,8 +503,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
                     float t0, t1;
                     f2_unpack(ffma2(f2_pack(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])),
                                     sx2, R2), t0, t1);
-                    const float z0 = ex2_approx(fminf(t0, static_cast<float>(Z13)));
-                    const float z1 = ex2_approx(fminf(t1, static_cast<float>(Z13)));
+                    const float z0 = ex2_approx(fminf(t0, clampv));
+                    const float z1 = ex2_approx(fminf(t1, clampv));
                     const float h0 = __uint_as_float(__float_as_uint(z0) & 0xFFFFE000u);
                     const float h1 = __uint_as_float(__float_as_uint(z1) & 0xFFFFE000u);
                     float l0, l1;
@@ -541,14 +542,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
             const int gc0 = cb * N2 + c0;
             if (gc0 >= p.b_eff || K1_ABL(2)) return;
             const float4* cs4 = reinterpret_cast<const float4*>(p.col_scale + gc0);
+            // the row's exponent normalisation (1 unless the probe shifted it, probe_kernels.cuh)
+            const float rsc = p.row_aux[rt * PM + r_pair].rscale;
             float v[32];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 const float4 sc = ldg_f4_inorder(cs4 + i);
-                v[4 * i + 0] = rs[m * 32 + 4 * i + 0] * sc.x;
-                v[4 * i + 1] = rs[m * 32 + 4 * i + 1] * sc.y;
-                v[4 * i + 2] = rs[m * 32 + 4 * i + 2] * sc.z;
-                v[4 * i + 3] = rs[m * 32 + 4 * i + 3] * sc.w;
+                v[4 * i + 0] = rs[m * 32 + 4 * i + 0] * (sc.x * rsc);
+                v[4 * i + 1] = rs[m * 32 + 4 * i + 1] * (sc.y * rsc);
+                v[4 * i + 2] = rs[m * 32 + 4 * i + 2] * (sc.z * rsc);
+                v[4 * i + 3] = rs[m * 32 + 4 * i + 3] * (sc.w * rsc);
             }
             // 32 rows x SLAB columns per store; 128-byte swizzled staging rows
             // (16-byte chunk c of row r at chunk c ^ (r & 7)): conflict-free STS.
@@ -612,8 +615,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
         if (pair < num_tiles) write_x(0);
         for (int tile = pair; tile < num_tiles; tile += num_pairs, ++it) {
             const int rt = tile % p.n_row_tiles;
-            const float2 ra = p.row_aux[rt * PM + r_pair];
-            const uint64_t R2 = f2_pack(ra.x, ra.x), sx2 = f2_pack(ra.y, ra.y);
+            const RowAux ra = p.row_aux[rt * PM + r_pair];
+            const uint64_t R2 = f2_pack(ra.R, ra.R), sx2 = f2_pack(ra.sx, ra.sx);
             const int next = tile + num_pairs;
             bool first = true;  // no segment of this tile read yet
             for (int j = 0; j < n; ++j) {
@@ -631,7 +634,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
                     if (lane == 0) mbar_arrive_cluster(z_full_l + 8 * b);
                     ++cnt;
                 } else {
-                    produce_z(R2, sx2);
+                    produce_z(R2, sx2, ra.clamp);
                 }
                 store_some();
             }

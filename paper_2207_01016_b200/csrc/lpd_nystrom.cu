@@ -41,6 +41,7 @@
 #include "pointdv_kernels.cuh"
 #include "hp_kernels.cuh"
 #include "prep_kernels.cuh"
+#include "probe_kernels.cuh"
 
 extern "C" void lpd_host_widen_rows(const float* src, int64_t lds, double* dst, int64_t ldd,
                                     int64_t r0, int64_t r1, int64_t cols);
@@ -160,7 +161,8 @@ struct Slot {
     double* x = nullptr;     // [rows_cap × d] fp64
     __half* xhi = nullptr;   // [rows_cap × 64]
     __half* xlo = nullptr;
-    float2* raux = nullptr;  // [rows_cap]
+    lpd::RowAux* raux = nullptr;  // [rows_cap]
+    int* probe = nullptr;    // set by prep_rows when a row needs the exponent probe (K9)
     void* g = nullptr;       // [rows_cap × g_ld] fp32 G of the host-call path (device)
     int64_t g_cols = 0;      // b_eff of the current layout
     int64_t g_elems = 0;     // capacity of g / h in elements
@@ -288,6 +290,7 @@ struct DeviceState {
         s.hx = nullptr;
         s.hx_cap = 0;
         dev_free(s.x); dev_free(s.xhi); dev_free(s.xlo); dev_free(s.raux); dev_free(s.g);
+        dev_free(s.probe);
         dev_free(s.indptr); dev_free(s.indices); dev_free(s.values);
         s.rows_cap = 0; s.g_cols = 0; s.g_elems = 0; s.nnz_cap = 0;
     }
@@ -316,6 +319,7 @@ void ensure_slot(DeviceState& ds, Slot& s, int64_t rows, bool need_g, int64_t nn
         s.kd = ds.kd;
         s.d_cap = std::max<int64_t>(ds.d, 1);
         dev_alloc(&s.raux, static_cast<size_t>(cap));
+        if (!s.probe) dev_alloc(&s.probe, 1);
         if (need_g) {
             dev_alloc(reinterpret_cast<float**>(&s.g), static_cast<size_t>(cap * g_ld));
             s.g_elems = cap * g_ld;
@@ -856,6 +860,7 @@ void launch_factor_panels(DeviceState& ds, Slot& s, int64_t m, void* g_dev, int6
         pg.n_rows = static_cast<int>(rows);
         pg.n_cols = static_cast<int>(ds.b_eff);
         pg.col_scale = ds.col_scale;
+        pg.row_aux = s.raux + r0;
         const size_t es = out_dtype == LPD_OUT_F64 ? 8 : 4;
         pg.G = static_cast<char*>(g_dev) + static_cast<size_t>(r0) * ldg * es;
         pg.ldg = ldg;
@@ -893,9 +898,14 @@ void launch_factor(DeviceState& ds, Slot& s, const double* x_dev, int64_t m, int
         const int threads = 256, rows_per_block = threads / 32;
         const int64_t blocks = std::min<int64_t>((m_pad + rows_per_block - 1) / rows_per_block,
                                                  static_cast<int64_t>(ds.num_sms) * 16);
+        CUDA_TRY(cudaMemsetAsync(s.probe, 0, sizeof(int), st));
         lpd::prep_rows_kernel<<<static_cast<int>(blocks), threads, 0, st>>>(
             x_dev, ldx, static_cast<int>(m), static_cast<int>(ds.d), static_cast<int>(ds.kd), ds.mu,
-            ds.consts, s.xhi, s.xlo, s.raux, static_cast<int>(m_pad), ds.err);
+            ds.consts, s.xhi, s.xlo, s.raux, static_cast<int>(m_pad), ds.err, s.probe);
+        // K9: per-row exponent normalisation, only where prep_rows saw a possibly far
+        // nearest landmark (otherwise an empty launch)
+        lpd::row_shift_kernel<<<static_cast<int>((m + lpd::pr::BM - 1) / lpd::pr::BM), lpd::pr::THREADS, 0, st>>>(
+            s.xhi, static_cast<int>(ds.kd), static_cast<int>(m), ds.lm_hi, static_cast<int>(ds.B), s.raux, s.probe);
     }
     if (ds.large) {
         launch_factor_panels(ds, s, m, g_dev, ldg, out_dtype, st, time_it);

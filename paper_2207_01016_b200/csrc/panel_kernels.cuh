@@ -38,6 +38,7 @@
 // while the MMA fills the other accumulator — no tensor-pipe stall.
 #pragma once
 
+#include "prep_kernels.cuh"
 #include "ptx.cuh"
 
 namespace lpd {
@@ -50,7 +51,7 @@ struct PanelParams {
     int n_kchunks;            // K (padded) / 64
     int n_rows;               // valid rows (MODE_G stores only these)
     int n_cols;               // valid output columns (MODE_G)
-    const float2* row_aux;    // MODE_Z: (R_i, sx_i) per row, t = R_i + acc*sx_i
+    const RowAux* row_aux;    // per row: MODE_Z t = R_i + acc*sx_i and clamp; MODE_G rscale
     __half* z_hi;             // MODE_Z output planes [rows_pad × ldz]
     __half* z_lo;
     long long ldz;
@@ -250,12 +251,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kp::THREADS, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive_cluster(acc_empty_l + 8 * a);
             }
-            float R = 0.f, sx = 0.f;
-            if constexpr (MODE == PANEL_Z) {
-                const float2 ra = p.row_aux[row];
-                R = ra.x;
-                sx = ra.y;
-            }
+            const RowAux ra = p.row_aux[row];  // rows < n_row_pairs·256 are all prepared
+            const float R = ra.R, sx = ra.sx, clampv = ra.clamp, rsc = ra.rscale;
 #pragma unroll
             for (int m = 0; m < 4; ++m) {
                 const int c0 = half * 128 + m * 32;
@@ -267,8 +264,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kp::THREADS, 1)
                     for (int i = 0; i < 16; ++i) {
                         float t0, t1;
                         f2_unpack(ffma2(f2_pack(rs[m * 32 + 2 * i], rs[m * 32 + 2 * i + 1]), sx2, R2), t0, t1);
-                        const float z0 = ex2_approx(fminf(t0, 13.0f));
-                        const float z1 = ex2_approx(fminf(t1, 13.0f));
+                        const float z0 = ex2_approx(fminf(t0, clampv));
+                        const float z1 = ex2_approx(fminf(t1, clampv));
                         const float h0 = __uint_as_float(__float_as_uint(z0) & 0xFFFFE000u);
                         const float h1 = __uint_as_float(__float_as_uint(z1) & 0xFFFFE000u);
                         float l0, l1;
@@ -290,10 +287,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kp::THREADS, 1)
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
                         const float4 sc4 = __ldg(cs4 + i);
-                        out[4 * i + 0] = rs[m * 32 + 4 * i + 0] * sc4.x;
-                        out[4 * i + 1] = rs[m * 32 + 4 * i + 1] * sc4.y;
-                        out[4 * i + 2] = rs[m * 32 + 4 * i + 2] * sc4.z;
-                        out[4 * i + 3] = rs[m * 32 + 4 * i + 3] * sc4.w;
+                        out[4 * i + 0] = rs[m * 32 + 4 * i + 0] * (sc4.x * rsc);
+                        out[4 * i + 1] = rs[m * 32 + 4 * i + 1] * (sc4.y * rsc);
+                        out[4 * i + 2] = rs[m * 32 + 4 * i + 2] * (sc4.z * rsc);
+                        out[4 * i + 3] = rs[m * 32 + 4 * i + 3] * (sc4.w * rsc);
                     }
                     OutT* dst = static_cast<OutT*>(p.G) + row * p.ldg + gc0;
                     const int ncols = min(32, p.n_cols - gc0);

@@ -45,12 +45,26 @@ __device__ __forceinline__ int floor_log2(double v) { return ilogb(v); }
 //   beta   global power-of-two landmark scale (max |b - mu| lands in [2^13, 2^14))
 //   aug    2^-s, the augmented-column scale (landmark side 2^-s, point side 2^s)
 //   g      -gamma * log2(e)
+//   rmin   min_j |b_j - mu| (row prep's bound on a point's nearest-landmark distance)
 struct BasisConsts {
     double beta;
     double aug;
     double g;
-    double pad;
+    double rmin;
 };
+
+// Per-row epilogue operands of the factor kernels (prep_rows_kernel, then
+// row_shift_kernel where needed): t = R + acc*sx, Z'*2^13 = 2^min(t, clamp) with
+// clamp = 13 - shift, and G = (Z'·L)*col_scale*rscale with rscale = 2^shift.
+// shift <= 0 is the row's exponent normalisation (probe_kernels.cuh).
+struct RowAux {
+    float R, sx, clamp, rscale;
+};
+
+// A row whose nearest landmark may be farther than this (in log2 units of Z) gets its
+// exponent normalised by the probe (probe_kernels.cuh): below 2^-PROBE_LOG2Z the Z values
+// would lose fp16 mantissa bits to subnormals.
+constexpr double PROBE_LOG2Z = 8.0;
 
 // Exponent clamp for row scales: 2^(13-e) must stay inside fp16's normal range.
 __device__ __forceinline__ int clamp_exp(double mx) {
@@ -84,23 +98,28 @@ __global__ void landmark_stats_kernel(const double* __restrict__ Y, long long ld
 // entry beta*|b|^2/2 (kept below 2^15 so it fits fp16).
 __global__ void basis_consts_kernel(const double* __restrict__ nb, const double* __restrict__ mx,
                                     int m, double gamma, BasisConsts* __restrict__ out) {
-    __shared__ double smx[32], snb[32];
-    double a = 0.0, b = 0.0;
+    __shared__ double smx[32], snb[32], smn[32];
+    double a = 0.0, b = 0.0, c = 1e300;
     for (int i = threadIdx.x; i < m; i += blockDim.x) {
         a = fmax(a, mx[i]);
         b = fmax(b, nb[i]);
+        c = fmin(c, nb[i]);
     }
     a = warp_max_d(a);
     b = warp_max_d(b);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c = fmin(c, __shfl_xor_sync(0xffffffffu, c, o));
     if ((threadIdx.x & 31) == 0) {
         smx[threadIdx.x >> 5] = a;
         snb[threadIdx.x >> 5] = b;
+        smn[threadIdx.x >> 5] = c;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) {
             a = fmax(a, smx[w]);
             b = fmax(b, snb[w]);
+            c = fmin(c, smn[w]);
         }
         const double beta = ldexp(1.0, 13 - clamp_exp(a));
         const double maxw = 0.5 * beta * b;
@@ -108,7 +127,7 @@ __global__ void basis_consts_kernel(const double* __restrict__ nb, const double*
         out->beta = beta;
         out->aug = ldexp(1.0, -s);
         out->g = -gamma * 1.4426950408889634;
-        out->pad = 0.0;
+        out->rmin = m > 0 ? sqrt(c) : 0.0;
     }
 }
 
@@ -152,12 +171,16 @@ __global__ void prep_landmarks_kernel(const double* __restrict__ Y, long long ld
 // = sigma_i*beta*(<x-mu, b-mu> - |b-mu|^2/2):
 //   t = 13 + g*d2 = R_i + acc*sx_i,  R_i = 13 + g*|x-mu|^2,  sx_i = -2g/(sigma_i*beta)
 // (g = -gamma*log2 e), i.e. Z*2^13 = ex2(min(t, 13)): the reference's clamp of d2 at
-// 0 (kernel.cpp:49-51). aux[i] = (R_i, sx_i). Rows in [m, m_pad) are zero padding.
-// Sets *err if a row's entries would overflow fp16 (|x - mu| >= 2^28).
+// 0 (kernel.cpp:49-51). aux[i] = (R_i, sx_i, 13, 1): no exponent shift. Rows in
+// [m, m_pad) are zero padding. Sets *err if a row's entries would overflow fp16
+// (|x - mu| >= 2^28), and *probe if some row's nearest landmark may be so far that its Z
+// values fall below 2^-PROBE_LOG2Z: |x - b_j| <= |x - mu| + rmin for the landmark
+// closest to mu, so max_j Z_ij >= 2^(g·(|x - mu| + rmin)^2).
 __global__ void prep_rows_kernel(const double* __restrict__ X, long long ldx, int m, int d, int kd,
                                  const double* __restrict__ mu, const BasisConsts* __restrict__ kc,
                                  __half* __restrict__ hi, __half* __restrict__ lo,
-                                 float2* __restrict__ aux, int m_pad, int* __restrict__ err) {
+                                 RowAux* __restrict__ aux, int m_pad, int* __restrict__ err,
+                                 int* __restrict__ probe) {
     const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -182,9 +205,11 @@ __global__ void prep_rows_kernel(const double* __restrict__ X, long long ldx, in
             split_store(hi, lo, base + c, c == d ? sigma / aug : v * sigma);
         }
         if (lane == 0) {
-            aux[row] = make_float2(static_cast<float>(13.0 + g * ss),
-                                   static_cast<float>(-2.0 * g / (sigma * beta)));
+            aux[row] = RowAux{static_cast<float>(13.0 + g * ss), static_cast<float>(-2.0 * g / (sigma * beta)),
+                              13.0f, 1.0f};
             if (row < m && mx >= 0x1p28) atomicOr(err, LPD_FLAG_OVERFLOW);
+            const double far = sqrt(ss) + kc->rmin;
+            if (row < m && g * far * far < -PROBE_LOG2Z && *probe == 0) atomicExch(probe, 1);
         }
     }
 }

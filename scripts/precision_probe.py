@@ -70,8 +70,38 @@ def main():
                 })
                 print(f"scale {scale:4} mult {mult:5} shift {shift:3} b_eff {L.shape[1]:5} est {est:.2e} "
                       f"max err {np.nanmax(err):.2e} zero rows {(~ok).sum()}", flush=True)
+    # cost of the probe (K9) on a C2-shaped chunk: γ = 1/d (no row flagged: empty launch)
+    # vs γ = 16/d (every row probed and shifted)
+    import torch
+
+    timing = {}
+    nt, dt, Bt = 262144, 54, 4096
+    Xt = rng.standard_normal((nt, dt)).astype(np.float32).astype(np.float64)
+    Yt = Xt[:Bt].copy()
+    X_dev = torch.from_numpy(Xt).cuda()
+    for mult in (1.0, 16.0):
+        gamma = mult / dt
+        Lt = np_gaussian_L(Yt, gamma, tau=1e-6)
+        ctx.set_precision("fast")
+        ctx.set_basis_dense(Yt, Lt, gamma)
+        G_dev = torch.empty((nt, Lt.shape[1]), dtype=torch.float64, device="cuda")
+        for _ in range(2):
+            ctx.compute_g_device(X_dev, G_dev)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(5):
+            ctx.compute_g_device(X_dev, G_dev)
+        e1.record()
+        torch.cuda.synchronize()
+        timing[f"gamma_{mult:g}_over_d_ms"] = e0.elapsed_time(e1) / 5
+        Gs = G_dev[:2048].cpu().numpy()
+        R = g64(Xt[:2048], Yt, Lt, gamma)
+        timing[f"gamma_{mult:g}_over_d_max_err"] = float(np.max(np.linalg.norm(Gs - R, axis=1) / np.linalg.norm(R, axis=1)))
+        del G_dev
+    print(json.dumps(timing), flush=True)
     os.makedirs(os.path.dirname(out_path) or ".", exist_ok=True)
-    json.dump(res, open(out_path, "w"))
+    json.dump({"cases": res, "timing": timing}, open(out_path, "w"))
 
 
 if __name__ == "__main__":

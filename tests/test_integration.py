@@ -184,3 +184,22 @@ def test_model_decision_values_on_device_match_reference(tmp_path, classes, extr
     scale = float(np.max(np.abs(r)))
     assert float(np.max(np.abs(g - r))) <= 1e-12 * scale, float(np.max(np.abs(g - r))) / scale
     assert float(np.mean(g == r)) >= 0.5, float(np.mean(g == r))
+
+
+@pytest.mark.gpu
+def test_output_matrix_fast_path_matches_reference_constructor(tmp_path):
+    """compute_G's output Matrix (80 MB here, above the 64 MB cut) built without the
+    reference's zero-fill (adapter make_output_matrix) against LPD_FAST_MATRIX=0, the
+    reference's own Matrix(rows, cols): the same training run must give bitwise the same
+    model and predictions."""
+    import json
+
+    args = ["--n", "20000", "--n-test", "2000", "--budget", "500", "--d", "20", "--train-only"]
+    _run(INTEG, str(tmp_path / "fast.json"), *args)
+    _run(INTEG, str(tmp_path / "plain.json"), *args, env={"LPD_FAST_MATRIX": "0"})
+    f = json.load(open(tmp_path / "fast.json"))
+    p = json.load(open(tmp_path / "plain.json"))
+    for k in ("test_error", "epochs", "effective_rank"):
+        assert f[k] == p[k], k
+    assert np.array_equal(np.load(str(tmp_path / "fast.json") + ".pred.npy"),
+                          np.load(str(tmp_path / "plain.json") + ".pred.npy"))
