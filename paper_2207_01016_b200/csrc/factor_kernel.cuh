@@ -542,16 +542,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
             const int gc0 = cb * N2 + c0;
             if (gc0 >= p.b_eff || K1_ABL(2)) return;
             const float4* cs4 = reinterpret_cast<const float4*>(p.col_scale + gc0);
-            // the row's exponent normalisation (1 unless the probe shifted it, probe_kernels.cuh)
-            const float rsc = p.row_aux[rt * PM + r_pair].rscale;
+            // the row's exponent normalisation 2^shift (shift 0 unless the probe moved the
+            // row, probe_kernels.cuh): in fp64 for fp64 G, in fp32 (range to 2^-149) otherwise
+            const int sh = static_cast<int>(p.row_aux[rt * PM + r_pair].shift);
+            const float rsc = sizeof(OutT) == 8 ? 1.0f : ldexpf(1.0f, sh);
+            const double rsd = ldexp(1.0, sh);
             float v[32];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 const float4 sc = ldg_f4_inorder(cs4 + i);
-                v[4 * i + 0] = rs[m * 32 + 4 * i + 0] * (sc.x * rsc);
-                v[4 * i + 1] = rs[m * 32 + 4 * i + 1] * (sc.y * rsc);
-                v[4 * i + 2] = rs[m * 32 + 4 * i + 2] * (sc.z * rsc);
-                v[4 * i + 3] = rs[m * 32 + 4 * i + 3] * (sc.w * rsc);
+                v[4 * i + 0] = (rs[m * 32 + 4 * i + 0] * sc.x) * rsc;
+                v[4 * i + 1] = (rs[m * 32 + 4 * i + 1] * sc.y) * rsc;
+                v[4 * i + 2] = (rs[m * 32 + 4 * i + 2] * sc.z) * rsc;
+                v[4 * i + 3] = (rs[m * 32 + 4 * i + 3] * sc.w) * rsc;
             }
             // 32 rows x SLAB columns per store; 128-byte swizzled staging rows
             // (16-byte chunk c of row r at chunk c ^ (r & 7)): conflict-free STS.
@@ -567,7 +570,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
                 for (int c = 0; c < 8; ++c) {
                     uint32_t w[4];
                     if constexpr (sizeof(OutT) == 8) {
-                        const double d0 = v[sl * SLAB + 2 * c], d1 = v[sl * SLAB + 2 * c + 1];
+                        const double d0 = v[sl * SLAB + 2 * c] * rsd, d1 = v[sl * SLAB + 2 * c + 1] * rsd;
                         w[0] = __double2loint(d0); w[1] = __double2hiint(d0);
                         w[2] = __double2loint(d1); w[3] = __double2hiint(d1);
                     } else {

@@ -55,10 +55,11 @@ struct BasisConsts {
 
 // Per-row epilogue operands of the factor kernels (prep_rows_kernel, then
 // row_shift_kernel where needed): t = R + acc*sx, Z'*2^13 = 2^min(t, clamp) with
-// clamp = 13 - shift, and G = (Z'·L)*col_scale*rscale with rscale = 2^shift.
-// shift <= 0 is the row's exponent normalisation (probe_kernels.cuh).
+// clamp = 13 - shift, and G = (Z'·L)*col_scale*2^shift. shift (an integer, <= 0) is the
+// row's exponent normalisation (probe_kernels.cuh), applied in fp64 by the fp64-output
+// drains and in fp32 by the fp32 ones (whose range ends at 2^-149).
 struct RowAux {
-    float R, sx, clamp, rscale;
+    float R, sx, clamp, shift;
 };
 
 // A row whose nearest landmark may be farther than this (in log2 units of Z) gets its
@@ -206,7 +207,7 @@ __global__ void prep_rows_kernel(const double* __restrict__ X, long long ldx, in
         }
         if (lane == 0) {
             aux[row] = RowAux{static_cast<float>(13.0 + g * ss), static_cast<float>(-2.0 * g / (sigma * beta)),
-                              13.0f, 1.0f};
+                              13.0f, 0.0f};
             if (row < m && mx >= 0x1p28) atomicOr(err, LPD_FLAG_OVERFLOW);
             const double far = sqrt(ss) + kc->rmin;
             if (row < m && g * far * far < -PROBE_LOG2Z && *probe == 0) atomicExch(probe, 1);

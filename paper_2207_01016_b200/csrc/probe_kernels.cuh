@@ -9,7 +9,8 @@
 // so the row can be computed as 2^shift · (Z_i·2^-shift)·L with any integer shift: the
 // probe estimates t_max,i = max_j t_ij, sets shift_i so that the row's largest Z'·2^13
 // lands in [2^11, 2^14], and the factor kernels apply clamp 13 - shift in the exponent
-// and rscale = 2^shift in their drain (RowAux, prep_kernels.cuh).
+// and 2^shift in their drain (RowAux, prep_kernels.cuh; in fp64 for fp64 G, so only the
+// fp32 outputs keep fp32's range, to 2^-149).
 //
 // t_max only has to be right to about ±1: one fp16 pass on the hi planes (legacy
 // mma.sync m16n8k16, fp32 accumulation) — the same augmented-column GEMM the factor
@@ -40,7 +41,7 @@ __device__ __forceinline__ void hmma16816(float* c, const uint32_t* a, const uin
 }
 
 // rows [0, m) of the hi point plane [m_pad × kd] against landmarks [0, B) of the hi
-// landmark plane [B_pad × kd]; updates aux[i] (R, clamp, rscale) of every valid row.
+// landmark plane [B_pad × kd]; updates aux[i] (R, clamp, shift) of the rows it moves.
 __global__ void __launch_bounds__(pr::THREADS) row_shift_kernel(const __half* __restrict__ xhi, int kd, int m,
                                                                 const __half* __restrict__ lmhi, int B,
                                                                 RowAux* __restrict__ aux,
@@ -119,11 +120,12 @@ __global__ void __launch_bounds__(pr::THREADS) row_shift_kernel(const __half* __
         // i.e. in (2^12, 2^13] for an exact estimate; never above 2^15.5 (fp16 max 65504) even
         // for an estimate that is 3.5 too low. Rows already near 1 keep shift 0 (unchanged).
         const float tm = fminf(tmax, 13.0f);
-        const int sh = max(-120, min(0, static_cast<int>(ceilf(tm)) - 12));
+        // (fp64's range ends near 2^-1074: rows beyond it are zero in fp64 too)
+        const int sh = max(-1100, min(0, static_cast<int>(ceilf(tm)) - 12));
         if (sh == 0) return;
         a0.R -= static_cast<float>(sh);
         a0.clamp = fminf(13.0f - static_cast<float>(sh), 15.5f);
-        a0.rscale = __int_as_float((127 + sh) << 23);  // 2^sh, sh >= -120: normal fp32
+        a0.shift = static_cast<float>(sh);
         aux[r] = a0;
     };
     shift_row(ra, mx_a, aux_a);

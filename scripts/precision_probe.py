@@ -30,6 +30,8 @@ def g64(X, Y, L, gamma):
 
 
 def main():
+    import torch
+
     out_path = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/precision_probe.json"
     rng = np.random.default_rng(5)
     d, B, n = 32, 1024, 3072
@@ -51,12 +53,18 @@ def main():
                 ctx.set_precision("fast")
                 ctx.set_basis_dense(Y, L, gamma)
                 hp, est = ctx.basis_precision()
-                G = ctx.compute_g_dense(X)
+                G = ctx.compute_g_dense(X)  # host path: fp32 G on the wire, widened
+                Xd = torch.from_numpy(X).cuda()
+                Gd = torch.empty((n, L.shape[1]), dtype=torch.float64, device="cuda")
+                ctx.compute_g_device(Xd, Gd)  # device path, fp64 G
+                G64 = Gd.cpu().numpy()
                 R = g64(X, Y, L, gamma)
                 nr = np.linalg.norm(R, axis=1)
                 ok = nr > 0
                 err = np.full(n, np.nan)
                 err[ok] = np.linalg.norm(G - R, axis=1)[ok] / nr[ok]
+                err64 = np.full(n, np.nan)
+                err64[ok] = np.linalg.norm(G64 - R, axis=1)[ok] / nr[ok]
                 mu = Y.mean(0)
                 r = np.linalg.norm(X - mu, axis=1)
                 rb = np.linalg.norm(Y - mu, axis=1)
@@ -64,15 +72,17 @@ def main():
                 res.append({
                     "scale": scale, "gamma_mult": mult, "gamma": gamma, "shift": shift, "b_eff": int(L.shape[1]),
                     "est": est, "Rb_max": float(rb.max()), "Rb_min": float(rb.min()),
-                    "max_err": float(np.nanmax(err)), "zero_rows": int((~ok).sum()),
+                    "max_err": float(np.nanmax(err)), "max_err_f64": float(np.nanmax(err64)),
+                    "zero_rows": int((~ok).sum()),
                     "rows": {"r": r.round(4).tolist(), "dmin": dmin.round(4).tolist(),
-                             "err": [None if not np.isfinite(e) else float(f"{e:.4g}") for e in err]},
+                             "err": [None if not np.isfinite(e) else float(f"{e:.4g}") for e in err],
+                             "err_f64": [None if not np.isfinite(e) else float(f"{e:.4g}") for e in err64]},
                 })
                 print(f"scale {scale:4} mult {mult:5} shift {shift:3} b_eff {L.shape[1]:5} est {est:.2e} "
-                      f"max err {np.nanmax(err):.2e} zero rows {(~ok).sum()}", flush=True)
+                      f"max err fp32-out {np.nanmax(err):.2e} fp64-out {np.nanmax(err64):.2e} "
+                      f"zero rows {(~ok).sum()}", flush=True)
     # cost of the probe (K9) on a C2-shaped chunk: γ = 1/d (no row flagged: empty launch)
     # vs γ = 16/d (every row probed and shifted)
-    import torch
 
     timing = {}
     nt, dt, Bt = 262144, 54, 4096

@@ -546,3 +546,70 @@ def test_precision_auto_choice(gpu_ctx):
     print(f"gamma=2^-7 tau=1e-12 B=1024: estimate {est:.3g}, high-precision row error {err:.3g}, "
           f"fast path {err_fast:.3g}")
     assert err_fast > err
+
+
+def _far_rows_case(d, mult, shift, n=1536, B=384, seed=7):
+    """Unit-variance points; a third of them moved shift·√d away from the landmark
+    cloud along one direction; γ = mult/d."""
+    rng = np.random.default_rng(seed + d + int(10 * mult) + int(10 * shift))
+    base = rng.standard_normal((B + n, d)).astype(np.float32).astype(np.float64)
+    Y, X = base[:B], base[B:].copy()
+    u = rng.standard_normal(d)
+    X[: n // 3] += shift * np.sqrt(d) * u / np.linalg.norm(u)
+    X = X.astype(np.float32).astype(np.float64)
+    gamma = mult / d
+    return X, Y, np_gaussian_L(Y, gamma, 1e-6), gamma
+
+
+@pytest.mark.parametrize("d,mult,shift", [(32, 16, 0), (32, 16, 2), (32, 8, 4), (32, 64, 1), (100, 16, 2)])
+def test_far_rows_and_large_gamma(gpu_ctx, d, mult, shift):
+    """K9 (probe_kernels.cuh): rows whose nearest landmark is far — large γ (up to 64/d)
+    or points several √d from the landmark cloud — have all their kernel values below
+    fp16's normal range; the probe normalises each such row's exponent so K1 (d = 32)
+    and the panel path (d = 100) keep the 1e-4 row bound. fp64 G (device path), so the
+    2^shift row scale is applied in fp64: every row with a nonzero reference meets it,
+    including rows whose kernel values are far below fp32's range. Before K9 these cases
+    measured 0.43 to 1.0 row error (scripts/precision_probe.py)."""
+    import torch
+
+    X, Y, L, gamma = _far_rows_case(d, mult, shift)
+    gpu_ctx.set_precision("fast")
+    try:
+        gpu_ctx.set_basis_dense(Y, L, gamma)
+        Gd = torch.empty((X.shape[0], L.shape[1]), dtype=torch.float64, device="cuda")
+        gpu_ctx.compute_g_device(torch.from_numpy(X).cuda(), Gd)
+        torch.cuda.synchronize()
+        G = Gd.cpu().numpy()
+    finally:
+        gpu_ctx.set_precision("auto")
+    R = _oracle_G(X, Y, L, gamma)
+    nr = np.linalg.norm(R, axis=1)
+    live = nr > 0
+    assert live.sum() >= X.shape[0] // 2
+    assert np.all(G[~live] == 0.0)
+    err = np.linalg.norm(G - R, axis=1)[live] / nr[live]
+    assert float(err.max()) <= TOL_G, float(err.max())
+
+
+def test_far_rows_host_path_fp32_range(gpu_ctx):
+    """The host-call path carries G as fp32 to the host (widened there), so a row is
+    exact to the 1e-4 bound while its values are inside fp32's normal range (here
+    max |G_ref,i| >= 2^-100) and comes back as zeros or fp32 subnormals once they are
+    all below it (the rows 4·√d from the cloud at γ = 8/d: kernel values e^-90 and
+    less) — the stated limit of the fp32 wire format."""
+    X, Y, L, gamma = _far_rows_case(32, 8, 4)
+    gpu_ctx.set_precision("fast")
+    try:
+        gpu_ctx.set_basis_dense(Y, L, gamma)
+        G = gpu_ctx.compute_g_dense(X)
+    finally:
+        gpu_ctx.set_precision("auto")
+    R = _oracle_G(X, Y, L, gamma)
+    rmax = np.abs(R).max(axis=1)
+    tiny = float(np.finfo(np.float32).tiny)
+    normal, below = rmax >= 2.0 ** -100, rmax < tiny
+    assert normal.sum() >= X.shape[0] // 2 and below.sum() > 0
+    nr = np.linalg.norm(R, axis=1)
+    err = np.linalg.norm(G - R, axis=1)[normal] / nr[normal]
+    assert float(err.max()) <= TOL_G, float(err.max())
+    assert np.all(np.abs(G[below]) < tiny)
