@@ -217,11 +217,19 @@ int lpd_kernel_block(lpd_context* ctx, int64_t m, const int64_t* a_indptr, const
  * last call could not keep it (HBM short). */
 int lpd_set_keep_resident(lpd_context* ctx, int enable);
 int lpd_resident_shape(const lpd_context* ctx, int64_t* n, int64_t* b_eff);
-/* D[i][p] = sum_j G[rows[i]][j] * W[p][j] (fp64 accumulation; W is P x b_eff, D is
- * count x P): the held-out scoring of cross-validation (proj/src/modelsel.cpp:123-140)
- * and the gradients 1 - y_i G_i.w of reactivation_pass (proj/src/dcd.cpp:150-172). */
+/* D[i][p] = sum_j G[rows[i]][j] * W[p][j] (W is P x b_eff, D is count x P), each sum in
+ * ascending j with every product rounded then added — the reference's scoring loop
+ * (proj/src/modelsel.cpp:129-136) bit for bit: the held-out scoring of cross-validation
+ * (modelsel.cpp:123-140) and the gradients 1 - y_i G_i.w of reactivation_pass
+ * (proj/src/dcd.cpp:150-172). */
 int lpd_resident_gw(lpd_context* ctx, const int32_t* rows, int64_t count, const double* W,
                     int64_t P, double* D);
+/* The same D for the P = num_classes*(num_classes-1)/2 pair vectors of a one-vs-one model
+ * (W in the reference's pair order, multiclass.cpp:24-32), then the reference's vote
+ * (multiclass.cpp:153-168) on the device: classes[i] = the winning class index of listed
+ * row i. cross_validate's held-out scoring (modelsel.cpp:123-140) without shipping D. */
+int lpd_resident_vote(lpd_context* ctx, const int32_t* rows, int64_t count, const double* W,
+                      int64_t num_classes, int32_t* classes);
 /* w[j] = sum_i coef[i] * G[rows[i]][j] (fp64, deterministic order): rebuild_w of the
  * warm starts (proj/src/dcd.cpp:91-102). */
 int lpd_resident_gtv(lpd_context* ctx, const int32_t* rows, const double* coef, int64_t count,

@@ -76,6 +76,7 @@ EXPORTED_SYMBOLS = (
     "lpd_set_keep_resident",
     "lpd_resident_shape",
     "lpd_resident_gw",
+    "lpd_resident_vote",
     "lpd_resident_gtv",
     "lpd_set_model_dense",
     "lpd_set_model_csr",
@@ -170,6 +171,7 @@ def load_library(path: Optional[str] = None) -> ctypes.CDLL:
     lib.lpd_set_keep_resident.argtypes = [vp, ctypes.c_int]
     lib.lpd_resident_shape.argtypes = [vp, _c_i64_p, _c_i64_p]
     lib.lpd_resident_gw.argtypes = [vp, _c_i32_p, i64, _c_dbl_p, i64, _c_dbl_p]
+    lib.lpd_resident_vote.argtypes = [vp, _c_i32_p, i64, _c_dbl_p, i64, _c_i32_p]
     lib.lpd_resident_gtv.argtypes = [vp, _c_i32_p, _c_dbl_p, i64, _c_dbl_p]
     lib.lpd_predict_ovo_dense.argtypes = [vp, _c_dbl_p, i64, i64, i64, i64, _c_i32_p]
     lib.lpd_predict_ovo_csr.argtypes = [vp, i64, i64, _c_i64_p, _c_i32_p, _c_dbl_p, i64, _c_i32_p]
@@ -488,6 +490,18 @@ class Context:
         _check(self._lib.lpd_resident_gw(self._h, _ptr(r, ctypes.c_int32), r.shape[0], _ptr(w), w.shape[0],
                                          _ptr(D)))
         return D
+
+    def resident_vote(self, rows, W: np.ndarray, num_classes: int) -> np.ndarray:
+        """Class index per listed row: D = G[rows]·Wᵀ for the c(c-1)/2 one-vs-one pair
+        vectors, then the reference's vote (multiclass.cpp:153-168), all on the device."""
+        r = np.ascontiguousarray(rows, dtype=np.int32)
+        w = _f64(np.atleast_2d(W))
+        if w.shape[0] != num_classes * (num_classes - 1) // 2:
+            raise ValueError("W must hold num_classes*(num_classes-1)/2 pair vectors")
+        out = np.empty(r.shape[0], dtype=np.int32)
+        _check(self._lib.lpd_resident_vote(self._h, _ptr(r, ctypes.c_int32), r.shape[0], _ptr(w), num_classes,
+                                           _ptr(out, ctypes.c_int32)))
+        return out
 
     def resident_gtv(self, rows, coef) -> np.ndarray:
         """w = Σ_i coef_i · G[rows_i] on the resident G (rebuild_w, dcd.cpp:91-102)."""

@@ -682,7 +682,8 @@ namespace lpdsvm {
 // cross_validate (modelsel.hpp:49-51, modelsel.cpp:65-161): per fold, train every pair on
 // the other folds (ovo_train, warm-started from the store when given) and score the
 // held-out rows on their G rows — the scoring D = G_heldout·pair_wᵀ runs on the device
-// copy of G (then the reference's vote), the rest is the reference's orchestration.
+// copy of G together with the reference's vote (lpd_resident_vote), the rest is the
+// reference's orchestration.
 CvResult cross_validate(const LowRankFactor& factor, std::span<const double> labels,
                         const LabelMap& label_map, const FoldAssignment& folds, double C,
                         const CvOptions& options, WarmStore* warm) {
@@ -741,34 +742,37 @@ CvResult cross_validate(const LowRankFactor& factor, std::span<const double> lab
             out.total_epochs += rep.epochs;
         }
 
-        // held-out decisions D (|held| × pairs)
+        // held-out decisions D (|held| × pairs) and the vote: on the device (the reference's
+        // summation order bit for bit, then its vote; only the class indices come back)
         const std::size_t be = trained.pair_w.cols();
-        std::vector<double> D(held.size() * num_pairs, 0.0);
+        std::vector<int32_t> voted(held.size(), 0);
         bool on_device = false;
         if (held.size() * be >= device_min_elems()) {
             std::lock_guard<std::mutex> lock(g_mu);
             if (resident_matches(factor.G)) {
-                const int rc = lpd_resident_gw(context(), held.data(), static_cast<int64_t>(held.size()),
-                                               trained.pair_w.data(), static_cast<int64_t>(num_pairs),
-                                               D.data());
-                if (rc != LPD_OK) rethrow_status(rc, "lpd_resident_gw");
+                const int rc = lpd_resident_vote(context(), held.data(), static_cast<int64_t>(held.size()),
+                                                 trained.pair_w.data(), static_cast<int64_t>(c), voted.data());
+                if (rc != LPD_OK) rethrow_status(rc, "lpd_resident_vote");
                 ++g_score_calls;
                 on_device = true;
             }
         }
-        if (!on_device)
+        if (!on_device) {
+            std::vector<double> D(num_pairs);
             for (std::size_t h = 0; h < held.size(); ++h) {
                 const double* g = factor.G.row(static_cast<std::size_t>(held[h]));
                 for (std::size_t p = 0; p < num_pairs; ++p) {
                     const double* wv = trained.pair_w.row(p);
                     double acc = 0.0;
                     for (std::size_t j = 0; j < be; ++j) acc += g[j] * wv[j];
-                    D[h * num_pairs + p] = acc;
+                    D[p] = acc;
                 }
+                voted[h] = vote(D, c);
             }
+        }
         std::size_t wrong = 0;
         for (std::size_t h = 0; h < held.size(); ++h) {
-            const int v = vote(std::span<const double>(D.data() + h * num_pairs, num_pairs), c);
+            const int v = voted[h];
             if (label_map.classes[static_cast<std::size_t>(v)] != labels[static_cast<std::size_t>(held[h])]) ++wrong;
         }
         out.fold_valid[static_cast<std::size_t>(f)] = 1;

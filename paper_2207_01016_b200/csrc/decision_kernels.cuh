@@ -9,6 +9,8 @@
 
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace lpd {
 
 template <typename GT>
@@ -212,6 +214,130 @@ __global__ void __launch_bounds__(256) gather_gw_kernel(const float* __restrict_
                 for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
                 if (lane == 0 && q < np && i0 + r < count) D[static_cast<long long>(i0 + r) * P + p0 + q] = v;
             }
+        }
+    }
+}
+
+// gather_gw_seq: the same product, each D[i][p] summed by one thread in ascending column
+//   order with every product rounded and then added (__dmul_rn / __dadd_rn) — the
+//   reference's scoring loop exactly (modelsel.cpp:129-136, `d += g_row[j] * w_row[j]`,
+//   compiled without FP contraction), so on the same G the device's decision values are
+//   the reference's bit for bit and the CV vote cannot differ.
+//
+//   Listed rows are gathered into shared memory GWS_KC
+//   columns at a time (coalesced 16-byte loads, widened to fp64 and transposed to
+//   [column][row]) with the W columns ([column][p]); a thread owns RT rows × PT vectors
+//   (p = tx + TX·j, so a warp's W reads are consecutive), the block RT·(256/TX) rows ×
+//   PT·TX vectors. The next chunk's G and W are loaded into registers while the current
+//   one is summed. Shapes: RT = 1, TX = 1 (256 rows, PT <= 4 vectors per thread) for a
+//   binary problem's held-out scoring and the reactivation gradients — HBM-bound, 4·b_eff
+//   bytes per row; RT = 4, TX = 16 (64 rows × 16·PT vectors) for every pair of a
+//   multiclass fold at once, each G row read once instead of once per few vectors —
+//   fp64-bound, rows·P·b_eff (product, add) pairs.
+constexpr int GWS_THREADS = 256, GWS_KC = 32;
+template <int RT, int PT, int TX>
+__global__ void __launch_bounds__(GWS_THREADS) gather_gw_seq_kernel(const float* __restrict__ G, long long ldg,
+                                                                    int b_eff, const int32_t* __restrict__ rows,
+                                                                    int count, const double* __restrict__ W, int P,
+                                                                    double* __restrict__ D) {
+    constexpr int PTILE = PT * TX, TY = GWS_THREADS / TX, ROWS = TY * RT;
+    constexpr int GQ = ROWS * GWS_KC / 4 / GWS_THREADS;        // float4 pieces of G per thread per chunk
+    constexpr int WQ = (PTILE * GWS_KC / 2 + GWS_THREADS - 1) / GWS_THREADS;  // double2 pieces of W
+    // the 256-row shape keeps G as fp32 in shared memory (widened per use): static shared
+    // memory ends at 48 KB
+    using GsT = typename std::conditional<RT == 1, float, double>::type;
+    __shared__ __align__(16) GsT Gs[GWS_KC][ROWS + 2];
+    __shared__ __align__(16) double Ws[GWS_KC][PTILE + 2];
+    const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
+    const int r0 = blockIdx.x * ROWS, p0 = blockIdx.y * PTILE;
+    float4 gq[GQ];
+    double2 wq[WQ];
+    auto load = [&](int k0) {
+#pragma unroll
+        for (int u = 0; u < GQ; ++u) {
+            const int c = tid + u * GWS_THREADS, r = c >> 3, q = c & 7;  // 8 pieces per row
+            const int row = rows[min(r0 + r, count - 1)];
+            const float* src = G + static_cast<long long>(row) * ldg + k0 + 4 * q;
+            if (k0 + 4 * q + 3 < b_eff) {
+                gq[u] = *reinterpret_cast<const float4*>(src);
+            } else {
+                float v[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) v[e] = k0 + 4 * q + e < b_eff ? src[e] : 0.0f;
+                gq[u] = make_float4(v[0], v[1], v[2], v[3]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < WQ; ++u) {
+            const int c = tid + u * GWS_THREADS, p = c / (GWS_KC / 2), q = c % (GWS_KC / 2);
+            double2 v = make_double2(0.0, 0.0);
+            if (p < PTILE && p0 + p < P) {
+                const double* src = W + static_cast<long long>(p0 + p) * b_eff + k0 + 2 * q;
+                if (k0 + 2 * q < b_eff) v.x = src[0];
+                if (k0 + 2 * q + 1 < b_eff) v.y = src[1];
+            }
+            wq[u] = v;
+        }
+    };
+    auto stash = [&]() {
+#pragma unroll
+        for (int u = 0; u < GQ; ++u) {
+            const int c = tid + u * GWS_THREADS, r = c >> 3, q = c & 7;
+            Gs[4 * q + 0][r] = static_cast<GsT>(gq[u].x);
+            Gs[4 * q + 1][r] = static_cast<GsT>(gq[u].y);
+            Gs[4 * q + 2][r] = static_cast<GsT>(gq[u].z);
+            Gs[4 * q + 3][r] = static_cast<GsT>(gq[u].w);
+        }
+#pragma unroll
+        for (int u = 0; u < WQ; ++u) {
+            const int c = tid + u * GWS_THREADS, p = c / (GWS_KC / 2), q = c % (GWS_KC / 2);
+            if (p < PTILE) {
+                Ws[2 * q][p] = wq[u].x;
+                Ws[2 * q + 1][p] = wq[u].y;
+            }
+        }
+    };
+    double acc[RT][PT];
+#pragma unroll
+    for (int i = 0; i < RT; ++i)
+#pragma unroll
+        for (int j = 0; j < PT; ++j) acc[i][j] = 0.0;
+    load(0);
+    for (int k0 = 0; k0 < b_eff; k0 += GWS_KC) {
+        __syncthreads();  // the previous chunk is summed
+        stash();
+        __syncthreads();
+        if (k0 + GWS_KC < b_eff) load(k0 + GWS_KC);
+        const int kn = min(GWS_KC, b_eff - k0);
+#pragma unroll 4
+        for (int kk = 0; kk < kn; ++kk) {
+            double g[RT], w[PT];
+            if constexpr (RT == 1) {
+                g[0] = static_cast<double>(Gs[kk][ty]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < RT; i += 2) {
+                    const double2 v = *reinterpret_cast<const double2*>(&Gs[kk][ty * RT + i]);
+                    g[i] = v.x;
+                    g[i + 1] = v.y;
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < PT; ++j) w[j] = Ws[kk][tx + TX * j];
+#pragma unroll
+            for (int i = 0; i < RT; ++i)
+#pragma unroll
+                for (int j = 0; j < PT; ++j) acc[i][j] = __dadd_rn(acc[i][j], __dmul_rn(g[i], w[j]));
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < RT; ++i) {
+        const int r = r0 + ty * RT + i;
+        if (r >= count) continue;
+#pragma unroll
+        for (int j = 0; j < PT; ++j) {
+            const int p = p0 + tx + TX * j;
+            if (p < P) D[static_cast<long long>(r) * P + p] = acc[i][j];
         }
     }
 }

@@ -407,7 +407,13 @@ void init_device(DeviceState& ds, int device) {
             reinterpret_cast<const void*>(lpd::gram_f64_kernel),
             reinterpret_cast<const void*>(lpd::ovo_vote_kernel<float>),
             reinterpret_cast<const void*>(lpd::ovo_pair_table_kernel),
-            reinterpret_cast<const void*>(lpd::gather_gw_kernel<4>),
+            reinterpret_cast<const void*>(lpd::gather_gw_seq_kernel<1, 1, 1>),
+            reinterpret_cast<const void*>(lpd::gather_gw_seq_kernel<1, 4, 1>),
+            reinterpret_cast<const void*>(lpd::gather_gw_seq_kernel<4, 1, 16>),
+            reinterpret_cast<const void*>(lpd::gather_gw_seq_kernel<4, 2, 16>),
+            reinterpret_cast<const void*>(lpd::gather_gw_seq_kernel<4, 3, 16>),
+            reinterpret_cast<const void*>(lpd::gather_gw_seq_kernel<4, 4, 16>),
+            reinterpret_cast<const void*>(lpd::ovo_vote_kernel<double>),
             reinterpret_cast<const void*>(lpd::gather_gtv_partial_kernel<1>),
             reinterpret_cast<const void*>(lpd::gather_gtv_partial_kernel<8>),
             reinterpret_cast<const void*>(lpd::row_sqnorm_seq_kernel),
@@ -1591,6 +1597,88 @@ std::vector<std::vector<std::pair<int32_t, int64_t>>> split_rows(lpd_context* ct
     return parts;
 }
 
+// D = G[rows]·Wᵀ on the resident G (K6 gather_gw_row / gather_gw_seq: the reference's
+// summation order, bitwise), then either D to the host or — with num_classes — the
+// reference's one-vs-one vote on the device (ovo_vote_kernel) and only the class indices
+// to the host: the held-out scoring of cross_validate (modelsel.cpp:123-140) ships 4 bytes
+// per row instead of 8·P.
+void resident_gw(lpd_context* ctx, const int32_t* rows, int64_t count, const double* W, int64_t P, double* D,
+                 int64_t num_classes, int32_t* classes) {
+    check_resident(ctx, rows, count);
+    if (P < 0 || (P > 0 && !W) || (count > 0 && P > 0 && !D && !classes)) fail(LPD_ERR_INVALID_ARGUMENT, "bad W / D");
+    if (count == 0 || P == 0) return;
+    const int64_t b_eff = ctx->res_b_eff;
+    // one device holding every row: the caller's list is the device's list
+    const bool single = ctx->dev.size() == 1 && ctx->dev[0].res_r0 == 0;
+    auto parts = single ? std::vector<std::vector<std::pair<int32_t, int64_t>>>(1) : split_rows(ctx, rows, count);
+    run_parallel(ctx, [&](DeviceState& ds, int di) {
+        const auto& part = parts[static_cast<size_t>(di)];
+        if (!single && part.empty()) return;
+        CUDA_TRY(cudaSetDevice(ds.device));
+        cudaStream_t st = ds.slot[0].stream;
+        const int64_t m = single ? count : static_cast<int64_t>(part.size());
+        const size_t off_w = round_up(sizeof(int32_t) * m, 256);
+        const size_t off_d = off_w + round_up(sizeof(double) * P * b_eff, 256);
+        const size_t off_c = off_d + round_up(sizeof(double) * m * P, 256);
+        char* base = static_cast<char*>(scratch(ds, off_c + sizeof(int32_t) * m));
+        std::vector<int32_t> local(single ? 0 : static_cast<size_t>(m));
+        for (int64_t i = 0; i < static_cast<int64_t>(local.size()); ++i) local[i] = part[i].first;
+        int32_t* drows = reinterpret_cast<int32_t*>(base);
+        double* dw = reinterpret_cast<double*>(base + off_w);
+        double* dd = reinterpret_cast<double*>(base + off_d);
+        int32_t* dc = reinterpret_cast<int32_t*>(base + off_c);
+        CUDA_TRY(cudaMemcpyAsync(drows, single ? rows : local.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaMemcpyAsync(dw, W, sizeof(double) * P * b_eff, cudaMemcpyHostToDevice, st));
+        const int bi = static_cast<int>(b_eff), mi = static_cast<int>(m), pi = static_cast<int>(P);
+        if (P <= 4) {  // one listed row per thread, 256 per block
+            const dim3 grid(static_cast<unsigned>((m + 255) / 256), 1);
+            if (P == 1)
+                lpd::gather_gw_seq_kernel<1, 1, 1><<<grid, lpd::GWS_THREADS, 0, st>>>(ds.res_g, ds.res_ld, bi, drows, mi, dw, pi, dd);
+            else
+                lpd::gather_gw_seq_kernel<1, 4, 1><<<grid, lpd::GWS_THREADS, 0, st>>>(ds.res_g, ds.res_ld, bi, drows, mi, dw, pi, dd);
+        } else {
+            // 16 threads across P, each PT = ceil(P / 16) <= 4 vectors: a P-tile of 16·PT
+            const int pt = static_cast<int>(std::min<int64_t>(4, (P + 15) / 16));
+            const dim3 grid(static_cast<unsigned>((m + 63) / 64), static_cast<unsigned>((P + 16 * pt - 1) / (16 * pt)));
+            switch (pt) {
+                case 1: lpd::gather_gw_seq_kernel<4, 1, 16><<<grid, lpd::GWS_THREADS, 0, st>>>(ds.res_g, ds.res_ld, bi, drows, mi, dw, pi, dd); break;
+                case 2: lpd::gather_gw_seq_kernel<4, 2, 16><<<grid, lpd::GWS_THREADS, 0, st>>>(ds.res_g, ds.res_ld, bi, drows, mi, dw, pi, dd); break;
+                case 3: lpd::gather_gw_seq_kernel<4, 3, 16><<<grid, lpd::GWS_THREADS, 0, st>>>(ds.res_g, ds.res_ld, bi, drows, mi, dw, pi, dd); break;
+                default: lpd::gather_gw_seq_kernel<4, 4, 16><<<grid, lpd::GWS_THREADS, 0, st>>>(ds.res_g, ds.res_ld, bi, drows, mi, dw, pi, dd); break;
+            }
+        }
+        CUDA_TRY(cudaGetLastError());
+        if (classes) {
+            if (ds.pairs_classes != num_classes) {
+                dev_free(ds.pairs);
+                ds.pairs_classes = 0;
+                dev_alloc(&ds.pairs, static_cast<size_t>(P));
+                lpd::ovo_pair_table_kernel<<<static_cast<int>(num_classes), 128, 0, st>>>(static_cast<int>(num_classes),
+                                                                                         ds.pairs);
+                CUDA_TRY(cudaGetLastError());
+                ds.pairs_classes = static_cast<int>(num_classes);
+            }
+            const int vb = static_cast<int>(std::min<int64_t>((m + lpd::VOTE_WARPS - 1) / lpd::VOTE_WARPS,
+                                                              static_cast<int64_t>(ds.num_sms) * 8));
+            lpd::ovo_vote_kernel<double><<<vb, 32 * lpd::VOTE_WARPS, sizeof(int) * lpd::VOTE_WARPS * num_classes, st>>>(
+                dd, P, mi, static_cast<int>(num_classes), ds.pairs, pi, dc);
+            CUDA_TRY(cudaGetLastError());
+        }
+        const size_t es = classes ? sizeof(int32_t) : sizeof(double) * P;  // bytes per row out
+        void* src = classes ? static_cast<void*>(dc) : static_cast<void*>(dd);
+        char* dst = classes ? reinterpret_cast<char*>(classes) : reinterpret_cast<char*>(D);
+        if (single || m == count) {  // every listed row on this device, in order: straight out
+            CUDA_TRY(cudaMemcpyAsync(dst, src, es * m, cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaStreamSynchronize(st));
+            return;
+        }
+        std::vector<char> h(es * static_cast<size_t>(m));
+        CUDA_TRY(cudaMemcpyAsync(h.data(), src, es * m, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        for (int64_t i = 0; i < m; ++i) std::memcpy(dst + part[i].second * es, h.data() + i * es, es);
+    });
+}
+
 // ------------------------------------------------------------------ K8 (per-point decision values)
 // Host rows, dense (X, ldx) or CSR, read as dense fp64 of width d with implicit zeros
 // (dataio.hpp:14-24). A CSR index outside [0, d) is an error, not a silent drop.
@@ -2326,47 +2414,17 @@ int lpd_resident_shape(const lpd_context* ctx, int64_t* n, int64_t* b_eff) {
 
 int lpd_resident_gw(lpd_context* ctx, const int32_t* rows, int64_t count, const double* W, int64_t P,
                     double* D) {
+    return guarded([&] { resident_gw(ctx, rows, count, W, P, D, 0, nullptr); });
+}
+
+int lpd_resident_vote(lpd_context* ctx, const int32_t* rows, int64_t count, const double* W,
+                      int64_t num_classes, int32_t* classes) {
     return guarded([&] {
-        check_resident(ctx, rows, count);
-        if (P < 0 || (P > 0 && !W) || (count > 0 && P > 0 && !D)) fail(LPD_ERR_INVALID_ARGUMENT, "bad W / D");
-        if (count == 0 || P == 0) return;
-        const int64_t b_eff = ctx->res_b_eff;
-        // one device holding every row: the caller's list is the device's list
-        const bool single = ctx->dev.size() == 1 && ctx->dev[0].res_r0 == 0;
-        auto parts = single ? std::vector<std::vector<std::pair<int32_t, int64_t>>>(1) : split_rows(ctx, rows, count);
-        run_parallel(ctx, [&](DeviceState& ds, int di) {
-            const auto& part = parts[static_cast<size_t>(di)];
-            if (!single && part.empty()) return;
-            CUDA_TRY(cudaSetDevice(ds.device));
-            cudaStream_t st = ds.slot[0].stream;
-            const int64_t m = single ? count : static_cast<int64_t>(part.size());
-            const size_t off_w = round_up(sizeof(int32_t) * m, 256);
-            const size_t off_d = off_w + round_up(sizeof(double) * P * b_eff, 256);
-            char* base = static_cast<char*>(scratch(ds, off_d + sizeof(double) * m * P));
-            std::vector<int32_t> local(single ? 0 : static_cast<size_t>(m));
-            for (int64_t i = 0; i < static_cast<int64_t>(local.size()); ++i) local[i] = part[i].first;
-            int32_t* drows = reinterpret_cast<int32_t*>(base);
-            double* dw = reinterpret_cast<double*>(base + off_w);
-            double* dd = reinterpret_cast<double*>(base + off_d);
-            CUDA_TRY(cudaMemcpyAsync(drows, single ? rows : local.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, st));
-            CUDA_TRY(cudaMemcpyAsync(dw, W, sizeof(double) * P * b_eff, cudaMemcpyHostToDevice, st));
-            const int blocks = static_cast<int>(std::min<int64_t>((m + 31) / 32, static_cast<int64_t>(ds.num_sms) * 16));
-            for (int64_t p0 = 0; p0 < P; p0 += 4)
-                lpd::gather_gw_kernel<4><<<blocks, 256, 0, st>>>(ds.res_g, ds.res_ld, static_cast<int>(b_eff), drows,
-                                                                 static_cast<int>(m), dw, static_cast<int>(P),
-                                                                 static_cast<int>(p0), dd);
-            CUDA_TRY(cudaGetLastError());
-            if (single || m == count) {  // every listed row on this device, in order: straight into D
-                CUDA_TRY(cudaMemcpyAsync(D, dd, sizeof(double) * m * P, cudaMemcpyDeviceToHost, st));
-                CUDA_TRY(cudaStreamSynchronize(st));
-                return;
-            }
-            std::vector<double> hd(static_cast<size_t>(m * P));
-            CUDA_TRY(cudaMemcpyAsync(hd.data(), dd, sizeof(double) * m * P, cudaMemcpyDeviceToHost, st));
-            CUDA_TRY(cudaStreamSynchronize(st));
-            for (int64_t i = 0; i < m; ++i)
-                std::memcpy(D + part[i].second * P, hd.data() + i * P, sizeof(double) * P);
-        });
+        if (num_classes < 2 || num_classes > lpd::VOTE_MAX_CLASSES)
+            fail(num_classes < 2 ? LPD_ERR_INVALID_ARGUMENT : LPD_ERR_UNSUPPORTED,
+                 "num_classes must be in [2, " + std::to_string(lpd::VOTE_MAX_CLASSES) + "]");
+        if (count > 0 && !classes) fail(LPD_ERR_INVALID_ARGUMENT, "classes is null");
+        resident_gw(ctx, rows, count, W, num_classes * (num_classes - 1) / 2, nullptr, num_classes, classes);
     });
 }
 

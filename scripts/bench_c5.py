@@ -35,7 +35,23 @@ def main():
     Y, L = bench.make_basis(X, cfg)
     n, b_eff = X.shape[0], L.shape[1]
     peaks = bench.load_peaks()
+    # fp64 roofline denominator: cuBLAS DGEMM (torch float64 matmul) on this GPU
+    import torch
+
+    a = torch.randn(8192, 8192, dtype=torch.float64, device="cuda")
+    for _ in range(2):
+        a @ a
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        a @ a
+    e1.record()
+    torch.cuda.synchronize()
+    fp64_tflops = 5 * 2 * 8192.0 ** 3 / (e0.elapsed_time(e1) * 1e-3) / 1e12
+    del a
     out = {"config": "c5: C2 factor resident in HBM, CV scoring + warm-start rebuild on device",
+           "fp64_dgemm_tflops_measured": fp64_tflops,
            "n": n, "B": Y.shape[0], "b_eff": b_eff, "hbm_peak_gbs": peaks["hbm"], "peak_source": peaks["src"]}
     with P.Context(1) as ctx:
         ctx.set_basis_dense(Y, L, cfg.gamma)
@@ -58,11 +74,17 @@ def main():
                 ctx.resident_gw(held, W)
                 ts.append(time.perf_counter() - t0)
             t = float(np.median(ts))
-            byts = held.size * b_eff * 4  # fp32 resident G rows, read once per pass of <= 4 vectors
-            passes = -(-P_ // 4)
+            # roofline: the G rows once (fp32) from HBM, and rows·P·b_eff (product, add) pairs in
+            # fp64 — separate DMUL and DADD (the reference's rounding), i.e. half the fp64 FMA rate
+            byts = held.size * b_eff * 4
+            ops = 2.0 * held.size * P_ * b_eff
+            t_hbm = byts / (peaks["hbm"] * 1e9)
+            t_f64 = ops / (fp64_tflops * 0.5e12)
             out[f"score_P{P_}"] = {"rows": int(held.size), "seconds": t, "rows_per_s": held.size / t,
-                                   "algorithmic_gbs": byts * passes / t / 1e9,
-                                   "frac_of_hbm": byts * passes / t / 1e9 / peaks["hbm"]}
+                                   "hbm_gbs": byts / t / 1e9, "frac_of_hbm": t_hbm / t,
+                                   "fp64_tflops": ops / t / 1e12, "frac_of_fp64_mul_add": t_f64 / t,
+                                   "bound": "hbm" if t_hbm >= t_f64 else "fp64",
+                                   "frac_of_roofline": max(t_hbm, t_f64) / t}
             if P_ == 1:
                 sub = held[:20000]
                 t0 = time.perf_counter()
@@ -72,6 +94,19 @@ def main():
                 out["score_P1"]["reference_loop_sample"] = f"{sub.size} held-out rows, 1 thread (modelsel.cpp:123-140 restated)"
                 err = np.max(np.abs(D[: sub.size] - Dc)) / np.max(np.abs(Dc))
                 out["score_P1"]["max_rel_diff_vs_reference_loop"] = float(err)
+                out["score_P1"]["bitwise_equal_to_reference_loop"] = bool(np.array_equal(D[: sub.size], Dc))
+        # cross_validate's held-out scoring of a 10-class fold as the adapter runs it: the 45
+        # pair vectors, then the vote, on the device; only class indices come back
+        W = rng.standard_normal((45, b_eff))
+        ctx.resident_vote(held, W, 10)
+        ts = []
+        for _ in range(args.reps):
+            t0 = time.perf_counter()
+            ctx.resident_vote(held, W, 10)
+            ts.append(time.perf_counter() - t0)
+        t = float(np.median(ts))
+        out["vote_P45"] = {"rows": int(held.size), "seconds": t, "rows_per_s": held.size / t,
+                           "d2h_bytes": int(held.size * 4)}
         coef = rng.standard_normal(train.size)
         w = ctx.resident_gtv(train, coef)
         ts = []

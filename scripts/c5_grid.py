@@ -31,6 +31,8 @@ def main():
     ap.add_argument("--folds", type=int, default=3)
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--tau", type=float, default=1e-12)
+    ap.add_argument("--gamma-mults", default="0.5,1,2", help="γ = mult/d, comma separated")
+    ap.add_argument("--Cs", default="0.25,1,4")
     args = ap.parse_args()
 
     mdir = args.module_dir if os.path.isabs(args.module_dir) else os.path.join(ROOT, args.module_dir)
@@ -45,8 +47,9 @@ def main():
     X, y = synthetic.blobs(args.n, args.d, seed=2)
     data = lpdsvm.parse_dataset(libsvm_text(X, y))
     g0 = 1.0 / args.d
-    gammas = [g0 / 2, g0, 2 * g0]  # log2 γ around γ* (PAPER.md:828-832 style grid)
-    Cs = [0.25, 1.0, 4.0]
+    # log2 γ around γ* (PAPER.md:828-832 style grid)
+    gammas = [float(m) * g0 for m in args.gamma_mults.split(",")]
+    Cs = [float(c) for c in args.Cs.split(",")]
     threads = args.threads or os.cpu_count()
     t0 = time.perf_counter()
     rep = lpdsvm.grid_search(data, gammas=gammas, Cs=Cs, budget=args.budget, folds=args.folds,

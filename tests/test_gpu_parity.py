@@ -379,7 +379,8 @@ def test_kernel_block_fp64_matches_reference(gpu_ctx, m, n, d, gamma):
 @pytest.mark.parametrize("nb", [300, 301])  # b_eff % 4 == 0: 16-byte path; else scalar path
 def test_resident_g_products(gpu_ctx, nb):
     """K6: G kept resident (fp32, bit-identical to the returned fp64 G) serves the
-    held-out scoring G[rows]·Wᵀ and rebuild_w's Σ coef_i·G_i in fp64 on the device."""
+    held-out scoring G[rows]·Wᵀ (bitwise the reference's loop) and rebuild_w's
+    Σ coef_i·G_i in fp64 on the device."""
     rng = np.random.default_rng(12)
     X = rng.standard_normal((3000, 20)).astype(np.float32).astype(np.float64)
     Y = X[:nb]
@@ -390,10 +391,21 @@ def test_resident_g_products(gpu_ctx, nb):
         G = gpu_ctx.compute_g_dense(X)
         assert gpu_ctx.resident_shape() == (3000, L.shape[1])
         rows = rng.choice(3000, 777, replace=False).astype(np.int32)
-        W = rng.standard_normal((6, L.shape[1]))  # two passes of <= 4 vectors
-        D = gpu_ctx.resident_gw(rows, W)
-        Dref = G[rows] @ W.T
-        assert np.max(np.abs(D - Dref)) <= 1e-12 * np.max(np.abs(Dref))
+        # the reference's scoring loop (modelsel.cpp:129-136): per (row, vector) products
+        # rounded, then added in ascending column order — bit for bit, for P = 1 and 3
+        # (the 256-row shape) and P = 6, 45, 70 (64 × 64 tiles, two tiles in P at 70)
+        for P_ in (1, 3, 6, 45, 70):
+            W = rng.standard_normal((P_, L.shape[1]))
+            D = gpu_ctx.resident_gw(rows, W)
+            Dseq = np.add.accumulate(G[rows][:, None, :] * W[None, :, :], axis=2)[:, :, -1]
+            assert np.array_equal(D, Dseq), (P_, float(np.max(np.abs(D - Dseq))))
+        # ... and the one-vs-one vote on the device over those decision values: class
+        # indices equal to the reference's vote (multiclass.cpp:153-168) on the same D
+        for c in (2, 3, 10):
+            Wc = rng.standard_normal((c * (c - 1) // 2, L.shape[1]))
+            cls = gpu_ctx.resident_vote(rows, Wc, c)
+            Dc = gpu_ctx.resident_gw(rows, Wc)
+            assert np.array_equal(cls, [O.ora_vote(Dc[i], c) for i in range(rows.size)]), c
         coef = rng.standard_normal(777)
         w = gpu_ctx.resident_gtv(rows, coef)
         wref = coef @ G[rows]
