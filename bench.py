@@ -274,7 +274,7 @@ def main():
     N = world
     res = measure(args, cfg, n, N, rank, local, dist, dev, P, args.steps, args.warmup, not args.no_e2e)
 
-    cpu = dropin = trains = c4 = None
+    cpu = dropin = trains = c4 = c5 = None
     if rank == 0 and N == 1:
         if not args.no_cpu_baseline:
             from oracle import oracle as O
@@ -287,6 +287,7 @@ def main():
                        "sample": f"{rows} contiguous rows of the {n}-row workload, same landmarks/L, "
                                  f"{secs:.1f}s, chunk_size={max(64, -(-rows // threads))}"}
         if not args.no_extras:
+            c5 = c5_resident(res, cfg, P)
             dropin = e2e_dropin("b200", cfg, res, n)
             trains = {c: e2e_train("b200", c) for c in ("c1", "c2")}
             if args.workload != "c4":
@@ -322,6 +323,8 @@ def main():
             # lpdsvm.train's train_impl (module.cpp:35-78) end to end on the drop-in build
             "train_seconds": trains,
             "c4_shard": c4,
+            # config 5: the products cross_validate / the solver run on the resident G
+            "c5_resident": c5,
             "gpu_launches": launches_per_step(n, cfg.d, res["B"]) * args.steps,
             "clocks": res["clocks"],
         }
@@ -329,6 +332,74 @@ def main():
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def c5_resident(res, cfg, P, reps=5):
+    """BASELINE config 5's device products on this workload's factor kept resident in HBM
+    (lpd_set_keep_resident): a 5-fold split's held-out scoring — binary (P = 1, the
+    reference's loop order bit for bit, lpd_resident_gw) and a 10-class fold (45 pair
+    vectors + the one-vs-one vote on the device, lpd_resident_vote) — and the warm-start
+    rebuild w = Σ coef_i·G_i over the training rows (lpd_resident_gtv). Wall time through
+    the C ABI (row list and W up, results down), median of `reps`; roofline = HBM time of
+    the G rows read vs fp64 time of the (product, add) pairs at half the DGEMM rate."""
+    import torch
+
+    X, Y, L = res["X"], res["Y"], res["L"]
+    n, b_eff = X.shape[0], L.shape[1]
+    a = torch.randn(4096, 4096, dtype=torch.float64, device="cuda")
+    a @ a
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(4):
+        a @ a
+    torch.cuda.synchronize()
+    dgemm = 4 * 2 * 4096.0 ** 3 / (time.perf_counter() - t0) / 1e12
+    del a
+    peaks = load_peaks()
+    rng = np.random.default_rng(5)
+    fold = rng.permutation(n) % 5
+    held = np.flatnonzero(fold == 0).astype(np.int32)
+    train = np.flatnonzero(fold != 0).astype(np.int32)
+    out = {"n": n, "b_eff": b_eff, "held_out_rows": int(held.size), "train_rows": int(train.size),
+           "fp64_dgemm_tflops": dgemm, "hbm_peak_gbs": peaks["hbm"]}
+    G = np.empty((n, b_eff))
+    with P.Context(1) as ctx:
+        ctx.set_basis_dense(Y, L, cfg.gamma)
+        ctx.set_keep_resident(True)
+        ctx.compute_g_dense(X, out=G)
+        if ctx.resident_shape() != (n, b_eff):
+            return {"skipped": "resident G did not fit"}
+
+        def timed(f):
+            f()
+            ts = []
+            for _ in range(reps):
+                t0 = time.perf_counter()
+                f()
+                ts.append(time.perf_counter() - t0)
+            return statistics.median(ts)
+
+        def roof(t, rows, pairs):
+            t_hbm = rows * b_eff * 4 / (peaks["hbm"] * 1e9)
+            t_f64 = 2.0 * rows * pairs * b_eff / (dgemm * 0.5e12)
+            return {"seconds": t, "rows_per_s": rows / t, "bound": "hbm" if t_hbm >= t_f64 else "fp64",
+                    "frac_of_roofline_c_abi": max(t_hbm, t_f64) / t}
+
+        w1 = rng.standard_normal((1, b_eff))
+        D = ctx.resident_gw(held, w1)
+        k = min(2000, held.size)
+        seq = np.add.accumulate(G[held[:k]] * w1[0], axis=1)[:, -1]
+        out["score_binary"] = {**roof(timed(lambda: ctx.resident_gw(held, w1)), held.size, 1),
+                               "bitwise_equal_to_reference_loop_sample": bool(np.array_equal(D[:k, 0], seq))}
+        w45 = rng.standard_normal((45, b_eff))
+        out["score_vote_10class"] = roof(timed(lambda: ctx.resident_vote(held, w45, 10)), held.size, 45)
+        coef = rng.standard_normal(train.size)
+        t = timed(lambda: ctx.resident_gtv(train, coef))
+        out["rebuild_w"] = {"seconds": t, "rows": int(train.size),
+                            "frac_of_hbm_c_abi": train.size * b_eff * 4 / (peaks["hbm"] * 1e9) / t}
+        ctx.set_keep_resident(False)
+    del G
+    return out
 
 
 def _run_e2e_subprocess(argv, timeout):
