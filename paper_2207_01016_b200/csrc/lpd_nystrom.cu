@@ -33,6 +33,9 @@
 #include <thread>
 #include <vector>
 
+#include <pthread.h>
+#include <sched.h>
+
 #include "../../include/lpd_nystrom.h"
 #include "decision_kernels.cuh"
 #include "factor_kernel.cuh"
@@ -198,6 +201,12 @@ struct DeviceState {
     __half* z_lo = nullptr;
     int64_t z_rows = 0;
     int host_share = 1;                // device states of this context sharing the host's cores
+    // host CPUs local to this GPU (its PCI device's NUMA node) when that is a proper subset of
+    // the process's CPUs: the delivery / staging threads run there and the pinned ring and
+    // the caller's G pages they first-touch land on that node (LPD_NUMA=0: off)
+    cpu_set_t local_cpus;
+    int local_count = 0;               // 0: no binding (one node, unknown, or off)
+    int allowed_count = 0;             // CPUs this process may run on
     unsigned int* sync_ctr = nullptr;  // panel GEMM K-progress rendezvous counters [kSyncCtrs]
     static constexpr int kSyncCtrs = 64;
     int sync_seq = 0;
@@ -356,10 +365,94 @@ FactorKernel factor_kernel_for(bool f64, int ks1) {
     }
 }
 
+// CPUs in a sysfs list ("0-27,56-83").
+void parse_cpulist(const std::string& text, cpu_set_t* set) {
+    CPU_ZERO(set);
+    size_t i = 0;
+    while (i < text.size()) {
+        size_t j = i;
+        while (j < text.size() && text[j] != ',') ++j;
+        const std::string part = text.substr(i, j - i);
+        const size_t dash = part.find('-');
+        char* end = nullptr;
+        const long a = std::strtol(part.c_str(), &end, 10);
+        const long b = dash == std::string::npos ? a : std::strtol(part.c_str() + dash + 1, &end, 10);
+        if (end != part.c_str())
+            for (long c = a; c <= b && c < CPU_SETSIZE; ++c)
+                if (c >= 0) CPU_SET(static_cast<int>(c), set);
+        i = j + 1;
+    }
+}
+
+// The GPU's local CPUs (sysfs local_cpulist of its PCI function) ∩ this process's allowed
+// CPUs; left empty (local_count = 0) on a single-node box, when unknown, or LPD_NUMA=0.
+void find_local_cpus(DeviceState& ds) {
+    CPU_ZERO(&ds.local_cpus);
+    ds.local_count = 0;
+    cpu_set_t allowed;
+    if (sched_getaffinity(0, sizeof(allowed), &allowed) != 0) return;
+    ds.allowed_count = CPU_COUNT(&allowed);
+    const char* e = std::getenv("LPD_NUMA");
+    if (e && e[0] == '0') return;
+    char bus[64] = {};
+    if (cudaDeviceGetPCIBusId(bus, sizeof(bus), ds.device) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    std::string id(bus);
+    for (char& c : id) c = static_cast<char>(std::tolower(static_cast<unsigned char>(c)));
+    if (id.size() == 12) id = "0000" + id.substr(4);  // 8-digit domain -> sysfs's 4-digit form
+    FILE* f = std::fopen(("/sys/bus/pci/devices/" + id + "/local_cpulist").c_str(), "r");
+    if (!f) return;
+    char buf[4096] = {};
+    const size_t got = std::fread(buf, 1, sizeof(buf) - 1, f);
+    std::fclose(f);
+    if (got == 0) return;
+    cpu_set_t local;
+    parse_cpulist(std::string(buf, got), &local);
+    CPU_AND(&local, &local, &allowed);
+    const int cnt = CPU_COUNT(&local);
+    if (cnt == 0 || cnt == ds.allowed_count) return;  // no locality to exploit
+    ds.local_cpus = local;
+    ds.local_count = cnt;
+}
+
+// Binds the calling thread to a device's local CPUs for a scope, restoring its affinity.
+struct ScopedAffinity {
+    cpu_set_t saved;
+    bool on = false;
+    explicit ScopedAffinity(const DeviceState& ds) {
+        if (ds.local_count == 0) return;
+        if (pthread_getaffinity_np(pthread_self(), sizeof(saved), &saved) != 0) return;
+        on = pthread_setaffinity_np(pthread_self(), sizeof(ds.local_cpus), &ds.local_cpus) == 0;
+    }
+    ~ScopedAffinity() {
+        if (on) pthread_setaffinity_np(pthread_self(), sizeof(saved), &saved);
+    }
+};
+
+// Host worker threads for one device: min(16, its CPUs / the devices and local ranks
+// sharing them). Local CPUs when the box has several nodes: the devices of a context and
+// the torchrun ranks of a node (LOCAL_WORLD_SIZE spread over the nodes) share them.
+int host_workers(const DeviceState& ds) {
+    static const int local_ranks = [] {
+        const char* e = std::getenv("LOCAL_WORLD_SIZE");
+        return e ? std::max(1, std::atoi(e)) : 1;
+    }();
+    const int hw = std::max(1u, std::thread::hardware_concurrency());
+    if (ds.local_count > 0) {
+        const int nodes = std::max(1, ds.allowed_count / ds.local_count);
+        const int share = std::max(1, (ds.host_share + nodes - 1) / nodes) * std::max(1, (local_ranks + nodes - 1) / nodes);
+        return std::max(1, std::min(16, ds.local_count / share));
+    }
+    return std::max(1, std::min(16, hw / (ds.host_share * local_ranks)));
+}
+
 void init_device(DeviceState& ds, int device) {
     ds.device = device;
     CUDA_TRY(cudaSetDevice(device));
     CUDA_TRY(cudaDeviceGetAttribute(&ds.num_sms, cudaDevAttrMultiProcessorCount, device));
+    find_local_cpus(ds);
     int major = 0, minor = 0;
     CUDA_TRY(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
     CUDA_TRY(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device));
@@ -1019,8 +1112,13 @@ void check_range_flag(DeviceState& ds) {
 // condition-variable wake-up per item would cost more than the copy.
 class SpinTeam {
 public:
-    explicit SpinTeam(int n) : n_(std::max(1, n)) {
-        for (int i = 1; i < n_; ++i) th_.emplace_back([this, i] { loop(i); });
+    explicit SpinTeam(int n, const DeviceState* bind = nullptr) : n_(std::max(1, n)) {
+        for (int i = 1; i < n_; ++i)
+            th_.emplace_back([this, i, bind] {
+                if (bind && bind->local_count > 0)
+                    pthread_setaffinity_np(pthread_self(), sizeof(bind->local_cpus), &bind->local_cpus);
+                loop(i);
+            });
     }
     ~SpinTeam() {
         {
@@ -1239,12 +1337,11 @@ void h2d_staged(DeviceState& ds, void* dst, const void* src, size_t bytes, cudaS
         CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
         return;
     }
+    ScopedAffinity bind(ds);  // the pinned ring and the copy team on the GPU's node
     ensure_delivery_ring(ds);
     const int R = static_cast<int>(ds.dring.size());
     const size_t piece = ds.dring_bytes;
-    const int hw = std::max(1u, std::thread::hardware_concurrency());
-    const char* lws = std::getenv("LOCAL_WORLD_SIZE");
-    SpinTeam team(std::max(1, std::min(16, hw / (ds.host_share * (lws ? std::max(1, std::atoi(lws)) : 1)))));
+    SpinTeam team(host_workers(ds), &ds);
     const char* s8 = static_cast<const char*>(src);
     char* d8 = static_cast<char*>(dst);
     for (size_t g = 0, off = 0; off < bytes; ++g, off += piece) {
@@ -1292,18 +1389,10 @@ void compute_rows_host(lpd_context* ctx, int64_t n, double* G, int64_t ldg, lpd_
     const int64_t chunk_bytes = 512ll << 20;
     const int64_t chunk = std::max<int64_t>(
         256, std::min<int64_t>(round_up(n, 256), chunk_bytes / (4 * b_eff) / 256 * 256));
-    const int hw = std::max(1u, std::thread::hardware_concurrency());
     static const int env_workers = [] {
         const char* e = std::getenv("LPD_WIDEN_THREADS");
         return e ? std::max(1, std::atoi(e)) : 0;
     }();
-    // host threads per device: the box's cores shared by this context's devices and, under
-    // torchrun (one process per GPU), by the other local ranks
-    static const int local_ranks = [] {
-        const char* e = std::getenv("LOCAL_WORLD_SIZE");
-        return e ? std::max(1, std::atoi(e)) : 1;
-    }();
-    const int workers = env_workers ? env_workers : std::max(1, std::min(16, hw / (nd * local_ranks)));
     ctx->res_n = 0;
     std::vector<int> resident_ok(nd, 0);
     run_parallel(ctx, [&](DeviceState& ds, int di) {
@@ -1338,8 +1427,11 @@ void compute_rows_host(lpd_context* ctx, int64_t n, double* G, int64_t ldg, lpd_
         resident_ok[di] = resident || r_end <= r_begin;
         if (r_end <= r_begin) return;
 
+        // host side on the GPU's NUMA node (multi-node boxes): the pinned ring, the widen
+        // team, and so the first touch of this device's rows of the caller's G
+        ScopedAffinity bind(ds);
         ensure_delivery_ring(ds);
-        SpinTeam team(workers);
+        SpinTeam team(env_workers ? env_workers : host_workers(ds), &ds);
         const int R = static_cast<int>(ds.dring.size());
         const int64_t g_ld = round_up(b_eff, 4);
         const int64_t sub_rows = std::max<int64_t>(1, static_cast<int64_t>(ds.dring_bytes / (4 * g_ld)));
