@@ -180,6 +180,31 @@ struct Slot {
     double* values = nullptr;
 };
 
+// A grow-only device buffer (the basis staging of lpd_set_basis_*): cudaMalloc / cudaFree
+// of the 134 MB fp64 L at C2 on every call cost 1–20 ms each and, on some boxes, a
+// cudaFree stalled the call by up to 0.4 s (LPD_TRACE, scripts/e2e_probe.py).
+struct GrowBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    void* get(size_t bytes) {
+        bytes = std::max<size_t>(bytes, 8);
+        if (bytes > cap) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            cap = 0;
+            CUDA_TRY(cudaMalloc(&p, bytes));
+            cap = bytes;
+        }
+        return p;
+    }
+    double* d(size_t bytes) { return static_cast<double*>(get(bytes)); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
 struct DeviceState {
     int device = 0;
     int num_sms = 0;
@@ -200,6 +225,7 @@ struct DeviceState {
     __half* z_hi = nullptr;    // large path: Z panel scratch [z_rows × B_pad]
     __half* z_lo = nullptr;
     int64_t z_rows = 0;
+    GrowBuf stage_lm, stage_L, stage_ip, stage_idx, stage_val;  // basis staging (lpd_set_basis_*)
     int host_share = 1;                // device states of this context sharing the host's cores
     // host CPUs local to this GPU (its PCI device's NUMA node) when that is a proper subset of
     // the process's CPUs: the delivery / staging threads run there and the pinned ring and
@@ -762,26 +788,6 @@ struct PhaseTrace {
 
 void h2d_staged(DeviceState& ds, void* dst, const void* src, size_t bytes, cudaStream_t st);
 
-// A device buffer freed on scope exit (basis staging).
-struct DevBuf {
-    void* p = nullptr;
-    int device = 0;
-    DevBuf() = default;
-    DevBuf(const DevBuf&) = delete;
-    DevBuf& operator=(const DevBuf&) = delete;
-    void alloc(int dev, size_t bytes) {
-        device = dev;
-        CUDA_TRY(cudaSetDevice(dev));
-        CUDA_TRY(cudaMalloc(&p, std::max<size_t>(bytes, 8)));
-    }
-    ~DevBuf() {
-        if (p) {
-            cudaSetDevice(device);
-            cudaFree(p);
-        }
-    }
-    double* d() { return static_cast<double*>(p); }
-};
 
 // The basis of one γ on every device of the context ("one broadcast of
 // the basis per γ"): the landmarks (dense fp64 [B × max(d, 1)], produced on the first
@@ -797,29 +803,28 @@ void set_basis_all(lpd_context* ctx, int64_t B, int64_t d, const double* L_host,
     const size_t lm_bytes = sizeof(double) * static_cast<size_t>(B * std::max<int64_t>(d, 1));
     const size_t L_bytes = sizeof(double) * static_cast<size_t>(B * b_eff);
     PhaseTrace tr{"set_basis"};
-    DevBuf lm0, L0;
-    lm0.alloc(d0.device, lm_bytes);
-    L0.alloc(d0.device, L_bytes);
+    CUDA_TRY(cudaSetDevice(d0.device));
+    double* lm0 = d0.stage_lm.d(lm_bytes);
+    double* L0 = d0.stage_L.d(L_bytes);
     tr.lap("alloc");
     cudaStream_t st0 = d0.slot[0].stream;
-    fill_lm0(d0, lm0.d());
+    fill_lm0(d0, lm0);
     tr.lap("landmarks to device 0");
-    h2d_staged(d0, L0.d(), L_host, L_bytes, st0);
+    h2d_staged(d0, L0, L_host, L_bytes, st0);
     CUDA_TRY(cudaStreamSynchronize(st0));
     tr.lap("L to device 0");
     run_parallel(ctx, [&](DeviceState& ds, int di) {
         CUDA_TRY(cudaSetDevice(ds.device));
         cudaStream_t st = ds.slot[0].stream;
         if (di == 0) {
-            build_basis(ds, lm0.d(), B, d, std::max<int64_t>(d, 1), L0.d(), b_eff, gamma, st, true);
+            build_basis(ds, lm0, B, d, std::max<int64_t>(d, 1), L0, b_eff, gamma, st, true);
             return;
         }
-        DevBuf lm, L;
-        lm.alloc(ds.device, lm_bytes);
-        L.alloc(ds.device, L_bytes);
-        CUDA_TRY(cudaMemcpyPeerAsync(lm.p, ds.device, lm0.p, d0.device, lm_bytes, st));
-        CUDA_TRY(cudaMemcpyPeerAsync(L.p, ds.device, L0.p, d0.device, L_bytes, st));
-        build_basis(ds, lm.d(), B, d, std::max<int64_t>(d, 1), L.d(), b_eff, gamma, st, true);
+        double* lm = ds.stage_lm.d(lm_bytes);
+        double* L = ds.stage_L.d(L_bytes);
+        CUDA_TRY(cudaMemcpyPeerAsync(lm, ds.device, lm0, d0.device, lm_bytes, st));
+        CUDA_TRY(cudaMemcpyPeerAsync(L, ds.device, L0, d0.device, L_bytes, st));
+        build_basis(ds, lm, B, d, std::max<int64_t>(d, 1), L, b_eff, gamma, st, true);
     });
     tr.lap("peer copies + K2");
 }
@@ -2057,6 +2062,7 @@ int lpd_context_destroy(lpd_context* ctx) {
         ds.model.free_all();
         ds.free_hp();
         dev_free(ds.hp_norms);
+        for (GrowBuf* g : {&ds.stage_lm, &ds.stage_L, &ds.stage_ip, &ds.stage_idx, &ds.stage_val}) g->release();
         if (ds.scratch) cudaFree(ds.scratch);
         if (ds.gtmp) cudaFree(ds.gtmp);
         for (auto& s : ds.slot) {
@@ -2115,18 +2121,17 @@ int lpd_set_basis_csr(lpd_context* ctx, int64_t B, int64_t d, const int64_t* ind
         set_basis_all(ctx, B, d, L, b_eff, gamma, [&](DeviceState& ds, double* lm) {
             std::vector<int64_t> ip(static_cast<size_t>(B + 1));
             for (int64_t i = 0; i <= B; ++i) ip[i] = indptr[i] - indptr[0];
-            DevBuf dip, didx, dval;
-            dip.alloc(ds.device, sizeof(int64_t) * static_cast<size_t>(B + 1));
-            didx.alloc(ds.device, sizeof(int32_t) * static_cast<size_t>(nnz));
-            dval.alloc(ds.device, sizeof(double) * static_cast<size_t>(nnz));
-            CUDA_TRY(cudaMemcpy(dip.p, ip.data(), sizeof(int64_t) * (B + 1), cudaMemcpyHostToDevice));
+            void* dip = ds.stage_ip.get(sizeof(int64_t) * static_cast<size_t>(B + 1));
+            void* didx = ds.stage_idx.get(sizeof(int32_t) * static_cast<size_t>(nnz));
+            double* dval = ds.stage_val.d(sizeof(double) * static_cast<size_t>(nnz));
+            CUDA_TRY(cudaMemcpy(dip, ip.data(), sizeof(int64_t) * (B + 1), cudaMemcpyHostToDevice));
             if (nnz > 0) {
-                CUDA_TRY(cudaMemcpy(didx.p, indices + indptr[0], sizeof(int32_t) * nnz, cudaMemcpyHostToDevice));
-                CUDA_TRY(cudaMemcpy(dval.p, values + indptr[0], sizeof(double) * nnz, cudaMemcpyHostToDevice));
+                CUDA_TRY(cudaMemcpy(didx, indices + indptr[0], sizeof(int32_t) * nnz, cudaMemcpyHostToDevice));
+                CUDA_TRY(cudaMemcpy(dval, values + indptr[0], sizeof(double) * nnz, cudaMemcpyHostToDevice));
             }
             if (d > 0)
                 lpd::csr_to_dense_kernel<<<static_cast<int>((B + 7) / 8), 256, 0, ds.slot[0].stream>>>(
-                    static_cast<const int64_t*>(dip.p), static_cast<const int32_t*>(didx.p), dval.d(),
+                    static_cast<const int64_t*>(dip), static_cast<const int32_t*>(didx), dval,
                     static_cast<int>(B), static_cast<int>(d), lm, ds.err);
             else
                 CUDA_TRY(cudaMemsetAsync(lm, 0, sizeof(double) * static_cast<size_t>(B), ds.slot[0].stream));

@@ -34,14 +34,19 @@ def main():
         for classes in (2, 10):
             Pp = classes * (classes - 1) // 2
             betas = rng.standard_normal((Pp, cfg.budget)) * 1e-2
-            ts = []
+            ts, tb = [], []
+            bt = np.ascontiguousarray(betas.T)
             for _ in range(args.reps + 1):
                 t0 = time.perf_counter()
-                ctx.set_basis_dense(Y, np.ascontiguousarray(betas.T), cfg.gamma)
+                ctx.set_basis_dense(Y, bt, cfg.gamma)
+                t1 = time.perf_counter()
                 cls = ctx.predict_ovo_dense(Xt, classes)
                 ts.append(time.perf_counter() - t0)
+                tb.append(t1 - t0)
             t = float(np.median(ts[1:]))
             out[f"classes_{classes}"] = {"P": Pp, "seconds": t, "rows_per_s": Xt.shape[0] / t,
+                                         "set_basis_seconds": float(np.median(tb[1:])),
+                                         "high_precision_basis": bool(ctx.basis_precision()[0]),
                                          "class_histogram": np.bincount(cls, minlength=classes).tolist()}
     print(json.dumps(out))
 
