@@ -49,6 +49,12 @@ extern "C" {
 #define LPD_ERR_OUT_OF_MEMORY 4
 #define LPD_ERR_NO_DEVICE 5
 
+/* Fault-injection sites (lpd_inject_fault; tests) */
+#define LPD_FAULT_NONE 0
+#define LPD_FAULT_ALLOC 1  /* a device allocation fails: LPD_ERR_OUT_OF_MEMORY */
+#define LPD_FAULT_LAUNCH 2 /* a factor-kernel launch fails: LPD_ERR_CUDA */
+#define LPD_FAULT_D2H 3    /* a device-to-host transfer of G fails: LPD_ERR_CUDA */
+
 #define LPD_OUT_F64 0
 #define LPD_OUT_F32 1
 
@@ -80,6 +86,12 @@ typedef struct lpd_timings {
 } lpd_timings;
 
 const char* lpd_last_error(void);
+/* Test hook (the reference has no fault injection): the `after`-th next pass
+ * through `site` (process-wide, once) fails the way the real CUDA failure would; the call
+ * returns the error, in-flight work of the call is drained, and the context stays usable.
+ * site = LPD_FAULT_NONE disarms. Also armed by LPD_FAULT_INJECT=<alloc|launch|d2h>:<after>
+ * at context creation. */
+int lpd_inject_fault(int site, int after);
 int lpd_version(void);
 /* Number of visible CUDA devices (0 on a machine without a GPU; never fails). */
 int lpd_device_count(void);

@@ -45,6 +45,10 @@ LPD_ERR_CUDA = 2
 LPD_ERR_UNSUPPORTED = 3
 LPD_ERR_OUT_OF_MEMORY = 4
 LPD_ERR_NO_DEVICE = 5
+LPD_FAULT_NONE = 0
+LPD_FAULT_ALLOC = 1
+LPD_FAULT_LAUNCH = 2
+LPD_FAULT_D2H = 3
 LPD_OUT_F64 = 0
 LPD_OUT_F32 = 1
 LPD_PRECISION_AUTO = 0
@@ -56,6 +60,7 @@ EXPORTED_SYMBOLS = (
     "lpd_last_error",
     "lpd_version",
     "lpd_device_count",
+    "lpd_inject_fault",
     "lpd_context_create",
     "lpd_context_create_devices",
     "lpd_context_destroy",
@@ -201,6 +206,14 @@ def _check(status: int) -> None:
 
 def device_count() -> int:
     return int(load_library().lpd_device_count())
+
+
+def inject_fault(site: int, after: int = 0) -> None:
+    """Test hook: the after-th next pass through `site` (LPD_FAULT_ALLOC / _LAUNCH / _D2H)
+    fails like the real CUDA failure would; LPD_FAULT_NONE disarms."""
+    lib = load_library()
+    lib.lpd_inject_fault.argtypes = [ctypes.c_int, ctypes.c_int]
+    _check(lib.lpd_inject_fault(int(site), int(after)))
 
 
 def _f64(a) -> np.ndarray:

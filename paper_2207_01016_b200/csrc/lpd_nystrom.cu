@@ -60,6 +60,21 @@ struct LpdError : std::runtime_error {
 
 [[noreturn]] void fail(int code, const std::string& msg) { throw LpdError(code, msg); }
 
+// Fault injection (tests): lpd_inject_fault(site, after) or
+// LPD_FAULT_INJECT=<alloc|launch|d2h>:<after> makes the after-th next pass through `site`
+// fail the way the real CUDA failure would (device allocation -> LPD_ERR_OUT_OF_MEMORY,
+// kernel launch / transfer -> LPD_ERR_CUDA), once.
+std::atomic<int> g_fault_site{0};
+std::atomic<int> g_fault_after{0};
+void fault_point(int site) {
+    if (g_fault_site.load(std::memory_order_relaxed) != site) return;
+    if (g_fault_after.fetch_sub(1) != 0) return;
+    g_fault_site.store(0);
+    static const char* names[] = {"", "device allocation", "kernel launch", "device-to-host transfer"};
+    fail(site == LPD_FAULT_ALLOC ? LPD_ERR_OUT_OF_MEMORY : LPD_ERR_CUDA,
+         std::string("injected fault: ") + names[site < 4 ? site : 0]);
+}
+
 #define CUDA_TRY(expr)                                                                   \
     do {                                                                                 \
         cudaError_t _e = (expr);                                                         \
@@ -87,6 +102,23 @@ int guarded(F&& f) {
 }
 
 int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+// LPD_FAULT_INJECT=<alloc|launch|d2h>:<after>, read once at the first context creation
+void arm_fault_from_env() {
+    static std::once_flag once;
+    std::call_once(once, [] {
+        const char* e = std::getenv("LPD_FAULT_INJECT");
+        if (!e) return;
+        const std::string v(e);
+        const size_t c = v.find(':');
+        const std::string site = v.substr(0, c);
+        const int after = c == std::string::npos ? 0 : std::atoi(v.c_str() + c + 1);
+        const int code = site == "alloc" ? LPD_FAULT_ALLOC : site == "launch" ? LPD_FAULT_LAUNCH
+                       : site == "d2h" ? LPD_FAULT_D2H : LPD_FAULT_NONE;
+        g_fault_after.store(std::max(0, after));
+        g_fault_site.store(code);
+    });
+}
 
 // ------------------------------------------------------------------ TMA descriptors
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -149,6 +181,7 @@ template <typename T>
 void dev_alloc(T** p, size_t count) {
     *p = nullptr;
     if (count == 0) count = 1;
+    fault_point(LPD_FAULT_ALLOC);
     CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T)));
 }
 template <typename T>
@@ -192,6 +225,7 @@ struct GrowBuf {
             if (p) cudaFree(p);
             p = nullptr;
             cap = 0;
+            fault_point(LPD_FAULT_ALLOC);
             CUDA_TRY(cudaMalloc(&p, bytes));
             cap = bytes;
         }
@@ -348,6 +382,8 @@ void ensure_slot(DeviceState& ds, Slot& s, int64_t rows, bool need_g, int64_t nn
         s.kd != ds.kd || s.d_cap < ds.d) {
         dev_free(s.x); dev_free(s.xhi); dev_free(s.xlo); dev_free(s.raux); dev_free(s.g);
         const int64_t cap = std::max(rows_pad, s.rows_cap);
+        // a failed allocation below must leave an empty slot, not stale capacities
+        s.rows_cap = 0; s.g_elems = 0; s.kd = 0; s.d_cap = 0;
         dev_alloc(&s.x, static_cast<size_t>(cap * std::max<int64_t>(ds.d, 1)));
         dev_alloc(&s.xhi, static_cast<size_t>(cap * ds.kd));
         dev_alloc(&s.xlo, static_cast<size_t>(cap * ds.kd));
@@ -370,6 +406,7 @@ void ensure_slot(DeviceState& ds, Slot& s, int64_t rows, bool need_g, int64_t nn
     s.g_cols = ds.b_eff;
     if (nnz > s.nnz_cap) {
         dev_free(s.indptr); dev_free(s.indices); dev_free(s.values);
+        s.nnz_cap = 0;
         dev_alloc(&s.indptr, static_cast<size_t>(s.rows_cap + 1));
         dev_alloc(&s.indices, static_cast<size_t>(nnz));
         dev_alloc(&s.values, static_cast<size_t>(nnz));
@@ -606,12 +643,14 @@ void choose_precision(DeviceState& ds, const double* lm_dev, int64_t B, int64_t 
     if (ds.hp_lm_cap < static_cast<size_t>(B * dp)) {
         CUDA_TRY(cudaStreamSynchronize(st));
         dev_free(ds.hp_lm);
+        ds.hp_lm_cap = 0;
         dev_alloc(&ds.hp_lm, static_cast<size_t>(B * dp));
         ds.hp_lm_cap = static_cast<size_t>(B * dp);
     }
     if (ds.hp_lt_cap < static_cast<size_t>(npad * kpad)) {
         CUDA_TRY(cudaStreamSynchronize(st));
         dev_free(ds.hp_lt);
+        ds.hp_lt_cap = 0;
         dev_alloc(&ds.hp_lt, static_cast<size_t>(npad * kpad));
         ds.hp_lt_cap = static_cast<size_t>(npad * kpad);
     }
@@ -643,6 +682,7 @@ void launch_factor_hp(DeviceState& ds, const double* x_dev, int64_t m, int64_t l
     if (ds.hp_z_rows < panel) {
         CUDA_TRY(cudaStreamSynchronize(st));
         dev_free(ds.hp_z);
+        ds.hp_z_rows = 0;
         dev_alloc(&ds.hp_z, static_cast<size_t>(panel * kpad));
         CUDA_TRY(cudaMemsetAsync(ds.hp_z, 0, sizeof(double) * static_cast<size_t>(panel * kpad), st));
         ds.hp_z_rows = panel;
@@ -673,6 +713,7 @@ void launch_factor_hp(DeviceState& ds, const double* x_dev, int64_t m, int64_t l
             lpd::hp_dgemm_nt_kernel<float><<<gg, lpd::hp::THREADS, lpd::hp::SMEM_BYTES, st>>>(
                 ds.hp_z, kpad, ds.hp_lt, kpad, static_cast<int>(rows), static_cast<int>(ds.b_eff),
                 static_cast<int>(kpad), static_cast<float*>(gout), ldg);
+        fault_point(LPD_FAULT_LAUNCH);
         CUDA_TRY(cudaGetLastError());
     }
     if (time_it) {
@@ -702,6 +743,7 @@ void build_basis(DeviceState& ds, const double* lm_dev, int64_t B, int64_t d, in
             if (need > cap) {
                 CUDA_TRY(cudaDeviceSynchronize());
                 dev_free(ptr);
+                cap = 0;
                 dev_alloc(&ptr, need);
                 cap = need;
             }
@@ -891,6 +933,7 @@ void launch_factor_panels(DeviceState& ds, Slot& s, int64_t m, void* g_dev, int6
         CUDA_TRY(cudaStreamSynchronize(st));
         dev_free(ds.z_hi);
         dev_free(ds.z_lo);
+        ds.z_rows = 0;
         dev_alloc(&ds.z_hi, static_cast<size_t>(panel * ds.B_pad));
         dev_alloc(&ds.z_lo, static_cast<size_t>(panel * ds.B_pad));
         ds.z_rows = panel;
@@ -980,6 +1023,7 @@ void launch_factor_panels(DeviceState& ds, Slot& s, int64_t m, void* g_dev, int6
         else
             launch_panel(lpd::panel_gemm_kernel<lpd::PANEL_G, float>, gg, st, tm_zhi, tm_zlo, ds.tm_lthi,
                          ds.tm_ltlo, pg);
+        fault_point(LPD_FAULT_LAUNCH);
         CUDA_TRY(cudaGetLastError());
     }
     if (time_it) {
@@ -1091,6 +1135,7 @@ void launch_factor(DeviceState& ds, Slot& s, const double* x_dev, int64_t m, int
         if (ds.ring_count < DeviceState::kRing) CUDA_TRY(cudaEventRecord(pr[1], st));
         ++ds.ring_count;
     }
+    fault_point(LPD_FAULT_LAUNCH);
     CUDA_TRY(cudaGetLastError());
     if (g_out != g_dev)
         CUDA_TRY(cudaMemcpy2DAsync(g_dev, es * ldg, g_out, es * ld_out, es * ds.b_eff,
@@ -1400,6 +1445,23 @@ void compute_rows_host(lpd_context* ctx, int64_t n, double* G, int64_t ldg, lpd_
     }();
     ctx->res_n = 0;
     std::vector<int> resident_ok(nd, 0);
+    // a failure mid-pipeline (real or injected) leaves copies and kernels in flight on this
+    // call's streams: drain them before reporting, so the next call starts clean
+    struct Drain {
+        lpd_context* ctx;
+        bool armed = true;
+        ~Drain() {
+            if (!armed) return;
+            for (auto& ds : ctx->dev) {
+                cudaSetDevice(ds.device);
+                for (auto& sl : ds.slot) cudaStreamSynchronize(sl.stream);
+                if (ds.dstream) cudaStreamSynchronize(ds.dstream);
+                if (ds.dstream2) cudaStreamSynchronize(ds.dstream2);
+                ds.res_rows = 0;
+            }
+            cudaGetLastError();
+        }
+    } drain{ctx};
     run_parallel(ctx, [&](DeviceState& ds, int di) {
         CUDA_TRY(cudaSetDevice(ds.device));
         const int64_t per = round_up((n + nd - 1) / nd, 256);
@@ -1492,6 +1554,7 @@ void compute_rows_host(lpd_context* ctx, int64_t n, double* G, int64_t ldg, lpd_
                 CUDA_TRY(cudaEventRecord(s.ev[3], ds.dstream));
             }
             const float* src = gdst(u.k) + (u.r0 - (r_begin + u.k * chunk)) * g_ld;
+            fault_point(LPD_FAULT_D2H);
             CUDA_TRY(cudaMemcpyAsync(ds.dring[g % R], src, sizeof(float) * static_cast<size_t>(u.rows * g_ld),
                                      cudaMemcpyDeviceToHost, ds_g));
             CUDA_TRY(cudaEventRecord(ds.dring_ev[g % R], ds_g));
@@ -1551,6 +1614,7 @@ void compute_rows_host(lpd_context* ctx, int64_t n, double* G, int64_t ldg, lpd_
         host[di] += widen_s;
         check_range_flag(ds);
     });
+    drain.armed = false;
     if (ctx->keep_resident && std::all_of(resident_ok.begin(), resident_ok.end(), [](int v) { return v; })) {
         ctx->res_n = n;
         ctx->res_b_eff = b_eff;
@@ -1617,6 +1681,7 @@ void predict_rows_host(lpd_context* ctx, int64_t n, int64_t num_classes, int32_t
         Slot& s = ds.slot[0];
         if (ds.pairs_classes != num_classes) {
             dev_free(ds.pairs);
+            ds.pairs_classes = 0;
             dev_alloc(&ds.pairs, static_cast<size_t>(P));
             lpd::ovo_pair_table_kernel<<<static_cast<int>(num_classes), 128, 0, s.stream>>>(
                 static_cast<int>(num_classes), ds.pairs);
@@ -1625,6 +1690,7 @@ void predict_rows_host(lpd_context* ctx, int64_t n, int64_t num_classes, int32_t
         }
         if (ds.votes_cap < chunk) {
             dev_free(ds.votes);
+            ds.votes_cap = 0;
             dev_alloc(&ds.votes, static_cast<size_t>(chunk));
             ds.votes_cap = chunk;
         }
@@ -1856,13 +1922,16 @@ void model_decision_values(lpd_context* ctx, int64_t n, const HostRows& xs, doub
     if (m.rows_cap < chunk || m.x_cols < xc) {
         dev_free(m.x); dev_free(m.zt); dev_free(m.dv);
         m.rows_cap = m.x_cols = 0;
+        m.set = false;
         dev_alloc(&m.x, static_cast<size_t>(chunk * xc));
         dev_alloc(&m.zt, static_cast<size_t>(chunk * m.B));
         m.rows_cap = chunk;
         m.x_cols = xc;
     }
     dev_free(m.dv);
+    m.set = false;  // until the buffers are whole again
     dev_alloc(&m.dv, static_cast<size_t>(m.rows_cap * m.P));
+    m.set = true;
     const size_t hx_need = sizeof(double) * static_cast<size_t>(chunk * xc);
     const size_t hd_need = sizeof(double) * static_cast<size_t>(chunk * m.P);
     if (m.hx_cap < hx_need) {
@@ -2005,6 +2074,7 @@ int lpd_context_create(lpd_context** out, int num_devices) {
             fail(LPD_ERR_INVALID_ARGUMENT, "requested " + std::to_string(want) +
                                                " devices, only " + std::to_string(avail) +
                                                " visible");
+        arm_fault_from_env();
         auto* ctx = new lpd_context();
         try {
             ctx->dev.resize(want);
@@ -2031,6 +2101,7 @@ int lpd_context_create_devices(lpd_context** out, const int* device_ids, int cou
         for (int i = 0; i < count; ++i)
             if (device_ids[i] < 0 || device_ids[i] >= avail)
                 fail(LPD_ERR_INVALID_ARGUMENT, "device id " + std::to_string(device_ids[i]) + " not visible");
+        arm_fault_from_env();
         auto* ctx = new lpd_context();
         try {
             ctx->dev.resize(count);
@@ -2045,6 +2116,16 @@ int lpd_context_create_devices(lpd_context** out, const int* device_ids, int cou
         }
         *out = ctx;
     });
+}
+
+int lpd_inject_fault(int site, int after) {
+    if (site < 0 || site > LPD_FAULT_D2H || after < 0) {
+        g_last_error = "fault site must be LPD_FAULT_NONE..LPD_FAULT_D2H and after >= 0";
+        return LPD_ERR_INVALID_ARGUMENT;
+    }
+    g_fault_after.store(after);
+    g_fault_site.store(site);
+    return LPD_OK;
 }
 
 int lpd_context_destroy(lpd_context* ctx) {

@@ -625,3 +625,32 @@ def test_far_rows_host_path_fp32_range(gpu_ctx):
     err = np.linalg.norm(G - R, axis=1)[normal] / nr[normal]
     assert float(err.max()) <= TOL_G, float(err.max())
     assert np.all(np.abs(G[below]) < tiny)
+
+
+@pytest.mark.parametrize("site,code", [(P.LPD_FAULT_ALLOC, P.LPD_ERR_OUT_OF_MEMORY),
+                                       (P.LPD_FAULT_LAUNCH, P.LPD_ERR_CUDA),
+                                       (P.LPD_FAULT_D2H, P.LPD_ERR_CUDA)])
+def test_injected_fault_fails_loudly_and_context_recovers(site, code):
+    """Failure detection (the reference has exceptions only, no fault
+    injection): a device allocation, a factor-kernel launch or a G transfer that fails
+    mid-call returns the matching status with a message, never a silently wrong G; the
+    call's in-flight work is drained, and the same context then computes G bitwise equal
+    to a clean context's. A host-row call with 17 delivery sub-chunks of 8 MB, so the
+    D2H fault lands mid-pipeline."""
+    rng = np.random.default_rng(21)
+    X = rng.standard_normal((70000, 20)).astype(np.float32).astype(np.float64)
+    Y = X[:512]
+    L = np_gaussian_L(Y, 0.05, 1e-8)
+    with P.Context(1) as clean:
+        clean.set_basis_dense(Y, L, 0.05)
+        ref = clean.compute_g_dense(X)
+    with P.Context(1) as ctx:
+        ctx.set_basis_dense(Y, L, 0.05)
+        P.inject_fault(site, 2 if site == P.LPD_FAULT_D2H else 0)
+        try:
+            with pytest.raises(P.LpdError) as ei:
+                ctx.compute_g_dense(X)
+        finally:
+            P.inject_fault(P.LPD_FAULT_NONE)
+        assert ei.value.code == code and "injected fault" in str(ei.value)
+        assert np.array_equal(ctx.compute_g_dense(X), ref)

@@ -203,3 +203,15 @@ def test_output_matrix_fast_path_matches_reference_constructor(tmp_path):
         assert f[k] == p[k], k
     assert np.array_equal(np.load(str(tmp_path / "fast.json") + ".pred.npy"),
                           np.load(str(tmp_path / "plain.json") + ".pred.npy"))
+
+
+@pytest.mark.gpu
+def test_injected_device_fault_reaches_the_reference_api_as_runtime_error(tmp_path):
+    """A device failure inside the drop-in compute_G (injected: LPD_FAULT_INJECT) surfaces
+    through the reference's Python API as RuntimeError — the reference's own contract for
+    device/driver failures (std::runtime_error, SURVEY.md §5) — not as a wrong model."""
+    r = _run(INTEG, str(tmp_path / "x.npz"), "--n", "2000", "--n-test", "200", "--budget", "200",
+             check=False, env={"LPD_FAULT_INJECT": "launch:0"})
+    assert r.returncode != 0
+    out = r.stderr + r.stdout
+    assert "RuntimeError" in out and "injected fault: kernel launch" in out, out[-2000:]
