@@ -243,19 +243,24 @@ __global__ void __launch_bounds__(GWS_THREADS) gather_gw_seq_kernel(const float*
     constexpr int PTILE = PT * TX, TY = GWS_THREADS / TX, ROWS = TY * RT;
     constexpr int GQ = ROWS * GWS_KC / 4 / GWS_THREADS;        // float4 pieces of G per thread per chunk
     constexpr int WQ = (PTILE * GWS_KC / 2 + GWS_THREADS - 1) / GWS_THREADS;  // double2 pieces of W
+    // the row-per-thread shape runs with any multiple of 32 threads up to 256 (one row each:
+    // the host sizes blocks so the grid fills the GPU in one wave); the tile shape with 256
+    constexpr bool ROW_SHAPE = RT == 1 && TX == 1;
+    const int nth = ROW_SHAPE ? static_cast<int>(blockDim.x) : GWS_THREADS;
+    const int rows_blk = ROW_SHAPE ? nth : ROWS;
     // the 256-row shape keeps G as fp32 in shared memory (widened per use): static shared
     // memory ends at 48 KB
     using GsT = typename std::conditional<RT == 1, float, double>::type;
     __shared__ __align__(16) GsT Gs[GWS_KC][ROWS + 2];
     __shared__ __align__(16) double Ws[GWS_KC][PTILE + 2];
     const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
-    const int r0 = blockIdx.x * ROWS, p0 = blockIdx.y * PTILE;
+    const int r0 = blockIdx.x * rows_blk, p0 = blockIdx.y * PTILE;
     float4 gq[GQ];
     double2 wq[WQ];
     auto load = [&](int k0) {
 #pragma unroll
         for (int u = 0; u < GQ; ++u) {
-            const int c = tid + u * GWS_THREADS, r = c >> 3, q = c & 7;  // 8 pieces per row
+            const int c = tid + u * nth, r = c >> 3, q = c & 7;  // 8 pieces per row
             const int row = rows[min(r0 + r, count - 1)];
             const float* src = G + static_cast<long long>(row) * ldg + k0 + 4 * q;
             if (k0 + 4 * q + 3 < b_eff) {
@@ -269,7 +274,7 @@ __global__ void __launch_bounds__(GWS_THREADS) gather_gw_seq_kernel(const float*
         }
 #pragma unroll
         for (int u = 0; u < WQ; ++u) {
-            const int c = tid + u * GWS_THREADS, p = c / (GWS_KC / 2), q = c % (GWS_KC / 2);
+            const int c = tid + u * nth, p = c / (GWS_KC / 2), q = c % (GWS_KC / 2);
             double2 v = make_double2(0.0, 0.0);
             if (p < PTILE && p0 + p < P) {
                 const double* src = W + static_cast<long long>(p0 + p) * b_eff + k0 + 2 * q;
@@ -282,7 +287,7 @@ __global__ void __launch_bounds__(GWS_THREADS) gather_gw_seq_kernel(const float*
     auto stash = [&]() {
 #pragma unroll
         for (int u = 0; u < GQ; ++u) {
-            const int c = tid + u * GWS_THREADS, r = c >> 3, q = c & 7;
+            const int c = tid + u * nth, r = c >> 3, q = c & 7;
             Gs[4 * q + 0][r] = static_cast<GsT>(gq[u].x);
             Gs[4 * q + 1][r] = static_cast<GsT>(gq[u].y);
             Gs[4 * q + 2][r] = static_cast<GsT>(gq[u].z);
@@ -290,7 +295,7 @@ __global__ void __launch_bounds__(GWS_THREADS) gather_gw_seq_kernel(const float*
         }
 #pragma unroll
         for (int u = 0; u < WQ; ++u) {
-            const int c = tid + u * GWS_THREADS, p = c / (GWS_KC / 2), q = c % (GWS_KC / 2);
+            const int c = tid + u * nth, p = c / (GWS_KC / 2), q = c % (GWS_KC / 2);
             if (p < PTILE) {
                 Ws[2 * q][p] = wq[u].x;
                 Ws[2 * q + 1][p] = wq[u].y;

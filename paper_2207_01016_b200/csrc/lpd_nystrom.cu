@@ -1760,6 +1760,30 @@ std::vector<std::vector<std::pair<int32_t, int64_t>>> split_rows(lpd_context* ct
     return parts;
 }
 
+// Threads (= listed rows) per block of the row-per-thread scoring kernel: a row's sum is
+// sequential, so a grid whose last wave is nearly empty costs a whole extra wave (116,203
+// rows in 256-row blocks: 454 blocks on 444 slots, two wave-times). Picks the multiple of
+// 32 in [64, 256] whose blocks fill the slots best, larger blocks on ties.
+int row_block_threads(const DeviceState& ds, const void* kfn, int64_t m) {
+    int best_t = 256;
+    double best_eff = -1.0;
+    for (int t = 256; t >= 64; t -= 32) {
+        int nb = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kfn, t, 0) != cudaSuccess || nb <= 0) {
+            cudaGetLastError();
+            continue;
+        }
+        const int64_t blocks = (m + t - 1) / t, slots = static_cast<int64_t>(nb) * ds.num_sms;
+        const int64_t waves = (blocks + slots - 1) / slots;
+        const double eff = static_cast<double>(m) / static_cast<double>(waves * slots * t);
+        if (eff > best_eff + 1e-9) {
+            best_eff = eff;
+            best_t = t;
+        }
+    }
+    return best_t;
+}
+
 // D = G[rows]·Wᵀ on the resident G (K6 gather_gw_row / gather_gw_seq: the reference's
 // summation order, bitwise), then either D to the host or — with num_classes — the
 // reference's one-vs-one vote on the device (ovo_vote_kernel) and only the class indices
@@ -1793,12 +1817,15 @@ void resident_gw(lpd_context* ctx, const int32_t* rows, int64_t count, const dou
         CUDA_TRY(cudaMemcpyAsync(drows, single ? rows : local.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, st));
         CUDA_TRY(cudaMemcpyAsync(dw, W, sizeof(double) * P * b_eff, cudaMemcpyHostToDevice, st));
         const int bi = static_cast<int>(b_eff), mi = static_cast<int>(m), pi = static_cast<int>(P);
-        if (P <= 4) {  // one listed row per thread, 256 per block
-            const dim3 grid(static_cast<unsigned>((m + 255) / 256), 1);
+        if (P <= 4) {  // one listed row per thread, blocks sized so the grid is one full wave
+            const void* kfn = P == 1 ? reinterpret_cast<const void*>(lpd::gather_gw_seq_kernel<1, 1, 1>)
+                                     : reinterpret_cast<const void*>(lpd::gather_gw_seq_kernel<1, 4, 1>);
+            const int t = row_block_threads(ds, kfn, m);
+            const dim3 grid(static_cast<unsigned>((m + t - 1) / t), 1);
             if (P == 1)
-                lpd::gather_gw_seq_kernel<1, 1, 1><<<grid, lpd::GWS_THREADS, 0, st>>>(ds.res_g, ds.res_ld, bi, drows, mi, dw, pi, dd);
+                lpd::gather_gw_seq_kernel<1, 1, 1><<<grid, t, 0, st>>>(ds.res_g, ds.res_ld, bi, drows, mi, dw, pi, dd);
             else
-                lpd::gather_gw_seq_kernel<1, 4, 1><<<grid, lpd::GWS_THREADS, 0, st>>>(ds.res_g, ds.res_ld, bi, drows, mi, dw, pi, dd);
+                lpd::gather_gw_seq_kernel<1, 4, 1><<<grid, t, 0, st>>>(ds.res_g, ds.res_ld, bi, drows, mi, dw, pi, dd);
         } else {
             // 16 threads across P, each PT = ceil(P / 16) <= 4 vectors: a P-tile of 16·PT
             const int pt = static_cast<int>(std::min<int64_t>(4, (P + 15) / 16));
