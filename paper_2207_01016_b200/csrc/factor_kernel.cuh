@@ -57,7 +57,8 @@ struct FactorParams {
     int n_col_blocks;       // Beff_pad / 256
     int b_eff;              // valid G columns
     int ksteps1;            // ceil((d + 1) / 16): K-steps of GEMM1 (d features + norm column)
-    const RowAux* row_aux;  // [n_pad] t = R_i + acc*sx_i, clamp, rscale (prep_kernels.cuh)
+    const RowAux* row_aux;  // [n_pad] t = R_i + acc*sx_i and the exponent clamp (prep_kernels.cuh);
+                            // a probed row's 2^shift is applied after the kernel (row_rescale)
     const float* col_scale; // [Beff_pad] 2^-13 / u_k (undoes Z and Lᵀ-row scaling)
     // output G: the tm_g tensor map (TMA store, 16-byte aligned rows; the host stages
     // through an aligned buffer otherwise)
@@ -542,19 +543,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
             const int gc0 = cb * N2 + c0;
             if (gc0 >= p.b_eff || K1_ABL(2)) return;
             const float4* cs4 = reinterpret_cast<const float4*>(p.col_scale + gc0);
-            // the row's exponent normalisation 2^shift (shift 0 unless the probe moved the
-            // row, probe_kernels.cuh): in fp64 for fp64 G, in fp32 (range to 2^-149) otherwise
-            const int sh = static_cast<int>(p.row_aux[rt * PM + r_pair].shift);
-            const float rsc = sizeof(OutT) == 8 ? 1.0f : ldexpf(1.0f, sh);
-            const double rsd = ldexp(1.0, sh);
             float v[32];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 const float4 sc = ldg_f4_inorder(cs4 + i);
-                v[4 * i + 0] = (rs[m * 32 + 4 * i + 0] * sc.x) * rsc;
-                v[4 * i + 1] = (rs[m * 32 + 4 * i + 1] * sc.y) * rsc;
-                v[4 * i + 2] = (rs[m * 32 + 4 * i + 2] * sc.z) * rsc;
-                v[4 * i + 3] = (rs[m * 32 + 4 * i + 3] * sc.w) * rsc;
+                v[4 * i + 0] = rs[m * 32 + 4 * i + 0] * sc.x;
+                v[4 * i + 1] = rs[m * 32 + 4 * i + 1] * sc.y;
+                v[4 * i + 2] = rs[m * 32 + 4 * i + 2] * sc.z;
+                v[4 * i + 3] = rs[m * 32 + 4 * i + 3] * sc.w;
             }
             // 32 rows x SLAB columns per store; 128-byte swizzled staging rows
             // (16-byte chunk c of row r at chunk c ^ (r & 7)): conflict-free STS.
@@ -570,7 +566,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
                 for (int c = 0; c < 8; ++c) {
                     uint32_t w[4];
                     if constexpr (sizeof(OutT) == 8) {
-                        const double d0 = v[sl * SLAB + 2 * c] * rsd, d1 = v[sl * SLAB + 2 * c + 1] * rsd;
+                        const double d0 = v[sl * SLAB + 2 * c], d1 = v[sl * SLAB + 2 * c + 1];
                         w[0] = __double2loint(d0); w[1] = __double2hiint(d0);
                         w[2] = __double2loint(d1); w[3] = __double2hiint(d1);
                     } else {
@@ -618,8 +614,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
         if (pair < num_tiles) write_x(0);
         for (int tile = pair; tile < num_tiles; tile += num_pairs, ++it) {
             const int rt = tile % p.n_row_tiles;
-            const RowAux ra = p.row_aux[rt * PM + r_pair];
-            const uint64_t R2 = f2_pack(ra.R, ra.R), sx2 = f2_pack(ra.sx, ra.sx);
+            const RowAux* rap = p.row_aux + rt * PM + r_pair;
+            const float2 ra = *reinterpret_cast<const float2*>(rap);  // (R, sx)
+            const uint64_t R2 = f2_pack(ra.x, ra.x), sx2 = f2_pack(ra.y, ra.y);
+            const float clampv = rap->clamp;
             const int next = tile + num_pairs;
             bool first = true;  // no segment of this tile read yet
             for (int j = 0; j < n; ++j) {
@@ -637,7 +635,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
                     if (lane == 0) mbar_arrive_cluster(z_full_l + 8 * b);
                     ++cnt;
                 } else {
-                    produce_z(R2, sx2, ra.clamp);
+                    produce_z(R2, sx2, clampv);
                 }
                 store_some();
             }

@@ -577,6 +577,9 @@ void init_device(DeviceState& ds, int device) {
             reinterpret_cast<const void*>(lpd::pointdv_z_kernel<false>),
             reinterpret_cast<const void*>(lpd::pointdv_beta_kernel),
             reinterpret_cast<const void*>(lpd::gather_gtv_sum_kernel),
+            reinterpret_cast<const void*>(lpd::row_shift_kernel),
+            reinterpret_cast<const void*>(lpd::row_rescale_kernel<float>),
+            reinterpret_cast<const void*>(lpd::row_rescale_kernel<double>),
         };
         for (const void* f : fns) CUDA_TRY(cudaFuncGetAttributes(&fa, f));
     }
@@ -924,6 +927,19 @@ void launch_panel(Kernel kernel, int grid, cudaStream_t st, const CUtensorMap& a
 // Large-d factor (d >= 64) for m prepped rows in slot s: per row panel, the Z GEMM
 // (MODE_Z, exp epilogue, fp16 hi/lo planes in a device scratch) and the projection
 // GEMM (MODE_G). The scratch holds at most ~2 GB of Z planes.
+// K9's second half (probe_kernels.cuh): 2^shift on the rows the probe moved; an empty
+// launch unless prep_rows flagged this chunk.
+void launch_row_rescale(DeviceState& ds, Slot& s, int64_t m, void* g, int64_t ldg, int out_dtype, cudaStream_t st) {
+    const int blocks = static_cast<int>(std::min<int64_t>((m + 7) / 8, static_cast<int64_t>(ds.num_sms) * 8));
+    if (out_dtype == LPD_OUT_F64)
+        lpd::row_rescale_kernel<double><<<blocks, 256, 0, st>>>(static_cast<double*>(g), ldg, static_cast<int>(m),
+                                                                static_cast<int>(ds.b_eff), s.raux, s.probe);
+    else
+        lpd::row_rescale_kernel<float><<<blocks, 256, 0, st>>>(static_cast<float*>(g), ldg, static_cast<int>(m),
+                                                               static_cast<int>(ds.b_eff), s.raux, s.probe);
+    CUDA_TRY(cudaGetLastError());
+}
+
 void launch_factor_panels(DeviceState& ds, Slot& s, int64_t m, void* g_dev, int64_t ldg,
                           int out_dtype, cudaStream_t st, bool time_it) {
     const int64_t m_pad = round_up(m, lpd::kp::PM);
@@ -1007,7 +1023,6 @@ void launch_factor_panels(DeviceState& ds, Slot& s, int64_t m, void* g_dev, int6
         pg.n_rows = static_cast<int>(rows);
         pg.n_cols = static_cast<int>(ds.b_eff);
         pg.col_scale = ds.col_scale;
-        pg.row_aux = s.raux + r0;
         const size_t es = out_dtype == LPD_OUT_F64 ? 8 : 4;
         pg.G = static_cast<char*>(g_dev) + static_cast<size_t>(r0) * ldg * es;
         pg.ldg = ldg;
@@ -1031,6 +1046,7 @@ void launch_factor_panels(DeviceState& ds, Slot& s, int64_t m, void* g_dev, int6
         if (ds.ring_count < DeviceState::kRing) CUDA_TRY(cudaEventRecord(pr[1], st));
         ++ds.ring_count;
     }
+    launch_row_rescale(ds, s, m, g_dev, ldg, out_dtype, st);
 }
 
 // prep + fused factor kernel for m rows of dense fp64 X already on the device.
@@ -1137,6 +1153,7 @@ void launch_factor(DeviceState& ds, Slot& s, const double* x_dev, int64_t m, int
     }
     fault_point(LPD_FAULT_LAUNCH);
     CUDA_TRY(cudaGetLastError());
+    launch_row_rescale(ds, s, m, g_out, ld_out, out_dtype, st);
     if (g_out != g_dev)
         CUDA_TRY(cudaMemcpy2DAsync(g_dev, es * ldg, g_out, es * ld_out, es * ds.b_eff,
                                    static_cast<size_t>(m), cudaMemcpyDeviceToDevice, st));

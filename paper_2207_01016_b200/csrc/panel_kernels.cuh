@@ -51,7 +51,7 @@ struct PanelParams {
     int n_kchunks;            // K (padded) / 64
     int n_rows;               // valid rows (MODE_G stores only these)
     int n_cols;               // valid output columns (MODE_G)
-    const RowAux* row_aux;    // per row: MODE_Z t = R_i + acc*sx_i and clamp; MODE_G rscale
+    const RowAux* row_aux;    // MODE_Z, per row: t = R_i + acc*sx_i and the exponent clamp
     __half* z_hi;             // MODE_Z output planes [rows_pad × ldz]
     __half* z_lo;
     long long ldz;
@@ -251,12 +251,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kp::THREADS, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive_cluster(acc_empty_l + 8 * a);
             }
-            const RowAux ra = p.row_aux[row];  // rows < n_row_pairs·256 are all prepared
-            const float R = ra.R, sx = ra.sx, clampv = ra.clamp;
-            // the row's exponent normalisation 2^shift (probe_kernels.cuh): fp64 for fp64 G
-            const int sh = static_cast<int>(ra.shift);
-            const float rsc = sizeof(OutT) == 8 ? 1.0f : ldexpf(1.0f, sh);
-            const double rsd = ldexp(1.0, sh);
+            float R = 0.f, sx = 0.f, clampv = 13.f;
+            if constexpr (MODE == PANEL_Z) {
+                const RowAux ra = p.row_aux[row];  // rows < n_row_pairs·256 are all prepared
+                R = ra.R;
+                sx = ra.sx;
+                clampv = ra.clamp;
+            }
 #pragma unroll
             for (int m = 0; m < 4; ++m) {
                 const int c0 = half * 128 + m * 32;
@@ -291,10 +292,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kp::THREADS, 1)
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
                         const float4 sc4 = __ldg(cs4 + i);
-                        out[4 * i + 0] = (rs[m * 32 + 4 * i + 0] * sc4.x) * rsc;
-                        out[4 * i + 1] = (rs[m * 32 + 4 * i + 1] * sc4.y) * rsc;
-                        out[4 * i + 2] = (rs[m * 32 + 4 * i + 2] * sc4.z) * rsc;
-                        out[4 * i + 3] = (rs[m * 32 + 4 * i + 3] * sc4.w) * rsc;
+                        out[4 * i + 0] = rs[m * 32 + 4 * i + 0] * sc4.x;
+                        out[4 * i + 1] = rs[m * 32 + 4 * i + 1] * sc4.y;
+                        out[4 * i + 2] = rs[m * 32 + 4 * i + 2] * sc4.z;
+                        out[4 * i + 3] = rs[m * 32 + 4 * i + 3] * sc4.w;
                     }
                     OutT* dst = static_cast<OutT*>(p.G) + row * p.ldg + gc0;
                     const int ncols = min(32, p.n_cols - gc0);
@@ -304,12 +305,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kp::THREADS, 1)
 #pragma unroll
                             for (int i = 0; i < 16; ++i)
                                 reinterpret_cast<double2*>(dst)[i] =
-                                    make_double2(static_cast<double>(out[2 * i]) * rsd,
-                                                 static_cast<double>(out[2 * i + 1]) * rsd);
+                                    make_double2(static_cast<double>(out[2 * i]), static_cast<double>(out[2 * i + 1]));
                         } else {
 #pragma unroll
                             for (int i = 0; i < 32; ++i)
-                                if (i < ncols) dst[i] = static_cast<double>(out[i]) * rsd;
+                                if (i < ncols) dst[i] = static_cast<OutT>(out[i]);
                         }
                     } else {
                         if (vec) {

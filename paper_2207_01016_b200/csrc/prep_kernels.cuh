@@ -62,6 +62,20 @@ struct RowAux {
     float R, sx, clamp, shift;
 };
 
+// 2^sh as the product of two normal powers of two (sh >= -252 for fp32 / -2044 for fp64;
+// the products underflow to subnormal or zero below the types' normal range), built from
+// the exponent bits: no libm call on the factor kernels' register-tight drain paths.
+__device__ __forceinline__ void pow2_f(int sh, float& a, float& b) {
+    const int s1 = max(sh, -126), s2 = max(sh - s1, -126);
+    a = __int_as_float((127 + s1) << 23);
+    b = __int_as_float((127 + s2) << 23);
+}
+__device__ __forceinline__ void pow2_d(int sh, double& a, double& b) {
+    const int s1 = max(sh, -1022), s2 = max(sh - s1, -1022);
+    a = __longlong_as_double(static_cast<long long>(1023 + s1) << 52);
+    b = __longlong_as_double(static_cast<long long>(1023 + s2) << 52);
+}
+
 // A row whose nearest landmark may be farther than this (in log2 units of Z) gets its
 // exponent normalised by the probe (probe_kernels.cuh): below 2^-PROBE_LOG2Z the Z values
 // would lose fp16 mantissa bits to subnormals.

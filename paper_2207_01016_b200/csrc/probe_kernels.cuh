@@ -132,4 +132,31 @@ __global__ void __launch_bounds__(pr::THREADS) row_shift_kernel(const __half* __
     shift_row(rb, mx_b, aux_b);
 }
 
+// Second half of K9: the rows the probe moved get their 2^shift after the factor kernels
+// (whose drains store the normalised rows as they are — keeping the shift out of K1's
+// register-tight drain, where even an untaken branch cost 3 %). One warp per row,
+// grid-stride; returns at once when no row was probed. In fp64 for fp64 G; fp32 G keeps
+// fp32's range (subnormal or zero below 2^-126).
+template <typename OutT>
+__global__ void row_rescale_kernel(OutT* __restrict__ G, long long ldg, int m, int b_eff,
+                                   const RowAux* __restrict__ aux, const int* __restrict__ probe) {
+    if (*probe == 0) return;
+    const int lane = threadIdx.x & 31;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < m; row += nwarps) {
+        const int sh = static_cast<int>(aux[row].shift);
+        if (sh == 0) continue;
+        OutT* g = G + static_cast<long long>(row) * ldg;
+        if constexpr (sizeof(OutT) == 8) {
+            double a, b;
+            pow2_d(sh, a, b);
+            for (int c = lane; c < b_eff; c += 32) g[c] = (g[c] * a) * b;
+        } else {
+            float a, b;
+            pow2_f(sh, a, b);
+            for (int c = lane; c < b_eff; c += 32) g[c] = (g[c] * a) * b;
+        }
+    }
+}
+
 }  // namespace lpd
