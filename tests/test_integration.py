@@ -73,8 +73,8 @@ def test_no_cpu_fallback_without_gpu(tmp_path):
 
 @pytest.mark.skipif(_core_so(INTEG) is None or _core_so(REF) is None,
                     reason="integration build / oracle/_ref need /root/reference at build time")
-@pytest.mark.parametrize("classes", [2, 3])
-def test_high_dimensional_sparse_runs_reference_host_code(tmp_path, classes):
+@pytest.mark.parametrize("classes,d,stride", [(2, 20, 4000), (3, 20, 4000), (2, 2, 59000)])
+def test_high_dimensional_sparse_runs_reference_host_code(tmp_path, classes, d, stride):
     """Inputs above the device's 65,536-feature limit (the sparse text sets: news20,
     url, webspam) train through the drop-in exactly as on the reference: the adapter
     hands compute_G, the landmark Gram, ovo_predict and decision_values to the
@@ -82,8 +82,10 @@ def test_high_dimensional_sparse_runs_reference_host_code(tmp_path, classes):
     overrides take their host loops on the host-only G. Every result is bitwise equal
     to the unmodified reference build — this also pins the host branches of the
     rebuild_w / reactivation_pass / make_binary_problem / cross_validate overrides
-    against the reference's own code. No GPU is touched."""
-    args = ["--n", "600", "--n-test", "200", "--budget", "100", "--d", "20", "--index-stride", "4000",
+    against the reference's own code. No GPU is touched. The third case has 59,002
+    features (under the device's 65,536 limit) but at most 2 stored per row, so the cost
+    rule (d > 2.3e4 · nnz per row) sends it to the host as well."""
+    args = ["--n", "600", "--n-test", "200", "--budget", "100", "--d", str(d), "--index-stride", str(stride),
             "--classes", str(classes), "--threads", "4"]
     _run(INTEG, str(tmp_path / "gpu.npz"), *args)
     _run(REF, str(tmp_path / "ref.npz"), *args)
