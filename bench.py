@@ -36,16 +36,17 @@ sys.path.insert(0, ROOT)
 
 METRIC = "Nyström factor rows/s"
 UNIT = "rows/s"
-# per step: K2 (column_mean, landmark_stats, basis_consts, prep_landmarks, col_absmax,
-# lt_split) + K3 prep_rows + the factor: one fused K1 launch (d <= 63) or, on the panel
-# path, a Z GEMM and a projection GEMM per <= 2 GB Z panel
+# per step: K2 (column_sum_partial, column_mean_finalize, landmark_stats, basis_consts,
+# prep_landmarks, col_stats, lt_split, col_norm_finalize) + K3 prep_rows + K9 row_shift and
+# row_rescale + the factor: one fused K1 launch (d <= 63) or, on the panel path, a Z GEMM and
+# a projection GEMM per <= 2 GB Z panel
 def launches_per_step(n, d, B):
     if d <= 63:
-        return 8
+        return 12
     bpad = -(-B // 256) * 256
     panel = max(256, (2 * 2**30 // (4 * bpad)) // 256 * 256)
     npad = -(-n // 256) * 256
-    return 7 + 2 * (-(-npad // panel))
+    return 11 + 2 * (-(-npad // panel))
 
 
 def parse():

@@ -140,16 +140,14 @@ __global__ void hp_transpose_kernel(const double* __restrict__ L, int B, int b_e
 // Column norms of L for the precision choice: the columns of L = U·D^-1/2 are orthogonal
 // with norms 1/√λ_j. out[0] = max_j ‖L[:, j]‖² (= 1/λ_min), out[1] = min_j (= 1/λ_max),
 // out[2] = Σ_j ‖L[:, j]‖² (= ‖L‖_F²). The caller zeroes out[0] and out[2] and fills out[1]
-// with 0xff bytes. One thread per column (coalesced across a warp); non-negative doubles
-// order like their bit patterns.
-__global__ void col_norm_range_kernel(const double* __restrict__ L, int B, int b_eff, double* __restrict__ out) {
+// with 0xff bytes. One thread per column adds its row-slice partials in slice order
+// (col_stats_kernel, prep_kernels.cuh); non-negative doubles order like their bit patterns.
+__global__ void col_norm_finalize_kernel(const double* __restrict__ partial, int slices, int b_eff,
+                                         double* __restrict__ out) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     double s = 0.0;
     if (c < b_eff)
-        for (int k = 0; k < B; ++k) {
-            const double v = L[static_cast<long long>(k) * b_eff + c];
-            s += v * v;
-        }
+        for (int k = 0; k < slices; ++k) s += partial[static_cast<long long>(k) * b_eff + c];
     __shared__ double mx[256], mn[256], sm[256];
     mx[threadIdx.x] = s;
     sm[threadIdx.x] = s;

@@ -260,6 +260,8 @@ struct DeviceState {
     __half* z_lo = nullptr;
     int64_t z_rows = 0;
     GrowBuf stage_lm, stage_L, stage_ip, stage_idx, stage_val;  // basis staging (lpd_set_basis_*)
+    GrowBuf col_part;        // row-slice partials of the basis column statistics (K2)
+    int col_slices = 0;      // slices in col_part (column sums of L²)
     int host_share = 1;                // device states of this context sharing the host's cores
     // host CPUs local to this GPU (its PCI device's NUMA node) when that is a proper subset of
     // the process's CPUs: the delivery / staging threads run there and the pinned ring and
@@ -556,8 +558,10 @@ void init_device(DeviceState& ds, int device) {
             reinterpret_cast<const void*>(lpd::prep_landmarks_kernel),
             reinterpret_cast<const void*>(lpd::landmark_stats_kernel),
             reinterpret_cast<const void*>(lpd::basis_consts_kernel),
-            reinterpret_cast<const void*>(lpd::column_mean_kernel),
-            reinterpret_cast<const void*>(lpd::col_absmax_kernel),
+            reinterpret_cast<const void*>(lpd::column_sum_partial_kernel),
+            reinterpret_cast<const void*>(lpd::column_mean_finalize_kernel),
+            reinterpret_cast<const void*>(lpd::col_stats_kernel),
+            reinterpret_cast<const void*>(lpd::col_norm_finalize_kernel),
             reinterpret_cast<const void*>(lpd::lt_split_kernel),
             reinterpret_cast<const void*>(lpd::csr_to_dense_kernel),
             reinterpret_cast<const void*>(lpd::gram_f64_kernel),
@@ -628,8 +632,9 @@ void choose_precision(DeviceState& ds, const double* lm_dev, int64_t B, int64_t 
     if (!ds.hp_norms) dev_alloc(&ds.hp_norms, 3);
     CUDA_TRY(cudaMemsetAsync(ds.hp_norms, 0, 3 * sizeof(double), st));
     CUDA_TRY(cudaMemsetAsync(ds.hp_norms + 1, 0xff, sizeof(double), st));
-    lpd::col_norm_range_kernel<<<static_cast<int>((b_eff + 255) / 256), 256, 0, st>>>(
-        L_dev, static_cast<int>(B), static_cast<int>(b_eff), ds.hp_norms);
+    // the Σ L[:, k]² partials col_stats_kernel left in col_part (build_basis, just before)
+    lpd::col_norm_finalize_kernel<<<static_cast<int>((b_eff + 255) / 256), 256, 0, st>>>(
+        static_cast<const double*>(ds.col_part.p), ds.col_slices, static_cast<int>(b_eff), ds.hp_norms);
     CUDA_TRY(cudaGetLastError());
     double h[3] = {0.0, 0.0, 0.0};
     CUDA_TRY(cudaMemcpyAsync(h, ds.hp_norms, sizeof(h), cudaMemcpyDeviceToHost, st));
@@ -782,8 +787,23 @@ void build_basis(DeviceState& ds, const double* lm_dev, int64_t B, int64_t d, in
     ds.has_basis = false;
     ds.B = B; ds.d = d; ds.b_eff = b_eff; ds.gamma = gamma;
 
-    lpd::column_mean_kernel<<<static_cast<int>(kd / 32), dim3(32, 8), 0, st>>>(
-        lm_dev, ld_lm, static_cast<int>(B), static_cast<int>(d), static_cast<int>(kd), ds.mu);
+    // row slices so the statistics kernels fill the GPU (~4 blocks per SM)
+    auto slices_for = [&](int64_t rows, int64_t cols) {
+        const int64_t cblocks = (cols + 31) / 32;
+        const int64_t want = std::max<int64_t>(1, (4 * ds.num_sms + cblocks - 1) / cblocks);
+        const int64_t per = std::max<int64_t>(lpd::CS_LANES, round_up((rows + want - 1) / want, lpd::CS_LANES));
+        return std::make_pair((rows + per - 1) / per, per);
+    };
+    {
+        const auto [sl, per] = slices_for(B, d);
+        double* part = ds.col_part.d(sizeof(double) * static_cast<size_t>(std::max<int64_t>(sl, 1) * kd));
+        lpd::column_sum_partial_kernel<<<dim3(static_cast<unsigned>(kd / 32), static_cast<unsigned>(std::max<int64_t>(sl, 1))),
+                                         dim3(32, lpd::CS_LANES), 0, st>>>(
+            lm_dev, ld_lm, static_cast<int>(B), static_cast<int>(d), static_cast<int>(per), part, static_cast<int>(kd));
+        lpd::column_mean_finalize_kernel<<<static_cast<int>((kd + 127) / 128), 128, 0, st>>>(
+            part, static_cast<int>(std::max<int64_t>(sl, 1)), static_cast<int>(kd), static_cast<int>(B),
+            static_cast<int>(d), static_cast<int>(kd), ds.mu);
+    }
     {
         const int threads = 256, rows_per_block = threads / 32;
         const int blocks = static_cast<int>((B + rows_per_block - 1) / rows_per_block);
@@ -797,8 +817,18 @@ void build_basis(DeviceState& ds, const double* lm_dev, int64_t B, int64_t d, in
             lm_dev, ld_lm, static_cast<int>(B), static_cast<int>(d), static_cast<int>(kd), ds.mu,
             ds.consts, ds.lm_hi, ds.lm_lo, static_cast<int>(B_pad));
     }
-    lpd::col_absmax_kernel<<<static_cast<int>((b_eff + 127) / 128), 128, 0, st>>>(
-        L_dev, static_cast<int>(B), static_cast<int>(b_eff), ds.colmax);
+    {
+        // max |L[:, k]| into colmax (the Lᵀ scaling) and Σ L[:, k]² partials (the precision
+        // choice), one pass over L
+        const auto [sl, per] = slices_for(B, b_eff);
+        ds.col_slices = static_cast<int>(sl);
+        double* part = ds.col_part.d(sizeof(double) * static_cast<size_t>(sl * b_eff));
+        CUDA_TRY(cudaMemsetAsync(ds.colmax, 0, sizeof(double) * static_cast<size_t>(b_eff), st));
+        lpd::col_stats_kernel<<<dim3(static_cast<unsigned>((b_eff + 31) / 32), static_cast<unsigned>(sl)),
+                                dim3(32, lpd::CS_LANES), 0, st>>>(
+            L_dev, static_cast<int>(B), static_cast<int>(b_eff), static_cast<int>(per),
+            reinterpret_cast<unsigned long long*>(ds.colmax), part);
+    }
     dim3 grid(static_cast<unsigned>(B_pad / 32), static_cast<unsigned>(Beff_pad / 32));
     lpd::lt_split_kernel<<<grid, dim3(32, 8), 0, st>>>(L_dev, static_cast<int>(B),
                                                         static_cast<int>(b_eff), ds.colmax, ds.lt_hi,
@@ -2187,7 +2217,8 @@ int lpd_context_destroy(lpd_context* ctx) {
         ds.model.free_all();
         ds.free_hp();
         dev_free(ds.hp_norms);
-        for (GrowBuf* g : {&ds.stage_lm, &ds.stage_L, &ds.stage_ip, &ds.stage_idx, &ds.stage_val}) g->release();
+        for (GrowBuf* g : {&ds.stage_lm, &ds.stage_L, &ds.stage_ip, &ds.stage_idx, &ds.stage_val, &ds.col_part})
+            g->release();
         if (ds.scratch) cudaFree(ds.scratch);
         if (ds.gtmp) cudaFree(ds.gtmp);
         for (auto& s : ds.slot) {

@@ -39,9 +39,11 @@ def test_issued_work_and_launch_counts():
     sys.path.insert(0, ROOT)
     import bench
 
-    assert bench.launches_per_step(581_012, 54, 4096) == 8          # K2 (6) + K3 + K1
-    # C4 panel path: 7 prep launches + Z and projection GEMMs per <= 2 GB Z panel
-    assert bench.launches_per_step(160_146, 2048, 16_384) == 7 + 2 * 5
+    # K2 (8) + K3 + K9 probe + K1 + K9 rescale (profiles/r02 launch lists: 11 before the
+    # sliced column statistics split col_absmax/col_norm_range/column_mean into 5)
+    assert bench.launches_per_step(581_012, 54, 4096) == 12
+    # C4 panel path: 11 prep/probe launches + Z and projection GEMMs per <= 2 GB Z panel
+    assert bench.launches_per_step(160_146, 2048, 16_384) == 11 + 2 * 5
 
 
 @pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref is built where /root/reference exists")
