@@ -204,20 +204,37 @@ __global__ void prep_rows_kernel(const double* __restrict__ X, long long ldx, in
     for (int row = warp_global; row < m_pad; row += nwarps) {
         const double* x = X + static_cast<long long>(row) * ldx;
         const long long base = static_cast<long long>(row) * kd;
+        // lanes take column pairs (2·lane, 2·lane + 1) + 64·k: one __half2 store per plane
+        // per pair (kd is a multiple of 64, so the pairs never straddle a row)
         double ss = 0.0, mx = 0.0;
         if (row < m)
-            for (int c = lane; c < d; c += 32) {
-                const double v = x[c] - mu[c];
-                ss += v * v;
-                mx = fmax(mx, fabs(v));
+            for (int c = 2 * lane; c < d; c += 64) {
+                const double v0 = x[c] - mu[c];
+                ss += v0 * v0;
+                mx = fmax(mx, fabs(v0));
+                if (c + 1 < d) {
+                    const double v1 = x[c + 1] - mu[c + 1];
+                    ss += v1 * v1;
+                    mx = fmax(mx, fabs(v1));
+                }
             }
         ss = warp_sum_d(ss);
         mx = warp_max_d(mx);
         const int e = max(clamp_exp(mx), s_exp - 1);
         const double sigma = ldexp(1.0, 13 - e);
-        for (int c = lane; c < kd; c += 32) {
-            const double v = (row < m && c < d) ? x[c] - mu[c] : 0.0;
-            split_store(hi, lo, base + c, c == d ? sigma / aug : v * sigma);
+        for (int c = 2 * lane; c < kd; c += 64) {
+            double a[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int cc = c + q;
+                const double v = (row < m && cc < d) ? x[cc] - mu[cc] : 0.0;
+                a[q] = cc == d ? sigma / aug : v * sigma;
+            }
+            const __half h0 = __double2half(a[0]), h1 = __double2half(a[1]);
+            const __half l0 = __double2half(a[0] - static_cast<double>(__half2float(h0)));
+            const __half l1 = __double2half(a[1] - static_cast<double>(__half2float(h1)));
+            *reinterpret_cast<__half2*>(hi + base + c) = __halves2half2(h0, h1);
+            *reinterpret_cast<__half2*>(lo + base + c) = __halves2half2(l0, l1);
         }
         if (lane == 0) {
             aux[row] = RowAux{static_cast<float>(13.0 + g * ss), static_cast<float>(-2.0 * g / (sigma * beta)),
