@@ -829,7 +829,7 @@ void build_basis(DeviceState& ds, const double* lm_dev, int64_t B, int64_t d, in
             L_dev, static_cast<int>(B), static_cast<int>(b_eff), static_cast<int>(per),
             reinterpret_cast<unsigned long long*>(ds.colmax), part);
     }
-    dim3 grid(static_cast<unsigned>(B_pad / 32), static_cast<unsigned>(Beff_pad / 32));
+    dim3 grid(static_cast<unsigned>(B_pad / 64), static_cast<unsigned>(Beff_pad / 32));
     lpd::lt_split_kernel<<<grid, dim3(32, 8), 0, st>>>(L_dev, static_cast<int>(B),
                                                         static_cast<int>(b_eff), ds.colmax, ds.lt_hi,
                                                         ds.lt_lo, static_cast<int>(B_pad),

@@ -334,34 +334,37 @@ __global__ void col_stats_kernel(const double* __restrict__ L, int B, int b_eff,
 
 
 // Lᵀ split planes [Beff_pad × B_pad]: lt[k][j] = L[j][k]·u_k (hi/lo), padded with 0.
-// 32×32 tiles through shared memory so both the read and the write coalesce.
+// 64 (landmarks j) × 32 (columns k) tiles through shared memory: the reads are 256-byte
+// rows of L, and each lane writes two consecutive landmarks of an Lᵀ row as one __half2 per
+// plane (128-byte warp stores; B_pad is a multiple of 64).
 __global__ void lt_split_kernel(const double* __restrict__ L, int B, int b_eff,
                                 const double* __restrict__ colmax, __half* __restrict__ lt_hi,
                                 __half* __restrict__ lt_lo, int B_pad, int Beff_pad,
                                 float* __restrict__ col_scale) {
-    __shared__ double tile[32][33];
-    const int j0 = blockIdx.x * 32;  // landmark (K) index
+    __shared__ double tile[64][33];
+    const int j0 = blockIdx.x * 64;  // landmark (K) index
     const int k0 = blockIdx.y * 32;  // G column index
     const int tx = threadIdx.x, ty = threadIdx.y;  // 32 × 8
-    for (int yy = ty; yy < 32; yy += 8) {
+    for (int yy = ty; yy < 64; yy += 8) {
         const int j = j0 + yy, k = k0 + tx;
         tile[yy][tx] = (j < B && k < b_eff) ? L[static_cast<long long>(j) * b_eff + k] : 0.0;
     }
     __syncthreads();
-    for (int yy = ty; yy < 32; yy += 8) {
-        const int k = k0 + yy, j = j0 + tx;
+    for (int kk = ty; kk < 32; kk += 8) {
+        const int k = k0 + kk, j = j0 + 2 * tx;
         if (k >= Beff_pad || j >= B_pad) continue;
         double u = 1.0;
         if (k < b_eff) {
             const double m = colmax[k];
             if (m > 0.0) u = ldexp(1.0, 13 - ilogb(m));
         }
-        const double a = tile[tx][yy] * u;
-        const __half h = __double2half(a);
-        const __half l = __double2half(a - static_cast<double>(__half2float(h)));
+        const double a0 = tile[2 * tx][kk] * u, a1 = tile[2 * tx + 1][kk] * u;
+        const __half h0 = __double2half(a0), h1 = __double2half(a1);
+        const __half l0 = __double2half(a0 - static_cast<double>(__half2float(h0)));
+        const __half l1 = __double2half(a1 - static_cast<double>(__half2float(h1)));
         const long long o = static_cast<long long>(k) * B_pad + j;
-        lt_hi[o] = h;
-        lt_lo[o] = l;
+        *reinterpret_cast<__half2*>(lt_hi + o) = __halves2half2(h0, h1);
+        *reinterpret_cast<__half2*>(lt_lo + o) = __halves2half2(l0, l1);
         if (blockIdx.x == 0 && tx == 0)
             col_scale[k] = (k < b_eff) ? static_cast<float>(ldexp(1.0, -13) / u) : 0.0f;
     }
