@@ -130,13 +130,27 @@ def run_train(lib, args):
     # warm-up on a small problem: process-level one-time costs (CUDA context on the B200
     # build, thread pools, page cache) stay out of the timed train
     train(X[:2000], y[:2000], X[n:n + 100], y[n:n + 100], 100)
+    vm0 = vmstat()
     o = train(X[:n], y[:n], X[n:], y[n:], cfg.budget)
+    vm1 = vmstat()
     return {"build": args.build, "workload": cfg.name, "n": n, "n_test": n_test, "d": cfg.d, "B": cfg.budget,
             "gamma": cfg.gamma, "C": cfg.C, "eps": 1e-3, "tau": 1e-12, "threads": threads,
             "train_seconds": o[0], "preparation_seconds": o[1], "gmatrix_seconds": o[2],
             "training_seconds": o[3], "predict_seconds": o[4], "test_error": o[5], "epochs": int(o[6]),
             "b_eff": int(o[7]), "unconverged_pairs": int(o[8]), "dual_objective": o[9],
-            "coordinate_visits": int(o[10])}
+            "coordinate_visits": int(o[10]),
+            # the host's huge-page faults during the train (the gmatrix stage's fresh 19 GB G is
+            # first-touched on huge pages; fallbacks / direct compaction slow it down)
+            "host_thp": {k: vm1.get(k, 0) - vm0.get(k, 0) for k in vm1}}
+
+
+def vmstat():
+    keys = ("thp_fault_alloc", "thp_fault_fallback", "compact_stall")
+    try:
+        with open("/proc/vmstat") as f:
+            return {k: int(v) for k, v in (line.split() for line in f) if k in keys}
+    except OSError:
+        return {}
 
 
 def main():
