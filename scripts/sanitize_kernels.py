@@ -30,6 +30,8 @@ for n, d, B in ((300, 50, 100), (600, 100, 300)):  # fused K1, then the d >= 64 
     rows = np.arange(0, n, 3, dtype=np.int32)
     ctx.resident_gw(rows, rng.standard_normal((1, G.shape[1])))
     ctx.resident_gw(rows, rng.standard_normal((5, G.shape[1])))
+    ctx.resident_gw(rows, rng.standard_normal((45, G.shape[1])))  # 64-row tile shape, P-tile of 48
+    ctx.resident_vote(rows, rng.standard_normal((3, G.shape[1])), 3)
     ctx.resident_gtv(rows, rng.standard_normal(rows.shape[0]))
     if hasattr(ctx, "resident_gtv_sets"):
         ctx.resident_gtv_sets(rows, rng.standard_normal((rows.shape[0], 11)))
@@ -43,5 +45,21 @@ for n, d, B in ((300, 50, 100), (600, 100, 300)):  # fused K1, then the d >= 64 
     ctx.set_model_dense(Y, betas, 1.0 / d)
     ctx.model_decision_values_dense(X[:50])
     ctx.ovo_vote(rng.standard_normal((100, 3)), 3)
+# K9: rows far from every landmark at a large γ raise the probe flag, so row_shift and
+# row_rescale run for real (fused path, then the d >= 64 panel path; fp32 and fp64 G)
+import torch  # noqa: E402
+
+for d in (32, 96):
+    Y = rng.standard_normal((160, d))
+    X = rng.standard_normal((600, d))
+    X[:200] += 3.0 * np.sqrt(d)
+    gamma = 16.0 / d
+    ctx.set_precision("fast")
+    ctx.set_basis_dense(Y, np_gaussian_L(Y, gamma, 1e-6), gamma)
+    ctx.compute_g_dense(X)
+    Gd = torch.empty((600, ctx.b_eff), dtype=torch.float64, device="cuda")
+    ctx.compute_g_device(torch.from_numpy(X).cuda(), Gd)
+    torch.cuda.synchronize()
+    ctx.set_precision("auto")
 ctx.close()
 print("sanitize_kernels: every kernel ran")
