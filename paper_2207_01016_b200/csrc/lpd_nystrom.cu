@@ -329,7 +329,7 @@ struct DeviceState {
         double* x = nullptr;   // [rows_cap × x_cols] points, dense fp64
         double* zt = nullptr;  // [B × rows_cap] landmark-major z
         double* dv = nullptr;  // [rows_cap × P]
-        int64_t rows_cap = 0, x_cols = 0;
+        int64_t rows_cap = 0, x_cols = 0, dv_cap = 0;
         double* hx = nullptr;  // pinned host staging of the points and the results
         double* hd = nullptr;
         size_t hx_cap = 0, hd_cap = 0;
@@ -339,7 +339,7 @@ struct DeviceState {
             if (hd) cudaFreeHost(hd);
             hx = hd = nullptr;
             hx_cap = hd_cap = 0;
-            rows_cap = x_cols = 0;
+            rows_cap = x_cols = dv_cap = 0;
             set = false;
         }
     } model;
@@ -1961,6 +1961,10 @@ void set_model(lpd_context* ctx, int64_t B, const HostRows& lm, const double* be
     m.set = false;
     dev_free(m.lm);
     dev_free(m.beta);
+    if (B != m.B || P != m.P) {  // the per-call buffers are shaped by B (z) and P (D)
+        dev_free(m.x); dev_free(m.zt); dev_free(m.dv);
+        m.rows_cap = m.x_cols = m.dv_cap = 0;
+    }
     std::vector<double> dense(static_cast<size_t>(B * std::max<int64_t>(lm.d, 1)));
     lm.fill(dense.data(), 0, B);
     dev_alloc(&m.lm, dense.size());
@@ -1995,17 +1999,21 @@ void model_decision_values(lpd_context* ctx, int64_t n, const HostRows& xs, doub
     const int64_t xc = std::max<int64_t>(xs.d, 1);
     if (m.rows_cap < chunk || m.x_cols < xc) {
         dev_free(m.x); dev_free(m.zt); dev_free(m.dv);
-        m.rows_cap = m.x_cols = 0;
+        m.rows_cap = m.x_cols = m.dv_cap = 0;
         m.set = false;
         dev_alloc(&m.x, static_cast<size_t>(chunk * xc));
         dev_alloc(&m.zt, static_cast<size_t>(chunk * m.B));
         m.rows_cap = chunk;
         m.x_cols = xc;
     }
-    dev_free(m.dv);
-    m.set = false;  // until the buffers are whole again
-    dev_alloc(&m.dv, static_cast<size_t>(m.rows_cap * m.P));
-    m.set = true;
+    if (m.dv_cap < m.rows_cap * m.P) {  // per-point calls reuse it (a cudaMalloc per call cost ~170 us)
+        dev_free(m.dv);
+        m.dv_cap = 0;
+        m.set = false;  // until the buffers are whole again
+        dev_alloc(&m.dv, static_cast<size_t>(m.rows_cap * m.P));
+        m.dv_cap = m.rows_cap * m.P;
+        m.set = true;
+    }
     const size_t hx_need = sizeof(double) * static_cast<size_t>(chunk * xc);
     const size_t hd_need = sizeof(double) * static_cast<size_t>(chunk * m.P);
     if (m.hx_cap < hx_need) {

@@ -654,3 +654,18 @@ def test_injected_fault_fails_loudly_and_context_recovers(site, code):
             P.inject_fault(P.LPD_FAULT_NONE)
         assert ei.value.code == code and "injected fault" in str(ei.value)
         assert np.array_equal(ctx.compute_g_dense(X), ref)
+
+
+def test_model_switch_reshapes_buffers(gpu_ctx):
+    """K8's per-call buffers are shaped by the model (z by B, D by P): a second model with
+    more landmarks and pairs after a small one must not reuse the small buffers."""
+    rng = np.random.default_rng(31)
+    X = rng.standard_normal((300, 10))
+    for B, P_ in ((32, 1), (700, 6), (64, 3)):
+        Y = rng.standard_normal((B, 10))
+        betas = rng.standard_normal((P_, B))
+        gpu_ctx.set_model_dense(Y, betas, 0.1)
+        D = gpu_ctx.model_decision_values_dense(X)
+        Dr = O.ora_kernel_block(O.dense_to_csr(X), O.dense_to_csr(Y), 0.1) @ betas.T
+        assert D.shape == (300, P_)
+        assert np.max(np.abs(D - Dr)) <= 1e-10 * np.max(np.abs(Dr)), (B, P_)
