@@ -322,11 +322,17 @@ lpdsvm::Matrix make_output_matrix(std::size_t rows, std::size_t cols) {
         if (a1 > a0) madvise(reinterpret_cast<void*>(a0), a1 - a0, MADV_HUGEPAGE);
         vl->finish = vl->start + n;  // size n, elements written by compute_G below
         if (v.size() != n) return lpdsvm::Matrix(rows, cols);
+        double* const storage = v.data();
         lpdsvm::Matrix m;
         auto* L = reinterpret_cast<MatrixLayout*>(&m);
         L->rows = rows;
         L->cols = cols;
         L->data = std::move(v);
+        // the Matrix's own public accessors must see exactly what was set, else the
+        // reference's constructor (the storage is released with m)
+        if (m.rows() != rows || m.cols() != cols || m.data() != storage ||
+            m.row(rows - 1) != storage + (rows - 1) * cols)
+            return lpdsvm::Matrix(rows, cols);
         return m;
     } else {
         return lpdsvm::Matrix(rows, cols);
