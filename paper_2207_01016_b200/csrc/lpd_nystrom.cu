@@ -307,6 +307,7 @@ struct DeviceState {
     int precision_mode = LPD_PRECISION_AUTO;
     bool hp = false;
     double cond_est = 0.0;
+    double exp_mag = 0.0;        // T_b, the basis exponent magnitude (choose_precision)
     double* hp_norms = nullptr;  // [2] column-norm range of L
     double* hp_lm = nullptr;
     double* hp_lt = nullptr;
@@ -627,6 +628,16 @@ double hp_threshold() {
     return t;
 }
 
+// LPD_HP_EXP_THRESHOLD (default 200): the basis exponent magnitude above which AUTO takes
+// the high-precision path (choose_precision)
+double hp_exp_threshold() {
+    static const double t = [] {
+        const char* e = std::getenv("LPD_HP_EXP_THRESHOLD");
+        return e ? std::atof(e) : 200.0;
+    }();
+    return t;
+}
+
 void choose_precision(DeviceState& ds, const double* lm_dev, int64_t B, int64_t d, int64_t ld_lm,
                       const double* L_dev, int64_t b_eff, cudaStream_t st) {
     if (!ds.hp_norms) dev_alloc(&ds.hp_norms, 3);
@@ -637,12 +648,22 @@ void choose_precision(DeviceState& ds, const double* lm_dev, int64_t B, int64_t 
         static_cast<const double*>(ds.col_part.p), ds.col_slices, static_cast<int>(b_eff), ds.hp_norms);
     CUDA_TRY(cudaGetLastError());
     double h[3] = {0.0, 0.0, 0.0};
+    lpd::BasisConsts kc{};
     CUDA_TRY(cudaMemcpyAsync(h, ds.hp_norms, sizeof(h), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(&kc, ds.consts, sizeof(kc), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     ds.cond_est = (h[1] > 0.0 && std::isfinite(h[2])) ? std::ldexp(std::sqrt(h[2] / (static_cast<double>(B) * h[1])), -22)
                                                       : std::numeric_limits<double>::infinity();
+    // The exponent magnitude of the basis, T_b = γ·log2(e)·(2·max_j |b_j − μ|)²: how large the
+    // terms of t = R_i + acc·sx_i get for points inside the landmark cloud. The fast path forms
+    // acc with fp32 tensor-core accumulation, whose rounding grows with that magnitude; above
+    // T_b ≈ 200 (points several kernel widths apart, K ≈ I: unscaled features at a large γ) it
+    // exceeds the 1e-4 row bound whatever L's conditioning (scripts/fuzz_diag.py: every
+    // failing draw had T_b ≥ 300, none below 200 did; C1–C4 have T_b ≈ 10–25).
+    ds.exp_mag = -kc.g * 4.0 * kc.nbmax;
     ds.hp = ds.precision_mode == LPD_PRECISION_HIGH ||
-            (ds.precision_mode == LPD_PRECISION_AUTO && ds.cond_est > hp_threshold());
+            (ds.precision_mode == LPD_PRECISION_AUTO &&
+             (ds.cond_est > hp_threshold() || ds.exp_mag > hp_exp_threshold()));
     if (!ds.hp) return;
     // fp64 landmarks (packed B × max(d, 1)) and Lᵀ (zero-padded to 128-row N tiles and a
     // K that is a multiple of 16) for the DMMA projection

@@ -46,11 +46,13 @@ __device__ __forceinline__ int floor_log2(double v) { return ilogb(v); }
 //   aug    2^-s, the augmented-column scale (landmark side 2^-s, point side 2^s)
 //   g      -gamma * log2(e)
 //   rmin   min_j |b_j - mu| (row prep's bound on a point's nearest-landmark distance)
+//   nbmax  max_j |b_j - mu|^2 (the precision choice's exponent magnitude, choose_precision)
 struct BasisConsts {
     double beta;
     double aug;
     double g;
     double rmin;
+    double nbmax;
 };
 
 // Per-row epilogue operands of the factor kernels (prep_rows_kernel, then
@@ -143,6 +145,7 @@ __global__ void basis_consts_kernel(const double* __restrict__ nb, const double*
         out->aug = ldexp(1.0, -s);
         out->g = -gamma * 1.4426950408889634;
         out->rmin = m > 0 ? sqrt(c) : 0.0;
+        out->nbmax = b;
     }
 }
 

@@ -669,3 +669,49 @@ def test_model_switch_reshapes_buffers(gpu_ctx):
         Dr = O.ora_kernel_block(O.dense_to_csr(X), O.dense_to_csr(Y), 0.1) @ betas.T
         assert D.shape == (300, P_)
         assert np.max(np.abs(D - Dr)) <= 1e-10 * np.max(np.abs(Dr)), (B, P_)
+
+
+@pytest.mark.parametrize("seed", [*range(12), 17, 23, 33, 121])  # 17-121: large exponent magnitudes
+def test_random_shapes_fuzz(gpu_ctx, seed):
+    """Seeded random problems across both factor paths and all three host/device entry
+    points: n in [1, 1500], d in [1, 160] (the fused kernel below 64, the panel path
+    above), B in [1, 400], b_eff up to B (truncated spectra), γ log-uniform in
+    [0.1/d, 10/d], dense or ~30 %-sparse points, unscaled features in some draws. Every row
+    inside fp32's range meets the conditioned bound against the oracle (rows whose values
+    are all below 2^-100 — e.g. a 9e-42 row, unscaled points at a large γ — are the fp32
+    output's stated range limit and must merely stay that small); dense, CSR and device
+    entries agree bitwise."""
+    import torch
+
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.integers(1, 1501))
+    d = int(rng.integers(1, 161))
+    B = int(rng.integers(1, 401))
+    gamma = float(np.exp(rng.uniform(np.log(0.1 / d), np.log(10.0 / d))))
+    scale = float(rng.choice([1.0, 1.0, 7.0]))
+    X = (rng.standard_normal((n, d)) * scale).astype(np.float32).astype(np.float64)
+    if rng.random() < 0.5:
+        X[rng.random(X.shape) < 0.7] = 0.0
+    Y = X[rng.choice(n, B, replace=False)] if B <= n else (rng.standard_normal((B, d)) * scale).astype(np.float32).astype(np.float64)
+    L = np_gaussian_L(Y, gamma, float(rng.choice([1e-10, 1e-6, 1e-3])))
+    # the product's own precision choice (auto: the fp64 path for ill-conditioned bases and
+    # for exponent magnitudes the fast path cannot hold)
+    gpu_ctx.set_precision("auto")
+    try:
+        gpu_ctx.set_basis_dense(Y, L, gamma)
+        G = gpu_ctx.compute_g_dense(X)
+        ip, ix, vv = O.dense_to_csr(X)
+        lp, li, lv = O.dense_to_csr(Y)
+        gpu_ctx.set_basis_csr(lp, li, lv, d, L, gamma)
+        assert np.array_equal(G, gpu_ctx.compute_g_csr(ip, ix, vv))
+        Gd = torch.empty((n, L.shape[1]), dtype=torch.float32, device="cuda")
+        gpu_ctx.compute_g_device(torch.from_numpy(X).cuda(), Gd)
+        torch.cuda.synchronize()
+        assert np.array_equal(G, Gd.cpu().numpy().astype(np.float64))
+    finally:
+        gpu_ctx.set_precision("auto")
+    R = _oracle_G(X, Y, L, gamma)
+    live = np.abs(R).max(axis=1) >= 2.0 ** -100
+    assert np.all(np.abs(G[~live]) < 2.0 ** -99)
+    if live.any():
+        assert_conditioned_parity(G[live], X[live], Y, L, gamma)
