@@ -715,3 +715,31 @@ def test_random_shapes_fuzz(gpu_ctx, seed):
     assert np.all(np.abs(G[~live]) < 2.0 ** -99)
     if live.any():
         assert_conditioned_parity(G[live], X[live], Y, L, gamma)
+
+
+@pytest.mark.parametrize("d,extra_x,extra_g", [(20, 3, 1), (20, 0, 5), (100, 7, 3), (33, 1, 0)])
+def test_caller_pitches_bitwise(gpu_ctx, d, extra_x, extra_g):
+    """The C ABI's leading dimensions: X rows with ldx > d and G rows with ldg > b_eff
+    (odd pitches the kernel's TMA store cannot target go through the aligned staging) give
+    G bitwise equal to the contiguous call, and the padding columns of the caller's G are
+    left untouched."""
+    import ctypes
+
+    rng = np.random.default_rng(d * 10 + extra_x + extra_g)
+    n, B = 777, 130
+    X = rng.standard_normal((n, d)).astype(np.float32).astype(np.float64)
+    Y = X[rng.choice(n, B, replace=False)]
+    L = np_gaussian_L(Y, 1.0 / d, 1e-8)
+    be = L.shape[1]
+    gpu_ctx.set_basis_dense(Y, L, 1.0 / d)
+    ref = gpu_ctx.compute_g_dense(X)
+    Xp = np.full((n, d + extra_x), 123.0)
+    Xp[:, :d] = X
+    Gp = np.full((n, be + extra_g), -7.0)
+    lib = P.load_library()
+    dp = ctypes.POINTER(ctypes.c_double)
+    st = lib.lpd_compute_g_dense(gpu_ctx.handle, Xp.ctypes.data_as(dp), n, d, d + extra_x,
+                                 Gp.ctypes.data_as(dp), be + extra_g, None)
+    assert st == 0, P.load_library().lpd_last_error()
+    assert np.array_equal(Gp[:, :be], ref)
+    assert np.all(Gp[:, be:] == -7.0)
