@@ -1054,12 +1054,16 @@ void launch_factor_panels(DeviceState& ds, Slot& s, int64_t m, void* g_dev, int6
         pz.group_r = group_r;
         // the Z GEMM's K is only d + 1 (33 chunks at C4): segments of 8 chunks keep its
         // share of the error (C4 full shard 3.0e-5 at 2 or 8, 3.9e-5 unsegmented) with
-        // fewer read-outs (LPD_SEG_Z overrides)
-        static const int seg_z = [] {
+        // fewer read-outs. Its accumulator holds the exponent terms, though, whose rounding
+        // grows with the basis exponent magnitude T_b (choose_precision): above T_b = 25
+        // segments of 2 (random draws at T_b ≈ 130, d ≈ 1,800: 1.75× the row bound at 8,
+        // 0.52× at 2; +1.2 % on the C4 step, which has T_b ≈ 5 and keeps 8). LPD_SEG_Z
+        // overrides.
+        static const int seg_z_env = [] {
             const char* e = std::getenv("LPD_SEG_Z");
-            return e ? std::max(1, std::atoi(e)) : 8;
+            return e ? std::max(1, std::atoi(e)) : 0;
         }();
-        pz.seg_chunks = seg_z;
+        pz.seg_chunks = seg_z_env ? seg_z_env : (ds.exp_mag > 25.0 ? 2 : 8);
         // no rendezvous for the Z GEMM: its tiles are short (K = d + 1, 33 chunks at C4)
         // and its operands small; a tile-start wait costs it more (72.7 vs 85.8 % tensor)
         pz.sync = nullptr;

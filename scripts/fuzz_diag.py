@@ -17,9 +17,15 @@ from conftest import np_gaussian_L  # noqa: E402
 from oracle import oracle as O  # noqa: E402
 
 
+BIG = os.environ.get("FUZZ_BIG") == "1"  # the panel path at large d and B
+
+
 def case(seed):
-    rng = np.random.default_rng(1000 + seed)
-    n = int(rng.integers(1, 1501)); d = int(rng.integers(1, 161)); B = int(rng.integers(1, 401))
+    rng = np.random.default_rng((3000 if BIG else 1000) + seed)
+    if BIG:
+        n = int(rng.integers(1, 3001)); d = int(rng.integers(200, 2101)); B = int(rng.integers(256, 2049))
+    else:
+        n = int(rng.integers(1, 1501)); d = int(rng.integers(1, 161)); B = int(rng.integers(1, 401))
     gamma = float(np.exp(rng.uniform(np.log(0.1 / d), np.log(10.0 / d))))
     scale = float(rng.choice([1.0, 1.0, 7.0]))
     X = (rng.standard_normal((n, d)) * scale).astype(np.float32).astype(np.float64)
@@ -33,10 +39,11 @@ def case(seed):
 
 first = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 count = int(sys.argv[2]) if len(sys.argv) > 2 else 100
+only = [int(x) for x in os.environ.get("FUZZ_SEEDS", "").split(",") if x]
 ctx = P.Context(1)
 ctx.set_precision(os.environ.get("FUZZ_PRECISION", "auto"))
 worst = (0.0, None)
-for seed in range(first, first + count):
+for seed in (only or range(first, first + count)):
     n, d, B, gamma, scale, X, Y, L = case(seed)
     ctx.set_basis_dense(Y, L, gamma)
     G = ctx.compute_g_dense(X)
