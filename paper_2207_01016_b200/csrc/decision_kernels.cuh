@@ -136,14 +136,11 @@ __global__ void ovo_pair_table_kernel(int num_classes, int2* __restrict__ pairs)
 
 namespace lpd {
 
-// K6 — products with the resident fp32 G for the host solver and CV scoring.
+// K6 — products with the resident fp32 G for the host solver and CV scoring:
+//   D[i][p] = Σ_j G[rows[i]][j]·W[p][j] over listed rows. Held-out scoring
+//   (modelsel.cpp:123-140) and the reactivation gradients 1 − y_i·G_i·w (dcd.cpp:150-172).
 //
-// gather_gw: D[i][p] = Σ_j G[rows[i]][j]·W[p][j] (fp64 accumulation), one warp per listed
-//   row, PB weight vectors per pass. Held-out scoring (modelsel.cpp:123-140) and the
-//   reactivation gradients 1 − y_i·G_i·w (dcd.cpp:150-172). HBM-bound on the G rows:
-//   16-byte streaming loads of G (4 columns per lane, four in flight per lane), W read
-//   as double2 through L1 (it is shared by every row). Per-lane partial sums in column
-//   order, then a fixed warp-shuffle tree: deterministic.
+// 16-byte streaming load of G (read once, not kept in L1).
 __device__ __forceinline__ float4 ld_stream_f4(const float4* p) {
     float4 v;
     asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
@@ -151,74 +148,8 @@ __device__ __forceinline__ float4 ld_stream_f4(const float4* p) {
                  : "l"(p));
     return v;
 }
-template <int PB>
-__global__ void __launch_bounds__(256) gather_gw_kernel(const float* __restrict__ G, long long ldg, int b_eff,
-                                                        const int32_t* __restrict__ rows, int count,
-                                                        const double* __restrict__ W, int P, int p0,
-                                                        double* __restrict__ D) {
-    constexpr int RW = 4;  // rows per warp: each W load (L1) serves four rows
-    const int lane = threadIdx.x & 31;
-    const int nwarps = (gridDim.x * blockDim.x) >> 5;
-    const int np = min(PB, P - p0);
-    // 16-byte path: rows and W rows 16-byte aligned (res_ld and b_eff multiples of 4)
-    const bool vec = ((ldg & 3) == 0) && ((b_eff & 3) == 0) && ((reinterpret_cast<uintptr_t>(G) & 15) == 0) &&
-                     ((reinterpret_cast<uintptr_t>(W) & 15) == 0);
-    for (int i0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * RW; i0 < count; i0 += nwarps * RW) {
-        double acc[RW][PB];
-#pragma unroll
-        for (int r = 0; r < RW; ++r)
-#pragma unroll
-            for (int q = 0; q < PB; ++q) acc[r][q] = 0.0;
-        const float* g[RW];
-#pragma unroll
-        for (int r = 0; r < RW; ++r) g[r] = G + static_cast<long long>(rows[min(i0 + r, count - 1)]) * ldg;
-        if (vec) {
-            const int n4 = b_eff >> 2;
-            for (int k4 = lane; k4 < n4; k4 += 32) {
-                float4 v[RW];
-#pragma unroll
-                for (int r = 0; r < RW; ++r) v[r] = ld_stream_f4(reinterpret_cast<const float4*>(g[r]) + k4);
-#pragma unroll
-                for (int q = 0; q < PB; ++q) {
-                    if (q < np) {
-                        const double2* w2 = reinterpret_cast<const double2*>(W + static_cast<long long>(p0 + q) * b_eff + 4 * k4);
-                        const double2 wa = __ldg(w2), wb = __ldg(w2 + 1);
-#pragma unroll
-                        for (int r = 0; r < RW; ++r) {
-                            acc[r][q] = fma(static_cast<double>(v[r].x), wa.x, acc[r][q]);
-                            acc[r][q] = fma(static_cast<double>(v[r].y), wa.y, acc[r][q]);
-                            acc[r][q] = fma(static_cast<double>(v[r].z), wb.x, acc[r][q]);
-                            acc[r][q] = fma(static_cast<double>(v[r].w), wb.y, acc[r][q]);
-                        }
-                    }
-                }
-            }
-        } else {
-            for (int k = lane; k < b_eff; k += 32) {
-#pragma unroll
-                for (int q = 0; q < PB; ++q) {
-                    if (q < np) {
-                        const double w = __ldg(W + static_cast<long long>(p0 + q) * b_eff + k);
-#pragma unroll
-                        for (int r = 0; r < RW; ++r) acc[r][q] = fma(static_cast<double>(g[r][k]), w, acc[r][q]);
-                    }
-                }
-            }
-        }
-#pragma unroll
-        for (int r = 0; r < RW; ++r) {
-#pragma unroll
-            for (int q = 0; q < PB; ++q) {
-                double v = acc[r][q];
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                if (lane == 0 && q < np && i0 + r < count) D[static_cast<long long>(i0 + r) * P + p0 + q] = v;
-            }
-        }
-    }
-}
 
-// gather_gw_seq: the same product, each D[i][p] summed by one thread in ascending column
+// gather_gw_seq: each D[i][p] summed by one thread in ascending column
 //   order with every product rounded and then added (__dmul_rn / __dadd_rn) — the
 //   reference's scoring loop exactly (modelsel.cpp:129-136, `d += g_row[j] * w_row[j]`,
 //   compiled without FP contraction), so on the same G the device's decision values are
