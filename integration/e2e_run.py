@@ -65,6 +65,18 @@ def check(lib, rc):
         raise RuntimeError(lib.e2e_last_error().decode())
 
 
+def adapter_phases(lib):
+    """The B200 build's breakdown of its last compute_G call (None for the reference build)."""
+    if not hasattr(lib, "lpd_adapter_phases"):
+        return None
+    ph = (ctypes.c_double * 4)()
+    lib.lpd_adapter_phases(ph)
+    tm = (ctypes.c_double * 8)()  # lpd_timings: total, h2d, kernel, d2h, host_copy (s), ...
+    lib.lpd_adapter_last_timings(ctypes.cast(tm, ctypes.c_void_p))
+    return {"flatten": ph[0], "basis": ph[1], "matrix_alloc": ph[2], "device_call": ph[3],
+            "h2d_event_s": tm[1], "kernel_event_s": tm[2], "d2h_event_s": tm[3], "host_widen_s": tm[4]}
+
+
 def run_compute_g(lib, args):
     from paper_2207_01016_b200 import synthetic
 
@@ -81,10 +93,14 @@ def run_compute_g(lib, args):
     sample = np.empty((k, b_eff))
     secs = np.zeros(3)
 
+    per_call = []
+
     def call():
         check(lib, lib.e2e_compute_g(n, _p(xp, ctypes.c_int64), _p(xi, ctypes.c_int32), _p(xv), b,
                                      _p(lp, ctypes.c_int64), _p(li, ctypes.c_int32), _p(lv), _p(L), b_eff, gamma,
                                      4096, threads, k, _p(sample), _p(secs)))
+        if args.per_call:
+            per_call.append({"gmatrix_seconds": secs[0], "phases": adapter_phases(lib)})
         return secs.copy()
 
     for _ in range(args.warmup):
@@ -95,14 +111,10 @@ def run_compute_g(lib, args):
            "gmatrix_seconds": stage, "compute_G_seconds": statistics.median(r[1] for r in runs),
            "matrix_free_seconds": statistics.median(r[2] for r in runs), "rows_per_s": n / stage,
            "steps": args.steps, "warmup": args.warmup}
-    if hasattr(lib, "lpd_adapter_phases"):  # the B200 build: where the last call's time went
-        ph = (ctypes.c_double * 4)()
-        lib.lpd_adapter_phases(ph)
-        tm = (ctypes.c_double * 8)()  # lpd_timings: total, h2d, kernel, d2h, host_copy (s), ...
-        lib.lpd_adapter_last_timings(ctypes.cast(tm, ctypes.c_void_p))
-        out["adapter_phases"] = {"flatten": ph[0], "basis": ph[1], "matrix_alloc": ph[2], "device_call": ph[3],
-                                 "h2d_event_s": tm[1], "kernel_event_s": tm[2], "d2h_event_s": tm[3],
-                                 "host_widen_s": tm[4]}
+    if per_call:
+        out["per_call"] = per_call
+    if (ph := adapter_phases(lib)) is not None:  # the B200 build: where the last call's time went
+        out["adapter_phases"] = ph
     if "G_sample" in z.files:  # spot check against the device-path rows bench.py produced
         ref = z["G_sample"][:k]
         out["sample_max_row_rel_diff"] = float(np.max(np.linalg.norm(sample - ref, axis=1)
@@ -141,7 +153,8 @@ def run_train(lib, args):
             "coordinate_visits": int(o[10]),
             # the host's huge-page faults during the train (the gmatrix stage's fresh 19 GB G is
             # first-touched on huge pages; fallbacks / direct compaction slow it down)
-            "host_thp": {k: vm1.get(k, 0) - vm0.get(k, 0) for k in vm1}}
+            "host_thp": {k: vm1.get(k, 0) - vm0.get(k, 0) for k in vm1},
+            "adapter_phases": adapter_phases(lib)}
 
 
 def vmstat():
@@ -162,6 +175,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=1)
     ap.add_argument("--n-test", type=int, default=10_000)
+    ap.add_argument("--per-call", action="store_true", help="compute_g: record every call (warm-up included)")
     args = ap.parse_args()
     lib = load(args.build)
     t0 = time.perf_counter()
