@@ -30,7 +30,9 @@ for n, d, B in ((300, 50, 100), (600, 100, 300)):  # fused K1, then the d >= 64 
     rows = np.arange(0, n, 3, dtype=np.int32)
     ctx.resident_gw(rows, rng.standard_normal((1, G.shape[1])))
     ctx.resident_gw(rows, rng.standard_normal((5, G.shape[1])))
-    ctx.resident_gw(rows, rng.standard_normal((45, G.shape[1])))  # 64-row tile shape, P-tile of 48
+    ctx.resident_gw(rows, rng.standard_normal((20, G.shape[1])))  # 8-row tile shape, 2 vectors per thread
+    ctx.resident_gw(rows, rng.standard_normal((45, G.shape[1])))  # 8-row tile shape, 3 vectors per thread
+    ctx.resident_gw(rows, rng.standard_normal((70, G.shape[1])))  # 4-row tile shape, P-tiles of 64
     ctx.resident_vote(rows, rng.standard_normal((3, G.shape[1])), 3)
     ctx.resident_gtv(rows, rng.standard_normal(rows.shape[0]))
     if hasattr(ctx, "resident_gtv_sets"):

@@ -75,6 +75,21 @@ def test_kernel_values_identity_basis(gpu_ctx):
     assert Z.max() <= 1.0 + TOL_Z and Z.min() >= 0.0
 
 
+@pytest.mark.parametrize("d,gamma", [(50, 0.02), (18, 1.0 / 18), (100, 0.01), (300, 1.0 / 300)])
+def test_kernel_values_elementwise_relative(gpu_ctx, d, gamma):
+    """SURVEY §8(c) criterion (1): Z elementwise within 1e-5 relative of the reference's
+    kernel_block (kernel.cpp:31-57), on the fused path (d <= 63) and the panel path."""
+    rng = np.random.default_rng(d)
+    X = rng.standard_normal((900, d)).astype(np.float32).astype(np.float64)
+    Y = X[rng.choice(900, 256, replace=False)]
+    gpu_ctx.set_basis_dense(Y, np.eye(256), gamma)
+    Z = gpu_ctx.compute_g_dense(X)
+    Zr = O.ora_kernel_block(O.dense_to_csr(X), O.dense_to_csr(Y), gamma)
+    live = Zr > 1e-30  # fp32 wire format: relative precision holds above its normal range
+    assert live.mean() > 0.99
+    assert np.max(np.abs(Z - Zr)[live] / Zr[live]) <= 1e-5
+
+
 @pytest.mark.parametrize("n,d,B,beff_cut,gamma", [
     (1, 5, 1, 0, 0.5),        # single row, single landmark (SPEC.md:211)
     (127, 3, 65, 0, 1.0),     # ragged rows (< one tile), landmarks = 64 + 1
