@@ -2,12 +2,25 @@
 launches, total ms and share of this library's device time (cold-cache, serialised
 ncu replays: compare shares, not absolute times)."""
 import csv
+import subprocess
 import sys
 from collections import defaultdict
 
-OURS = ("nystrom_factor_kernel", "panel_gemm_kernel", "prep_rows_kernel", "column_mean_kernel",
-        "landmark_stats_kernel", "basis_consts_kernel", "prep_landmarks_kernel", "col_absmax_kernel",
-        "lt_split_kernel", "csr_to_dense_kernel", "ovo_vote_kernel", "gram_", "gather_g", "decision_")
+OURS = ("nystrom_factor_kernel", "panel_gemm_kernel", "prep_rows_kernel", "column_sum_partial_kernel",
+        "column_mean_finalize_kernel", "col_stats_kernel", "col_norm_finalize_kernel", "landmark_stats_kernel",
+        "basis_consts_kernel", "prep_landmarks_kernel", "lt_split_kernel", "row_shift_kernel",
+        "row_rescale_kernel", "csr_to_dense_kernel", "ovo_vote_kernel", "gram_", "gather_g", "decision_", "hp_",
+        "pointdv_", "lpd::")
+UNIT_MS = {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0, "s": 1e3, "second": 1e3}
+
+
+def demangle(names):
+    """c++filt over mangled names (launch lists taken with --kernel-name-base mangled)."""
+    mangled = sorted({n for n in names if n.startswith("_Z")})
+    if not mangled:
+        return {}
+    out = subprocess.run(["c++filt"], input="\n".join(mangled), capture_output=True, text=True).stdout.splitlines()
+    return dict(zip(mangled, out))
 
 
 def main(path, title):
@@ -17,12 +30,13 @@ def main(path, title):
     tot = defaultdict(float)
     cnt = defaultdict(int)
     all_ms = 0.0
+    dm = demangle(r["Kernel Name"] for r in rows)
     for r in rows:
         if r["Metric Name"] != "gpu__time_duration.sum":
             continue
-        ms = float(r["Metric Value"].replace(",", "")) * (1e-6 if r["Metric Unit"] == "ns" else 1e-3 if r["Metric Unit"] == "us" else 1.0)
+        ms = float(r["Metric Value"].replace(",", "")) * UNIT_MS[r["Metric Unit"]]
         all_ms += ms
-        name = r["Kernel Name"].split("(")[0].strip()
+        name = dm.get(r["Kernel Name"], r["Kernel Name"]).split("(")[0].strip()
         if any(k in name for k in OURS):
             tot[name] += ms
             cnt[name] += 1
