@@ -883,7 +883,8 @@ struct PhaseTrace {
     }
 };
 
-void h2d_staged(DeviceState& ds, void* dst, const void* src, size_t bytes, cudaStream_t st);
+void h2d_staged(DeviceState& ds, void* dst, const void* src, size_t bytes, cudaStream_t st,
+                size_t min_bytes = size_t(32) << 20);
 
 
 // The basis of one γ on every device of the context ("one broadcast of
@@ -1451,12 +1452,24 @@ void run_parallel(lpd_context* ctx, const std::function<void(DeviceState&, int)>
         if (codes[i] != LPD_OK) fail(codes[i], "device " + std::to_string(i) + ": " + errs[i]);
 }
 
+// page-locked (cudaHostAlloc / cudaHostRegister) host memory
+bool host_pinned(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
 // Host -> device copy of a caller's (pageable) buffer through the pinned delivery ring:
 // the host team copies 8 MB pieces into ring buffers while earlier pieces are in
 // flight. A plain pageable cudaMemcpy runs at ~10 GB/s; this at the DMA rate (C4's
-// 2.1 GB L: ~0.2 s -> ~0.05 s per set_basis).
-void h2d_staged(DeviceState& ds, void* dst, const void* src, size_t bytes, cudaStream_t st) {
-    if (bytes < (size_t(32) << 20)) {  // small: the driver's own staging is fine
+// 2.1 GB L: ~0.2 s -> ~0.05 s per set_basis). Below `min_bytes`, or from page-locked
+// memory, a plain DMA.
+void h2d_staged(DeviceState& ds, void* dst, const void* src, size_t bytes, cudaStream_t st,
+                size_t min_bytes) {
+    if (bytes < min_bytes || host_pinned(src)) {  // small or already pinned: a plain DMA
         CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
         return;
     }
@@ -1711,8 +1724,11 @@ void compute_rows_host(lpd_context* ctx, int64_t n, double* G, int64_t ldg, lpd_
 // Stages CSR rows [r0, r0 + rows) into slot.x as dense fp64 (H2D of the chunk's
 // CSR arrays + device densify), recording ev[0]. Zeros are implicit, as in the
 // reference's SparseVector (dataio.hpp:23-24).
+// `via_ring`: copy the pageable index/value arrays through the pinned delivery ring
+// (h2d_staged) — only where the ring is not delivering G at the same time (prediction).
 void stage_csr_rows(DeviceState& ds, Slot& s, int64_t r0, int64_t rows, int64_t d,
-                    const int64_t* indptr, const int32_t* indices, const double* values) {
+                    const int64_t* indptr, const int32_t* indices, const double* values,
+                    bool via_ring = false) {
     const int64_t e0 = indptr[r0], e1 = indptr[r0 + rows];
     ensure_slot(ds, s, rows, true, e1 - e0);
     // rebase indptr for this chunk on the host (small), then densify on device
@@ -1721,7 +1737,10 @@ void stage_csr_rows(DeviceState& ds, Slot& s, int64_t r0, int64_t rows, int64_t 
     CUDA_TRY(cudaEventRecord(s.ev[0], s.stream));
     CUDA_TRY(cudaMemcpyAsync(s.indptr, ip.data(), sizeof(int64_t) * (rows + 1), cudaMemcpyHostToDevice,
                              s.stream));
-    if (e1 > e0) {
+    if (e1 > e0 && via_ring) {
+        h2d_staged(ds, s.indices, indices + e0, sizeof(int32_t) * (e1 - e0), s.stream, size_t(4) << 20);
+        h2d_staged(ds, s.values, values + e0, sizeof(double) * (e1 - e0), s.stream, size_t(4) << 20);
+    } else if (e1 > e0) {
         CUDA_TRY(cudaMemcpyAsync(s.indices, indices + e0, sizeof(int32_t) * (e1 - e0),
                                  cudaMemcpyHostToDevice, s.stream));
         CUDA_TRY(cudaMemcpyAsync(s.values, values + e0, sizeof(double) * (e1 - e0),
@@ -2579,7 +2598,11 @@ int lpd_predict_ovo_dense(lpd_context* ctx, const double* X, int64_t n, int64_t 
         predict_rows_host(ctx, n, num_classes, classes, [&](DeviceState& ds, Slot& s, int64_t r0, int64_t rows) {
             ensure_slot(ds, s, rows, true, 0);
             CUDA_TRY(cudaEventRecord(s.ev[0], s.stream));
-            if (d > 0)
+            // the points are the whole transfer of a prediction (K5 takes ~0.5 ms per 100k
+            // C2-shaped points): contiguous pageable rows go through the pinned ring
+            if (d > 0 && ldx == d)
+                h2d_staged(ds, s.x, X + r0 * ldx, sizeof(double) * d * rows, s.stream, size_t(4) << 20);
+            else if (d > 0)
                 CUDA_TRY(cudaMemcpy2DAsync(s.x, sizeof(double) * d, X + r0 * ldx, sizeof(double) * ldx,
                                            sizeof(double) * d, static_cast<size_t>(rows),
                                            cudaMemcpyHostToDevice, s.stream));
@@ -2596,7 +2619,7 @@ int lpd_predict_ovo_csr(lpd_context* ctx, int64_t n, int64_t d, const int64_t* i
         if (d != ctx->dev[0].d) fail(LPD_ERR_INVALID_ARGUMENT, "point dimension does not match the basis");
         if (n > 0 && !indptr) fail(LPD_ERR_INVALID_ARGUMENT, "null buffer");
         predict_rows_host(ctx, n, num_classes, classes, [&](DeviceState& ds, Slot& s, int64_t r0, int64_t rows) {
-            stage_csr_rows(ds, s, r0, rows, d, indptr, indices, values);
+            stage_csr_rows(ds, s, r0, rows, d, indptr, indices, values, true);
         });
     });
 }

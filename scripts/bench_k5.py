@@ -29,6 +29,10 @@ def main():
     X, _ = synthetic.make(cfg, rows=slice(0, args.n_test + cfg.budget))
     Y, Xt = X[: cfg.budget], np.ascontiguousarray(X[cfg.budget:])
     rng = np.random.default_rng(3)
+    nnz = np.full(Xt.shape[0], cfg.d)
+    ip = np.concatenate([[0], np.cumsum(nnz)]).astype(np.int64)
+    ix = np.tile(np.arange(cfg.d, dtype=np.int32), Xt.shape[0])
+    vv = Xt.ravel()
     out = {"n_test": int(Xt.shape[0]), "B": cfg.budget, "d": cfg.d, "gamma": cfg.gamma}
     with P.Context(1) as ctx:
         for classes in (2, 10):
@@ -44,8 +48,15 @@ def main():
                 ts.append(time.perf_counter() - t0)
                 tb.append(t1 - t0)
             t = float(np.median(ts[1:]))
+            tc = []  # the same points as CSR (the adapter's ovo_predict path), basis already set
+            for _ in range(args.reps + 1):
+                t0 = time.perf_counter()
+                cls_csr = ctx.predict_ovo_csr(ip, ix, vv, classes)
+                tc.append(time.perf_counter() - t0)
+            assert np.array_equal(cls_csr, cls)
             out[f"classes_{classes}"] = {"P": Pp, "seconds": t, "rows_per_s": Xt.shape[0] / t,
                                          "set_basis_seconds": float(np.median(tb[1:])),
+                                         "csr_predict_seconds": float(np.median(tc[1:])),
                                          "high_precision_basis": bool(ctx.basis_precision()[0]),
                                          "class_histogram": np.bincount(cls, minlength=classes).tolist()}
     print(json.dumps(out))
