@@ -218,6 +218,34 @@ def test_two_shard_context_on_one_gpu(gpu_ctx):
         ctx2.close()
 
 
+@pytest.mark.parametrize("shards", [3, 4, 8])
+def test_shard_count_invariance(gpu_ctx, shards):
+    """SURVEY §8(b) determinism: G is bitwise the same for 1 and k device shards (here k
+    device states on GPU 0), with a ragged row count that leaves the last shard short,
+    through the dense and CSR entry points; predictions too."""
+    rng = np.random.default_rng(40 + shards)
+    n, d, B = 40_003, 30, 768
+    X = rng.standard_normal((n, d)).astype(np.float32).astype(np.float64)
+    Y = np.ascontiguousarray(X[rng.choice(n, B, replace=False)])
+    L = np_gaussian_L(Y, 1.0 / d, 1e-10)
+    gpu_ctx.set_basis_dense(Y, L, 1.0 / d)
+    G1 = gpu_ctx.compute_g_dense(X)
+    ctxk = P.Context(device_ids=[0] * shards)
+    try:
+        assert ctxk.num_devices == shards
+        ctxk.set_basis_dense(Y, L, 1.0 / d)
+        assert np.array_equal(G1, ctxk.compute_g_dense(X))
+        ip, ix, vv = O.dense_to_csr(X)
+        assert np.array_equal(G1, ctxk.compute_g_csr(ip, ix, vv))
+        betas = rng.standard_normal((6, B)) * 1e-2  # 4 classes
+        bt = np.ascontiguousarray(betas.T)
+        gpu_ctx.set_basis_dense(Y, bt, 1.0 / d)
+        ctxk.set_basis_dense(Y, bt, 1.0 / d)
+        assert np.array_equal(gpu_ctx.predict_ovo_dense(X, 4), ctxk.predict_ovo_dense(X, 4))
+    finally:
+        ctxk.close()
+
+
 def test_empty_and_duplicate_points(gpu_ctx):
     rng = np.random.default_rng(4)
     X = rng.standard_normal((260, 12))
