@@ -184,15 +184,15 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def make_basis(X0, cfg, seed=1, device=None, return_ids=False):
+def make_basis(X0, cfg, seed=1, device=None, return_ids=False, host_max_b=8192):
     """Landmarks: B rows of rank 0's data drawn uniformly without replacement
     (as the reference's select_landmarks does, factor.cpp:27-31; numpy's seeded
     generator here); L from the eigendecomposition of K (factor.cpp:33-81).
-    Setup only, outside the timed region: numpy LAPACK for B <= 8192, cuSOLVER
+    Setup only, outside the timed region: numpy LAPACK for B <= host_max_b, cuSOLVER
     through torch on the GPU for larger bases (C4: B = 16384)."""
     ids = np.random.default_rng(seed).choice(X0.shape[0], cfg.budget, replace=False)
     Y = np.ascontiguousarray(X0[ids])
-    if cfg.budget <= 8192 or device is None:
+    if cfg.budget <= host_max_b or device is None:
         ny = (Y * Y).sum(1)
         K = np.exp(-cfg.gamma * np.maximum(ny[:, None] + ny[None, :] - 2.0 * Y @ Y.T, 0.0))
         w, U = np.linalg.eigh(0.5 * (K + K.T))
@@ -314,7 +314,7 @@ def main():
     N = world
     res = measure(args, cfg, n, N, rank, local, dist, dev, P, args.steps, args.warmup, not args.no_e2e)
 
-    cpu = dropin = trains = c4 = c5 = None
+    cpu = dropin = trains = c3 = c4 = c5 = None
     if rank == 0 and N == 1:
         if not args.no_cpu_baseline:
             from oracle import oracle as O
@@ -342,6 +342,16 @@ def main():
                       "path": "panel path: Z GEMM + projection GEMM (d >= 64)",
                       "roofline": r4["roofline"], "e2e": r4["e2e"], "clocks": r4["clocks"]}
                 del r4
+            if args.workload != "c3":  # device value only (its e2e needs an 82 GB host G)
+                c3cfg = synthetic.CONFIGS["c3"]
+                r3 = measure(args, c3cfg, synthetic.rows_per_gpu(c3cfg), 1, 0, local, None, dev, P,
+                             max(2, min(args.steps, 5)), 3, False, host_max_b=0)
+                c3 = {"workload": c3cfg.name, "value": r3["value"], "unit": UNIT, "n_per_gpu": r3["n"],
+                      "d": c3cfg.d, "B": r3["B"], "b_eff": r3["b_eff"], "gamma": c3cfg.gamma,
+                      "ms_per_step": r3["ms_per_step"], "steps": r3["steps"], "path": "fused K1 (d <= 63)",
+                      "basis": "L from cuSOLVER eigh on the device (setup)",
+                      "roofline": r3["roofline"], "clocks": r3["clocks"]}
+                del r3
 
     if rank == 0:
         line = {
@@ -364,6 +374,7 @@ def main():
             "e2e_dropin": dropin,
             # lpdsvm.train's train_impl (module.cpp:35-78) end to end on the drop-in build
             "train_seconds": trains,
+            "c3_shard": c3,
             "c4_shard": c4,
             # config 5: the products cross_validate / the solver run on the resident G
             "c5_resident": c5,
@@ -484,14 +495,14 @@ def e2e_train(build, config):
     return _run_e2e_subprocess([build, "train", config, "--n-test", "10000" if config == "c1" else "20000"], 1500)
 
 
-def measure(args, cfg, n, N, rank, local, dist, dev, P, steps, warmup, want_e2e):
+def measure(args, cfg, n, N, rank, local, dist, dev, P, steps, warmup, want_e2e, host_max_b=8192):
     """Device value (inputs resident in HBM), the factor kernel's roofline and the C-ABI
     e2e for one workload; rank r owns rows [r·n, (r+1)·n) of an N·n-row dataset."""
     import torch
 
     X, _ = synthetic_rows(cfg, rank, n, N)
     if rank == 0:
-        Y, L = make_basis(X, cfg, device=dev)
+        Y, L = make_basis(X, cfg, device=dev, host_max_b=host_max_b)
         meta = torch.tensor([Y.shape[0], L.shape[1]], dtype=torch.int64, device=dev)
     else:
         meta = torch.zeros(2, dtype=torch.int64, device=dev)
