@@ -65,6 +65,10 @@ struct FactorParams {
     int seg_chunks;         // chunks per G accumulator segment (>= 1)
     int dbg;                // profiling ablations (LPD_K1_DEBUG), 0 in production
     unsigned long long* dbg_out;  // [2 roles x 8 phases] cycle sums when dbg & 16
+    // Z·β mode (ZBP > 0, b_eff <= ZBP): G = Z·L reduced in the epilogue, no GEMM2
+    const float* zb_beta;   // [B_pad][ZBP] fp32, L·2^-13 (zero past B and b_eff)
+    void* zb_out;           // G rows (OutT), leading dimension zb_ld
+    long long zb_ld;
 };
 
 // Phase-cycle probe for profiling builds (compile with -DLPD_K1_PROBE=1 and run with
@@ -178,7 +182,15 @@ __device__ __forceinline__ bool seg_start(int j, int n, int S) { return j == 0 |
 
 // KS1 = ceil((d + 1) / 16), the K-steps of GEMM1 (1..4): a compile-time count, so the
 // MMA warp's GEMM1 issue is fully unrolled (its issue slots are on the critical path).
-template <typename OutT, int KS1>
+//
+// ZBP > 0 (Z·β mode, for a projection of at most ZBP columns — K5 on binary and
+// few-class models, where a padded N = 256 GEMM2 would issue 256/P times the useful
+// work): no GEMM2, no Lᵀ stream and no accumulator segments. The epilogue reads S,
+// releases the buffer to GEMM1 at once, forms Z in fp32 and reduces it against the
+// fp32 table L·2^-13 (each thread: one row × 32 landmarks of a chunk, fp32 partial
+// per chunk, fp64 across chunks); the two column halves of a row meet in shared
+// memory at the end of the tile and the row's b_eff values are stored directly.
+template <typename OutT, int KS1, int ZBP = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
     nystrom_factor_kernel(const __grid_constant__ CUtensorMap tm_xhi,
                           const __grid_constant__ CUtensorMap tm_xlo,
@@ -239,7 +251,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
         tma_prefetch_desc(&tm_xhi); tma_prefetch_desc(&tm_xlo);
         tma_prefetch_desc(&tm_lmhi); tma_prefetch_desc(&tm_lmlo);
         tma_prefetch_desc(&tm_lthi); tma_prefetch_desc(&tm_ltlo);
-        tma_prefetch_desc(&tm_g);
+        if (ZBP == 0) tma_prefetch_desc(&tm_g);
     }
     if (warp == 2) tmem_alloc_2sm(tmem_slot, TMEM_COLS);
     tc_fence_before();
@@ -281,7 +293,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
                 }
             }
         }
-      } else if (warp == 3) {
+      } else if (warp == 3 && ZBP == 0) {
         // ============ TMA producer: this CTA's half of the tile's Lᵀ rows, hi and lo per chunk ============
         if (lane == 0) {
             const uint64_t keep = policy_evict_last();
@@ -316,7 +328,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
         auto gemm1 = [&](int q) {
             const uint32_t b = c1 % NSZ, ph = (c1 / NSZ) & 1;
             pr.mark(5);
-            mbar_wait(sz_empty + b, ph ^ 1);
+            if constexpr (ZBP > 0)
+                mbar_wait_cluster(z_full + b, ph ^ 1);  // the epilogue has read S out of buffer b
+            else
+                mbar_wait(sz_empty + b, ph ^ 1);
             pr.mark(0);
             mbar_wait_cluster(lm_full + lm_s, lm_ph);
             pr.mark(1);
@@ -391,6 +406,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
             pr.mark(6);
             tc_fence_after();
             // GEMM1 runs two chunks ahead of GEMM2 (three S/Z buffers).
+            if constexpr (ZBP > 0) {
+                for (int j = 0; j < p.n_chunks; ++j) gemm1(j);
+                continue;
+            }
             gemm1(0);
             if (p.n_chunks > 1) gemm1(1);
             for (int j = 0; j < p.n_chunks; ++j) {
@@ -610,6 +629,100 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
         // tile's first GEMM1s overlap the drain).
         // Tiles run column-block-major (tile = cb·n_row_tiles + rt), so the CTAs in
         // flight share one 4 MB Lᵀ column block in L2.
+        if constexpr (ZBP > 0) {
+            // ===== Z·β mode: G[i, :b_eff] = Σ_j Z_ij · L[j, :] in the epilogue =====
+            static_assert(ZBP == 1 || ZBP == 4, "Z·β mode: table rows of 1 or 4 floats");
+            double* xch = reinterpret_cast<double*>(smem + OFF_STG);  // [BM][ZBP] half-1 partials
+            const float4* beta4 = reinterpret_cast<const float4*>(p.zb_beta);
+            uint32_t itz = 0;
+            if (pair < num_tiles) write_x(0);
+            for (int tile = pair; tile < num_tiles; tile += num_pairs, ++itz) {
+                const int rt = tile % p.n_row_tiles;
+                const RowAux* rap = p.row_aux + rt * PM + r_pair;
+                const float2 ra = *reinterpret_cast<const float2*>(rap);  // (R, sx)
+                const uint64_t R2 = f2_pack(ra.x, ra.x), sx2 = f2_pack(ra.y, ra.y);
+                const float clampv = rap->clamp;
+                double acc[ZBP];
+#pragma unroll
+                for (int q = 0; q < ZBP; ++q) acc[q] = 0.0;
+                // S of chunk j + 1 is loaded from TMEM (asynchronously) while chunk j is
+                // reduced, so the two epilogue warps of an SM sub-partition keep the MUFU busy
+                // instead of waiting out the load latency in step.
+                auto load_s = [&](uint32_t (&dst)[32]) {
+                    const uint32_t b = cnt % NSZ, ph = (cnt / NSZ) & 1;
+                    mbar_wait_cluster(s_full + b, ph);
+                    tc_fence_after();
+                    tmem_ld_32x32b_x32(tmem_base + lane_off + TM_SZ + b * NC + half * 32, dst);
+                };
+                auto release_s = [&](uint32_t (&dst)[32]) {  // the load has landed: buffer back to GEMM1
+                    tmem_wait_ld();
+                    reg_fence32(dst);
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster(z_full_l + 8 * (cnt % NSZ));
+                    ++cnt;
+                };
+                auto chunk = [&](uint32_t (&sv)[32], uint32_t (&sn)[32], int j) {
+                    // this thread's 32 landmarks of the chunk: their table rows in registers.
+                    // Warp-uniform 16-byte loads, whose L1 write-back (16 B to each of 32
+                    // lanes) limits the 4-wide table: 32·ZBP/4 of them per warp and chunk.
+                    float bv[32 * ZBP];
+                    const float4* bp = beta4 + static_cast<size_t>(j * NC + half * 32) * ZBP / 4;
+#pragma unroll
+                    for (int i = 0; i < 8 * ZBP; ++i) {
+                        const float4 t4 = __ldg(bp + i);
+                        bv[4 * i] = t4.x; bv[4 * i + 1] = t4.y; bv[4 * i + 2] = t4.z; bv[4 * i + 3] = t4.w;
+                    }
+                    const bool more = j + 1 < n;
+                    if (more) load_s(sn);
+                    // two independent FMA chains (even / odd landmarks) per output column
+                    float pe[ZBP], po[ZBP];
+#pragma unroll
+                    for (int q = 0; q < ZBP; ++q) pe[q] = po[q] = 0.f;
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        if K1_ABL(32) break;  // bypass: keep the loads and the barrier protocol
+                        float t0, t1;
+                        f2_unpack(ffma2(f2_pack(__uint_as_float(sv[2 * i]), __uint_as_float(sv[2 * i + 1])),
+                                        sx2, R2), t0, t1);
+                        const float z0 = ex2_approx(fminf(t0, clampv));
+                        const float z1 = ex2_approx(fminf(t1, clampv));
+#pragma unroll
+                        for (int q = 0; q < ZBP; ++q) {
+                            pe[q] = fmaf(z0, bv[(2 * i) * ZBP + q], pe[q]);
+                            po[q] = fmaf(z1, bv[(2 * i + 1) * ZBP + q], po[q]);
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < ZBP; ++q) acc[q] += static_cast<double>(pe[q] + po[q]);
+                    if (more) release_s(sn);
+                };
+                uint32_t sa[32], sb[32];
+                load_s(sa);
+                release_s(sa);
+                for (int j = 0; j < n; j += 2) {
+                    chunk(sa, sb, j);
+                    if (j + 1 < n) chunk(sb, sa, j + 1);
+                }
+                if (tile + num_pairs < num_tiles) write_x(itz + 1);
+                // the two column halves of row r meet in shared memory
+                if (half == 1) {
+#pragma unroll
+                    for (int q = 0; q < ZBP; ++q) xch[r * ZBP + q] = acc[q];
+                }
+                named_bar_sync(1, 32 * EPI_WARPS);
+                if (half == 0) {
+                    const int row = rt * PM + r_pair;
+                    if (row < p.n_rows) {
+                        OutT* g = static_cast<OutT*>(p.zb_out) + static_cast<long long>(row) * p.zb_ld;
+#pragma unroll
+                        for (int q = 0; q < ZBP; ++q)
+                            if (q < p.b_eff) g[q] = static_cast<OutT>(acc[q] + xch[r * ZBP + q]);
+                    }
+                }
+                named_bar_sync(1, 32 * EPI_WARPS);
+            }
+        } else {
         uint32_t it = 0;
         if (pair < num_tiles) write_x(0);
         for (int tile = pair; tile < num_tiles; tile += num_pairs, ++it) {
@@ -656,6 +769,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
         store_all();
         if (lane == 0) bulk_wait_group<0>();
         __syncwarp();
+        }
         pr.mark(7);
         if (lane == 0) pr.flush(p.dbg_out ? p.dbg_out + 8 : nullptr);
     }

@@ -161,9 +161,15 @@ CUtensorMap make_plane_map(const void* base, uint64_t rows, uint64_t cols, uint3
 // factor kernel: box = 32 rows × one 128-byte row segment, 128-byte swizzle.
 // Returns false when the layout cannot be described (unaligned base or pitch).
 bool make_g_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint64_t ld,
-                bool f64) {
+                bool f64, bool exact_end = false) {
     const uint64_t es = f64 ? 8 : 4;
-    if ((reinterpret_cast<uintptr_t>(base) & 15) != 0 || (ld * es) % 16 != 0 || rows == 0 ||
+    // TMA stores clip the row end at 16-byte granularity: a row of cols·es bytes that is
+    // not a multiple of 16 has its last partial 16 bytes written in full, i.e. the padding
+    // columns after b_eff (found by test_narrow_projection_z_beta_mode: one fp64 column per
+    // row at odd b_eff). A caller's rows (exact_end) then go through the aligned staging;
+    // the library's own row buffers may take the write.
+    if ((reinterpret_cast<uintptr_t>(base) & 15) != 0 || (ld * es) % 16 != 0 ||
+        (exact_end && (cols * es) % 16 != 0) || rows == 0 ||
         cols == 0 || rows >= (1ull << 31) || cols >= (1ull << 31))
         return false;
     cuuint64_t dims[2] = {cols, rows};
@@ -261,6 +267,8 @@ struct DeviceState {
     int64_t z_rows = 0;
     GrowBuf stage_lm, stage_L, stage_ip, stage_idx, stage_val;  // basis staging (lpd_set_basis_*)
     GrowBuf col_part;        // row-slice partials of the basis column statistics (K2)
+    GrowBuf zb_beta;         // K1 Z·β table [B_pad][zb_p] fp32 (bases with b_eff <= 4)
+    int zb_p = 0;            // its width (1 or 4); 0: GEMM2 path
     int col_slices = 0;      // slices in col_part (column sums of L²)
     int host_share = 1;                // device states of this context sharing the host's cores
     // host CPUs local to this GPU (its PCI device's NUMA node) when that is a proper subset of
@@ -431,6 +439,20 @@ FactorKernel factor_kernel_for(bool f64, int ks1) {
     }
 }
 
+// K1 in Z·β mode (projection width <= zbp, 1 or 4)
+template <int ZBP>
+FactorKernel factor_kernel_zb_w(bool f64, int ks1) {
+    switch (ks1) {
+        case 1: return f64 ? lpd::nystrom_factor_kernel<double, 1, ZBP> : lpd::nystrom_factor_kernel<float, 1, ZBP>;
+        case 2: return f64 ? lpd::nystrom_factor_kernel<double, 2, ZBP> : lpd::nystrom_factor_kernel<float, 2, ZBP>;
+        case 3: return f64 ? lpd::nystrom_factor_kernel<double, 3, ZBP> : lpd::nystrom_factor_kernel<float, 3, ZBP>;
+        default: return f64 ? lpd::nystrom_factor_kernel<double, 4, ZBP> : lpd::nystrom_factor_kernel<float, 4, ZBP>;
+    }
+}
+FactorKernel factor_kernel_zb_for(bool f64, int ks1, int zbp) {
+    return zbp == 1 ? factor_kernel_zb_w<1>(f64, ks1) : factor_kernel_zb_w<4>(f64, ks1);
+}
+
 // CPUs in a sysfs list ("0-27,56-83").
 void parse_cpulist(const std::string& text, cpu_set_t* set) {
     CPU_ZERO(set);
@@ -549,6 +571,10 @@ void init_device(DeviceState& ds, int device) {
                                       lpd::k1::SMEM_BYTES));
         CUDA_TRY(cudaFuncSetAttribute(factor_kernel_for(false, ks), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       lpd::k1::SMEM_BYTES));
+        for (int zbp : {1, 4})
+            for (bool f64 : {true, false})
+                CUDA_TRY(cudaFuncSetAttribute(factor_kernel_zb_for(f64, ks, zbp),
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, lpd::k1::SMEM_BYTES));
     }
     // Load every kernel now (CUDA lazy loading would otherwise charge the first call of
     // each one): context creation runs in the background when the adapter loads.
@@ -856,6 +882,20 @@ void build_basis(DeviceState& ds, const double* lm_dev, int64_t B, int64_t d, in
                                                         static_cast<int>(b_eff), ds.colmax, ds.lt_hi,
                                                         ds.lt_lo, static_cast<int>(B_pad),
                                                         static_cast<int>(Beff_pad), ds.col_scale);
+    // narrow projections (K5 on binary and 3-class models): Z·β in K1's epilogue instead
+    // of a GEMM2 padded to N = 256 (LPD_ZBETA=0: the GEMM2 path, for A/B studies)
+    static const bool zbeta_on = [] {
+        const char* e = std::getenv("LPD_ZBETA");
+        return !(e && e[0] == '0');
+    }();
+    ds.zb_p = 0;
+    if (zbeta_on && !large && b_eff <= 4) {
+        ds.zb_p = b_eff == 1 ? 1 : 4;
+        const int64_t cnt = B_pad * ds.zb_p;
+        float* zb = static_cast<float*>(ds.zb_beta.get(sizeof(float) * static_cast<size_t>(cnt)));
+        lpd::zb_table_kernel<<<static_cast<int>((cnt + 255) / 256), 256, 0, st>>>(
+            L_dev, static_cast<int>(B), static_cast<int>(b_eff), static_cast<int>(B_pad), ds.zb_p, zb);
+    }
     CUDA_TRY(cudaGetLastError());
     choose_precision(ds, lm_dev, B, d, ld_lm, L_dev, b_eff, st);
     if (sync) CUDA_TRY(cudaStreamSynchronize(st));
@@ -1107,8 +1147,10 @@ void launch_factor_panels(DeviceState& ds, Slot& s, int64_t m, void* g_dev, int6
 }
 
 // prep + fused factor kernel for m rows of dense fp64 X already on the device.
+// caller_g: G rows belong to the caller (their padding after b_eff must stay untouched).
 void launch_factor(DeviceState& ds, Slot& s, const double* x_dev, int64_t m, int64_t ldx,
-                   void* g_dev, int64_t ldg, int out_dtype, cudaStream_t st, bool time_it) {
+                   void* g_dev, int64_t ldg, int out_dtype, cudaStream_t st, bool time_it,
+                   bool caller_g = false) {
     if (m <= 0) return;
     if (ds.hp) {
         launch_factor_hp(ds, x_dev, m, ldx, g_dev, ldg, out_dtype, st, time_it);
@@ -1132,6 +1174,50 @@ void launch_factor(DeviceState& ds, Slot& s, const double* x_dev, int64_t m, int
         launch_factor_panels(ds, s, m, g_dev, ldg, out_dtype, st, time_it);
         return;
     }
+    if (ds.zb_p > 0) {
+        // K1 in Z·β mode: plain row stores (any pitch), no Lᵀ stream, one column block
+        lpd::FactorParams p{};
+        p.n_rows = static_cast<int>(m);
+        p.n_row_tiles = static_cast<int>(m_pad / lpd::k1::PM);
+        p.n_chunks = static_cast<int>(ds.B_pad / lpd::k1::NC);
+        p.n_col_blocks = 1;
+        p.b_eff = static_cast<int>(ds.b_eff);
+        p.ksteps1 = static_cast<int>((ds.d + 1 + 15) / 16);
+        p.row_aux = s.raux;
+        p.col_scale = ds.col_scale;
+        p.seg_chunks = 1;
+        static const int zb_dbg = [] {  // ablation switches (LPD_K1_ABLATIONS builds only)
+            const char* e = std::getenv("LPD_K1_DEBUG");
+            return e ? std::atoi(e) & ~16 : 0;
+        }();
+        p.dbg = zb_dbg;
+        p.zb_beta = static_cast<const float*>(ds.zb_beta.p);
+        p.zb_out = g_dev;
+        p.zb_ld = ldg;
+        CUtensorMap tm_none;
+        std::memset(&tm_none, 0, sizeof(tm_none));
+        const int grid = 2 * static_cast<int>(std::min<int64_t>(p.n_row_tiles, ds.num_sms / 2));
+        cudaEvent_t* pr = nullptr;
+        if (time_it) {
+            pr = ds.ring[ds.ring_count % DeviceState::kRing];
+            CUDA_TRY(cudaEventRecord(ds.kev[0], st));
+            if (ds.ring_count < DeviceState::kRing) CUDA_TRY(cudaEventRecord(pr[0], st));
+        }
+        const CUtensorMap tm_xhi = make_plane_map(s.xhi, m_pad, lpd::KD_MAX, lpd::k1::BM, 64);
+        const CUtensorMap tm_xlo = make_plane_map(s.xlo, m_pad, lpd::KD_MAX, lpd::k1::BM, 64);
+        factor_kernel_zb_for(out_dtype == LPD_OUT_F64, p.ksteps1, ds.zb_p)<<<grid, lpd::k1::THREADS,
+                                                                             lpd::k1::SMEM_BYTES, st>>>(
+            tm_xhi, tm_xlo, ds.tm_lmhi, ds.tm_lmlo, ds.tm_lthi, ds.tm_ltlo, tm_none, p);
+        if (time_it) {
+            CUDA_TRY(cudaEventRecord(ds.kev[1], st));
+            if (ds.ring_count < DeviceState::kRing) CUDA_TRY(cudaEventRecord(pr[1], st));
+            ++ds.ring_count;
+        }
+        fault_point(LPD_FAULT_LAUNCH);
+        CUDA_TRY(cudaGetLastError());
+        launch_row_rescale(ds, s, m, g_dev, ldg, out_dtype, st);
+        return;
+    }
     // The kernel stores G with TMA, which needs 16-byte aligned rows; an unaligned
     // caller layout is served through an aligned device buffer and a 2-D copy.
     CUtensorMap tm_g;
@@ -1140,7 +1226,7 @@ void launch_factor(DeviceState& ds, Slot& s, const double* x_dev, int64_t m, int
     void* g_out = g_dev;
     int64_t ld_out = ldg;
     if (!make_g_map(&tm_g, g_dev, static_cast<uint64_t>(m), static_cast<uint64_t>(ds.b_eff),
-                    static_cast<uint64_t>(ldg), out_dtype == LPD_OUT_F64)) {
+                    static_cast<uint64_t>(ldg), out_dtype == LPD_OUT_F64, caller_g)) {
         ld_out = round_up(ds.b_eff, 4);
         const size_t need = static_cast<size_t>(m * ld_out) * es;
         if (ds.gtmp_bytes < need) {
@@ -1152,7 +1238,7 @@ void launch_factor(DeviceState& ds, Slot& s, const double* x_dev, int64_t m, int
             ds.gtmp_bytes = need;
         }
         g_out = ds.gtmp;
-        if (!make_g_map(&tm_g, g_out, static_cast<uint64_t>(m), static_cast<uint64_t>(ds.b_eff),
+        if (!make_g_map(&tm_g, g_out, static_cast<uint64_t>(m), static_cast<uint64_t>(ld_out),
                         static_cast<uint64_t>(ld_out), out_dtype == LPD_OUT_F64))
             fail(LPD_ERR_CUDA, "cannot describe the G staging buffer as a TMA tensor");
     }
@@ -1166,6 +1252,9 @@ void launch_factor(DeviceState& ds, Slot& s, const double* x_dev, int64_t m, int
     p.row_aux = s.raux;
     p.col_scale = ds.col_scale;
     p.seg_chunks = seg_chunks(ds.B_pad > 4096 ? 2 : 4);
+    p.zb_beta = nullptr;
+    p.zb_out = nullptr;
+    p.zb_ld = 0;
     static const int dbg = [] {
         const char* e = std::getenv("LPD_K1_DEBUG");
         return e ? std::atoi(e) : 0;
@@ -2273,7 +2362,8 @@ int lpd_context_destroy(lpd_context* ctx) {
         ds.model.free_all();
         ds.free_hp();
         dev_free(ds.hp_norms);
-        for (GrowBuf* g : {&ds.stage_lm, &ds.stage_L, &ds.stage_ip, &ds.stage_idx, &ds.stage_val, &ds.col_part})
+        for (GrowBuf* g : {&ds.stage_lm, &ds.stage_L, &ds.stage_ip, &ds.stage_idx, &ds.stage_val, &ds.col_part,
+                           &ds.zb_beta})
             g->release();
         if (ds.scratch) cudaFree(ds.scratch);
         if (ds.gtmp) cudaFree(ds.gtmp);
@@ -2465,7 +2555,7 @@ int lpd_compute_g_device(lpd_context* ctx, int device_index, const double* X_dev
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ds.slot[0].stream;
         Slot& s = ds.slot[0];
         ensure_slot(ds, s, n, false, 0);
-        launch_factor(ds, s, X_dev, n, ldx, G_dev, ldg, out_dtype, st, true);
+        launch_factor(ds, s, X_dev, n, ldx, G_dev, ldg, out_dtype, st, true, true);
         if (!stream) {
             CUDA_TRY(cudaStreamSynchronize(st));
             check_range_flag(ds);

@@ -337,6 +337,16 @@ __global__ void col_stats_kernel(const double* __restrict__ L, int B, int b_eff,
 
 
 // Lᵀ split planes [Beff_pad × B_pad]: lt[k][j] = L[j][k]·u_k (hi/lo), padded with 0.
+// K1's Z·β table (ZBP > 0): zb[j][q] = L[j][q]·2^-13 in fp32 (K1's Z carries 2^13), zero
+// past B landmarks and b_eff columns. One thread per entry; B_pad·ZBP entries.
+__global__ void zb_table_kernel(const double* __restrict__ L, int B, int b_eff, int B_pad, int zbp,
+                                float* __restrict__ zb) {
+    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (i >= static_cast<long long>(B_pad) * zbp) return;
+    const int j = static_cast<int>(i / zbp), q = static_cast<int>(i % zbp);
+    zb[i] = (j < B && q < b_eff) ? static_cast<float>(ldexp(L[static_cast<long long>(j) * b_eff + q], -13)) : 0.f;
+}
+
 // 64 (landmarks j) × 32 (columns k) tiles through shared memory: the reads are 256-byte
 // rows of L, and each lane writes two consecutive landmarks of an Lᵀ row as one __half2 per
 // plane (128-byte warp stores; B_pad is a multiple of 64).

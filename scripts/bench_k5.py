@@ -35,7 +35,7 @@ def main():
     vv = Xt.ravel()
     out = {"n_test": int(Xt.shape[0]), "B": cfg.budget, "d": cfg.d, "gamma": cfg.gamma}
     with P.Context(1) as ctx:
-        for classes in (2, 10):
+        for classes in (2, 3, 10):
             Pp = classes * (classes - 1) // 2
             betas = rng.standard_normal((Pp, cfg.budget)) * 1e-2
             ts, tb = [], []

@@ -786,3 +786,38 @@ def test_caller_pitches_bitwise(gpu_ctx, d, extra_x, extra_g):
     assert st == 0, P.load_library().lpd_last_error()
     assert np.array_equal(Gp[:, :be], ref)
     assert np.all(Gp[:, be:] == -7.0)
+
+
+@pytest.mark.parametrize("k", [1, 3, 4, 5, 15, 16, 17])
+def test_narrow_projection_z_beta_mode(gpu_ctx, k):
+    """K1's Z·β mode (b_eff <= 4: no GEMM2, Z reduced against L in the epilogue; K5 on
+    binary and 3-class models) and the GEMM2 path just past it (5, 15, 16, 17). L = k columns of the identity exposes Z itself (1e-5 relative,
+    SURVEY §8(c) criterion 1); random β rows are the prediction case (multiclass.cpp:192);
+    fp64 device output, fp32 device output and the host entry agree."""
+    import torch
+
+    rng = np.random.default_rng(100 + k)
+    n, d, B, gamma = 3000, 54, 700, 1.0 / 54
+    X = rng.standard_normal((n, d)).astype(np.float32).astype(np.float64)
+    Y = X[rng.choice(n, B, replace=False)]
+    E = np.ascontiguousarray(np.eye(B)[:, rng.choice(B, k, replace=False)])
+    gpu_ctx.set_basis_dense(Y, E, gamma)
+    Z = gpu_ctx.compute_g_dense(X)
+    Zr = O.ora_kernel_block(O.dense_to_csr(X), O.dense_to_csr(Y), gamma) @ E
+    live = Zr > 1e-30
+    assert np.max(np.abs(Z - Zr)[live] / Zr[live]) <= 1e-5
+    assert np.all(np.abs(Z[~live]) <= 1e-30)
+    betas = rng.standard_normal((B, k))
+    gpu_ctx.set_basis_dense(Y, betas, gamma)
+    G = gpu_ctx.compute_g_dense(X)
+    assert_conditioned_parity(G, X, Y, betas, gamma)
+    Xd = torch.from_numpy(X).cuda()
+    G64full = torch.full((n, k + 3), 7.0, dtype=torch.float64, device="cuda")
+    G64 = G64full[:, :k]  # pitch k + 3
+    G32 = torch.empty((n, k), dtype=torch.float32, device="cuda")
+    gpu_ctx.compute_g_device(Xd, G64)
+    gpu_ctx.compute_g_device(Xd, G32)
+    torch.cuda.synchronize()
+    assert np.array_equal(G32.cpu().numpy(), G.astype(np.float32))
+    assert np.max(np.abs(G64.cpu().numpy() - G)) <= 1e-6 * np.abs(G).max()
+    assert np.all(G64full.cpu().numpy()[:, k:] == 7.0)  # padding untouched
