@@ -63,5 +63,16 @@ for d in (32, 96):
     ctx.compute_g_device(torch.from_numpy(X).cuda(), Gd)
     torch.cuda.synchronize()
     ctx.set_precision("auto")
+# K1 Z·β mode (b_eff <= 4): 1- and 4-wide tables, host rows, device rows (fp64, pitched) and K5
+for k in (1, 4):
+    X = rng.standard_normal((700, 40))
+    Y = X[:150]
+    ctx.set_basis_dense(Y, rng.standard_normal((150, k)), 1.0 / 40)
+    ctx.compute_g_dense(X)
+    Gf = torch.zeros((700, k + 3), dtype=torch.float64, device="cuda")
+    ctx.compute_g_device(torch.from_numpy(X).cuda(), Gf[:, :k])
+    torch.cuda.synchronize()
+    if k == 1:
+        ctx.predict_ovo_dense(X, 2)
 ctx.close()
 print("sanitize_kernels: every kernel ran")
