@@ -821,3 +821,30 @@ def test_narrow_projection_z_beta_mode(gpu_ctx, k):
     assert np.array_equal(G32.cpu().numpy(), G.astype(np.float32))
     assert np.max(np.abs(G64.cpu().numpy() - G)) <= 1e-6 * np.abs(G).max()
     assert np.all(G64full.cpu().numpy()[:, k:] == 7.0)  # padding untouched
+
+
+@pytest.mark.parametrize("d,mult,shift,k", [(32, 16, 2, 1), (32, 64, 1, 3), (32, 8, 4, 4), (20, 1, 0, 2)])
+def test_far_rows_z_beta_mode(gpu_ctx, d, mult, shift, k):
+    """K9's per-row exponent normalisation under K1's Z·β mode (b_eff <= 4): the row
+    shift set by row_shift_kernel enters the epilogue's t and clamp and is undone by
+    row_rescale on the directly stored rows; same 1e-4 row bound as the GEMM2 path."""
+    import torch
+
+    X, Y, L, gamma = _far_rows_case(d, mult, shift)
+    L = np.ascontiguousarray(L[:, :k])
+    gpu_ctx.set_precision("fast")
+    try:
+        gpu_ctx.set_basis_dense(Y, L, gamma)
+        Gd = torch.empty((X.shape[0], k), dtype=torch.float64, device="cuda")
+        gpu_ctx.compute_g_device(torch.from_numpy(X).cuda(), Gd)
+        torch.cuda.synchronize()
+        G = Gd.cpu().numpy()
+    finally:
+        gpu_ctx.set_precision("auto")
+    R = _oracle_G(X, Y, L, gamma)
+    nr = np.linalg.norm(R, axis=1)
+    live = nr > 0
+    assert live.sum() >= X.shape[0] // 2
+    assert np.all(G[~live] == 0.0)
+    err = np.linalg.norm(G - R, axis=1)[live] / nr[live]
+    assert float(err.max()) <= TOL_G, float(err.max())
