@@ -326,12 +326,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
         // GEMM1 of chunk q: S(b) = X·B̃ᵀ, three split passes. The last one of a tile
         // also releases the X tile.
         auto gemm1 = [&](int q) {
+            // Z·β mode: a buffer takes two chunks (128 columns; no G accumulator in TMEM),
+            // so the epilogue meets the MMA once per two chunks
             const uint32_t b = c1 % NSZ, ph = (c1 / NSZ) & 1;
+            const bool opens = ZBP == 0 || (q & 1) == 0;
+            const bool closes = ZBP == 0 || (q & 1) || q == p.n_chunks - 1;
             pr.mark(5);
-            if constexpr (ZBP > 0)
-                mbar_wait_cluster(z_full + b, ph ^ 1);  // the epilogue has read S out of buffer b
-            else
+            if constexpr (ZBP > 0) {
+                if (opens) mbar_wait_cluster(z_full + b, ph ^ 1);  // the epilogue has read buffer b
+            } else {
                 mbar_wait(sz_empty + b, ph ^ 1);
+            }
             pr.mark(0);
             mbar_wait_cluster(lm_full + lm_s, lm_ph);
             pr.mark(1);
@@ -339,7 +344,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
             if (elect_one()) {
                 const uint64_t d_lmhi = d_lm0 + ((lm_s * 2 * LM_BYTES) >> 4);
                 const uint64_t d_lmlo = d_lmhi + (LM_BYTES >> 4);
-                const uint32_t d = tmem_base + TM_SZ + b * NC;
+                const uint32_t d = ZBP > 0 ? tmem_base + b * (2 * NC) + (q & 1) * NC : tmem_base + TM_SZ + b * NC;
 #pragma unroll
                 for (int pass = 0; pass < 3; ++pass) {
                     const uint32_t a = tmem_base + ((pass == 2) ? TM_XLO : TM_XHI);
@@ -349,12 +354,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
                         if (!K1_ABL(8)) mma_f16_ts_2sm(d, a + 8 * k, bb + 2 * k, IDESC_G1, (pass | k) != 0);
                 }
                 mma_commit_2sm_mc(lm_empty + lm_s, PAIR);
-                mma_commit_2sm_mc(s_full + b, PAIR);
+                if (closes) mma_commit_2sm_mc(s_full + b, PAIR);
                 if (q == p.n_chunks - 1) mma_commit_2sm_mc(x_empty, PAIR);
             }
             __syncwarp();
             if (++lm_s == NS_LM) { lm_s = 0; lm_ph ^= 1; }
-            ++c1;
+            if (closes) ++c1;
         };
         // GEMM2 of chunk j: G += Z_hi·Lᵀ_hi + Z_lo·Lᵀ_hi + Z_hi·Lᵀ_lo, Z from TMEM, one
         // N=256 MMA per K-step. At the start of a segment it first waits until the
@@ -645,64 +650,64 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k1::THREADS, 1)
                 double acc[ZBP];
 #pragma unroll
                 for (int q = 0; q < ZBP; ++q) acc[q] = 0.0;
-                // S of chunk j + 1 is loaded from TMEM (asynchronously) while chunk j is
-                // reduced, so the two epilogue warps of an SM sub-partition keep the MUFU busy
-                // instead of waiting out the load latency in step.
-                auto load_s = [&](uint32_t (&dst)[32]) {
+                // One S buffer holds two chunks (128 TMEM columns): one wait, one or two
+                // 32-column loads and one release per pair of chunks.
+                for (int j0 = 0; j0 < n; j0 += 2) {
+                    const int cnum = min(2, n - j0);
                     const uint32_t b = cnt % NSZ, ph = (cnt / NSZ) & 1;
+                    // the first chunk's table rows (L·2^-13) before the wait; warp-uniform
+                    // 16-byte loads, whose L1 write-back (16 B to each of 32 lanes) limits the
+                    // 4-wide table: 32·ZBP/4 of them per warp and chunk
+                    float bv[32 * ZBP];
+                    auto load_beta = [&](int j) {
+                        const float4* bp = beta4 + static_cast<size_t>(j * NC + half * 32) * ZBP / 4;
+#pragma unroll
+                        for (int i = 0; i < 8 * ZBP; ++i) {
+                            const float4 t4 = __ldg(bp + i);
+                            bv[4 * i] = t4.x; bv[4 * i + 1] = t4.y; bv[4 * i + 2] = t4.z; bv[4 * i + 3] = t4.w;
+                        }
+                    };
+                    load_beta(j0);
+                    uint32_t sv0[32], sv1[32];
                     mbar_wait_cluster(s_full + b, ph);
                     tc_fence_after();
-                    tmem_ld_32x32b_x32(tmem_base + lane_off + TM_SZ + b * NC + half * 32, dst);
-                };
-                auto release_s = [&](uint32_t (&dst)[32]) {  // the load has landed: buffer back to GEMM1
+                    const uint32_t col = tmem_base + lane_off + b * (2 * NC) + half * 32;
+                    tmem_ld_32x32b_x32(col, sv0);
+                    if (cnum == 2) tmem_ld_32x32b_x32(col + NC, sv1);
                     tmem_wait_ld();
-                    reg_fence32(dst);
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive_cluster(z_full_l + 8 * (cnt % NSZ));
+                    if (lane == 0) mbar_arrive_cluster(z_full_l + 8 * b);  // buffer back to GEMM1
                     ++cnt;
-                };
-                auto chunk = [&](uint32_t (&sv)[32], uint32_t (&sn)[32], int j) {
-                    // this thread's 32 landmarks of the chunk: their table rows in registers.
-                    // Warp-uniform 16-byte loads, whose L1 write-back (16 B to each of 32
-                    // lanes) limits the 4-wide table: 32·ZBP/4 of them per warp and chunk.
-                    float bv[32 * ZBP];
-                    const float4* bp = beta4 + static_cast<size_t>(j * NC + half * 32) * ZBP / 4;
 #pragma unroll
-                    for (int i = 0; i < 8 * ZBP; ++i) {
-                        const float4 t4 = __ldg(bp + i);
-                        bv[4 * i] = t4.x; bv[4 * i + 1] = t4.y; bv[4 * i + 2] = t4.z; bv[4 * i + 3] = t4.w;
-                    }
-                    const bool more = j + 1 < n;
-                    if (more) load_s(sn);
-                    // two independent FMA chains (even / odd landmarks) per output column
-                    float pe[ZBP], po[ZBP];
-#pragma unroll
-                    for (int q = 0; q < ZBP; ++q) pe[q] = po[q] = 0.f;
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        if K1_ABL(32) break;  // bypass: keep the loads and the barrier protocol
-                        float t0, t1;
-                        f2_unpack(ffma2(f2_pack(__uint_as_float(sv[2 * i]), __uint_as_float(sv[2 * i + 1])),
-                                        sx2, R2), t0, t1);
-                        const float z0 = ex2_approx(fminf(t0, clampv));
-                        const float z1 = ex2_approx(fminf(t1, clampv));
-#pragma unroll
-                        for (int q = 0; q < ZBP; ++q) {
-                            pe[q] = fmaf(z0, bv[(2 * i) * ZBP + q], pe[q]);
-                            po[q] = fmaf(z1, bv[(2 * i + 1) * ZBP + q], po[q]);
+                    for (int c = 0; c < 2; ++c) {
+                        if (c == 1) {
+                            if (cnum < 2) break;
+                            load_beta(j0 + 1);
                         }
-                    }
+                        // two independent FMA chains (even / odd landmarks) per output column
+                        float pe[ZBP], po[ZBP];
 #pragma unroll
-                    for (int q = 0; q < ZBP; ++q) acc[q] += static_cast<double>(pe[q] + po[q]);
-                    if (more) release_s(sn);
-                };
-                uint32_t sa[32], sb[32];
-                load_s(sa);
-                release_s(sa);
-                for (int j = 0; j < n; j += 2) {
-                    chunk(sa, sb, j);
-                    if (j + 1 < n) chunk(sb, sa, j + 1);
+                        for (int q = 0; q < ZBP; ++q) pe[q] = po[q] = 0.f;
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            if K1_ABL(32) break;  // bypass: keep the loads and the barrier protocol
+                            float t0, t1;
+                            const uint32_t s0 = c ? sv1[2 * i] : sv0[2 * i];
+                            const uint32_t s1 = c ? sv1[2 * i + 1] : sv0[2 * i + 1];
+                            f2_unpack(ffma2(f2_pack(__uint_as_float(s0), __uint_as_float(s1)),
+                                            sx2, R2), t0, t1);
+                            const float z0 = ex2_approx(fminf(t0, clampv));
+                            const float z1 = ex2_approx(fminf(t1, clampv));
+#pragma unroll
+                            for (int q = 0; q < ZBP; ++q) {
+                                pe[q] = fmaf(z0, bv[(2 * i) * ZBP + q], pe[q]);
+                                po[q] = fmaf(z1, bv[(2 * i + 1) * ZBP + q], po[q]);
+                            }
+                        }
+#pragma unroll
+                        for (int q = 0; q < ZBP; ++q) acc[q] += static_cast<double>(pe[q] + po[q]);
+                    }
                 }
                 if (tile + num_pairs < num_tiles) write_x(itz + 1);
                 // the two column halves of row r meet in shared memory

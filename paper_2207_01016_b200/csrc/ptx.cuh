@@ -346,18 +346,6 @@ __device__ __forceinline__ void tmem_wait_st() {
 __device__ __forceinline__ void tmem_wait_ld() {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
-// Ties 32 registers filled by an earlier tcgen05.ld to this point (place it after
-// tmem_wait_ld): later uses depend on its outputs, so the compiler cannot hoist them
-// above the wait when other work sits between the load and the wait.
-__device__ __forceinline__ void reg_fence32(uint32_t (&v)[32]) {
-#pragma unroll
-    for (int h = 0; h < 32; h += 16)
-        asm volatile(""
-                     : "+r"(v[h + 0]), "+r"(v[h + 1]), "+r"(v[h + 2]), "+r"(v[h + 3]), "+r"(v[h + 4]),
-                       "+r"(v[h + 5]), "+r"(v[h + 6]), "+r"(v[h + 7]), "+r"(v[h + 8]), "+r"(v[h + 9]),
-                       "+r"(v[h + 10]), "+r"(v[h + 11]), "+r"(v[h + 12]), "+r"(v[h + 13]), "+r"(v[h + 14]),
-                       "+r"(v[h + 15]));
-}
 
 // ---------------------------------------------------------------- UMMA descriptors
 // Instruction descriptor, kind::f16: A = B = fp16, D = fp32, both K-major.
